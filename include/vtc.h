@@ -1,0 +1,118 @@
+/* vtc -- C ABI of the B200-native executor for VTC-planned graphs.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and status codes, no
+ * C++ or torch types.  Each entry point replaces one reference interface
+ * (paths relative to /root/reference):
+ *
+ *   vtc_graph_parse       <- vtelim::parse_graph          proj/include/vtelim/graph_ir.hpp:108 (src/graph_ir.cpp:455-485)
+ *   vtc_graph_serialize   <- vtelim::serialize_graph      proj/include/vtelim/graph_ir.hpp:109
+ *   vtc_graph_vtog        <- vtelim::build_vtog           proj/include/vtelim/vtog.hpp:42
+ *   vtc_plan_create       <- vtelim::validate_ptg / all_physical_ptg (+ the planner's selection)
+ *                                                         proj/include/vtelim/vtog.hpp:58, cost_model.hpp:61
+ *   vtc_plan_info         <- PointsToGraph {roots, eliminated_ops} + vtelim::estimate
+ *                                                         proj/include/vtelim/vtog.hpp:45-53, cost_model.hpp:59
+ *   vtc_plan_upload / vtc_execute / vtc_plan_download
+ *                         <- vtelim::execute / execute_detailed / ExecutionResult::materialize
+ *                                                         proj/include/vtelim/executor.hpp:77-83, 71
+ *   vtc_map_eval          <- vtelim::IndexMap::eval       proj/include/vtelim/mapping.hpp:70
+ *   vtc_launch_gather_copy<- vtelim::load_virtual + store_virtual (one copy through two maps)
+ *                                                         proj/include/vtelim/executor.hpp:59-62
+ *
+ * Errors: C++ exceptions never cross this boundary.  Every int-returning call
+ * returns VTC_OK or the status code of the reference error class
+ * (proj/include/vtelim/errors.hpp:14-38); vtc_last_error() gives the message.
+ * Threading: one plan per host thread; plans are independent.
+ */
+#ifndef VTC_H
+#define VTC_H
+
+#include <stdint.h>
+
+#include "vtc_desc.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum vtc_status {
+    VTC_OK = 0,
+    VTC_ERR_GENERIC = 1,
+    VTC_ERR_SCHEMA = 2,
+    VTC_ERR_CYCLE = 3,
+    VTC_ERR_SHAPE = 4,
+    VTC_ERR_UNKNOWN_OPERATOR = 5,
+    VTC_ERR_OUT_OF_BOUNDS = 6,
+    VTC_ERR_MISSING_BASE_MAP = 7,
+    VTC_ERR_COMPOSE_LIMIT = 8,
+    VTC_ERR_CONFLICT = 9,
+    VTC_ERR_INCOMPLETE_SELECTION = 10,
+    VTC_ERR_CYCLE_DETECTED = 11,
+    VTC_ERR_WRITE_ALIASING = 12,
+    VTC_ERR_SPACE_TOO_LARGE = 13,
+    VTC_ERR_MISSING_INPUT = 14,
+    VTC_ERR_SHAPE_MISMATCH = 15,
+    VTC_ERR_EXECUTION = 16,
+    VTC_ERR_EQUIVALENCE = 17,
+    VTC_ERR_INVALID_VTOG = 18,
+    VTC_ERR_BUDGET = 19,
+    VTC_ERR_CUDA = 20,
+    VTC_ERR_NCCL = 21,
+    VTC_ERR_UNSUPPORTED = 22
+};
+
+enum vtc_plan_mode {
+    VTC_PLAN_MATERIALIZE = 0,     /* all-physical points-to graph: materialising baseline */
+    VTC_PLAN_SELECTED = 1,        /* caller-selected VTOG edges (validate_ptg) */
+    VTC_PLAN_MAX_ELIMINATION = 2  /* built-in strategy: eliminate every eliminable DM op */
+};
+
+enum vtc_plan_flags {
+    VTC_FLAG_FAST_FP = 1u << 0,  /* generic f32/f64 MatMul with FMA instead of the bit-exact mul+add */
+    VTC_FLAG_NO_GEMV = 1u << 1,  /* disable the weight-streaming decode kernel */
+    VTC_FLAG_NO_FUSE = 1u << 2   /* disable RMSNorm/SiLU*Mul/residual fusion into the GEMV */
+};
+
+typedef struct vtc_graph vtc_graph;
+typedef struct vtc_plan vtc_plan;
+
+const char* vtc_last_error(void);
+const char* vtc_version(void);
+
+int vtc_graph_parse(const char* json_text, vtc_graph** out);
+void vtc_graph_free(vtc_graph* g);
+/* Returned strings stay valid until the next call on the same thread. */
+int vtc_graph_serialize(vtc_graph* g, const char** json_out);
+int vtc_graph_vtog(vtc_graph* g, const char** json_out);
+
+int vtc_plan_create(vtc_graph* g, int mode, const int32_t* selected, int32_t n_selected, uint32_t flags,
+                    vtc_plan** out);
+void vtc_plan_free(vtc_plan* p);
+/* JSON: roots, eliminated_ops, selected, resolved map text, launches, bytes
+ * (all-physical vs this plan, per reference estimate), data_movement_kernels.
+ * dry != 0 plans the launch list without touching the GPU. */
+int vtc_plan_info(vtc_plan* p, int dry, const char** json_out);
+
+int vtc_plan_bind_root(vtc_plan* p, const char* tensor, void* dev_ptr);
+int vtc_plan_root_ptr(vtc_plan* p, const char* tensor, void** dev_ptr);
+int vtc_plan_upload(vtc_plan* p, const char* tensor, const void* host, int64_t bytes, void* stream);
+int vtc_plan_download(vtc_plan* p, const char* tensor, void* host, int64_t bytes, void* stream);
+int vtc_plan_prepare(vtc_plan* p);
+int vtc_execute(vtc_plan* p, void* stream);        /* async launches on `stream` (cudaStream_t) */
+int vtc_execute_graph(vtc_plan* p, void* stream);  /* CUDA-graph replay of the same launches */
+int vtc_plan_num_launches(vtc_plan* p);
+
+/* Host evaluation (no GPU) of a tensor's resolved map over its whole index
+ * space in row-major order: targets[i] = index into the sorted target list
+ * (vtc_plan_map_json "targets"), offsets[i] = element offset.  lowered != 0
+ * evaluates the device descriptor instead of the symbolic map. */
+int vtc_map_eval(vtc_plan* p, const char* tensor, int lowered, int32_t* targets, int64_t* offsets, int64_t cap);
+int vtc_plan_map_json(vtc_plan* p, const char* tensor, const char** json_out);
+
+/* Low-level kernel entry: dst[map_dst(I)] = src[map_src(I)] over dst->shape. */
+int vtc_launch_gather_copy(const vtc_map* dst, const vtc_map* src, int32_t elem_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VTC_H */

@@ -1,0 +1,84 @@
+// GPU executor for VTC-planned graphs.
+//
+// Same shape as the reference interpreter's execute_detailed
+// (proj/src/executor.cpp:448-498): only physical roots own device buffers,
+// nodes run in the graph's deterministic topological order, eliminated
+// data-movement operators launch nothing, and every operand is read / written
+// through its resolved map onto the roots -- inside the consumer kernel.
+// The all-physical points-to graph gives the materialising baseline executor
+// on the same kernels (each data-movement op becomes one gather-copy launch).
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "vtc/graph.hpp"
+#include "vtc/plan.hpp"
+
+namespace vtc {
+
+struct ExecOptions {
+    bool exact_fp = true;     // generic f32/f64 MatMul: unfused mul+add (bit-exact vs CPU reference)
+    bool use_gemv = true;     // bf16 decode projections on the weight-streaming kernel
+    bool fuse = true;         // RMSNorm->MatMul, SiLU*Mul->MatMul, MatMul->Add(residual) fusion
+    int attn_splits = 0;      // 0: automatic
+};
+
+struct RootBuffer {
+    std::string id;
+    DType dtype = DType::F32;
+    Index shape;
+    int64_t bytes = 0;
+    void* ptr = nullptr;
+    bool owned = false;
+};
+
+struct LaunchInfo {
+    std::string node;    // graph node id (or "node+node" for a fused group)
+    std::string kernel;  // kernel family
+};
+
+class Executor {
+public:
+    Executor(const CompGraph& g, PointsToGraph ptg, ExecOptions opt = {});
+    ~Executor();
+    Executor(const Executor&) = delete;
+    Executor& operator=(const Executor&) = delete;
+
+    const CompGraph& graph() const { return g_; }
+    const PointsToGraph& ptg() const { return ptg_; }
+
+    void bind_root(const std::string& id, void* dev_ptr);
+    void* root_ptr(const std::string& id);
+    const std::vector<RootBuffer>& roots() const { return roots_; }
+
+    // Lower descriptors against the current root pointers and build the launch list.
+    // dry: plan the launches without touching the device (no allocation; null pointers).
+    void prepare(bool dry = false);
+    // Enqueue every launch on `stream` (asynchronous).
+    void run(void* stream);
+    // Capture the launch list into a CUDA graph once, then replay it.
+    void run_graph(void* stream);
+
+    void upload(const std::string& id, const void* host, int64_t bytes, void* stream);
+    // Materialise any tensor (virtual or physical) into host memory.
+    void download(const std::string& id, void* host, int64_t bytes, void* stream);
+
+    const std::vector<LaunchInfo>& launches() const { return infos_; }
+    int num_kernel_launches() const;
+
+private:
+    struct Impl;
+    const CompGraph& g_;
+    PointsToGraph ptg_;
+    ExecOptions opt_;
+    std::vector<RootBuffer> roots_;
+    std::map<std::string, int> root_index_;
+    std::vector<LaunchInfo> infos_;
+    std::unique_ptr<Impl> impl_;
+    bool prepared_ = false;
+};
+
+}  // namespace vtc

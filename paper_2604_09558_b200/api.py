@@ -1,0 +1,204 @@
+"""Python mirror of the reference's executor-facing API over the C ABI.
+
+Names and argument meaning follow the reference (vtelim):
+  parse_graph(text) -> CompGraph              proj/src/graph_ir.cpp:455-485
+  CompGraph.vtog()                             build_vtog, proj/src/vtog.cpp:31-78
+  Plan(graph, mode, selected)                  all_physical_ptg / validate_ptg
+  execute(graph, plan, inputs) -> outputs      proj/src/executor.cpp:500-506
+and errors are raised as the reference's error classes
+(proj/include/vtelim/errors.hpp:14-38).  Host arrays are numpy; bf16 tensors
+travel as uint16 bit patterns.  All compute runs in libvtc.so on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from typing import Dict, Iterable, Optional
+
+import numpy as np
+
+from . import _lib
+
+
+class VtcError(RuntimeError):
+    code = 1
+
+
+_ERROR_NAMES = {
+    2: "SchemaError", 3: "CycleError", 4: "ShapeError", 5: "UnknownOperatorError",
+    6: "OutOfBoundsError", 7: "MissingBaseMapError", 8: "ComposeLimitError",
+    9: "ConflictViolationError", 10: "IncompleteSelectionError", 11: "CycleDetectedError",
+    12: "WriteAliasingError", 13: "SpaceTooLargeError", 14: "MissingInputError",
+    15: "ShapeMismatchError", 16: "ExecutionError", 17: "EquivalenceFailureError",
+    18: "InvalidVtogError", 19: "BudgetExceededError", 20: "CudaError", 21: "NcclError",
+    22: "UnsupportedError",
+}
+ERRORS = {code: type(name, (VtcError,), {"code": code}) for code, name in _ERROR_NAMES.items()}
+globals().update({cls.__name__: cls for cls in ERRORS.values()})
+
+MATERIALIZE, SELECTED, MAX_ELIMINATION = 0, 1, 2
+FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE = 1, 2, 4
+
+NP_DTYPES = {"f64": np.float64, "f32": np.float32, "i64": np.int64, "bf16": np.uint16}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib.load().vtc_last_error().decode()
+        raise ERRORS.get(rc, VtcError)(msg)
+
+
+def _stream(s) -> C.c_void_p:
+    if s is None:
+        return C.c_void_p(0)
+    if isinstance(s, int):
+        return C.c_void_p(s)
+    return C.c_void_p(int(s.cuda_stream))  # torch.cuda.Stream
+
+
+class CompGraph:
+    def __init__(self, handle: C.c_void_p, text: str):
+        self._h = handle
+        self.text = text
+        self.doc = json.loads(text)
+        self._specs = None
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.load().vtc_graph_free(self._h)
+            self._h = None
+
+    def serialize(self) -> str:
+        out = C.c_char_p()
+        _check(_lib.load().vtc_graph_serialize(self._h, C.byref(out)))
+        return out.value.decode()
+
+    def tensors(self) -> Dict[str, dict]:
+        if self._specs is None:
+            doc = json.loads(self.serialize())
+            self._specs = {t["id"]: t for t in doc["tensors"]}
+        return self._specs
+
+    def graph_inputs(self):
+        return [k for k, t in self.tensors().items() if t["kind"] == "input"]
+
+    def graph_outputs(self):
+        return [k for k, t in self.tensors().items() if t["kind"] == "output"]
+
+    def vtog(self) -> dict:
+        out = C.c_char_p()
+        _check(_lib.load().vtc_graph_vtog(self._h, C.byref(out)))
+        return json.loads(out.value.decode())
+
+
+def parse_graph(text) -> CompGraph:
+    if isinstance(text, dict):
+        text = json.dumps(text)
+    h = C.c_void_p()
+    _check(_lib.load().vtc_graph_parse(text.encode(), C.byref(h)))
+    return CompGraph(h, text)
+
+
+class Plan:
+    """A points-to graph bound to the GPU executor (roots own device memory)."""
+
+    def __init__(self, graph: CompGraph, mode: int = MAX_ELIMINATION, selected: Optional[Iterable[int]] = None,
+                 flags: int = 0):
+        self.graph = graph
+        sel = list(selected or [])
+        arr = (C.c_int32 * max(1, len(sel)))(*sel)
+        h = C.c_void_p()
+        _check(_lib.load().vtc_plan_create(graph._h, mode, arr, len(sel), flags, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.load().vtc_plan_free(self._h)
+            self._h = None
+
+    def info(self, dry: bool = False) -> dict:
+        out = C.c_char_p()
+        _check(_lib.load().vtc_plan_info(self._h, 1 if dry else 0, C.byref(out)))
+        return json.loads(out.value.decode())
+
+    def bind_root(self, tensor: str, dev_ptr: int) -> None:
+        _check(_lib.load().vtc_plan_bind_root(self._h, tensor.encode(), C.c_void_p(dev_ptr)))
+
+    def root_ptr(self, tensor: str) -> int:
+        p = C.c_void_p()
+        _check(_lib.load().vtc_plan_root_ptr(self._h, tensor.encode(), C.byref(p)))
+        return p.value or 0
+
+    def upload(self, tensor: str, arr: np.ndarray, stream=None) -> None:
+        arr = np.ascontiguousarray(arr)
+        _check(_lib.load().vtc_plan_upload(self._h, tensor.encode(), arr.ctypes.data_as(C.c_void_p),
+                                           arr.nbytes, _stream(stream)))
+
+    def download(self, tensor: str, stream=None) -> np.ndarray:
+        spec = self.graph.tensors()[tensor]
+        out = np.empty(spec["shape"], dtype=NP_DTYPES[spec["dtype"]])
+        _check(_lib.load().vtc_plan_download(self._h, tensor.encode(), out.ctypes.data_as(C.c_void_p),
+                                             out.nbytes, _stream(stream)))
+        return out
+
+    def prepare(self) -> None:
+        _check(_lib.load().vtc_plan_prepare(self._h))
+
+    def execute(self, stream=None) -> None:
+        _check(_lib.load().vtc_execute(self._h, _stream(stream)))
+
+    def execute_graph(self, stream=None) -> None:
+        _check(_lib.load().vtc_execute_graph(self._h, _stream(stream)))
+
+    def num_launches(self) -> int:
+        return _lib.load().vtc_plan_num_launches(self._h)
+
+    def map_json(self, tensor: str) -> dict:
+        out = C.c_char_p()
+        _check(_lib.load().vtc_plan_map_json(self._h, tensor.encode(), C.byref(out)))
+        return json.loads(out.value.decode())
+
+    def map_eval(self, tensor: str, lowered: bool = False):
+        """(target names, target index per element, offsets) in row-major order."""
+        mj = self.map_json(tensor)
+        n = int(np.prod(mj["shape"])) if mj["shape"] else 1
+        t = np.empty(n, np.int32)
+        o = np.empty(n, np.int64)
+        _check(_lib.load().vtc_map_eval(self._h, tensor.encode(), 1 if lowered else 0,
+                                        t.ctypes.data_as(C.POINTER(C.c_int32)),
+                                        o.ctypes.data_as(C.POINTER(C.c_int64)), n))
+        return mj["targets"], t, o
+
+
+def execute(graph: CompGraph, plan: Plan, inputs: Dict[str, np.ndarray], roots: Iterable[str] = (),
+            stream=None) -> Dict[str, np.ndarray]:
+    """Reference `execute` semantics: upload inputs, run, materialise outputs (and requested roots)."""
+    for name in graph.graph_inputs():
+        if name not in inputs:
+            raise ERRORS[14](f"input tensor {name} not provided")
+        spec = graph.tensors()[name]
+        a = inputs[name]
+        if list(a.shape) != spec["shape"] or a.dtype != NP_DTYPES[spec["dtype"]]:
+            raise ERRORS[15](f"input tensor {name} shape or dtype mismatch")
+        plan.upload(name, a, stream)
+    plan.execute(stream)
+    out = {name: plan.download(name, stream) for name in graph.graph_outputs()}
+    for r in roots:
+        out["root:" + r] = plan.download(r, stream)
+    return out
+
+
+# ---- bf16 helpers (host) ----------------------------------------------------
+def f32_to_bf16(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even float32 -> bf16 bit patterns (uint16)."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    lsb = (b >> 16) & 1
+    r = ((b + 0x7FFF + lsb) >> 16).astype(np.uint16)
+    nan = np.isnan(x)
+    if nan.any():
+        r = np.where(nan, np.uint16(0x7FC0), r)
+    return r
+
+
+def bf16_to_f32(x: np.ndarray) -> np.ndarray:
+    return (np.ascontiguousarray(x, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)

@@ -1,0 +1,305 @@
+// extern "C" boundary (include/vtc.h).  Exceptions are caught here and
+// turned into the status codes of the reference error classes.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "json.hpp"
+#include "kernels.hpp"
+#include "lower.hpp"
+#include "vtc.h"
+#include "vtc/exec.hpp"
+
+struct vtc_graph {
+    vtc::CompGraph g;
+    std::unique_ptr<vtc::Vtog> vtog;
+};
+
+struct vtc_plan {
+    vtc_graph* graph;
+    std::unique_ptr<vtc::Executor> exec;
+    uint32_t flags = 0;
+    int mode = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::string g_out;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return VTC_OK;
+    } catch (const vtc::Error& e) {
+        g_err = e.what();
+        return e.code();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return VTC_ERR_GENERIC;
+    }
+}
+
+vtc::Vtog& vtog_of(vtc_graph* g) {
+    if (!g->vtog) g->vtog = std::make_unique<vtc::Vtog>(vtc::build_vtog(g->g));
+    return *g->vtog;
+}
+
+vtc::json::Value str(const std::string& s) { return vtc::json::Value::string(s); }
+vtc::json::Value strs(const std::vector<std::string>& v) {
+    auto a = vtc::json::Value::array();
+    for (const auto& s : v) a.push(str(s));
+    return a;
+}
+
+vtc::json::Value estimate_json(const vtc::TrafficEstimate& e) {
+    using vtc::json::Value;
+    Value j = Value::object();
+    j.set("total_bytes", Value::integer(e.total_bytes()));
+    j.set("data_movement_bytes", Value::integer(e.data_movement_bytes()));
+    j.set("data_movement_kernels", Value::integer(e.data_movement_kernels));
+    j.set("compute_kernels", Value::integer(e.compute_kernels));
+    Value ks = Value::array();
+    for (const auto& k : e.kernels) {
+        Value kj = Value::object();
+        kj.set("node", str(k.node));
+        kj.set("data_movement", Value::boolean(k.data_movement));
+        int64_t rb = 0, wb = 0;
+        for (const auto& r : k.reads) rb += r.bytes;
+        for (const auto& w : k.writes) wb += w.bytes;
+        kj.set("read_bytes", Value::integer(rb));
+        kj.set("write_bytes", Value::integer(wb));
+        ks.push(kj);
+    }
+    j.set("kernels", ks);
+    return j;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vtc_last_error(void) { return g_err.c_str(); }
+const char* vtc_version(void) { return "vtc-b200 0.1 (sm_100a)"; }
+
+int vtc_graph_parse(const char* json_text, vtc_graph** out) {
+    return guard([&] {
+        auto g = std::make_unique<vtc_graph>();
+        g->g = vtc::parse_graph(json_text);
+        *out = g.release();
+    });
+}
+
+void vtc_graph_free(vtc_graph* g) { delete g; }
+
+int vtc_graph_serialize(vtc_graph* g, const char** json_out) {
+    return guard([&] {
+        g_out = vtc::serialize_graph(g->g);
+        *json_out = g_out.c_str();
+    });
+}
+
+int vtc_graph_vtog(vtc_graph* g, const char** json_out) {
+    return guard([&] {
+        using vtc::json::Value;
+        vtc::Vtog& v = vtog_of(g);
+        Value edges = Value::array();
+        for (const auto& e : v.edges) {
+            Value ej = Value::object();
+            ej.set("id", Value::integer(e.id));
+            ej.set("src", str(e.src));
+            ej.set("dst", str(e.dst));
+            ej.set("candidate", Value::integer(e.candidate));
+            ej.set("eliminated_op", str(e.eliminated_op));
+            ej.set("direction", str(vtc::to_string(e.direction)));
+            ej.set("type", str(vtc::to_string(e.static_class)));
+            ej.set("partial", Value::boolean(e.partial));
+            ej.set("map", str(e.map.to_string()));
+            edges.push(ej);
+        }
+        Value conf = Value::array();
+        for (const auto& [src, pairs] : v.conflicts)
+            for (const auto& pr : pairs) {
+                Value c = Value::array();
+                c.push(Value::integer(pr.first));
+                c.push(Value::integer(pr.second));
+                conf.push(c);
+            }
+        Value j = Value::object();
+        j.set("edges", edges);
+        j.set("conflicts", conf);
+        g_out = vtc::json::dump(j);
+        *json_out = g_out.c_str();
+    });
+}
+
+int vtc_plan_create(vtc_graph* g, int mode, const int32_t* selected, int32_t n_selected, uint32_t flags,
+                    vtc_plan** out) {
+    return guard([&] {
+        vtc::PointsToGraph ptg;
+        if (mode == VTC_PLAN_MATERIALIZE) {
+            ptg = vtc::all_physical_ptg(g->g);
+        } else if (mode == VTC_PLAN_SELECTED) {
+            std::vector<int> sel(selected, selected + n_selected);
+            ptg = vtc::validate_ptg(vtog_of(g), sel);
+        } else if (mode == VTC_PLAN_MAX_ELIMINATION) {
+            ptg = vtc::validate_ptg(vtog_of(g), vtc::plan_max_elimination(vtog_of(g)));
+        } else {
+            throw vtc::SchemaError("unknown plan mode");
+        }
+        vtc::ExecOptions opt;
+        opt.exact_fp = !(flags & VTC_FLAG_FAST_FP);
+        opt.use_gemv = !(flags & VTC_FLAG_NO_GEMV);
+        opt.fuse = !(flags & VTC_FLAG_NO_FUSE);
+        auto p = std::make_unique<vtc_plan>();
+        p->graph = g;
+        p->flags = flags;
+        p->mode = mode;
+        p->exec = std::make_unique<vtc::Executor>(g->g, std::move(ptg), opt);
+        *out = p.release();
+    });
+}
+
+void vtc_plan_free(vtc_plan* p) { delete p; }
+
+int vtc_plan_info(vtc_plan* p, int dry, const char** json_out) {
+    return guard([&] {
+        using vtc::json::Value;
+        const auto& ptg = p->exec->ptg();
+        if (dry) p->exec->prepare(true);
+        Value j = Value::object();
+        j.set("mode", Value::integer(p->mode));
+        j.set("roots", strs(ptg.roots));
+        j.set("eliminated_ops", strs(ptg.eliminated_ops));
+        Value sel = Value::array();
+        for (int e : ptg.selected) sel.push(Value::integer(e));
+        j.set("selected", sel);
+        Value maps = Value::object();
+        for (const auto& [id, m] : ptg.resolved)
+            if (!m.is_identity_of(id)) maps.set(id, str(m.to_string()));
+        j.set("virtual_maps", maps);
+        Value ls = Value::array();
+        int dm = 0;
+        for (const auto& l : p->exec->launches()) {
+            Value lj = Value::object();
+            lj.set("node", str(l.node));
+            lj.set("kernel", str(l.kernel));
+            ls.push(lj);
+            if (l.kernel == "gather_copy") ++dm;
+        }
+        j.set("launches", ls);
+        j.set("kernel_launches", Value::integer(p->exec->num_kernel_launches()));
+        j.set("data_movement_launches", Value::integer(dm));
+        auto est = vtc::estimate(p->exec->graph(), ptg);
+        auto phys = vtc::estimate(p->exec->graph(), vtc::all_physical_ptg(p->exec->graph()));
+        j.set("estimate", estimate_json(est));
+        j.set("estimate_all_physical", estimate_json(phys));
+        j.set("bytes_eliminated", Value::integer(phys.total_bytes() - est.total_bytes()));
+        g_out = vtc::json::dump(j);
+        *json_out = g_out.c_str();
+    });
+}
+
+int vtc_plan_bind_root(vtc_plan* p, const char* tensor, void* dev_ptr) {
+    return guard([&] { p->exec->bind_root(tensor, dev_ptr); });
+}
+
+int vtc_plan_root_ptr(vtc_plan* p, const char* tensor, void** dev_ptr) {
+    return guard([&] { *dev_ptr = p->exec->root_ptr(tensor); });
+}
+
+int vtc_plan_upload(vtc_plan* p, const char* tensor, const void* host, int64_t bytes, void* stream) {
+    return guard([&] { p->exec->upload(tensor, host, bytes, stream); });
+}
+
+int vtc_plan_download(vtc_plan* p, const char* tensor, void* host, int64_t bytes, void* stream) {
+    return guard([&] { p->exec->download(tensor, host, bytes, stream); });
+}
+
+int vtc_plan_prepare(vtc_plan* p) {
+    return guard([&] { p->exec->prepare(false); });
+}
+
+int vtc_execute(vtc_plan* p, void* stream) {
+    return guard([&] { p->exec->run(stream); });
+}
+
+int vtc_execute_graph(vtc_plan* p, void* stream) {
+    return guard([&] { p->exec->run_graph(stream); });
+}
+
+int vtc_plan_num_launches(vtc_plan* p) { return p->exec->num_kernel_launches(); }
+
+int vtc_map_eval(vtc_plan* p, const char* tensor, int lowered, int32_t* targets, int64_t* offsets, int64_t cap) {
+    return guard([&] {
+        const vtc::VMap& m = p->exec->ptg().map_of(tensor);
+        auto tl = m.targets();
+        int64_t vol = m.domain_volume();
+        if (vol > cap) throw vtc::ExecutionError("eval buffer too small");
+        vtc_map d{};
+        if (lowered)
+            d = vtc::lower_map(m, [&](const std::string& t) {
+                return vtc::TargetInfo{int(std::lower_bound(tl.begin(), tl.end(), t) - tl.begin()), 0};
+            });
+        vtc::Index idx(m.shape().size(), 0);
+        for (int64_t f = 0; f < vol; ++f) {
+            if (lowered) {
+                int pi = -1;
+                offsets[f] = vtc::desc_eval(d, idx.data(), &pi);
+                if (pi < 0) throw vtc::OutOfBoundsError("descriptor does not cover index");
+                targets[f] = d.piece[pi].target;
+            } else {
+                auto [t, off] = m.eval(idx);
+                targets[f] = int32_t(std::lower_bound(tl.begin(), tl.end(), t) - tl.begin());
+                offsets[f] = off;
+            }
+            for (int i = int(idx.size()) - 1; i >= 0; --i) {
+                if (++idx[size_t(i)] < m.shape()[size_t(i)]) break;
+                idx[size_t(i)] = 0;
+            }
+        }
+    });
+}
+
+int vtc_plan_map_json(vtc_plan* p, const char* tensor, const char** json_out) {
+    return guard([&] {
+        using vtc::json::Value;
+        const vtc::VMap& m = p->exec->ptg().map_of(tensor);
+        Value j = Value::object();
+        j.set("shape", Value::ints(m.shape()));
+        j.set("targets", strs(m.targets()));
+        j.set("pieces", Value::integer(int64_t(m.pieces().size())));
+        j.set("text", str(m.to_string()));
+        g_out = vtc::json::dump(j);
+        *json_out = g_out.c_str();
+    });
+}
+
+int vtc_launch_gather_copy(const vtc_map* dst, const vtc_map* src, int32_t elem_bytes, void* stream) {
+    return guard([&] {
+        vtc::EwParams p;
+        std::memset(&p, 0, sizeof(p));
+        p.rank = dst->rank;
+        int64_t n = 1;
+        for (int i = 0; i < dst->rank; ++i) {
+            p.shape[i] = dst->shape[i];
+            n *= dst->shape[i];
+        }
+        p.vec = 1;
+        p.op = vtc::EwOp::Copy;
+        p.esize = elem_bytes;
+        p.dt = elem_bytes == 8 ? vtc::KDType::I64 : elem_bytes == 4 ? vtc::KDType::F32 : vtc::KDType::BF16;
+        p.nvec = n;
+        p.nin = 1;
+        p.out.m = *dst;
+        p.a.m = *src;
+        vtc::launch_eltwise(p, static_cast<cudaStream_t>(stream));
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw vtc::CudaError(cudaGetErrorString(e));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,706 @@
+// GPU executor: points-to graph -> lowered descriptors -> kernel launches.
+// Mirrors execute_detailed (proj/src/executor.cpp:448-498); see exec.hpp.
+#include "vtc/exec.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <functional>
+#include <set>
+
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+#include "lower.hpp"
+
+namespace vtc {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+KDType kdt(DType d) {
+    switch (d) {
+        case DType::F64: return KDType::F64;
+        case DType::F32: return KDType::F32;
+        case DType::I64: return KDType::I64;
+        case DType::BF16: return KDType::BF16;
+    }
+    return KDType::F32;
+}
+
+struct Launch {
+    std::string node, kernel;
+    virtual ~Launch() = default;
+    virtual void run(cudaStream_t s) = 0;
+};
+
+template <class P, void (*F)(const P&, cudaStream_t)>
+struct LaunchT : Launch {
+    P p;
+    void run(cudaStream_t s) override { F(p, s); }
+};
+
+// Host-side digest of a lowered map along the kernel's fast axis.
+void finish_operand(VOperand& op, int fast_axis, int64_t tile, int64_t esize) {
+    op.fast_axis = fast_axis;
+    const vtc_map& d = op.m;
+    bool ok = fast_axis >= 0 && fast_axis < d.rank && desc_pieces_aligned(d, fast_axis, tile);
+    for (int pi = 0; pi < d.npieces && ok; ++pi) {
+        int64_t s = desc_tile_stride(d.piece[pi], fast_axis, tile);
+        if (s == INT64_MIN) ok = false;
+        else op.fast_stride[pi] = s;
+    }
+    op.fast_ok = ok ? 1 : 0;
+    // 16-byte vectors along the fast axis
+    int64_t vec = 16 / esize;
+    bool vok = ok && tile % vec == 0 && d.shape[fast_axis] % vec == 0 && desc_pieces_aligned(d, fast_axis, vec);
+    for (int pi = 0; pi < d.npieces && vok; ++pi) {
+        const vtc_piece& p = d.piece[pi];
+        if (op.fast_stride[pi] != 1 || p.base % vec != 0 || p.ptr % 16 != 0) vok = false;
+        for (int t = 0; t < p.ndigits && vok; ++t) {
+            const vtc_digit& g = p.dig[t];
+            bool linear_fast = g.axis == fast_axis && g.div == 1;
+            if (g.group >= 0) continue;
+            if (linear_fast) {
+                if (g.mod && g.mod % vec != 0) vok = false;
+            } else if (g.coeff % vec != 0) {
+                vok = false;
+            }
+        }
+        for (int gi = 0; gi < p.ngroups && vok; ++gi)
+            if (p.grp[gi].coeff % vec != 0) vok = false;
+    }
+    op.vec_ok = vok ? 1 : 0;
+}
+
+// Heads sharing identical K/V addresses: the map ignores (h mod G).
+bool ignores_mod(const vtc_map& d, int axis, int G) {
+    for (int pi = 0; pi < d.npieces; ++pi) {
+        const vtc_piece& p = d.piece[pi];
+        if (p.lo[axis] % G != 0 || (p.hi[axis] % G != 0 && p.hi[axis] != d.shape[axis])) return false;
+        for (int t = 0; t < p.ndigits; ++t) {
+            const vtc_digit& g = p.dig[t];
+            if (g.axis != axis) continue;
+            if (g.group >= 0) return false;
+            if (g.div % uint32_t(G) != 0) return false;
+        }
+    }
+    return true;
+}
+
+}  // namespace
+
+struct Executor::Impl {
+    std::vector<std::unique_ptr<Launch>> launches;
+    std::vector<void*> scratch;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t captured_on = nullptr;
+
+    void free_scratch() {
+        for (void* p : scratch) cudaFree(p);
+        scratch.clear();
+    }
+    void free_graph() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
+        gexec = nullptr;
+        graph = nullptr;
+    }
+    bool dry = false;
+    void* alloc(size_t bytes, bool zero) {
+        if (dry) return nullptr;
+        void* p = nullptr;
+        ck(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "cudaMalloc(scratch)");
+        if (zero) ck(cudaMemset(p, 0, std::max<size_t>(bytes, 16)), "cudaMemset(scratch)");
+        scratch.push_back(p);
+        return p;
+    }
+};
+
+Executor::Executor(const CompGraph& g, PointsToGraph ptg, ExecOptions opt)
+    : g_(g), ptg_(std::move(ptg)), opt_(opt), impl_(std::make_unique<Impl>()) {
+    for (const auto& id : ptg_.roots) {
+        const TensorSpec& t = g_.tensor(id);
+        RootBuffer rb;
+        rb.id = id;
+        rb.dtype = t.dtype;
+        rb.shape = t.shape;
+        rb.bytes = t.bytes();
+        root_index_[id] = int(roots_.size());
+        roots_.push_back(rb);
+    }
+}
+
+Executor::~Executor() {
+    impl_->free_graph();
+    impl_->free_scratch();
+    for (auto& r : roots_)
+        if (r.owned && r.ptr) cudaFree(r.ptr);
+}
+
+void Executor::bind_root(const std::string& id, void* dev_ptr) {
+    auto it = root_index_.find(id);
+    if (it == root_index_.end()) throw ExecutionError("tensor " + id + " is not a physical root of this plan");
+    RootBuffer& r = roots_[size_t(it->second)];
+    if (r.owned && r.ptr) cudaFree(r.ptr);
+    r.ptr = dev_ptr;
+    r.owned = false;
+    prepared_ = false;
+}
+
+void* Executor::root_ptr(const std::string& id) {
+    auto it = root_index_.find(id);
+    if (it == root_index_.end()) throw ExecutionError("tensor " + id + " is not a physical root of this plan");
+    RootBuffer& r = roots_[size_t(it->second)];
+    if (!r.ptr) {
+        ck(cudaMalloc(&r.ptr, size_t(std::max<int64_t>(r.bytes, 16))), "cudaMalloc(root)");
+        ck(cudaMemset(r.ptr, 0, size_t(std::max<int64_t>(r.bytes, 16))), "cudaMemset(root)");
+        r.owned = true;
+        prepared_ = false;
+    }
+    return r.ptr;
+}
+
+int Executor::num_kernel_launches() const {
+    int n = 0;
+    for (const auto& i : infos_) n += (i.kernel == "attention_splitkv") ? 2 : 1;
+    return n;
+}
+
+void Executor::prepare(bool dry) {
+    if (!dry)
+        for (auto& r : roots_) root_ptr(r.id);  // allocate every unbound root
+    impl_->free_graph();
+    impl_->free_scratch();
+    impl_->dry = dry;
+    impl_->launches.clear();
+    infos_.clear();
+
+    auto target = [&](const std::string& t) -> TargetInfo {
+        auto it = root_index_.find(t);
+        if (it == root_index_.end()) throw ExecutionError("map targets non-root tensor " + t);
+        return TargetInfo{it->second, reinterpret_cast<uint64_t>(roots_[size_t(it->second)].ptr)};
+    };
+    auto operand = [&](const VMap& m, int fast_axis, int64_t tile, int64_t esize) {
+        VOperand op{};
+        op.m = lower_map(m, target);
+        finish_operand(op, fast_axis, tile, esize);
+        return op;
+    };
+    auto map_of = [&](const std::string& t) -> const VMap& { return ptg_.map_of(t); };
+    auto targets_of = [&](const VMap& m) {
+        auto v = m.targets();
+        return std::set<std::string>(v.begin(), v.end());
+    };
+    auto lookup = [&](const std::string& t) -> const VMap* {
+        if (std::find(ptg_.roots.begin(), ptg_.roots.end(), t) != ptg_.roots.end()) return nullptr;
+        return &ptg_.resolved.at(t);
+    };
+    std::set<std::string> elim(ptg_.eliminated_ops.begin(), ptg_.eliminated_ops.end());
+
+    auto push = [&](std::unique_ptr<Launch> l) {
+        infos_.push_back({l->node, l->kernel});
+        impl_->launches.push_back(std::move(l));
+    };
+
+    // ---- elementwise / copy launches over an output shape ----
+    // A map with more pieces than the descriptor holds is handled by one launch
+    // per piece of the widest map, each iterating over that piece's box.
+    std::function<void(const std::string&, EwOp, DType, const Index&, const VMap&, const VMap*, const VMap*,
+                       const Index&, const Index&)>
+        eltwise_box;
+    eltwise_box = [&](const std::string& node, EwOp op, DType dt, const Index& shape, const VMap& out,
+                      const VMap* a, const VMap* b, const Index& lo, const Index& hi) {
+        auto L = std::make_unique<LaunchT<EwParams, launch_eltwise>>();
+        L->node = node;
+        L->kernel = op == EwOp::Copy ? "gather_copy" : "eltwise";
+        EwParams& p = L->p;
+        std::memset(&p, 0, sizeof(p));
+        int64_t es = dtype_size(dt);
+        int rank = int(shape.size());
+        Index ext(static_cast<size_t>(rank), 0);
+        for (int i = 0; i < rank; ++i) ext[size_t(i)] = hi[size_t(i)] - lo[size_t(i)];
+        int64_t vec = 16 / es;
+        if (rank == 0 || ext.back() % vec != 0 || lo.back() % vec != 0) vec = 1;
+        p.rank = rank;
+        for (int i = 0; i < rank; ++i) {
+            p.shape[i] = int32_t(ext[size_t(i)]);
+            p.origin[i] = int32_t(lo[size_t(i)]);
+        }
+        p.vec = int32_t(vec);
+        p.op = op;
+        p.dt = kdt(dt);
+        p.esize = int32_t(es);
+        p.nvec = volume(ext) / vec;
+        auto restrict_box = [&](const VMap& m) {
+            std::vector<VPiece> ps;
+            for (const auto& q : m.pieces()) {
+                VPiece r = q;
+                bool empty = false;
+                for (int i = 0; i < rank; ++i) {
+                    r.lo[size_t(i)] = std::max(q.lo[size_t(i)], lo[size_t(i)]);
+                    r.hi[size_t(i)] = std::min(q.hi[size_t(i)], hi[size_t(i)]);
+                    empty |= r.lo[size_t(i)] >= r.hi[size_t(i)];
+                }
+                if (empty) continue;
+                r.off = restrict_to(q.off, r.lo, r.hi);
+                ps.push_back(std::move(r));
+            }
+            return VMap(m.shape(), std::move(ps));
+        };
+        const VMap* maps[3] = {&out, a, b};
+        for (int k = 0; k < 3; ++k) {
+            if (!maps[k]) continue;
+            VMap rm = restrict_box(*maps[k]);
+            VOperand op2{};
+            try {
+                op2.m = lower_map(rm, target);
+            } catch (const UnsupportedError&) {
+                // split the iteration box along the pieces of this map, or bisect it
+                if (rm.pieces().size() > 1) {
+                    for (const auto& q : rm.pieces()) eltwise_box(node, op, dt, shape, out, a, b, q.lo, q.hi);
+                    return;
+                }
+                int best = -1;
+                int64_t bext = 1;
+                for (int i = 0; i < rank; ++i)
+                    if (ext[size_t(i)] > bext) {
+                        bext = ext[size_t(i)];
+                        best = i;
+                    }
+                if (best < 0) throw;
+                Index h1 = hi, l2 = lo;
+                h1[size_t(best)] = lo[size_t(best)] + bext / 2;
+                l2[size_t(best)] = h1[size_t(best)];
+                eltwise_box(node, op, dt, shape, out, a, b, lo, h1);
+                eltwise_box(node, op, dt, shape, out, a, b, l2, hi);
+                return;
+            }
+            finish_operand(op2, rank - 1, vec, es);
+            (k == 0 ? p.out : k == 1 ? p.a : p.b) = op2;
+        }
+        p.nin = b ? 2 : 1;
+        push(std::move(L));
+    };
+    auto eltwise = [&](const std::string& node, EwOp op, DType dt, const Index& shape, const VMap& out,
+                       const VMap* a, const VMap* b) {
+        eltwise_box(node, op, dt, shape, out, a, b, Index(shape.size(), 0), shape);
+    };
+
+    // A gather-copy that must not read what it writes: stage through scratch.
+    auto copy_checked = [&](const std::string& node, DType dt, const Index& shape, const VMap& dst, const VMap& src) {
+        auto td = targets_of(dst), ts = targets_of(src);
+        bool hazard = false;
+        for (const auto& t : td) hazard |= ts.count(t) > 0;
+        if (!hazard) {
+            eltwise(node, EwOp::Copy, dt, shape, dst, &src, nullptr);
+            return;
+        }
+        // stage: src -> temp (identity) -> dst
+        std::string tmp_id = "__stage_" + node + "_" + std::to_string(roots_.size());
+        RootBuffer rb;
+        rb.id = tmp_id;
+        rb.dtype = dt;
+        rb.shape = shape;
+        rb.bytes = volume(shape) * dtype_size(dt);
+        rb.ptr = impl_->alloc(size_t(rb.bytes), false);
+        root_index_[tmp_id] = int(roots_.size());
+        roots_.push_back(rb);
+        VMap tmp = VMap::identity(tmp_id, shape);
+        eltwise(node, EwOp::Copy, dt, shape, tmp, &src, nullptr);
+        eltwise(node, EwOp::Copy, dt, shape, dst, &tmp, nullptr);
+    };
+
+    // ---- fusion pre-pass (graph structure only, so virtual and materialised
+    //      plans fuse identically) ----
+    struct GemvFusion {
+        const OpNode* norm = nullptr;
+        const OpNode* silu = nullptr;
+        const OpNode* mul = nullptr;
+        const OpNode* add = nullptr;
+    };
+    std::map<std::string, GemvFusion> fusion;
+    std::set<std::string> absorbed;
+    std::map<std::string, int> topo_pos;
+    for (size_t i = 0; i < g_.topo_order().size(); ++i) topo_pos[g_.nodes()[size_t(g_.topo_order()[i])].id] = int(i);
+    auto only_consumer = [&](const std::string& t, const std::string& node) {
+        auto cs = g_.consumers(t);
+        return g_.tensor(t).kind == TensorKind::Intermediate && cs.size() == 1 && cs[0]->id == node;
+    };
+    auto gemv_eligible = [&](const OpNode& n) {
+        if (n.kind != OpKind::MatMul || !opt_.use_gemv) return false;
+        const TensorSpec& A = g_.tensor(n.inputs[0]);
+        const TensorSpec& B = g_.tensor(n.inputs[1]);
+        if (A.dtype != DType::BF16 || A.shape.size() != 2 || A.shape[0] > 16) return false;
+        if (B.shape[1] % 8 != 0) return false;
+        const VMap& bm = map_of(n.inputs[1]);
+        if (bm.pieces().size() != 1) return false;
+        const VPiece& p = bm.pieces()[0];
+        auto sk = VMap::tile_stride(p, 0, B.shape[0]);
+        auto sn = VMap::tile_stride(p, 1, B.shape[1]);
+        if (!sk || !sn || *sn != 1) return false;
+        for (const auto& tm : p.off.t)
+            if (tm.a->kind != AtomKind::Axis) return false;
+        if (p.off.c0 % 8 != 0 || *sk % 8 != 0) return false;
+        return true;
+    };
+    if (opt_.fuse) {
+        for (const auto& n : g_.nodes()) {
+            if (!gemv_eligible(n)) continue;
+            GemvFusion f;
+            const OpNode* pa = g_.producer(n.inputs[0]);
+            if (pa && pa->kind == OpKind::RMSNorm && g_.tensor(n.inputs[0]).kind == TensorKind::Intermediate &&
+                g_.tensor(pa->inputs[0]).shape.size() == 2) {
+                bool all = true;
+                for (const OpNode* c : g_.consumers(n.inputs[0])) all = all && gemv_eligible(*c) && c->inputs[0] == n.inputs[0];
+                if (all) f.norm = pa;
+            } else if (pa && pa->kind == OpKind::Mul && only_consumer(n.inputs[0], n.id)) {
+                for (int side = 0; side < 2 && !f.silu; ++side) {
+                    const OpNode* ps = g_.producer(pa->inputs[size_t(side)]);
+                    if (ps && ps->kind == OpKind::SiLU && only_consumer(pa->inputs[size_t(side)], pa->id) &&
+                        pa->inputs[0] != pa->inputs[1]) {
+                        f.silu = ps;
+                        f.mul = pa;
+                    }
+                }
+            }
+            auto cs = g_.consumers(n.outputs[0]);
+            if (only_consumer(n.outputs[0], cs.empty() ? "" : cs[0]->id) && cs[0]->kind == OpKind::Add &&
+                cs[0]->inputs[0] != cs[0]->inputs[1]) {
+                const OpNode* ad = cs[0];
+                const std::string& other = ad->inputs[0] == n.outputs[0] ? ad->inputs[1] : ad->inputs[0];
+                const OpNode* po = g_.producer(other);
+                if (!po || topo_pos[po->id] < topo_pos[n.id]) f.add = ad;
+            }
+            if (f.norm || f.silu || f.add) fusion[n.id] = f;
+        }
+        // a norm is absorbed only if every consumer MatMul fused it
+        for (auto& [id, f] : fusion) {
+            if (f.norm) absorbed.insert(f.norm->id);
+            if (f.silu) {
+                absorbed.insert(f.silu->id);
+                absorbed.insert(f.mul->id);
+            }
+            if (f.add) absorbed.insert(f.add->id);
+        }
+    }
+
+    for (int ni : g_.topo_order()) {
+        const OpNode& n = g_.nodes()[size_t(ni)];
+        if (absorbed.count(n.id)) continue;
+        const TensorSpec& o0 = g_.tensor(n.outputs[0]);
+        DType dt = g_.tensor(n.inputs[0]).dtype;
+        int64_t es = dtype_size(dt);
+
+        if (is_data_movement(n)) {
+            if (elim.count(n.id)) continue;  // eliminated: no kernel
+            for (const auto& o : n.outputs) {
+                VMap src = gather_map(n, o, g_).compose(lookup);
+                copy_checked(n.id, dt, g_.tensor(o).shape, map_of(o), src);
+            }
+            continue;
+        }
+
+        // hazard: a compute node writing a root it also reads (other than identical elementwise maps)
+        for (const auto& o : n.outputs)
+            for (const auto& in : n.inputs) {
+                auto to = targets_of(map_of(o)), ti = targets_of(map_of(in));
+                bool clash = false;
+                for (const auto& t : to) clash |= ti.count(t) > 0;
+                bool same_elementwise = (n.kind == OpKind::Add || n.kind == OpKind::Mul || n.kind == OpKind::SiLU ||
+                                         n.kind == OpKind::GELU) && map_of(o).equivalent(map_of(in));
+                if (clash && !same_elementwise)
+                    throw UnsupportedError("node " + n.id + " writes a root it reads (" + o + " / " + in + ")");
+            }
+
+        switch (n.kind) {
+            case OpKind::Add:
+            case OpKind::Mul:
+                eltwise(n.id, n.kind == OpKind::Add ? EwOp::Add : EwOp::Mul, dt, o0.shape, map_of(n.outputs[0]),
+                        &map_of(n.inputs[0]), &map_of(n.inputs[1]));
+                break;
+            case OpKind::SiLU:
+            case OpKind::GELU:
+                eltwise(n.id, n.kind == OpKind::SiLU ? EwOp::SiLU : EwOp::GELU, dt, o0.shape, map_of(n.outputs[0]),
+                        &map_of(n.inputs[0]), nullptr);
+                break;
+            case OpKind::AllReduce:
+                // single-rank execution: the sum over one rank is the identity
+                copy_checked(n.id, dt, o0.shape, map_of(n.outputs[0]), map_of(n.inputs[0]));
+                break;
+            case OpKind::RMSNorm:
+            case OpKind::LayerNorm:
+            case OpKind::Softmax: {
+                if (dt == DType::I64) throw UnsupportedError(std::string(to_string(n.kind)) + " on i64");
+                auto L = std::make_unique<LaunchT<RowParams, launch_rowop>>();
+                L->node = n.id;
+                L->kernel = "rowop";
+                RowParams& p = L->p;
+                std::memset(&p, 0, sizeof(p));
+                const Index& sh = o0.shape;
+                int rank = int(sh.size());
+                p.rank = rank;
+                for (int i = 0; i < rank; ++i) p.shape[i] = int32_t(sh[size_t(i)]);
+                p.D = sh.back();
+                p.rows = volume(sh) / p.D;
+                p.dt = kdt(dt);
+                p.op = n.kind == OpKind::RMSNorm ? RowOp::RMSNorm : n.kind == OpKind::LayerNorm ? RowOp::LayerNorm : RowOp::Softmax;
+                if (const auto* na = std::get_if<NormAttrs>(&n.attrs)) p.eps = float(na->eps);
+                p.x = operand(map_of(n.inputs[0]), rank - 1, p.D, es);
+                p.out = operand(map_of(n.outputs[0]), rank - 1, p.D, es);
+                if (n.kind != OpKind::Softmax) p.w = operand(map_of(n.inputs[1]), 0, p.D, es);
+                if (n.kind == OpKind::LayerNorm) p.bias = operand(map_of(n.inputs[2]), 0, p.D, es);
+                push(std::move(L));
+                break;
+            }
+            case OpKind::MatMul: {
+                const TensorSpec& A = g_.tensor(n.inputs[0]);
+                const TensorSpec& B = g_.tensor(n.inputs[1]);
+                int rank = int(A.shape.size());
+                int64_t M = A.shape[size_t(rank - 2)], K = A.shape[size_t(rank - 1)], N = B.shape[size_t(rank - 1)];
+                if (gemv_eligible(n)) {
+                    auto L = std::make_unique<LaunchT<GemvParams, launch_gemv>>();
+                    L->node = n.id;
+                    L->kernel = "gemv_bf16";
+                    GemvParams& p = L->p;
+                    std::memset(&p, 0, sizeof(p));
+                    p.M = M;
+                    p.N = N;
+                    p.K = K;
+                    GemvFusion f;
+                    auto fit = fusion.find(n.id);
+                    if (fit != fusion.end()) f = fit->second;
+                    if (f.norm) {
+                        p.prologue = GemvPrologue::RMSNorm;
+                        p.a = operand(map_of(f.norm->inputs[0]), 1, 1, es);
+                        p.normw = operand(map_of(f.norm->inputs[1]), 0, 1, es);
+                        p.eps = float(std::get<NormAttrs>(f.norm->attrs).eps);
+                        L->node = f.norm->id + "+" + n.id;
+                    } else if (f.silu) {
+                        p.prologue = GemvPrologue::SiLUMul;
+                        const std::string& sg = f.silu->outputs[0];
+                        const std::string& other = f.mul->inputs[0] == sg ? f.mul->inputs[1] : f.mul->inputs[0];
+                        p.a = operand(map_of(f.silu->inputs[0]), 1, 1, es);
+                        p.a2 = operand(map_of(other), 1, 1, es);
+                        L->node = f.silu->id + "+" + f.mul->id + "+" + n.id;
+                    } else {
+                        p.a = operand(map_of(n.inputs[0]), 1, 1, es);
+                    }
+                    if (f.add) {
+                        const std::string& other =
+                            f.add->inputs[0] == n.outputs[0] ? f.add->inputs[1] : f.add->inputs[0];
+                        p.has_res = 1;
+                        p.res = operand(map_of(other), 1, 1, es);
+                        p.c = operand(map_of(f.add->outputs[0]), 1, 1, es);
+                        L->node += "+" + f.add->id;
+                    } else {
+                        p.c = operand(map_of(n.outputs[0]), 1, 1, es);
+                    }
+                    const VMap& bm = map_of(n.inputs[1]);
+                    const VPiece& bp = bm.pieces()[0];
+                    TargetInfo bt = target(bp.target);
+                    p.b_base = reinterpret_cast<const char*>(bt.ptr) + bp.off.c0 * es;
+                    p.b_sk = *VMap::tile_stride(bp, 0, K);
+                    // grid: 256-column strips x K splits, ~3 CTAs per SM
+                    int64_t ntiles = (N + 255) / 256;
+                    int64_t want = (148 * 3 + ntiles - 1) / ntiles;
+                    int64_t maxsplit = std::max<int64_t>(1, K / 64);
+                    int64_t ks = std::min(want, maxsplit);
+                    int64_t kchunk = ((K + ks - 1) / ks + 63) / 64 * 64;
+                    int64_t smem_cap = 48 * 1024 / (4 * std::max<int64_t>(M, 1));
+                    if (kchunk > smem_cap) kchunk = smem_cap / 64 * 64;
+                    ks = (K + kchunk - 1) / kchunk;
+                    p.ksplit = int32_t(ks);
+                    p.kchunk = int32_t(kchunk);
+                    if (ks > 1) {
+                        p.work = static_cast<float*>(impl_->alloc(size_t(ks * M * N) * sizeof(float), false));
+                        p.counters = static_cast<unsigned*>(impl_->alloc(size_t(ntiles) * sizeof(unsigned), true));
+                    }
+                    push(std::move(L));
+                    break;
+                }
+                auto L = std::make_unique<LaunchT<MatmulParams, launch_matmul>>();
+                L->node = n.id;
+                L->kernel = "matmul_tiled";
+                MatmulParams& p = L->p;
+                std::memset(&p, 0, sizeof(p));
+                p.rank = rank;
+                for (int i = 0; i < rank; ++i) p.shape_c[i] = int32_t(o0.shape[size_t(i)]);
+                p.M = M;
+                p.N = N;
+                p.K = K;
+                p.batch = volume(o0.shape) / (M * N);
+                p.dt = kdt(dt);
+                p.exact = opt_.exact_fp ? 1 : 0;
+                p.a = operand(map_of(n.inputs[0]), rank - 1, 8, es);
+                p.b = operand(map_of(n.inputs[1]), rank - 1, 128, es);
+                p.c = operand(map_of(n.outputs[0]), rank - 1, 8, es);
+                // strides along M for A (tile 128) and along K for B (tile 8)
+                {
+                    const vtc_map& d = p.a.m;
+                    bool ok = desc_pieces_aligned(d, rank - 2, 128);
+                    for (int pi = 0; pi < d.npieces && ok; ++pi) {
+                        int64_t s = desc_tile_stride(d.piece[pi], rank - 2, 128);
+                        if (s == INT64_MIN) ok = false;
+                        else p.a_mstride[pi] = s;
+                    }
+                    p.a_m_ok = ok;
+                    const vtc_map& e = p.b.m;
+                    ok = desc_pieces_aligned(e, rank - 2, 8);
+                    for (int pi = 0; pi < e.npieces && ok; ++pi) {
+                        int64_t s = desc_tile_stride(e.piece[pi], rank - 2, 8);
+                        if (s == INT64_MIN) ok = false;
+                        else p.b_kstride[pi] = s;
+                    }
+                    p.b_k_ok = ok;
+                }
+                push(std::move(L));
+                break;
+            }
+            case OpKind::Attention: {
+                if (dt != DType::BF16 && dt != DType::F32) throw UnsupportedError("Attention supports bf16/f32");
+                const auto& at = std::get<AttentionAttrs>(n.attrs);
+                const Index& qs = g_.tensor(n.inputs[0]).shape;
+                const Index& ks = g_.tensor(n.inputs[1]).shape;
+                const Index& vs = g_.tensor(n.inputs[2]).shape;
+                int rank = int(qs.size());
+                if (rank < 3 || rank > VTC_MAX_RANK) throw UnsupportedError("Attention needs rank >= 3");
+                auto L = std::make_unique<LaunchT<AttnParams, launch_attention>>();
+                L->node = n.id;
+                AttnParams& p = L->p;
+                std::memset(&p, 0, sizeof(p));
+                p.rank = rank;
+                p.H = int32_t(qs[size_t(rank - 3)]);
+                p.Sq = int32_t(qs[size_t(rank - 2)]);
+                p.D = int32_t(qs[size_t(rank - 1)]);
+                p.Sk = int32_t(ks[size_t(rank - 2)]);
+                p.Dv = int32_t(vs[size_t(rank - 1)]);
+                if (p.D % 8 || p.Dv % 8 || p.D > 256 || p.Dv > 256) throw UnsupportedError("Attention head dims must be multiples of 8 and <= 256");
+                p.Bt = int32_t(volume(Index(qs.begin(), qs.end() - 3)));
+                p.scale = float(at.scale);
+                p.causal = at.causal ? 1 : 0;
+                p.dt = kdt(dt);
+                p.q = operand(map_of(n.inputs[0]), rank - 1, p.D, es);
+                p.k = operand(map_of(n.inputs[1]), rank - 1, p.D, es);
+                p.v = operand(map_of(n.inputs[2]), rank - 1, p.Dv, es);
+                p.o = operand(map_of(n.outputs[0]), rank - 1, p.Dv, es);
+                if (n.inputs.size() == 4) {
+                    p.has_bias = 1;
+                    p.bias = operand(map_of(n.inputs[3]), rank - 1, 1, es);
+                }
+                int G = 1;
+                for (int cand : {8, 4, 2})
+                    if (p.H % cand == 0 && ignores_mod(p.k.m, rank - 3, cand) && ignores_mod(p.v.m, rank - 3, cand)) {
+                        G = cand;
+                        break;
+                    }
+                p.group = G;
+                int64_t qblocks = int64_t(p.Bt) * (p.H / G) * p.Sq;
+                int splits = opt_.attn_splits;
+                if (splits <= 0) {
+                    splits = int((148 * 2 + qblocks - 1) / qblocks);
+                    splits = std::max(1, std::min(splits, (p.Sk + 31) / 32));
+                }
+                int chunk = (p.Sk + splits - 1) / splits;
+                chunk = (chunk + 31) / 32 * 32;
+                splits = (p.Sk + chunk - 1) / chunk;
+                p.splits = splits;
+                p.chunk = chunk;
+                L->kernel = splits > 1 ? "attention_splitkv" : "attention";
+                if (splits > 1) {
+                    int64_t rows = int64_t(p.Bt) * p.H * p.Sq;
+                    p.part_o = static_cast<float*>(impl_->alloc(size_t(rows * splits * p.Dv) * sizeof(float), false));
+                    p.part_ml = static_cast<float*>(impl_->alloc(size_t(rows * splits * 2) * sizeof(float), false));
+                }
+                push(std::move(L));
+                break;
+            }
+            default:
+                throw UnsupportedError(std::string("no kernel for operator ") + to_string(n.kind));
+        }
+    }
+    prepared_ = !dry;
+}
+
+void Executor::run(void* stream) {
+    if (!prepared_) prepare();
+    auto s = static_cast<cudaStream_t>(stream);
+    for (auto& l : impl_->launches) l->run(s);
+    ck(cudaGetLastError(), "kernel launch");
+}
+
+void Executor::run_graph(void* stream) {
+    if (!prepared_) prepare();
+    auto s = static_cast<cudaStream_t>(stream);
+    if (!impl_->gexec) {
+        cudaStream_t cap;
+        ck(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        for (auto& l : impl_->launches) l->run(cap);
+        cudaError_t e = cudaStreamEndCapture(cap, &impl_->graph);
+        cudaStreamDestroy(cap);
+        ck(e, "cudaStreamEndCapture");
+        ck(cudaGraphInstantiate(&impl_->gexec, impl_->graph, 0), "cudaGraphInstantiate");
+    }
+    ck(cudaGraphLaunch(impl_->gexec, s), "cudaGraphLaunch");
+}
+
+void Executor::upload(const std::string& id, const void* host, int64_t bytes, void* stream) {
+    auto it = root_index_.find(id);
+    if (it == root_index_.end()) throw ExecutionError("upload target " + id + " is not a physical root");
+    RootBuffer& r = roots_[size_t(it->second)];
+    if (bytes != r.bytes) throw ShapeMismatchError("upload of " + id + ": byte count mismatch");
+    void* d = root_ptr(id);
+    ck(cudaMemcpyAsync(d, host, size_t(bytes), cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)), "H2D");
+}
+
+void Executor::download(const std::string& id, void* host, int64_t bytes, void* stream) {
+    const TensorSpec& t = g_.tensor(id);
+    if (bytes != t.bytes()) throw ShapeMismatchError("download of " + id + ": byte count mismatch");
+    auto s = static_cast<cudaStream_t>(stream);
+    const VMap& m = ptg_.map_of(id);
+    auto it = root_index_.find(id);
+    if (it != root_index_.end() && m.is_identity_of(id)) {
+        ck(cudaMemcpyAsync(host, root_ptr(id), size_t(bytes), cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "sync");
+        return;
+    }
+    if (!prepared_) prepare();
+    // materialise through the map into a temporary buffer
+    void* tmp = nullptr;
+    ck(cudaMalloc(&tmp, size_t(std::max<int64_t>(bytes, 16))), "cudaMalloc(download)");
+    std::string tmp_id = "__download__";
+    auto target = [&](const std::string& tt) -> TargetInfo {
+        if (tt == tmp_id) return TargetInfo{-1, reinterpret_cast<uint64_t>(tmp)};
+        auto jt = root_index_.find(tt);
+        if (jt == root_index_.end()) throw ExecutionError("map targets non-root tensor " + tt);
+        return TargetInfo{jt->second, reinterpret_cast<uint64_t>(roots_[size_t(jt->second)].ptr)};
+    };
+    EwParams p;
+    std::memset(&p, 0, sizeof(p));
+    int rank = int(t.shape.size());
+    int64_t es = dtype_size(t.dtype);
+    p.rank = rank;
+    for (int i = 0; i < rank; ++i) p.shape[i] = int32_t(t.shape[size_t(i)]);
+    p.vec = 1;
+    p.op = EwOp::Copy;
+    p.dt = kdt(t.dtype);
+    p.esize = int32_t(es);
+    p.nvec = t.elems();
+    p.nin = 1;
+    p.out.m = lower_map(VMap::identity(tmp_id, t.shape), target);
+    finish_operand(p.out, rank - 1, 1, es);
+    p.a.m = lower_map(m, target);
+    finish_operand(p.a, rank - 1, 1, es);
+    launch_eltwise(p, s);
+    cudaError_t e = cudaMemcpyAsync(host, tmp, size_t(bytes), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(tmp);
+    ck(e, "download");
+}
+
+}  // namespace vtc

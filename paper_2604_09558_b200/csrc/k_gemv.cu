@@ -1,0 +1,184 @@
+// Weight-streaming GEMV / skinny GEMM for bf16 decode (M <= 16 rows).
+//
+// Replaces matmul_kernel (proj/src/executor.cpp:230-249) for the decode-step
+// projections, where the step is bound by streaming the weight matrix B once
+// from HBM.  Each CTA owns a 256-column strip of B and a K range; its 8 warps
+// walk consecutive rows with 16-byte non-allocating loads, `U` rows in flight
+// per warp.  A is staged into shared memory through its VirtualTensor map
+// (with an optional fused SiLU*Mul or RMSNorm prologue that reproduces the
+// unfused ops' bf16 roundings), C and the optional residual go through theirs.
+// Split-K partials are summed in split order by the last CTA to arrive, so the
+// result is deterministic and independent of the operand maps.
+#include "device.cuh"
+#include "rowreduce.cuh"
+
+namespace vtc {
+namespace {
+
+using dev::bf16;
+constexpr int NT = 256, COLS = 256, WARPS = 8;
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ float load_bf16_at(const VOperand& op, int32_t (&idx)[VTC_MAX_RANK]) {
+    return __bfloat162float(*dev::elem_ptr<bf16>(op.m, idx));
+}
+
+template <int MT, int U>
+__global__ void __launch_bounds__(NT) gemv_kernel(const __grid_constant__ GemvParams p) {
+    extern __shared__ float sA[];  // [M][kchunk]
+    __shared__ float red[WARPS][COLS];
+    __shared__ float s_rs[16];
+    __shared__ unsigned s_last;
+
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    const int64_t n0 = int64_t(blockIdx.x) * COLS;
+    const int split = blockIdx.y;
+    const int64_t kb = int64_t(split) * p.kchunk;
+    const int64_t ke = min(p.K, kb + p.kchunk);
+    const int klen = int(ke - kb);
+    const int M = int(p.M);
+
+    // ---- prologue: A rows -> shared memory (fp32), with fused transforms ----
+    if (p.prologue == GemvPrologue::RMSNorm) {
+        for (int m = 0; m < M; ++m) {
+            float ss = block_sumsq_row_bf16(p.a, m, p.K);
+            if (tid == 0) s_rs[m] = rsqrtf(ss / float(p.K) + p.eps);
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < M * klen; e += NT) {
+        int m = e / klen;
+        int64_t k = kb + e % klen;
+        int32_t idx[VTC_MAX_RANK] = {};
+        idx[0] = m;
+        idx[1] = int32_t(k);
+        float v = load_bf16_at(p.a, idx);
+        if (p.prologue == GemvPrologue::SiLUMul) {
+            float u = load_bf16_at(p.a2, idx);
+            float sg = __bfloat162float(__float2bfloat16_rn(v / (1.0f + expf(-v))));
+            v = __bfloat162float(__float2bfloat16_rn(sg * u));
+        } else if (p.prologue == GemvPrologue::RMSNorm) {
+            int32_t widx[VTC_MAX_RANK] = {};
+            widx[0] = int32_t(k);
+            float w = load_bf16_at(p.normw, widx);
+            v = __bfloat162float(__float2bfloat16_rn(v * s_rs[m] * w));
+        }
+        sA[e] = v;
+    }
+    __syncthreads();
+
+    // ---- stream B ----
+    float acc[MT][8];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[m][j] = 0.f;
+    const int64_t col = n0 + lane * 8;
+    const bool col_ok = col < p.N;
+    const bf16* bcol = reinterpret_cast<const bf16*>(p.b_base) + col;
+    for (int base = 0; base < klen; base += WARPS * U) {
+        uint4 w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            int k = base + u * WARPS + warp;
+            if (k < klen && col_ok) w[u] = ld_stream(bcol + (kb + k) * p.b_sk);
+            else w[u] = make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            int k = base + u * WARPS + warp;
+            if (k < klen) {
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[u]);
+                float b[8];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float2 f = __bfloat1622float2(h[j]);
+                    b[2 * j] = f.x;
+                    b[2 * j + 1] = f.y;
+                }
+#pragma unroll
+                for (int m = 0; m < MT; ++m) {
+                    if (m < M) {
+                        float a = sA[m * klen + k];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) acc[m][j] = fmaf(a, b[j], acc[m][j]);
+                    }
+                }
+            }
+        }
+    }
+
+    // ---- reduce the 8 warps, then the K splits ----
+    float outv[MT];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+        outv[m] = 0.f;
+        if (m < M) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) red[warp][lane * 8 + j] = acc[m][j];
+            __syncthreads();
+            float v = 0.f;
+#pragma unroll
+            for (int w2 = 0; w2 < WARPS; ++w2) v += red[w2][tid];
+            outv[m] = v;
+            __syncthreads();
+        }
+    }
+    const int64_t n = n0 + tid;
+    if (p.ksplit > 1) {
+        if (n < p.N)
+            for (int m = 0; m < M; ++m) p.work[(int64_t(split) * M + m) * p.N + n] = outv[m];
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = (atomicAdd(&p.counters[blockIdx.x], 1u) == unsigned(p.ksplit - 1));
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        if (n < p.N)
+            for (int m = 0; m < M; ++m) {
+                float v = 0.f;
+                for (int s2 = 0; s2 < p.ksplit; ++s2) v += __ldcg(&p.work[(int64_t(s2) * M + m) * p.N + n]);
+                outv[m] = v;
+            }
+        if (tid == 0) p.counters[blockIdx.x] = 0u;
+    }
+    if (n >= p.N) return;
+    // ---- epilogue: C = bf16(acc) [+ residual, rounded like an unfused Add] ----
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+        if (m >= M) continue;
+        int32_t idx[VTC_MAX_RANK] = {};
+        idx[0] = m;
+        idx[1] = int32_t(n);
+        bf16 c = __float2bfloat16_rn(outv[m]);
+        if (p.has_res) c = __float2bfloat16_rn(__bfloat162float(c) + load_bf16_at(p.res, idx));
+        *dev::elem_ptr<bf16>(p.c.m, idx) = c;
+    }
+}
+
+template <int MT, int U>
+void launch_mt(const GemvParams& p, cudaStream_t s) {
+    dim3 grid(unsigned((p.N + COLS - 1) / COLS), unsigned(p.ksplit));
+    size_t smem = size_t(p.M) * size_t(p.kchunk) * sizeof(float);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(gemv_kernel<MT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    gemv_kernel<MT, U><<<grid, NT, smem, s>>>(p);
+}
+
+}  // namespace
+
+void launch_gemv(const GemvParams& p, cudaStream_t s) {
+    if (p.M <= 1) launch_mt<1, 8>(p, s);
+    else if (p.M <= 2) launch_mt<2, 8>(p, s);
+    else if (p.M <= 4) launch_mt<4, 4>(p, s);
+    else if (p.M <= 8) launch_mt<8, 4>(p, s);
+    else launch_mt<16, 2>(p, s);
+}
+
+}  // namespace vtc

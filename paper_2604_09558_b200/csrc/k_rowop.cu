@@ -1,0 +1,103 @@
+// Row-wise RMSNorm / LayerNorm / Softmax over the last axis, one 256-thread
+// CTA per row, reading and writing through VirtualTensor maps.
+// These ops are absent from the reference (SURVEY.md §8 a'); their semantics
+// are fixed here and restated in oracle/vtc_oracle.py:
+//   RMSNorm   y = T((x * rsqrt(mean(x^2) + eps)) * w)
+//   LayerNorm y = T(((x - mu) * rsqrt(var + eps)) * g + b)
+//   Softmax   y = T(exp(x - max) / sum(exp(x - max)))
+// with fp32 math for f32/bf16 and fp64 math for f64.
+#include <type_traits>
+
+#include "device.cuh"
+#include "rowreduce.cuh"
+
+namespace vtc {
+namespace {
+
+using dev::bf16;
+
+template <typename T>
+struct RowIO {
+    const VOperand* op;
+    T* base;
+    int64_t stride;
+    bool fast;
+    int32_t idx[VTC_MAX_RANK];
+    int last;
+
+    __device__ void init(const VOperand& o, const int32_t (&rowidx)[VTC_MAX_RANK], int last_axis) {
+        op = &o;
+        last = last_axis;
+#pragma unroll
+        for (int a = 0; a < VTC_MAX_RANK; ++a) idx[a] = rowidx[a];
+        fast = o.fast_ok != 0;
+        if (fast) {
+            dev::set_axis(idx, last, 0);
+            dev::Loc l = dev::locate(o.m, idx);
+            base = dev::addr<T>(o.m, l);
+            stride = o.fast_stride[l.piece];
+        }
+    }
+    __device__ T* at(int64_t k) {
+        if (fast) return base + k * stride;
+        int32_t j[VTC_MAX_RANK];
+#pragma unroll
+        for (int a = 0; a < VTC_MAX_RANK; ++a) j[a] = idx[a];
+        dev::set_axis(j, last, int32_t(k));
+        return dev::elem_ptr<T>(op->m, j);
+    }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) row_kernel(const __grid_constant__ RowParams p) {
+    using A = std::conditional_t<std::is_same_v<T, double>, double, float>;
+    const int last = p.rank - 1;
+    for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+        int32_t idx[VTC_MAX_RANK];
+        dev::unflatten(row * p.D, p.shape, p.rank, idx);
+        RowIO<T> x, y;
+        x.init(p.x, idx, last);
+        y.init(p.out, idx, last);
+        auto xv = [&](int64_t k) -> A { return A(dev::to_acc<T>(*x.at(k))); };
+        int32_t z[VTC_MAX_RANK] = {};
+        RowIO<T> w, b;
+        if (p.op != RowOp::Softmax) w.init(p.w, z, 0);
+        if (p.op == RowOp::LayerNorm) b.init(p.bias, z, 0);
+        if (p.op == RowOp::RMSNorm) {
+            A ss = block_sum_256<A>([&](int64_t k) { A v = xv(k); return v * v; }, p.D);
+            A r;
+            if constexpr (std::is_same_v<A, double>) r = 1.0 / sqrt(ss / double(p.D) + double(p.eps));
+            else r = rsqrtf(ss / float(p.D) + p.eps);
+            for (int64_t k = threadIdx.x; k < p.D; k += 256)
+                *y.at(k) = dev::from_acc<T>((xv(k) * r) * A(dev::to_acc<T>(*w.at(k))));
+        } else if (p.op == RowOp::LayerNorm) {
+            A mu = block_sum_256<A>([&](int64_t k) { return xv(k); }, p.D) / A(p.D);
+            A var = block_sum_256<A>([&](int64_t k) { A v = xv(k) - mu; return v * v; }, p.D) / A(p.D);
+            A r;
+            if constexpr (std::is_same_v<A, double>) r = 1.0 / sqrt(var + double(p.eps));
+            else r = rsqrtf(var + p.eps);
+            for (int64_t k = threadIdx.x; k < p.D; k += 256)
+                *y.at(k) = dev::from_acc<T>(((xv(k) - mu) * r) * A(dev::to_acc<T>(*w.at(k))) +
+                                            A(dev::to_acc<T>(*b.at(k))));
+        } else {
+            A mx = block_max_256<A>([&](int64_t k) { return xv(k); }, p.D);
+            A s = block_sum_256<A>([&](int64_t k) { return A(exp(xv(k) - mx)); }, p.D);
+            for (int64_t k = threadIdx.x; k < p.D; k += 256) *y.at(k) = dev::from_acc<T>(A(exp(xv(k) - mx)) / s);
+        }
+    }
+}
+
+}  // namespace
+
+void launch_rowop(const RowParams& p, cudaStream_t s) {
+    if (p.rows == 0) return;
+    int grid = int(p.rows < 148 * 8 ? p.rows : 148 * 8);
+    switch (p.dt) {
+        case KDType::F64: row_kernel<double><<<grid, 256, 0, s>>>(p); break;
+        case KDType::F32: row_kernel<float><<<grid, 256, 0, s>>>(p); break;
+        case KDType::BF16: row_kernel<bf16><<<grid, 256, 0, s>>>(p); break;
+        default: break;
+    }
+}
+
+}  // namespace vtc

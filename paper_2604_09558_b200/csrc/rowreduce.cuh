@@ -1,0 +1,68 @@
+// Deterministic 256-thread row reductions shared by the row-op kernels and the
+// fused GEMV prologue, so a fused RMSNorm reproduces the standalone op bit for bit.
+#pragma once
+
+#include "device.cuh"
+
+namespace vtc {
+
+// Thread t accumulates f(t), f(t+256), ... in order, then a warp tree, then
+// the 8 warp partials in warp order.  Result broadcast to all threads.
+template <typename Acc, class F>
+__device__ __forceinline__ Acc block_sum_256(F f, int64_t D) {
+    __shared__ Acc s_part[8];
+    __shared__ Acc s_total;
+    Acc s = Acc(0);
+    for (int64_t k = threadIdx.x; k < D; k += 256) s += f(k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Acc t = Acc(0);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += s_part[w];
+        s_total = t;
+    }
+    __syncthreads();
+    Acc r = s_total;
+    __syncthreads();
+    return r;
+}
+
+template <typename Acc, class F>
+__device__ __forceinline__ Acc block_max_256(F f, int64_t D) {
+    __shared__ Acc s_part[8];
+    __shared__ Acc s_total;
+    Acc s = -INFINITY;
+    for (int64_t k = threadIdx.x; k < D; k += 256) s = max(s, f(k));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = max(s, __shfl_xor_sync(0xffffffffu, s, o));
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Acc t = s_part[0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) t = max(t, s_part[w]);
+        s_total = t;
+    }
+    __syncthreads();
+    Acc r = s_total;
+    __syncthreads();
+    return r;
+}
+
+// Sum of squares of row `row` of a rank-2 bf16 operand [rows, D].
+__device__ __forceinline__ float block_sumsq_row_bf16(const VOperand& x, int row, int64_t D) {
+    return block_sum_256<float>(
+        [&](int64_t k) {
+            int32_t idx[VTC_MAX_RANK] = {};
+            idx[0] = row;
+            idx[1] = int32_t(k);
+            float v = __bfloat162float(*dev::elem_ptr<dev::bf16>(x.m, idx));
+            return v * v;
+        },
+        D);
+}
+
+}  // namespace vtc

@@ -1,0 +1,219 @@
+"""Graph builders for the BASELINE.json workloads, in the reference JSON schema
+(proj/src/graph_ir.cpp:455-485).
+
+  c1_chain            configs[0]: reshape -> transpose -> slice feeding an fp32 matmul
+  llama_decode_layer  configs[1]/[2]: Llama-3-8B decoder layer decode step with a
+                      pos-major KV cache [S, B, Hkv, d] updated by ScatterND
+  frame2_subgraph     the paper's Fig. 2 frame-2 chain (QKV -> KV-cache update -> QK)
+                      in the reference's own operator vocabulary
+Graphs are plain dicts; only reference operators plus the documented
+extensions (RMSNorm, Attention, ...) are used.
+"""
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Optional
+
+
+class GraphBuilder:
+    def __init__(self, dtype: str = "f32"):
+        self.dtype = dtype
+        self.tensors: List[dict] = []
+        self.nodes: List[dict] = []
+        self._ids = set()
+
+    def tensor(self, tid: str, shape=None, kind: str = "intermediate", dtype: Optional[str] = None) -> str:
+        assert tid not in self._ids, tid
+        self._ids.add(tid)
+        t = {"id": tid, "dtype": dtype or self.dtype, "kind": kind}
+        t["shape"] = list(shape) if shape is not None else []
+        self.tensors.append(t)
+        return tid
+
+    def input(self, tid, shape, dtype=None):
+        return self.tensor(tid, shape, "input", dtype)
+
+    def node(self, nid: str, kind: str, inputs, outputs, attrs: Optional[dict] = None, out_kind: str = "intermediate"):
+        outs = []
+        for o in ([outputs] if isinstance(outputs, str) else outputs):
+            if o not in self._ids:
+                self.tensor(o, None, out_kind)
+            outs.append(o)
+        self.nodes.append({"id": nid, "kind": kind, "attrs": attrs or {}, "inputs": list(inputs), "outputs": outs})
+        return outs[0] if len(outs) == 1 else outs
+
+    def output(self, tid: str):
+        for t in self.tensors:
+            if t["id"] == tid:
+                t["kind"] = "output"
+        return tid
+
+    def doc(self) -> dict:
+        return {"tensors": self.tensors, "nodes": self.nodes}
+
+
+def c1_chain(n: int = 1024, dtype: str = "f32") -> dict:
+    """x [n,2,n] -> Reshape [n,2n] -> Transpose [2n,n] -> Slice rows [n/2, 3n/2) -> MatMul w [n,n].
+
+    At n=1024 this is BASELINE configs[0]; s[m,k] = x_flat[n/2 + m + 2n*k].
+    """
+    g = GraphBuilder(dtype)
+    g.input("x", [n, 2, n])
+    g.input("w", [n, n])
+    g.node("reshape", "Reshape", ["x"], "a", {"shape": [n, 2 * n]})
+    g.node("transpose", "Transpose", ["a"], "t", {"perm": [1, 0]})
+    g.node("slice", "Slice", ["t"], "s", {"axes": [0], "starts": [n // 2], "ends": [n // 2 + n]})
+    g.node("matmul", "MatMul", ["s", "w"], "y", out_kind="output")
+    return g.doc()
+
+
+def llama_decode_layer(B: int = 1, L: int = 2048, pos: Optional[int] = None, D: int = 4096, Hq: int = 32,
+                       Hkv: int = 8, hd: int = 128, F: int = 14336, dtype: str = "bf16", eps: float = 1e-5,
+                       reference_ops_only: bool = False) -> dict:
+    """One Llama-3 decoder layer, decode step (one new token per sequence).
+
+    KV caches are pos-major [L, B, Hkv, hd] (the reference's ScatterND only
+    supports 1-tuples, SURVEY.md §0 finding 1); the new token is written at
+    `pos` and attention reads keys [0, pos].  RoPE uses the sign-folded
+    rotate-half form  q*cos + concat(q[hd/2:], q[:hd/2])*sin_signed  so the
+    rotation itself is a data-movement chain (Slice/Slice/Concat).
+    reference_ops_only replaces RMSNorm by a weight Mul and Attention by
+    MatMul(q, k^T) * scale -> MatMul(., v) (no softmax): the same data
+    movement and the same GEMM work in the reference's vocabulary, used for
+    the timed reference CPU arm.
+    """
+    pos = L - 1 if pos is None else pos
+    G = Hq // Hkv
+    half = hd // 2
+    nq, nkv = Hq * hd, Hkv * hd
+    g = GraphBuilder(dtype)
+    g.input("x", [B, D])
+    g.input("w_ln1", [D])
+    g.input("w_qkv", [D, nq + 2 * nkv])
+    g.input("cos", [B, hd])
+    g.input("sin", [B, hd])
+    g.input("k_cache", [L, B, Hkv, hd])
+    g.input("v_cache", [L, B, Hkv, hd])
+    g.input("w_o", [nq, D])
+    g.input("w_ln2", [D])
+    g.input("w_gate", [D, F])
+    g.input("w_up", [D, F])
+    g.input("w_down", [F, D])
+
+    def norm(nid, x, w, out):
+        if reference_ops_only:
+            g.node(nid + "_wu", "Unsqueeze", [w], nid + "_w1", {"axis": 0})
+            g.node(nid + "_we", "Expand", [nid + "_w1"], nid + "_wb", {"shape": [B, D]})
+            return g.node(nid, "Mul", [x, nid + "_wb"], out)
+        return g.node(nid, "RMSNorm", [x, w], out, {"eps": eps})
+
+    norm("ln1", "x", "w_ln1", "h1")
+    g.node("qkv_proj", "MatMul", ["h1", "w_qkv"], "qkv")
+    g.node("qkv_split", "Split", ["qkv"], ["q2", "k2", "v2"], {"axis": 1, "sizes": [nq, nkv, nkv]})
+    g.node("q_reshape", "Reshape", ["q2"], "q3", {"shape": [B, Hq, hd]})
+    g.node("k_reshape", "Reshape", ["k2"], "k3", {"shape": [B, Hkv, hd]})
+    g.node("v_reshape", "Reshape", ["v2"], "v3", {"shape": [B, Hkv, hd]})
+
+    def rope(tag, x, H, out):
+        g.node(f"{tag}_lo", "Slice", [x], f"{tag}_lo", {"axes": [2], "starts": [0], "ends": [half]})
+        g.node(f"{tag}_hi", "Slice", [x], f"{tag}_hi", {"axes": [2], "starts": [half], "ends": [hd]})
+        g.node(f"{tag}_rot", "Concat", [f"{tag}_hi", f"{tag}_lo"], f"{tag}_rot", {"axis": 2})
+        for tab in ("cos", "sin"):
+            g.node(f"{tag}_{tab}_u", "Unsqueeze", [tab], f"{tag}_{tab}_1", {"axis": 1})
+            g.node(f"{tag}_{tab}_e", "Expand", [f"{tag}_{tab}_1"], f"{tag}_{tab}_b", {"shape": [B, H, hd]})
+        g.node(f"{tag}_mc", "Mul", [x, f"{tag}_cos_b"], f"{tag}_xc")
+        g.node(f"{tag}_ms", "Mul", [f"{tag}_rot", f"{tag}_sin_b"], f"{tag}_xs")
+        return g.node(f"{tag}_add", "Add", [f"{tag}_xc", f"{tag}_xs"], out)
+
+    rope("rq", "q3", Hq, "q_r")
+    rope("rk", "k3", Hkv, "k_r")
+    # KV-cache update at `pos` (ScatterND with static 1-tuples)
+    g.node("k_unsq", "Unsqueeze", ["k_r"], "k_u", {"axis": 0})
+    g.node("k_scatter", "ScatterND", ["k_cache", "k_u"], "kc2", {"indices": [[pos]]})
+    g.node("v_unsq", "Unsqueeze", ["v3"], "v_u", {"axis": 0})
+    g.node("v_scatter", "ScatterND", ["v_cache", "v_u"], "vc2", {"indices": [[pos]]})
+    S = pos + 1
+
+    def kv_path(tag, cache, out):
+        src = cache
+        if S < L:
+            src = g.node(f"{tag}_slice", "Slice", [cache], f"{tag}_s", {"axes": [0], "starts": [0], "ends": [S]})
+        g.node(f"{tag}_t", "Transpose", [src], f"{tag}_t", {"perm": [1, 2, 0, 3]})       # [B,Hkv,S,hd]
+        g.node(f"{tag}_u", "Unsqueeze", [f"{tag}_t"], f"{tag}_u5", {"axis": 2})          # [B,Hkv,1,S,hd]
+        g.node(f"{tag}_e", "Expand", [f"{tag}_u5"], f"{tag}_e", {"shape": [B, Hkv, G, S, hd]})
+        return g.node(f"{tag}_r", "Reshape", [f"{tag}_e"], out, {"shape": [B, Hq, S, hd]})
+
+    kv_path("kp", "kc2", "k_h")
+    kv_path("vp", "vc2", "v_h")
+    g.node("q_unsq", "Unsqueeze", ["q_r"], "q4", {"axis": 2})                         # [B,Hq,1,hd]
+    scale = 1.0 / math.sqrt(hd)
+    if reference_ops_only:
+        g.node("k_tr", "Transpose", ["k_h"], "k_T", {"perm": [0, 1, 3, 2]})
+        g.node("qk", "MatMul", ["q4", "k_T"], "sc")
+        g.input("scale", [1, 1, 1, 1])
+        g.node("sc_e", "Expand", ["scale"], "scale_b", {"shape": [B, Hq, 1, S]})
+        g.node("sc_m", "Mul", ["sc", "scale_b"], "p")
+        g.node("pv", "MatMul", ["p", "v_h"], "o4")
+    else:
+        g.node("attn", "Attention", ["q4", "k_h", "v_h"], "o4", {"scale": scale, "causal": False})
+    g.node("o_reshape", "Reshape", ["o4"], "o2", {"shape": [B, nq]})
+    g.node("o_proj", "MatMul", ["o2", "w_o"], "ao")
+    g.node("res1", "Add", ["x", "ao"], "x2")
+    norm("ln2", "x2", "w_ln2", "h2")
+    g.node("gate_proj", "MatMul", ["h2", "w_gate"], "gt")
+    g.node("up_proj", "MatMul", ["h2", "w_up"], "up")
+    g.node("silu", "SiLU", ["gt"], "sg")
+    g.node("gate_mul", "Mul", ["sg", "up"], "mm")
+    g.node("down_proj", "MatMul", ["mm", "w_down"], "dn")
+    g.node("res2", "Add", ["x2", "dn"], "y", out_kind="output")
+    return g.doc()
+
+
+def llama_weight_scales(D: int = 4096, F: int = 14336) -> Dict[str, float]:
+    """1/sqrt(fan_in) scaling applied to uniform(-1,1) weights (SURVEY.md §8 d)."""
+    return {"w_qkv": 1 / math.sqrt(D), "w_o": 1 / math.sqrt(D), "w_gate": 1 / math.sqrt(D),
+            "w_up": 1 / math.sqrt(D), "w_down": 1 / math.sqrt(F), "w_ln1": 1.0, "w_ln2": 1.0}
+
+
+def rope_tables(B: int, positions, hd: int = 128, theta: float = 500000.0):
+    """cos and sign-folded sin tables [B, hd] for the rotate-half RoPE form."""
+    import numpy as np
+    half = hd // 2
+    inv = theta ** (-np.arange(half, dtype=np.float64) * 2.0 / hd)
+    pos = np.asarray(positions, dtype=np.float64).reshape(B, 1)
+    ang = pos * inv[None, :]
+    cos = np.concatenate([np.cos(ang), np.cos(ang)], axis=1)
+    sin = np.concatenate([-np.sin(ang), np.sin(ang)], axis=1)
+    return cos, sin
+
+
+def frame2_subgraph(B: int = 1, L: int = 64, pos: Optional[int] = None, D: int = 64, Hq: int = 4, Hkv: int = 1,
+                    hd: int = 8, dtype: str = "f32") -> dict:
+    """Paper Fig. 2 frame 2 in reference ops: QKV proj -> Split -> Reshape ->
+    ScatterND(KV cache) -> Slice -> Transpose -> Unsqueeze -> Expand -> Reshape -> QK MatMul."""
+    doc = llama_decode_layer(B=B, L=L, pos=pos, D=D, Hq=Hq, Hkv=Hkv, hd=hd, F=2 * D, dtype=dtype,
+                             reference_ops_only=True)
+    keep_nodes = []
+    wanted = {"ln1_wu", "ln1_we", "ln1", "qkv_proj", "qkv_split", "q_reshape", "k_reshape", "v_reshape",
+              "k_unsq", "k_scatter", "v_unsq", "v_scatter", "kp_slice", "kp_t", "kp_u", "kp_e", "kp_r",
+              "vp_slice", "vp_t", "vp_u", "vp_e", "vp_r", "q_unsq", "k_tr", "qk", "sc_e", "sc_m", "pv"}
+    for n in doc["nodes"]:
+        if n["id"] in wanted:
+            keep_nodes.append(n)
+    # q_unsq reads q_r (rope output); rewire to q3 so the subgraph has no RoPE
+    for n in keep_nodes:
+        if n["id"] == "q_unsq":
+            n["inputs"] = ["q3"]
+        if n["id"] == "k_unsq":
+            n["inputs"] = ["k3"]
+    used = set()
+    for n in keep_nodes:
+        used.update(n["inputs"])
+        used.update(n["outputs"])
+    tensors = [dict(t) for t in doc["tensors"] if t["id"] in used]
+    for t in tensors:
+        if t["id"] == "o4":
+            t["kind"] = "output"
+        elif t["kind"] == "output":
+            t["kind"] = "intermediate"
+    return {"tensors": tensors, "nodes": keep_nodes}

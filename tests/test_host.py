@@ -1,0 +1,167 @@
+"""CPU-only tests: C ABI surface, graph IR, map algebra and planning.
+
+The map algebra and the points-to-graph decisions are checked against the
+reference library itself (oracle/_ref): same VTOG edge numbering, same
+eliminated operators, and resolved maps equal pointwise (symbolic map AND the
+lowered device descriptor) wherever the reference can compose.
+"""
+import json
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from randgraphs import random_graph, uses_roll
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_capi_exports_every_declared_symbol(vtc):
+    lib = vtc._lib.load()
+    decl = (ROOT / "include" / "vtc.h").read_text()
+    names = sorted(set(re.findall(r"\b(vtc_[a-z_]+)\s*\(", decl)))
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(vtc._lib.SIGNATURES), "ctypes signatures out of sync with include/vtc.h"
+
+
+def test_reference_unit_tests_pass():
+    exe = ROOT / "oracle" / "_ref" / "ref_unit"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/ref_unit not built")
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "failed checks: 0" in r.stdout
+
+
+def test_graph_ir_roundtrip_and_errors(vtc):
+    tiny = {"tensors": [{"id": "x", "shape": [2, 3], "dtype": "f64", "kind": "input"},
+                        {"id": "y", "shape": [2, 3], "dtype": "f64", "kind": "output"}],
+            "nodes": [{"id": "t0", "kind": "Transpose", "attrs": {"perm": [0, 1]}, "inputs": ["x"], "outputs": ["y"]}]}
+    g = vtc.parse_graph(tiny)
+    s1 = g.serialize()
+    assert vtc.parse_graph(s1).serialize() == s1
+    bad_split = {"tensors": [{"id": "x", "shape": [5, 4], "dtype": "f64", "kind": "input"},
+                             {"id": "a", "shape": [], "dtype": "f64", "kind": "output"},
+                             {"id": "b", "shape": [], "dtype": "f64", "kind": "output"}],
+                 "nodes": [{"id": "s", "kind": "Split", "attrs": {"axis": 0, "sizes": [2, 2]},
+                            "inputs": ["x"], "outputs": ["a", "b"]}]}
+    with pytest.raises(vtc.ERRORS[4]):  # ShapeError
+        vtc.parse_graph(bad_split)
+    cyc = {"tensors": [{"id": "a", "shape": [2], "dtype": "f64", "kind": "intermediate"},
+                       {"id": "b", "shape": [2], "dtype": "f64", "kind": "intermediate"}],
+           "nodes": [{"id": "n1", "kind": "SiLU", "inputs": ["a"], "outputs": ["b"]},
+                     {"id": "n2", "kind": "SiLU", "inputs": ["b"], "outputs": ["a"]}]}
+    with pytest.raises(vtc.ERRORS[3]):  # CycleError
+        vtc.parse_graph(cyc)
+    unk = json.loads(json.dumps(tiny))
+    unk["nodes"][0]["kind"] = "Softplus"
+    with pytest.raises(vtc.ERRORS[5]):  # UnknownOperatorError
+        vtc.parse_graph(unk)
+
+
+def _compare_with_reference(vtc, ref, doc):
+    rg = ref.RefGraph(doc)
+    g = vtc.parse_graph(doc)
+    rv = [(e["src"], e["dst"], e["candidate"], e["direction"], e["eliminated_op"]) for e in rg.vtog()["edges"]]
+    mv = [(e["src"], e["dst"], e["candidate"], e["direction"], e["eliminated_op"]) for e in g.vtog()["edges"]]
+    assert rv == mv, "VTOG edge numbering differs from the reference"
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    info = p.info(dry=True)
+    try:
+        rp = rg.plan(info["selected"])
+    except ref.RefError as e:
+        if "ComposeLimit" in str(e) or "piece cap" in str(e):
+            return None
+        raise
+    assert sorted(rp.info["eliminated_ops"]) == sorted(info["eliminated_ops"])
+    assert sorted(rp.info["roots"]) == sorted(info["roots"])
+    for tid, m in rp.info["resolved"].items():
+        tr, ti, off = ref.map_eval_all(m)
+        for lowered in (False, True):
+            tv, vi, voff = p.map_eval(tid, lowered=lowered)
+            assert [tr[i] for i in ti] == [tv[i] for i in vi], (tid, lowered)
+            assert np.array_equal(off, voff), (tid, lowered, m, p.map_json(tid))
+    return info
+
+
+def test_c1_and_frame2_maps_match_reference(vtc, ref):
+    from paper_2604_09558_b200 import workloads as W
+    info = _compare_with_reference(vtc, ref, W.c1_chain(64))
+    assert sorted(info["eliminated_ops"]) == ["reshape", "slice", "transpose"]
+    assert info["launches"] == [{"node": "matmul", "kernel": "matmul_tiled"}]
+    for L in (16, 64):
+        info = _compare_with_reference(vtc, ref, W.frame2_subgraph(B=2, L=L, D=32, Hq=4, Hkv=2, hd=8))
+        assert info["data_movement_launches"] == 0
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_graph_maps_match_reference(vtc, ref, seed):
+    doc = random_graph(seed, "f64")
+    if uses_roll(doc):
+        doc = random_graph(seed + 1000, "f64", compute=True)
+    if uses_roll(doc):
+        pytest.skip("Roll is a vtc extension")
+    _compare_with_reference(vtc, ref, doc)
+
+
+def test_estimate_matches_reference_bytes(vtc, ref):
+    """Byte accounting (cost_model.cpp:117-176) equals the reference's estimate."""
+    from paper_2604_09558_b200 import workloads as W
+    for doc in (W.c1_chain(64), W.frame2_subgraph(B=1, L=16, D=32, Hq=4, Hkv=1, hd=8)):
+        g = vtc.parse_graph(doc)
+        p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+        info = p.info(dry=True)
+        rg = ref.RefGraph(doc)
+        re_v = rg.plan(info["selected"]).estimate()
+        re_p = rg.plan().estimate()
+        def tot(e):
+            return sum(sum(r["bytes"] for r in k["reads"]) + sum(w["bytes"] for w in k["writes"]) for k in e["kernels"])
+        assert info["estimate"]["total_bytes"] == tot(re_v)
+        assert info["estimate_all_physical"]["total_bytes"] == tot(re_p)
+        assert info["estimate"]["data_movement_kernels"] == re_v["data_movement_kernels"]
+
+
+def test_c1_bytes_eliminated_matches_survey(vtc):
+    from paper_2604_09558_b200 import workloads as W
+    info = vtc.Plan(vtc.parse_graph(W.c1_chain(1024)), vtc.MAX_ELIMINATION).info(dry=True)
+    # all-physical 54,525,952 B -> virtual 12,582,912 B (reference estimate)
+    assert info["estimate"]["total_bytes"] == 12582912
+    assert info["estimate_all_physical"]["total_bytes"] == 54525952
+
+
+@pytest.mark.parametrize("B,L", [(1, 2048), (64, 8192)])
+def test_llama_decode_plans_at_full_size_with_zero_dm_kernels(vtc, B, L):
+    """The reference throws ComposeLimitError at KV >= 512 (SURVEY.md §0 finding 2)."""
+    from paper_2604_09558_b200 import workloads as W
+    g = vtc.parse_graph(W.llama_decode_layer(B=B, L=L))
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    info = p.info(dry=True)
+    assert info["data_movement_launches"] == 0
+    assert len(info["eliminated_ops"]) == 32
+    kh = p.map_json("k_h")
+    assert kh["pieces"] == 1 and kh["targets"] == ["k_cache"]
+    assert "/4" in kh["text"]  # GQA head map h div 4
+    # 4x fewer K/V bytes than the expanded operand
+    att = [k for k in info["estimate"]["kernels"] if k["node"] == "attn"][0]
+    kv_bytes = 2 * L * B * 8 * 128 * 2
+    assert att["read_bytes"] < kv_bytes * 1.01 + 4 * B * 32 * 128
+    m = vtc.Plan(g, vtc.MATERIALIZE).info(dry=True)
+    assert m["data_movement_launches"] > 0
+
+
+def test_oracle_matches_reference_on_random_graphs(ref, oracle):
+    for seed in range(25):
+        for dt in ("f64", "f32", "i64"):
+            doc = random_graph(seed, dt)
+            if uses_roll(doc):
+                continue
+            rg = ref.RefGraph(doc)
+            x = rg.inputs_random(seed + 1)
+            want, _, _ = rg.plan().execute(x)
+            got = oracle.execute(doc, x)
+            for k in want:
+                assert np.array_equal(want[k].view(np.uint8), got[k].view(np.uint8)), (seed, dt, k)

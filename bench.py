@@ -1,0 +1,408 @@
+"""Benchmark: VTC-planned Llama-3-8B decoder-layer decode step on B200.
+
+Metric (BASELINE.json): decoder-layer latency (us) with HBM GB/s as a fraction
+of roofline and the DRAM bytes eliminated versus the materialising executor.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1] [--impl vtc|reference]
+
+Default workload: BASELINE configs[1] -- Llama-3-8B decoder layer, decode step,
+batch 1, KV length 2048, bf16 (random-init weights uniform(-1,1)/sqrt(fan_in)).
+Every timed step is one full layer on the GPU: zero data-movement kernels
+under the VTC plan.  L2 is flushed (256 MiB write) between timed steps,
+outside the timed events.  `--impl reference` times the reference's own CPU
+executor (oracle/_ref, built from /root/reference) on the same layer.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+CONFIGS = {
+    "c2": dict(B=1, L=2048, workload="llama3-8b-decoder-layer-decode-b1-kv2048"),
+    "c3": dict(B=64, L=8192, workload="llama3-8b-decoder-layer-decode-b64-kv8192"),
+    "c1": dict(n=1024, workload="reshape-transpose-slice-fp32-matmul-1024"),
+}
+METRIC = "decoder-layer latency (us) & HBM GB/s as % roofline; DRAM bytes eliminated"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def build_layer_inputs(doc, cfg, torch, dev):
+    """Random-init weights / caches directly on the device; per-step inputs on pinned host."""
+    from paper_2604_09558_b200 import workloads as W
+    specs = {t["id"]: t for t in doc["tensors"]}
+    scales = W.llama_weight_scales()
+    g = torch.Generator(device=dev)
+    g.manual_seed(1)
+    dev_tensors = {}
+    for tid in ("w_ln1", "w_qkv", "w_o", "w_ln2", "w_gate", "w_up", "w_down", "k_cache", "v_cache"):
+        shape = specs[tid]["shape"]
+        t = torch.empty(shape, dtype=torch.float32, device=dev).uniform_(-1.0, 1.0, generator=g)
+        dev_tensors[tid] = (t * scales.get(tid, 1.0)).to(torch.bfloat16).contiguous()
+    B = cfg["B"]
+    cos, sin = W.rope_tables(B, [cfg["L"] - 1] * B)
+    rng = np.random.default_rng(2)
+    host = {
+        "x": torch.from_numpy(rng.uniform(-1, 1, size=(B, 4096)).astype(np.float32)).to(torch.bfloat16),
+        "cos": torch.from_numpy(cos.astype(np.float32)).to(torch.bfloat16),
+        "sin": torch.from_numpy(sin.astype(np.float32)).to(torch.bfloat16),
+    }
+    host = {k: v.contiguous().pin_memory() for k, v in host.items()}
+    return dev_tensors, host
+
+
+def time_steps(fn, steps, torch, stream, flush):
+    """Per-step CUDA-event timing on `stream`; L2 flushed before each step, outside the events."""
+    times = []
+    for _ in range(steps):
+        flush()
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record(stream)
+        fn()
+        e.record(stream)
+        e.synchronize()
+        times.append(s.elapsed_time(e))
+    return float(np.mean(times)), times
+
+
+def _ref_layer_setup(cfg):
+    """The layer in the reference's own operator vocabulary (f32; RMSNorm ->
+    weight Mul, attention -> QK^T * scale -> .V without softmax: the same data
+    movement and GEMM work), planned by the reference (all-physical -- its
+    planner cannot compose at KV >= 512) on oracle/_ref."""
+    import ref
+    from paper_2604_09558_b200 import workloads as W
+    if not ref.available():
+        return None
+    doc = W.llama_decode_layer(B=1, L=cfg["L"], dtype="f32", reference_ops_only=True)
+    rg = ref.RefGraph(doc)
+    rng = np.random.default_rng(1)
+    scales = W.llama_weight_scales()
+    x = {}
+    for t in doc["tensors"]:
+        if t["kind"] == "input":
+            x[t["id"]] = (rng.uniform(-1, 1, size=t["shape"]) * scales.get(t["id"], 1.0)).astype(np.float32)
+    return rg, rg.plan(), x
+
+
+def _ref_sample(cfg, runs):
+    return (f"{runs} full decoder-layer step(s) for batch row 1 of {cfg['B']}, KV {cfg['L']}, f32, "
+            f"reference-ops variant (RMSNorm->Mul, softmax omitted), reference execute(), single thread; "
+            f"value = per-row time x {cfg['B']} rows (rows are independent)")
+
+
+def cpu_reference_layer(cfg, runs=2):
+    setup = _ref_layer_setup(cfg)
+    if setup is None:
+        return None
+    rg, plan, x = setup
+    ts = [plan.execute(x)[1] / 1e3 for _ in range(runs)]
+    v = float(np.median(ts)) * cfg["B"]
+    return {"value": v, "unit": "us", "cores": 1, "kind": "reference", "sample": _ref_sample(cfg, runs)}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    if args.config == "c1":
+        import ref
+        from paper_2604_09558_b200 import workloads as W
+        if not ref.available():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+            return
+        rg = ref.RefGraph(W.c1_chain(cfg["n"]))
+        x = rg.inputs_random(1)
+        plan = rg.plan()
+        sample = "full C1 chain + 1024^3 f32 matmul, reference execute (all-physical), single thread"
+        scale = 1
+    else:
+        setup = _ref_layer_setup(cfg)
+        if setup is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+            return
+        rg, plan, x = setup
+        sample = _ref_sample(cfg, args.steps)
+        scale = cfg["B"]
+    ts = []
+    for i in range(args.warmup + args.steps):
+        _, ns, _ = plan.execute(x)
+        if i >= args.warmup:
+            ts.append(ns / 1e3 * scale)
+    v = float(np.mean(ts))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "us", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"]},
+            "cpu_baseline": {"value": v, "unit": "us", "cores": 1, "kind": "reference", "sample": sample},
+            "e2e": {"value": v, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_vtc(args):
+    import torch
+    import paper_2604_09558_b200 as vtc
+    from paper_2604_09558_b200 import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    cfg = CONFIGS[args.config]
+    hbm_peak, tf_peak, peak_src = peaks()
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    read_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def flush():
+        # write a buffer larger than L2, then read another one so the dirty
+        # lines are written back here rather than inside the timed step
+        flush_buf.random_(0, 255)
+        read_buf.max()
+
+    if args.config == "c1":
+        return run_c1(args, torch, vtc, W, dev, stream, flush, hbm_peak, peak_src, world, rank)
+
+    B, L = cfg["B"], cfg["L"]
+    doc = W.llama_decode_layer(B=B, L=L)
+    g = vtc.parse_graph(doc)
+    dev_tensors, host = build_layer_inputs(doc, cfg, torch, dev)
+    plans = {}
+    for name, mode in (("virtual", vtc.MAX_ELIMINATION), ("materialized", vtc.MATERIALIZE)):
+        p = vtc.Plan(g, mode)
+        for tid, t in dev_tensors.items():
+            p.bind_root(tid, t.data_ptr())
+        for tid, t in host.items():
+            p.upload_ptr(tid, t.data_ptr(), t.numel() * t.element_size(), stream)
+        p.prepare()
+        plans[name] = p
+    info = plans["virtual"].info()
+    minfo = plans["materialized"].info()
+    # the caches are updated in place every step at the same position: repeated
+    # steps are idempotent, so every timed step does identical work
+
+    results = {}
+    for name, p in plans.items():
+        for _ in range(max(3, args.warmup)):
+            p.execute_graph(stream)
+        torch.cuda.synchronize()
+        if name == "virtual":
+            with ClockSampler(local) as clk:
+                mean_ms, _ = time_steps(lambda: p.execute_graph(stream), args.steps, torch, stream, flush)
+            clocks = clk.summary()
+        else:
+            mean_ms, _ = time_steps(lambda: p.execute_graph(stream), args.steps, torch, stream, flush)
+        results[name] = mean_ms
+
+    # per-launch device times (separate pass; same launches with events between them)
+    launches = info["launches"]
+    per = np.zeros(len(launches))
+    reps = max(3, min(args.steps, 10))
+    for _ in range(reps):
+        flush()
+        torch.cuda.synchronize()
+        per += plans["virtual"].execute_timed(len(launches), stream)[: len(launches)]
+    per /= reps
+    fam = {}
+    for l, ms in zip(launches, per):
+        f = fam.setdefault(l["kernel"], {"ms": 0.0, "bytes": 0, "launches": 0})
+        f["ms"] += float(ms)
+        f["bytes"] += int(l["bytes"])
+        f["launches"] += 1
+    dom = max(fam, key=lambda k: fam[k]["ms"])
+    achieved = fam[dom]["bytes"] / (fam[dom]["ms"] * 1e-3) / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+
+    # e2e through the C ABI with host buffers: H2D of the step's inputs, the layer, D2H of y
+    pv = plans["virtual"]
+    y_host = torch.empty((B, 4096), dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step():
+        for tid, t in host.items():
+            pv.upload_ptr(tid, t.data_ptr(), t.numel() * t.element_size(), stream)
+        pv.execute_graph(stream)
+        pv.download_ptr("y", y_host.data_ptr(), y_host.numel() * 2, stream)
+
+    for _ in range(2):
+        e2e_step()
+    e2e_ms, _ = time_steps(e2e_step, args.steps, torch, stream, flush)
+    h2d = sum(t.numel() * t.element_size() for t in host.values())
+    d2h = y_host.numel() * 2
+
+    lat_ms = results["virtual"]
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([lat_ms, e2e_ms, results["materialized"]], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        lat_ms, e2e_ms, mat_ms = t.tolist()
+    else:
+        mat_ms = results["materialized"]
+    if rank != 0:
+        return
+    bytes_step = sum(l["bytes"] for l in launches)
+    cpu = cpu_reference_layer(cfg) if world == 1 and not os.environ.get("BENCH_NO_CPU") else None
+    line = {
+        "metric": METRIC,
+        "value": lat_ms * 1e3,
+        "unit": "us",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": lat_ms,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (random-init weights uniform(-1,1)/sqrt(fan_in), random KV cache)",
+        "config": {"workload": cfg["workload"], "batch": B, "kv_len": L, "pos": L - 1,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
+                   "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events); per-step working set 445 MB > 126 MB L2",
+                   "plan": "VTC max-elimination (all data-movement ops virtual)", "cuda_graph": True},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic, "kernel": dom,
+                     "kernel_launches_per_step": fam[dom]["launches"],
+                     "algorithmic_bytes_per_step": fam[dom]["bytes"], "peak_source": peak_src},
+        "step_hbm_gbs": bytes_step / (lat_ms * 1e-3) / 1e9,
+        "step_hbm_frac": bytes_step / (lat_ms * 1e-3) / 1e9 / hbm_peak,
+        "bytes_per_step": bytes_step,
+        "materialized_us": mat_ms * 1e3,
+        "speedup_vs_materialized": mat_ms / lat_ms,
+        "dram_bytes_eliminated": info["bytes_eliminated"],
+        "data_movement_launches": {"virtual": info["data_movement_launches"],
+                                   "materialized": minfo["data_movement_launches"]},
+        "kernel_times_us": {k: round(v["ms"] * 1e3, 2) for k, v in fam.items()},
+        "e2e": {"value": e2e_ms * 1e3, "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": info["kernel_launches"] * args.steps,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_c1(args, torch, vtc, W, dev, stream, flush, hbm_peak, peak_src, world, rank):
+    import vtc_oracle as O
+    doc = W.c1_chain(1024)
+    g = vtc.parse_graph(doc)
+    x = O.random_inputs(doc, 1)
+    res = {}
+    for name, mode in (("virtual", vtc.MAX_ELIMINATION), ("materialized", vtc.MATERIALIZE)):
+        p = vtc.Plan(g, mode)
+        for tid, a in x.items():
+            p.upload(tid, a, stream)
+        p.prepare()
+        for _ in range(max(3, args.warmup)):
+            p.execute_graph(stream)
+        with ClockSampler(0) as clk:
+            res[name], _ = time_steps(lambda: p.execute_graph(stream), args.steps, torch, stream, flush)
+        if name == "virtual":
+            info = p.info()
+            clocks = clk.summary()
+    flops = 2 * 1024 ** 3
+    line = {"metric": METRIC, "value": res["virtual"] * 1e3, "unit": "us", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["virtual"], "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": CONFIGS["c1"]["workload"], "exact_fp32": True},
+            "tflops": flops / (res["virtual"] * 1e-3) / 1e12, "materialized_us": res["materialized"] * 1e3,
+            "dram_bytes_eliminated": info["bytes_eliminated"], "clocks": clocks,
+            "gpu_launches": info["kernel_launches"] * args.steps}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="vtc", choices=["vtc", "reference"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_vtc(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -69,7 +69,8 @@ enum vtc_plan_mode {
 enum vtc_plan_flags {
     VTC_FLAG_FAST_FP = 1u << 0,  /* generic f32/f64 MatMul with FMA instead of the bit-exact mul+add */
     VTC_FLAG_NO_GEMV = 1u << 1,  /* disable the weight-streaming decode kernel */
-    VTC_FLAG_NO_FUSE = 1u << 2   /* disable RMSNorm/SiLU*Mul/residual fusion into the GEMV */
+    VTC_FLAG_NO_FUSE = 1u << 2,  /* disable RMSNorm/SiLU*Mul/residual and elementwise-tree fusion */
+    VTC_FLAG_GEMV_TMA = 1u << 3  /* persistent bulk-copy (cp.async.bulk) GEMV instead of the LDG split-K GEMV */
 };
 
 typedef struct vtc_graph vtc_graph;
@@ -100,6 +101,9 @@ int vtc_plan_prepare(vtc_plan* p);
 int vtc_execute(vtc_plan* p, void* stream);        /* async launches on `stream` (cudaStream_t) */
 int vtc_execute_graph(vtc_plan* p, void* stream);  /* CUDA-graph replay of the same launches */
 int vtc_plan_num_launches(vtc_plan* p);
+/* Same launches with a CUDA event between each; ms[i] = device time of launch
+ * record i (vtc_plan_info "launches" order).  For measurement only. */
+int vtc_execute_timed(vtc_plan* p, void* stream, float* ms, int32_t n);
 
 /* Host evaluation (no GPU) of a tensor's resolved map over its whole index
  * space in row-major order: targets[i] = index into the sorted target list

@@ -22,6 +22,7 @@ namespace vtc {
 struct ExecOptions {
     bool exact_fp = true;     // generic f32/f64 MatMul: unfused mul+add (bit-exact vs CPU reference)
     bool use_gemv = true;     // bf16 decode projections on the weight-streaming kernel
+    bool gemv_tma = false;    // persistent cp.async.bulk-fed GEMV (M <= 4); default: the LDG split-K GEMV (faster today)
     bool fuse = true;         // RMSNorm->MatMul, SiLU*Mul->MatMul, MatMul->Add(residual) fusion
     int attn_splits = 0;      // 0: automatic
 };
@@ -38,6 +39,7 @@ struct RootBuffer {
 struct LaunchInfo {
     std::string node;    // graph node id (or "node+node" for a fused group)
     std::string kernel;  // kernel family
+    int64_t bytes = 0;   // algorithmic bytes: unique elements read through the maps + elements written
 };
 
 class Executor {
@@ -61,6 +63,9 @@ public:
     void run(void* stream);
     // Capture the launch list into a CUDA graph once, then replay it.
     void run_graph(void* stream);
+    // Enqueue every launch with a CUDA event on each side; per-launch device
+    // milliseconds are written to ms[0..n) after the stream drains.
+    void run_timed(void* stream, float* ms, int n);
 
     void upload(const std::string& id, const void* host, int64_t bytes, void* stream);
     // Materialise any tensor (virtual or physical) into host memory.

@@ -30,10 +30,13 @@ extern "C" {
 
 typedef struct vtc_digit {
     int64_t coeff;
-    uint32_t div; /* >= 1 */
-    uint32_t mod; /* 0: none */
-    int32_t axis;
-    int32_t group; /* -1: top level */
+    uint32_t div;      /* >= 1 */
+    uint32_t mod;      /* 0: none */
+    int8_t axis;
+    int8_t group;      /* -1: top level */
+    int8_t div_shift;  /* log2(div) when div is a power of two, else -1 */
+    int8_t mod_shift;  /* log2(mod) when mod is a power of two, else -1 */
+    int32_t pad;
 } vtc_digit;
 
 typedef struct vtc_group {

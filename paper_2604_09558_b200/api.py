@@ -134,6 +134,14 @@ class Plan:
         _check(_lib.load().vtc_plan_upload(self._h, tensor.encode(), arr.ctypes.data_as(C.c_void_p),
                                            arr.nbytes, _stream(stream)))
 
+    def upload_ptr(self, tensor: str, host_ptr: int, nbytes: int, stream=None) -> None:
+        """H2D from a raw host pointer (e.g. pinned memory)."""
+        _check(_lib.load().vtc_plan_upload(self._h, tensor.encode(), C.c_void_p(host_ptr), nbytes, _stream(stream)))
+
+    def download_ptr(self, tensor: str, host_ptr: int, nbytes: int, stream=None) -> None:
+        _check(_lib.load().vtc_plan_download(self._h, tensor.encode(), C.c_void_p(host_ptr), nbytes,
+                                             _stream(stream)))
+
     def download(self, tensor: str, stream=None) -> np.ndarray:
         spec = self.graph.tensors()[tensor]
         out = np.empty(spec["shape"], dtype=NP_DTYPES[spec["dtype"]])
@@ -149,6 +157,12 @@ class Plan:
 
     def execute_graph(self, stream=None) -> None:
         _check(_lib.load().vtc_execute_graph(self._h, _stream(stream)))
+
+    def execute_timed(self, n_records: int, stream=None) -> np.ndarray:
+        ms = np.zeros(max(1, n_records), np.float32)
+        _check(_lib.load().vtc_execute_timed(self._h, _stream(stream), ms.ctypes.data_as(C.POINTER(C.c_float)),
+                                             n_records))
+        return ms
 
     def num_launches(self) -> int:
         return _lib.load().vtc_plan_num_launches(self._h)

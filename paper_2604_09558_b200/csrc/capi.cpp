@@ -154,6 +154,7 @@ int vtc_plan_create(vtc_graph* g, int mode, const int32_t* selected, int32_t n_s
         opt.exact_fp = !(flags & VTC_FLAG_FAST_FP);
         opt.use_gemv = !(flags & VTC_FLAG_NO_GEMV);
         opt.fuse = !(flags & VTC_FLAG_NO_FUSE);
+        opt.gemv_tma = (flags & VTC_FLAG_GEMV_TMA) != 0;
         auto p = std::make_unique<vtc_plan>();
         p->graph = g;
         p->flags = flags;
@@ -187,6 +188,7 @@ int vtc_plan_info(vtc_plan* p, int dry, const char** json_out) {
             Value lj = Value::object();
             lj.set("node", str(l.node));
             lj.set("kernel", str(l.kernel));
+            lj.set("bytes", Value::integer(l.bytes));
             ls.push(lj);
             if (l.kernel == "gather_copy") ++dm;
         }
@@ -232,6 +234,10 @@ int vtc_execute_graph(vtc_plan* p, void* stream) {
 }
 
 int vtc_plan_num_launches(vtc_plan* p) { return p->exec->num_kernel_launches(); }
+
+int vtc_execute_timed(vtc_plan* p, void* stream, float* ms, int32_t n) {
+    return guard([&] { p->exec->run_timed(stream, ms, n); });
+}
 
 int vtc_map_eval(vtc_plan* p, const char* tensor, int lowered, int32_t* targets, int64_t* offsets, int64_t cap) {
     return guard([&] {
@@ -289,15 +295,22 @@ int vtc_launch_gather_copy(const vtc_map* dst, const vtc_map* src, int32_t elem_
             n *= dst->shape[i];
         }
         p.vec = 1;
-        p.op = vtc::EwOp::Copy;
+        p.copy_only = 1;
         p.esize = elem_bytes;
         p.dt = elem_bytes == 8 ? vtc::KDType::I64 : elem_bytes == 4 ? vtc::KDType::F32 : vtc::KDType::BF16;
         p.nvec = n;
         p.nin = 1;
         p.out.m = *dst;
-        p.a.m = *src;
-        vtc::launch_eltwise(p, static_cast<cudaStream_t>(stream));
-        cudaError_t e = cudaGetLastError();
+        p.in[0].m = *src;
+        vtc::EwParams* dp = nullptr;
+        cudaError_t e = cudaMalloc(&dp, sizeof(p));
+        if (e == cudaSuccess) e = cudaMemcpy(dp, &p, sizeof(p), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) {
+            vtc::launch_eltwise(p, dp, static_cast<cudaStream_t>(stream));
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+        cudaFree(dp);
         if (e != cudaSuccess) throw vtc::CudaError(cudaGetErrorString(e));
     });
 }

@@ -35,13 +35,36 @@ struct Launch {
     std::string node, kernel;
     virtual ~Launch() = default;
     virtual void run(cudaStream_t s) = 0;
+    virtual size_t param_bytes() const = 0;
+    virtual const void* host_params() const = 0;
+    virtual void set_device_params(void* d) = 0;
 };
 
-template <class P, void (*F)(const P&, cudaStream_t)>
+// Host copy of the parameter block (for dispatch decisions) + its device copy
+// (what the kernel reads).
+template <class P, void (*F)(const P&, const P*, cudaStream_t)>
 struct LaunchT : Launch {
     P p;
-    void run(cudaStream_t s) override { F(p, s); }
+    const P* dp = nullptr;
+    void run(cudaStream_t s) override { F(p, dp, s); }
+    size_t param_bytes() const override { return sizeof(P); }
+    const void* host_params() const override { return &p; }
+    void set_device_params(void* d) override { dp = static_cast<const P*>(d); }
 };
+
+void launch_gemv_any(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
+    if (p.tma) launch_gemv_tma(p, dp, s);
+    else launch_gemv(p, dp, s);
+}
+
+// Upload a parameter block for a one-off launch; caller frees.
+template <class P>
+P* upload_params(const P& p) {
+    P* d = nullptr;
+    ck(cudaMalloc(&d, sizeof(P)), "cudaMalloc(params)");
+    ck(cudaMemcpy(d, &p, sizeof(P), cudaMemcpyHostToDevice), "H2D(params)");
+    return d;
+}
 
 // Host-side digest of a lowered map along the kernel's fast axis.
 void finish_operand(VOperand& op, int fast_axis, int64_t tile, int64_t esize) {
@@ -202,22 +225,65 @@ void Executor::prepare(bool dry) {
     };
     std::set<std::string> elim(ptg_.eliminated_ops.begin(), ptg_.eliminated_ops.end());
 
+    // algorithmic bytes of a (possibly fused) launch: tensors read from outside
+    // the group (unique elements through their maps) + tensors the group emits
+    auto group_bytes = [&](const std::string& names) -> int64_t {
+        std::set<std::string> grp;
+        size_t st = 0;
+        while (st <= names.size()) {
+            size_t e = names.find('+', st);
+            if (e == std::string::npos) e = names.size();
+            grp.insert(names.substr(st, e - st));
+            st = e + 1;
+        }
+        std::set<std::string> produced, reads;
+        int64_t bytes = 0;
+        for (const auto& id : grp)
+            if (const OpNode* n = g_.node(id))
+                for (const auto& o : n->outputs) produced.insert(o);
+        for (const auto& id : grp) {
+            const OpNode* n = g_.node(id);
+            if (!n) continue;
+            for (const auto& in : n->inputs)
+                if (!produced.count(in) && reads.insert(in).second)
+                    bytes += ptg_.map_of(in).unique_elems() * dtype_size(g_.tensor(in).dtype);
+            for (const auto& o : n->outputs) {
+                bool internal = g_.tensor(o).kind == TensorKind::Intermediate;
+                auto cs = g_.consumers(o);
+                for (const OpNode* c : cs) internal = internal && grp.count(c->id);
+                if (cs.empty()) internal = false;
+                if (!internal) bytes += g_.tensor(o).bytes();
+            }
+        }
+        return bytes;
+    };
     auto push = [&](std::unique_ptr<Launch> l) {
-        infos_.push_back({l->node, l->kernel});
+        LaunchInfo li;
+        li.node = l->node;
+        li.kernel = l->kernel;
+        li.bytes = group_bytes(l->node);
+        infos_.push_back(li);
         impl_->launches.push_back(std::move(l));
     };
 
     // ---- elementwise / copy launches over an output shape ----
-    // A map with more pieces than the descriptor holds is handled by one launch
-    // per piece of the widest map, each iterating over that piece's box.
-    std::function<void(const std::string&, EwOp, DType, const Index&, const VMap&, const VMap*, const VMap*,
-                       const Index&, const Index&)>
+    // An EwSpec is a small program over up to EW_MAX_IN input maps.  A map with
+    // more pieces than the descriptor holds is handled by one launch per piece
+    // (or by bisecting the iteration box), each iterating over its own box.
+    struct EwSpec {
+        std::vector<const VMap*> ins;
+        std::vector<EwInstr> prog;
+        int result = 0;
+        bool copy = false;
+    };
+    std::function<void(const std::string&, const EwSpec&, DType, const Index&, const VMap&, const Index&,
+                       const Index&)>
         eltwise_box;
-    eltwise_box = [&](const std::string& node, EwOp op, DType dt, const Index& shape, const VMap& out,
-                      const VMap* a, const VMap* b, const Index& lo, const Index& hi) {
+    eltwise_box = [&](const std::string& node, const EwSpec& spec, DType dt, const Index& shape, const VMap& out,
+                      const Index& lo, const Index& hi) {
         auto L = std::make_unique<LaunchT<EwParams, launch_eltwise>>();
         L->node = node;
-        L->kernel = op == EwOp::Copy ? "gather_copy" : "eltwise";
+        L->kernel = spec.copy ? "gather_copy" : "eltwise";
         EwParams& p = L->p;
         std::memset(&p, 0, sizeof(p));
         int64_t es = dtype_size(dt);
@@ -232,10 +298,14 @@ void Executor::prepare(bool dry) {
             p.origin[i] = int32_t(lo[size_t(i)]);
         }
         p.vec = int32_t(vec);
-        p.op = op;
         p.dt = kdt(dt);
         p.esize = int32_t(es);
+        p.copy_only = spec.copy ? 1 : 0;
         p.nvec = volume(ext) / vec;
+        p.nin = int32_t(spec.ins.size());
+        p.nprog = int32_t(spec.prog.size());
+        p.result = spec.result;
+        for (size_t i = 0; i < spec.prog.size(); ++i) p.prog[i] = spec.prog[i];
         auto restrict_box = [&](const VMap& m) {
             std::vector<VPiece> ps;
             for (const auto& q : m.pieces()) {
@@ -252,9 +322,9 @@ void Executor::prepare(bool dry) {
             }
             return VMap(m.shape(), std::move(ps));
         };
-        const VMap* maps[3] = {&out, a, b};
-        for (int k = 0; k < 3; ++k) {
-            if (!maps[k]) continue;
+        std::vector<const VMap*> maps{&out};
+        for (auto* m : spec.ins) maps.push_back(m);
+        for (size_t k = 0; k < maps.size(); ++k) {
             VMap rm = restrict_box(*maps[k]);
             VOperand op2{};
             try {
@@ -262,7 +332,7 @@ void Executor::prepare(bool dry) {
             } catch (const UnsupportedError&) {
                 // split the iteration box along the pieces of this map, or bisect it
                 if (rm.pieces().size() > 1) {
-                    for (const auto& q : rm.pieces()) eltwise_box(node, op, dt, shape, out, a, b, q.lo, q.hi);
+                    for (const auto& q : rm.pieces()) eltwise_box(node, spec, dt, shape, out, q.lo, q.hi);
                     return;
                 }
                 int best = -1;
@@ -276,19 +346,23 @@ void Executor::prepare(bool dry) {
                 Index h1 = hi, l2 = lo;
                 h1[size_t(best)] = lo[size_t(best)] + bext / 2;
                 l2[size_t(best)] = h1[size_t(best)];
-                eltwise_box(node, op, dt, shape, out, a, b, lo, h1);
-                eltwise_box(node, op, dt, shape, out, a, b, l2, hi);
+                eltwise_box(node, spec, dt, shape, out, lo, h1);
+                eltwise_box(node, spec, dt, shape, out, l2, hi);
                 return;
             }
             finish_operand(op2, rank - 1, vec, es);
-            (k == 0 ? p.out : k == 1 ? p.a : p.b) = op2;
+            (k == 0 ? p.out : p.in[k - 1]) = op2;
         }
-        p.nin = b ? 2 : 1;
         push(std::move(L));
     };
-    auto eltwise = [&](const std::string& node, EwOp op, DType dt, const Index& shape, const VMap& out,
-                       const VMap* a, const VMap* b) {
-        eltwise_box(node, op, dt, shape, out, a, b, Index(shape.size(), 0), shape);
+    auto eltwise = [&](const std::string& node, const EwSpec& spec, DType dt, const Index& shape, const VMap& out) {
+        eltwise_box(node, spec, dt, shape, out, Index(shape.size(), 0), shape);
+    };
+    auto copy_spec = [](const VMap* src) {
+        EwSpec sp;
+        sp.ins = {src};
+        sp.copy = true;
+        return sp;
     };
 
     // A gather-copy that must not read what it writes: stage through scratch.
@@ -297,7 +371,7 @@ void Executor::prepare(bool dry) {
         bool hazard = false;
         for (const auto& t : td) hazard |= ts.count(t) > 0;
         if (!hazard) {
-            eltwise(node, EwOp::Copy, dt, shape, dst, &src, nullptr);
+            eltwise(node, copy_spec(&src), dt, shape, dst);
             return;
         }
         // stage: src -> temp (identity) -> dst
@@ -310,9 +384,51 @@ void Executor::prepare(bool dry) {
         rb.ptr = impl_->alloc(size_t(rb.bytes), false);
         root_index_[tmp_id] = int(roots_.size());
         roots_.push_back(rb);
-        VMap tmp = VMap::identity(tmp_id, shape);
-        eltwise(node, EwOp::Copy, dt, shape, tmp, &src, nullptr);
-        eltwise(node, EwOp::Copy, dt, shape, dst, &tmp, nullptr);
+        auto tmp = std::make_shared<VMap>(VMap::identity(tmp_id, shape));
+        eltwise(node, copy_spec(&src), dt, shape, *tmp);
+        eltwise(node, copy_spec(tmp.get()), dt, shape, dst);
+    };
+
+    // ---- elementwise-tree fusion: a tree of Add/Mul/SiLU/GELU nodes whose
+    //      internal tensors have a single consumer runs as one program ----
+    auto is_ew = [](OpKind k) { return k == OpKind::Add || k == OpKind::Mul || k == OpKind::SiLU || k == OpKind::GELU; };
+    auto ew_code = [](OpKind k) {
+        return k == OpKind::Add ? EwOp::Add : k == OpKind::Mul ? EwOp::Mul : k == OpKind::SiLU ? EwOp::SiLU : EwOp::GELU;
+    };
+    // build the program for the tree rooted at `root`; members collects fused nodes
+    std::function<bool(const OpNode&, EwSpec&, std::vector<std::string>&, std::vector<std::string>&, int&)> build_tree;
+    build_tree = [&](const OpNode& n, EwSpec& sp, std::vector<std::string>& in_names, std::vector<std::string>& members,
+                     int& reg) -> bool {
+        std::vector<int> regs;
+        for (const auto& t : n.inputs) {
+            const OpNode* p = g_.producer(t);
+            bool fuse = opt_.fuse && p && is_ew(p->kind) && g_.tensor(t).kind == TensorKind::Intermediate &&
+                        g_.consumers(t).size() == 1 && g_.tensor(t).shape == g_.tensor(n.outputs[0]).shape;
+            if (fuse) {
+                int r = 0;
+                if (!build_tree(*p, sp, in_names, members, r)) return false;
+                regs.push_back(r);
+            } else {
+                auto it = std::find(in_names.begin(), in_names.end(), t);
+                if (it != in_names.end()) {
+                    regs.push_back(int(it - in_names.begin()));
+                } else {
+                    if (int(in_names.size()) >= EW_MAX_IN) return false;
+                    in_names.push_back(t);
+                    regs.push_back(int(in_names.size()) - 1);
+                }
+            }
+        }
+        if (int(sp.prog.size()) >= EW_MAX_PROG) return false;
+        EwInstr ins{};
+        ins.op = ew_code(n.kind);
+        ins.a = int8_t(regs[0]);
+        ins.b = int8_t(regs.size() > 1 ? regs[1] : regs[0]);
+        ins.dst = int8_t(EW_MAX_IN + sp.prog.size());
+        sp.prog.push_back(ins);
+        members.push_back(n.id);
+        reg = ins.dst;
+        return true;
     };
 
     // ---- fusion pre-pass (graph structure only, so virtual and materialised
@@ -389,6 +505,63 @@ void Executor::prepare(bool dry) {
         }
     }
 
+    // elementwise trees: roots in reverse topological order; a root whose tree
+    // does not fit one program runs alone and its children become roots
+    struct EwTree {
+        EwSpec spec;
+        std::vector<std::string> in_names, members;
+        int reg = 0;
+    };
+    std::map<std::string, EwTree> ew_trees;
+    {
+        std::set<std::string> in_tree;
+        auto fusable_up = [&](const OpNode& n) {
+            // n's output feeds a single elementwise consumer of the same shape
+            const std::string& o = n.outputs[0];
+            auto cs = g_.consumers(o);
+            return opt_.fuse && g_.tensor(o).kind == TensorKind::Intermediate && cs.size() == 1 &&
+                   is_ew(cs[0]->kind) && !absorbed.count(cs[0]->id) && g_.tensor(cs[0]->outputs[0]).shape == g_.tensor(o).shape;
+        };
+        std::function<void(const OpNode&)> make_root = [&](const OpNode& n) {
+            EwTree t;
+            if (build_tree(n, t.spec, t.in_names, t.members, t.reg)) {
+                for (const auto& m : t.members) in_tree.insert(m);
+                ew_trees[n.id] = std::move(t);
+                return;
+            }
+            // fallback: n alone; each fusable child roots its own tree
+            EwTree single;
+            for (const auto& in : n.inputs) single.in_names.push_back(in);
+            EwInstr ins{};
+            ins.op = ew_code(n.kind);
+            ins.a = 0;
+            ins.b = int8_t(n.inputs.size() > 1 ? 1 : 0);
+            ins.dst = int8_t(EW_MAX_IN);
+            single.spec.prog = {ins};
+            single.reg = EW_MAX_IN;
+            single.members = {n.id};
+            in_tree.insert(n.id);
+            ew_trees[n.id] = std::move(single);
+            for (const auto& in : n.inputs) {
+                const OpNode* pr = g_.producer(in);
+                if (pr && is_ew(pr->kind) && !absorbed.count(pr->id) && !in_tree.count(pr->id)) make_root(*pr);
+            }
+        };
+        const auto& order = g_.topo_order();
+        for (auto it = order.rbegin(); it != order.rend(); ++it) {
+            const OpNode& n = g_.nodes()[size_t(*it)];
+            if (!is_ew(n.kind) || absorbed.count(n.id) || in_tree.count(n.id)) continue;
+            if (fusable_up(n)) continue;  // will be reached from its consumer's tree
+            make_root(n);
+        }
+        // anything fusable_up whose consumer did not take it (should not happen) runs alone
+        for (const auto& n : g_.nodes())
+            if (is_ew(n.kind) && !absorbed.count(n.id) && !in_tree.count(n.id)) make_root(n);
+        for (const auto& [root, t] : ew_trees)
+            for (const auto& m : t.members)
+                if (m != root) absorbed.insert(m);
+    }
+
     for (int ni : g_.topo_order()) {
         const OpNode& n = g_.nodes()[size_t(ni)];
         if (absorbed.count(n.id)) continue;
@@ -420,14 +593,17 @@ void Executor::prepare(bool dry) {
         switch (n.kind) {
             case OpKind::Add:
             case OpKind::Mul:
-                eltwise(n.id, n.kind == OpKind::Add ? EwOp::Add : EwOp::Mul, dt, o0.shape, map_of(n.outputs[0]),
-                        &map_of(n.inputs[0]), &map_of(n.inputs[1]));
-                break;
             case OpKind::SiLU:
-            case OpKind::GELU:
-                eltwise(n.id, n.kind == OpKind::SiLU ? EwOp::SiLU : EwOp::GELU, dt, o0.shape, map_of(n.outputs[0]),
-                        &map_of(n.inputs[0]), nullptr);
+            case OpKind::GELU: {
+                EwTree& t = ew_trees.at(n.id);
+                EwSpec sp = t.spec;
+                for (const auto& name : t.in_names) sp.ins.push_back(&map_of(name));
+                sp.result = t.reg;
+                std::string label;
+                for (const auto& m : t.members) label += (label.empty() ? "" : "+") + m;
+                eltwise(label, sp, dt, o0.shape, map_of(n.outputs[0]));
                 break;
+            }
             case OpKind::AllReduce:
                 // single-rank execution: the sum over one rank is the identity
                 copy_checked(n.id, dt, o0.shape, map_of(n.outputs[0]), map_of(n.inputs[0]));
@@ -463,7 +639,7 @@ void Executor::prepare(bool dry) {
                 int rank = int(A.shape.size());
                 int64_t M = A.shape[size_t(rank - 2)], K = A.shape[size_t(rank - 1)], N = B.shape[size_t(rank - 1)];
                 if (gemv_eligible(n)) {
-                    auto L = std::make_unique<LaunchT<GemvParams, launch_gemv>>();
+                    auto L = std::make_unique<LaunchT<GemvParams, launch_gemv_any>>();
                     L->node = n.id;
                     L->kernel = "gemv_bf16";
                     GemvParams& p = L->p;
@@ -476,35 +652,75 @@ void Executor::prepare(bool dry) {
                     if (fit != fusion.end()) f = fit->second;
                     if (f.norm) {
                         p.prologue = GemvPrologue::RMSNorm;
-                        p.a = operand(map_of(f.norm->inputs[0]), 1, 1, es);
-                        p.normw = operand(map_of(f.norm->inputs[1]), 0, 1, es);
+                        p.a = operand(map_of(f.norm->inputs[0]), 1, K, es);
+                        p.normw = operand(map_of(f.norm->inputs[1]), 0, K, es);
                         p.eps = float(std::get<NormAttrs>(f.norm->attrs).eps);
                         L->node = f.norm->id + "+" + n.id;
                     } else if (f.silu) {
                         p.prologue = GemvPrologue::SiLUMul;
                         const std::string& sg = f.silu->outputs[0];
                         const std::string& other = f.mul->inputs[0] == sg ? f.mul->inputs[1] : f.mul->inputs[0];
-                        p.a = operand(map_of(f.silu->inputs[0]), 1, 1, es);
-                        p.a2 = operand(map_of(other), 1, 1, es);
+                        p.a = operand(map_of(f.silu->inputs[0]), 1, K, es);
+                        p.a2 = operand(map_of(other), 1, K, es);
                         L->node = f.silu->id + "+" + f.mul->id + "+" + n.id;
                     } else {
-                        p.a = operand(map_of(n.inputs[0]), 1, 1, es);
+                        p.a = operand(map_of(n.inputs[0]), 1, K, es);
                     }
                     if (f.add) {
                         const std::string& other =
                             f.add->inputs[0] == n.outputs[0] ? f.add->inputs[1] : f.add->inputs[0];
                         p.has_res = 1;
-                        p.res = operand(map_of(other), 1, 1, es);
-                        p.c = operand(map_of(f.add->outputs[0]), 1, 1, es);
+                        p.res = operand(map_of(other), 1, 256, es);
+                        p.c = operand(map_of(f.add->outputs[0]), 1, 256, es);
                         L->node += "+" + f.add->id;
                     } else {
-                        p.c = operand(map_of(n.outputs[0]), 1, 1, es);
+                        p.c = operand(map_of(n.outputs[0]), 1, 256, es);
                     }
                     const VMap& bm = map_of(n.inputs[1]);
                     const VPiece& bp = bm.pieces()[0];
                     TargetInfo bt = target(bp.target);
                     p.b_base = reinterpret_cast<const char*>(bt.ptr) + bp.off.c0 * es;
                     p.b_sk = *VMap::tile_stride(bp, 0, K);
+                    // persistent TMA-fed variant: one CTA per SM, balanced (strip, k-tile) ranges
+                    int tma_stages = 0;
+                    for (int st = 6; st >= 3; --st)
+                        if (gemv_tma_smem(M, K, st) <= 220 * 1024) {
+                            tma_stages = st;
+                            break;
+                        }
+                    if (M <= 4 && tma_stages > 0 && opt_.gemv_tma) {
+                        L->kernel = "gemv_tma_bf16";
+                        int sms = 148;
+                        if (!impl_->dry) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+                        int64_t strips = (N + 255) / 256, kts = (K + 63) / 64, units = strips * kts;
+                        int grid = int(std::min<int64_t>(sms, units));
+                        std::vector<int32_t> first(size_t(strips), -1), count(size_t(strips), 0);
+                        for (int c = 0; c < grid; ++c) {
+                            int64_t ub = units * c / grid, ue = units * (c + 1) / grid;
+                            for (int64_t u = ub; u < ue; u = (u / kts + 1) * kts) {
+                                int64_t s2 = u / kts;
+                                if (first[size_t(s2)] < 0) first[size_t(s2)] = c;
+                                ++count[size_t(s2)];
+                            }
+                        }
+                        int maxc = *std::max_element(count.begin(), count.end());
+                        p.tma = 1;
+                        p.stages = tma_stages;
+                        p.grid = grid;
+                        p.max_contrib = maxc;
+                        p.work = static_cast<float*>(impl_->alloc(size_t(strips * maxc * M * 256) * sizeof(float), false));
+                        p.counters = static_cast<unsigned*>(impl_->alloc(size_t(strips) * sizeof(unsigned), true));
+                        auto* dfirst = static_cast<int32_t*>(impl_->alloc(size_t(strips) * 4, false));
+                        auto* dcount = static_cast<int32_t*>(impl_->alloc(size_t(strips) * 4, false));
+                        if (!impl_->dry) {
+                            ck(cudaMemcpy(dfirst, first.data(), size_t(strips) * 4, cudaMemcpyHostToDevice), "H2D");
+                            ck(cudaMemcpy(dcount, count.data(), size_t(strips) * 4, cudaMemcpyHostToDevice), "H2D");
+                        }
+                        p.strip_first = dfirst;
+                        p.strip_count = dcount;
+                        push(std::move(L));
+                        break;
+                    }
                     // grid: 256-column strips x K splits, ~3 CTAs per SM
                     int64_t ntiles = (N + 255) / 256;
                     int64_t want = (148 * 3 + ntiles - 1) / ntiles;
@@ -623,6 +839,24 @@ void Executor::prepare(bool dry) {
                 throw UnsupportedError(std::string("no kernel for operator ") + to_string(n.kind));
         }
     }
+    // all parameter blocks in one device allocation, uploaded once
+    if (!dry) {
+        size_t total = 0;
+        std::vector<size_t> offs;
+        for (auto& l : impl_->launches) {
+            offs.push_back(total);
+            total += (l->param_bytes() + 255) / 256 * 256;
+        }
+        if (total) {
+            auto* base = static_cast<char*>(impl_->alloc(total, false));
+            std::vector<char> host(total);
+            for (size_t i = 0; i < impl_->launches.size(); ++i) {
+                std::memcpy(host.data() + offs[i], impl_->launches[i]->host_params(), impl_->launches[i]->param_bytes());
+                impl_->launches[i]->set_device_params(base + offs[i]);
+            }
+            ck(cudaMemcpy(base, host.data(), total, cudaMemcpyHostToDevice), "H2D(params)");
+        }
+    }
     prepared_ = !dry;
 }
 
@@ -647,6 +881,36 @@ void Executor::run_graph(void* stream) {
         ck(cudaGraphInstantiate(&impl_->gexec, impl_->graph, 0), "cudaGraphInstantiate");
     }
     ck(cudaGraphLaunch(impl_->gexec, s), "cudaGraphLaunch");
+}
+
+void Executor::run_timed(void* stream, float* ms, int n) {
+    // Launches with an event between each, captured into a CUDA graph so the
+    // per-launch intervals contain no host launch gaps.
+    if (!prepared_) prepare();
+    auto s = static_cast<cudaStream_t>(stream);
+    size_t L = impl_->launches.size();
+    std::vector<cudaEvent_t> ev(L + 1);
+    for (auto& e : ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+    cudaStream_t cap;
+    ck(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    ck(cudaEventRecordWithFlags(ev[0], cap, cudaEventRecordExternal), "cudaEventRecord");
+    for (size_t i = 0; i < L; ++i) {
+        impl_->launches[i]->run(cap);
+        ck(cudaEventRecordWithFlags(ev[i + 1], cap, cudaEventRecordExternal), "cudaEventRecord");
+    }
+    cudaGraph_t graph;
+    cudaError_t e = cudaStreamEndCapture(cap, &graph);
+    cudaStreamDestroy(cap);
+    ck(e, "cudaStreamEndCapture");
+    cudaGraphExec_t gexec;
+    ck(cudaGraphInstantiate(&gexec, graph, 0), "cudaGraphInstantiate");
+    ck(cudaGraphLaunch(gexec, s), "cudaGraphLaunch");
+    ck(cudaStreamSynchronize(s), "sync");
+    for (size_t i = 0; i < L && int(i) < n; ++i) ck(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]), "elapsed");
+    cudaGraphExecDestroy(gexec);
+    cudaGraphDestroy(graph);
+    for (auto& x : ev) cudaEventDestroy(x);
 }
 
 void Executor::upload(const std::string& id, const void* host, int64_t bytes, void* stream) {
@@ -687,19 +951,21 @@ void Executor::download(const std::string& id, void* host, int64_t bytes, void* 
     p.rank = rank;
     for (int i = 0; i < rank; ++i) p.shape[i] = int32_t(t.shape[size_t(i)]);
     p.vec = 1;
-    p.op = EwOp::Copy;
+    p.copy_only = 1;
     p.dt = kdt(t.dtype);
     p.esize = int32_t(es);
     p.nvec = t.elems();
     p.nin = 1;
     p.out.m = lower_map(VMap::identity(tmp_id, t.shape), target);
     finish_operand(p.out, rank - 1, 1, es);
-    p.a.m = lower_map(m, target);
-    finish_operand(p.a, rank - 1, 1, es);
-    launch_eltwise(p, s);
+    p.in[0].m = lower_map(m, target);
+    finish_operand(p.in[0], rank - 1, 1, es);
+    EwParams* dp = upload_params(p);
+    launch_eltwise(p, dp, s);
     cudaError_t e = cudaMemcpyAsync(host, tmp, size_t(bytes), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaFree(tmp);
+    cudaFree(dp);
     ck(e, "download");
 }
 

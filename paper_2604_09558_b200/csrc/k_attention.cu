@@ -27,7 +27,8 @@ template <typename T>
 __device__ __forceinline__ float ldf(const T* p) { return float(dev::to_acc<T>(*p)); }
 
 template <typename T>
-__global__ void __launch_bounds__(NT) attn_kernel(const __grid_constant__ AttnParams p) {
+__global__ void __launch_bounds__(NT) attn_kernel(const AttnParams* __restrict__ pp) {
+    const AttnParams& p = *pp;
     __shared__ float sQ[MAXG][MAXD];
     __shared__ float sP[MAXG][TK];
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -230,7 +231,8 @@ __global__ void __launch_bounds__(NT) attn_kernel(const __grid_constant__ AttnPa
 }
 
 template <typename T>
-__global__ void __launch_bounds__(NT) combine_kernel(const __grid_constant__ AttnParams p) {
+__global__ void __launch_bounds__(NT) combine_kernel(const AttnParams* __restrict__ pp) {
+    const AttnParams& p = *pp;
     // one CTA per (lead, h, sq) row
     const int64_t row = blockIdx.x;
     const int r = p.rank;
@@ -267,21 +269,21 @@ __global__ void __launch_bounds__(NT) combine_kernel(const __grid_constant__ Att
 }
 
 template <typename T>
-void launch_t(const AttnParams& p, cudaStream_t s) {
+void launch_t(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
     int64_t qblocks = int64_t(p.Bt) * (p.H / p.group) * p.Sq;
     dim3 grid(unsigned(qblocks), unsigned(p.splits));
     size_t smem = size_t(TK) * size_t(p.D + 8 + p.Dv + 8) * sizeof(T);
     if (smem > 48 * 1024) cudaFuncSetAttribute(attn_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attn_kernel<T><<<grid, NT, smem, s>>>(p);
-    if (p.splits > 1) combine_kernel<T><<<unsigned(int64_t(p.Bt) * p.H * p.Sq), NT, 0, s>>>(p);
+    attn_kernel<T><<<grid, NT, smem, s>>>(dp);
+    if (p.splits > 1) combine_kernel<T><<<unsigned(int64_t(p.Bt) * p.H * p.Sq), NT, 0, s>>>(dp);
 }
 
 }  // namespace
 
-void launch_attention(const AttnParams& p, cudaStream_t s) {
+void launch_attention(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
     switch (p.dt) {
-        case KDType::BF16: launch_t<bf16>(p, s); break;
-        case KDType::F32: launch_t<float>(p, s); break;
+        case KDType::BF16: launch_t<bf16>(p, dp, s); break;
+        case KDType::F32: launch_t<float>(p, dp, s); break;
         default: break;
     }
 }

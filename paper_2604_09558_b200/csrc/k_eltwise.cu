@@ -114,71 +114,71 @@ __device__ __forceinline__ int64_t add_of<int64_t>(int64_t a, int64_t b) {
     return (int64_t)((uint64_t)a + (uint64_t)b);
 }
 
-template <typename T, EwOp OP, int VEC>
-__global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParams p) {
-    const int last = p.rank - 1;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < p.nvec; v += (int64_t)gridDim.x * blockDim.x) {
-        int32_t idx[VTC_MAX_RANK];
-        dev::unflatten(v * VEC, p.shape, p.rank, idx);
-#pragma unroll
-        for (int a = 0; a < VTC_MAX_RANK; ++a) idx[a] += p.origin[a];
-        T a[VEC], b[VEC], o[VEC];
-        load_vec<T, VEC>(p.a, idx, last, a);
-        if (OP == EwOp::Add || OP == EwOp::Mul || OP == EwOp::SiLUMul) load_vec<T, VEC>(p.b, idx, last, b);
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-            if constexpr (OP == EwOp::Copy) o[j] = a[j];
-            else if constexpr (OP == EwOp::Add) o[j] = add_of<T>(a[j], b[j]);
-            else if constexpr (OP == EwOp::Mul) o[j] = mul_of<T>(a[j], b[j]);
-            else if constexpr (OP == EwOp::SiLU) o[j] = silu_of<T>(a[j]);
-            else if constexpr (OP == EwOp::GELU) o[j] = gelu_of<T>(a[j]);
-            else o[j] = mul_of<T>(silu_of<T>(a[j]), b[j]);
-        }
-        store_vec<T, VEC>(p.out, idx, last, o);
+template <typename T>
+__device__ __forceinline__ T apply_op(EwOp op, T a, T b) {
+    switch (op) {
+        case EwOp::Add: return add_of<T>(a, b);
+        case EwOp::Mul: return mul_of<T>(a, b);
+        case EwOp::SiLU: return silu_of<T>(a);
+        case EwOp::GELU: return gelu_of<T>(a);
+        default: return a;
     }
 }
 
-template <typename T, EwOp OP>
-void launch_t(const EwParams& p, cudaStream_t s) {
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) ew_kernel(const EwParams* __restrict__ pp) {
+    const EwParams& p = *pp;
+    const int last = p.rank - 1;
+    const int nin = p.nin, nprog = p.nprog;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < p.nvec; v += (int64_t)gridDim.x * blockDim.x) {
+        int32_t idx[VTC_MAX_RANK];
+        dev::unflatten(v * VEC, p.shape, p.rank, idx);
+#pragma unroll 1
+        for (int a = 0; a < p.rank; ++a) idx[a] += p.origin[a];
+        T r[EW_MAX_PROG + EW_MAX_IN][VEC];
+#pragma unroll 1
+        for (int i = 0; i < nin; ++i) load_vec<T, VEC>(p.in[i], idx, last, r[i]);
+        if (nprog > 0) {
+#pragma unroll 1
+            for (int s = 0; s < nprog; ++s) {
+                const EwInstr ins = p.prog[s];
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) r[ins.dst][j] = apply_op<T>(ins.op, r[ins.a][j], r[ins.b][j]);
+            }
+        }
+        store_vec<T, VEC>(p.out, idx, last, r[p.result]);
+    }
+}
+
+template <typename T>
+void launch_t(const EwParams& p, const EwParams* dp, cudaStream_t s) {
     constexpr int V = 16 / sizeof(T);
     int64_t blocks = (p.nvec + 255) / 256;
     int grid = int(blocks < 148 * 16 ? blocks : 148 * 16);
     if (grid < 1) grid = 1;
     if (p.vec == V)
-        ew_kernel<T, OP, V><<<grid, 256, 0, s>>>(p);
+        ew_kernel<T, V><<<grid, 256, 0, s>>>(dp);
     else
-        ew_kernel<T, OP, 1><<<grid, 256, 0, s>>>(p);
-}
-
-template <typename T>
-void launch_op(const EwParams& p, cudaStream_t s) {
-    switch (p.op) {
-        case EwOp::Copy: launch_t<T, EwOp::Copy>(p, s); break;
-        case EwOp::Add: launch_t<T, EwOp::Add>(p, s); break;
-        case EwOp::Mul: launch_t<T, EwOp::Mul>(p, s); break;
-        case EwOp::SiLU: launch_t<T, EwOp::SiLU>(p, s); break;
-        case EwOp::GELU: launch_t<T, EwOp::GELU>(p, s); break;
-        case EwOp::SiLUMul: launch_t<T, EwOp::SiLUMul>(p, s); break;
-    }
+        ew_kernel<T, 1><<<grid, 256, 0, s>>>(dp);
 }
 
 }  // namespace
 
-void launch_eltwise(const EwParams& p, cudaStream_t s) {
+void launch_eltwise(const EwParams& p, const EwParams* dp, cudaStream_t s) {
     if (p.nvec == 0) return;
-    if (p.op == EwOp::Copy) {
+    if (p.copy_only) {
         // copies are dtype-agnostic: dispatch on element size
         switch (p.esize) {
-            case 8: launch_op<int64_t>(p, s); return;
-            case 4: launch_op<float>(p, s); return;
-            case 2: launch_op<bf16>(p, s); return;
+            case 8: launch_t<int64_t>(p, dp, s); return;
+            case 4: launch_t<float>(p, dp, s); return;
+            case 2: launch_t<bf16>(p, dp, s); return;
         }
     }
     switch (p.dt) {
-        case KDType::F64: launch_op<double>(p, s); break;
-        case KDType::F32: launch_op<float>(p, s); break;
-        case KDType::I64: launch_op<int64_t>(p, s); break;
-        case KDType::BF16: launch_op<bf16>(p, s); break;
+        case KDType::F64: launch_t<double>(p, dp, s); break;
+        case KDType::F32: launch_t<float>(p, dp, s); break;
+        case KDType::I64: launch_t<int64_t>(p, dp, s); break;
+        case KDType::BF16: launch_t<bf16>(p, dp, s); break;
     }
 }
 

@@ -31,7 +31,8 @@ __device__ __forceinline__ float load_bf16_at(const VOperand& op, int32_t (&idx)
 }
 
 template <int MT, int U>
-__global__ void __launch_bounds__(NT) gemv_kernel(const __grid_constant__ GemvParams p) {
+__global__ void __launch_bounds__(NT) gemv_kernel(const GemvParams* __restrict__ pp) {
+    const GemvParams& p = *pp;
     extern __shared__ float sA[];  // [M][kchunk]
     __shared__ float red[WARPS][COLS];
     __shared__ float s_rs[16];
@@ -46,31 +47,73 @@ __global__ void __launch_bounds__(NT) gemv_kernel(const __grid_constant__ GemvPa
     const int M = int(p.M);
 
     // ---- prologue: A rows -> shared memory (fp32), with fused transforms ----
+    // Row origins are evaluated once through the maps; elements step with the
+    // per-piece stride along K (host-proved affine over whole rows).
+    auto row_ptr = [&](const VOperand& op, int m, int64_t k0, int64_t& stride) -> const bf16* {
+        int32_t idx[VTC_MAX_RANK] = {};
+        idx[0] = m;
+        idx[1] = int32_t(k0);
+        dev::Loc l = dev::locate(op.m, idx);
+        stride = op.fast_stride[l.piece];
+        return dev::addr<bf16>(op.m, l);
+    };
+    auto a_at = [&](const VOperand& op, int m, int64_t k) -> float {
+        if (op.fast_ok) {
+            int64_t st;
+            const bf16* b0 = row_ptr(op, m, 0, st);
+            return __bfloat162float(b0[k * st]);
+        }
+        int32_t idx[VTC_MAX_RANK] = {};
+        idx[0] = m;
+        idx[1] = int32_t(k);
+        return load_bf16_at(op, idx);
+    };
     if (p.prologue == GemvPrologue::RMSNorm) {
         for (int m = 0; m < M; ++m) {
-            float ss = block_sumsq_row_bf16(p.a, m, p.K);
+            float ss;
+            if (p.a.fast_ok) {
+                int64_t st;
+                const bf16* b0 = row_ptr(p.a, m, 0, st);
+                ss = block_sum_256<float>([&](int64_t k) { float v = __bfloat162float(b0[k * st]); return v * v; }, p.K);
+            } else {
+                ss = block_sumsq_row_bf16(p.a, m, p.K);
+            }
             if (tid == 0) s_rs[m] = rsqrtf(ss / float(p.K) + p.eps);
         }
         __syncthreads();
     }
-    for (int e = tid; e < M * klen; e += NT) {
-        int m = e / klen;
-        int64_t k = kb + e % klen;
-        int32_t idx[VTC_MAX_RANK] = {};
-        idx[0] = m;
-        idx[1] = int32_t(k);
-        float v = load_bf16_at(p.a, idx);
-        if (p.prologue == GemvPrologue::SiLUMul) {
-            float u = load_bf16_at(p.a2, idx);
-            float sg = __bfloat162float(__float2bfloat16_rn(v / (1.0f + expf(-v))));
-            v = __bfloat162float(__float2bfloat16_rn(sg * u));
-        } else if (p.prologue == GemvPrologue::RMSNorm) {
+    for (int m = 0; m < M; ++m) {
+        int64_t sa = 0, sa2 = 0, sw = 0;
+        const bf16* pa = p.a.fast_ok ? row_ptr(p.a, m, kb, sa) : nullptr;
+        const bf16* pa2 = (p.prologue == GemvPrologue::SiLUMul && p.a2.fast_ok) ? row_ptr(p.a2, m, kb, sa2) : nullptr;
+        const bf16* pw = nullptr;
+        if (p.prologue == GemvPrologue::RMSNorm && p.normw.fast_ok) {
             int32_t widx[VTC_MAX_RANK] = {};
-            widx[0] = int32_t(k);
-            float w = load_bf16_at(p.normw, widx);
-            v = __bfloat162float(__float2bfloat16_rn(v * s_rs[m] * w));
+            widx[0] = int32_t(kb);
+            dev::Loc l = dev::locate(p.normw.m, widx);
+            sw = p.normw.fast_stride[l.piece];
+            pw = dev::addr<bf16>(p.normw.m, l);
         }
-        sA[e] = v;
+        for (int e = tid; e < klen; e += NT) {
+            int64_t k = kb + e;
+            float v = pa ? __bfloat162float(pa[e * sa]) : a_at(p.a, m, k);
+            if (p.prologue == GemvPrologue::SiLUMul) {
+                float u = pa2 ? __bfloat162float(pa2[e * sa2]) : a_at(p.a2, m, k);
+                float sg = __bfloat162float(__float2bfloat16_rn(v / (1.0f + expf(-v))));
+                v = __bfloat162float(__float2bfloat16_rn(sg * u));
+            } else if (p.prologue == GemvPrologue::RMSNorm) {
+                float w;
+                if (pw) {
+                    w = __bfloat162float(pw[e * sw]);
+                } else {
+                    int32_t widx[VTC_MAX_RANK] = {};
+                    widx[0] = int32_t(k);
+                    w = load_bf16_at(p.normw, widx);
+                }
+                v = __bfloat162float(__float2bfloat16_rn(v * s_rs[m] * w));
+            }
+            sA[m * klen + e] = v;
+        }
     }
     __syncthreads();
 
@@ -151,6 +194,7 @@ __global__ void __launch_bounds__(NT) gemv_kernel(const __grid_constant__ GemvPa
     }
     if (n >= p.N) return;
     // ---- epilogue: C = bf16(acc) [+ residual, rounded like an unfused Add] ----
+    // strip origins evaluated once per row; columns step with the piece stride
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
         if (m >= M) continue;
@@ -158,27 +202,43 @@ __global__ void __launch_bounds__(NT) gemv_kernel(const __grid_constant__ GemvPa
         idx[0] = m;
         idx[1] = int32_t(n);
         bf16 c = __float2bfloat16_rn(outv[m]);
-        if (p.has_res) c = __float2bfloat16_rn(__bfloat162float(c) + load_bf16_at(p.res, idx));
-        *dev::elem_ptr<bf16>(p.c.m, idx) = c;
+        if (p.has_res) {
+            float r;
+            if (p.res.fast_ok) {
+                int64_t st;
+                const bf16* r0 = row_ptr(p.res, m, n0, st);
+                r = __bfloat162float(r0[int64_t(tid) * st]);
+            } else {
+                r = load_bf16_at(p.res, idx);
+            }
+            c = __float2bfloat16_rn(__bfloat162float(c) + r);
+        }
+        if (p.c.fast_ok) {
+            int64_t st;
+            bf16* c0 = const_cast<bf16*>(row_ptr(p.c, m, n0, st));
+            c0[int64_t(tid) * st] = c;
+        } else {
+            *dev::elem_ptr<bf16>(p.c.m, idx) = c;
+        }
     }
 }
 
 template <int MT, int U>
-void launch_mt(const GemvParams& p, cudaStream_t s) {
+void launch_mt(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
     dim3 grid(unsigned((p.N + COLS - 1) / COLS), unsigned(p.ksplit));
     size_t smem = size_t(p.M) * size_t(p.kchunk) * sizeof(float);
     if (smem > 48 * 1024) cudaFuncSetAttribute(gemv_kernel<MT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    gemv_kernel<MT, U><<<grid, NT, smem, s>>>(p);
+    gemv_kernel<MT, U><<<grid, NT, smem, s>>>(dp);
 }
 
 }  // namespace
 
-void launch_gemv(const GemvParams& p, cudaStream_t s) {
-    if (p.M <= 1) launch_mt<1, 8>(p, s);
-    else if (p.M <= 2) launch_mt<2, 8>(p, s);
-    else if (p.M <= 4) launch_mt<4, 4>(p, s);
-    else if (p.M <= 8) launch_mt<8, 4>(p, s);
-    else launch_mt<16, 2>(p, s);
+void launch_gemv(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
+    if (p.M <= 1) launch_mt<1, 8>(p, dp, s);
+    else if (p.M <= 2) launch_mt<2, 8>(p, dp, s);
+    else if (p.M <= 4) launch_mt<4, 4>(p, dp, s);
+    else if (p.M <= 8) launch_mt<8, 4>(p, dp, s);
+    else launch_mt<16, 2>(p, dp, s);
 }
 
 }  // namespace vtc

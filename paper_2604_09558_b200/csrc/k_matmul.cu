@@ -76,7 +76,8 @@ __device__ __forceinline__ A mac(A acc, A a, A b, bool exact) {
 }
 
 template <typename T, bool EXACT>
-__global__ void __launch_bounds__(NT) mm_kernel(const __grid_constant__ MatmulParams p) {
+__global__ void __launch_bounds__(NT) mm_kernel(const MatmulParams* __restrict__ pp) {
+    const MatmulParams& p = *pp;
     using A = typename dev::Acc<T>::type;
     __shared__ A As[2][BK][BM + 4];
     __shared__ A Bs[2][BK][BN + 4];
@@ -190,22 +191,22 @@ __global__ void __launch_bounds__(NT) mm_kernel(const __grid_constant__ MatmulPa
 
 }  // namespace
 
-void launch_matmul(const MatmulParams& p, cudaStream_t s) {
+void launch_matmul(const MatmulParams& p, const MatmulParams* dp, cudaStream_t s) {
     dim3 grid(unsigned((p.N + BN - 1) / BN), unsigned((p.M + BM - 1) / BM), unsigned(p.batch));
     // exact: separate multiply and add roundings, k ascending -- bit-identical to
     // the reference's `acc += a * b` loop (executor.cpp:245) for f32 / f64.
     const bool ex = p.exact != 0;
     switch (p.dt) {
         case KDType::F64:
-            if (ex) mm_kernel<double, true><<<grid, NT, 0, s>>>(p);
-            else mm_kernel<double, false><<<grid, NT, 0, s>>>(p);
+            if (ex) mm_kernel<double, true><<<grid, NT, 0, s>>>(dp);
+            else mm_kernel<double, false><<<grid, NT, 0, s>>>(dp);
             break;
         case KDType::F32:
-            if (ex) mm_kernel<float, true><<<grid, NT, 0, s>>>(p);
-            else mm_kernel<float, false><<<grid, NT, 0, s>>>(p);
+            if (ex) mm_kernel<float, true><<<grid, NT, 0, s>>>(dp);
+            else mm_kernel<float, false><<<grid, NT, 0, s>>>(dp);
             break;
-        case KDType::I64: mm_kernel<int64_t, true><<<grid, NT, 0, s>>>(p); break;
-        case KDType::BF16: mm_kernel<bf16, false><<<grid, NT, 0, s>>>(p); break;
+        case KDType::I64: mm_kernel<int64_t, true><<<grid, NT, 0, s>>>(dp); break;
+        case KDType::BF16: mm_kernel<bf16, false><<<grid, NT, 0, s>>>(dp); break;
     }
 }
 

@@ -49,7 +49,8 @@ struct RowIO {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(256) row_kernel(const __grid_constant__ RowParams p) {
+__global__ void __launch_bounds__(256) row_kernel(const RowParams* __restrict__ pp) {
+    const RowParams& p = *pp;
     using A = std::conditional_t<std::is_same_v<T, double>, double, float>;
     const int last = p.rank - 1;
     for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
@@ -89,13 +90,13 @@ __global__ void __launch_bounds__(256) row_kernel(const __grid_constant__ RowPar
 
 }  // namespace
 
-void launch_rowop(const RowParams& p, cudaStream_t s) {
+void launch_rowop(const RowParams& p, const RowParams* dp, cudaStream_t s) {
     if (p.rows == 0) return;
     int grid = int(p.rows < 148 * 8 ? p.rows : 148 * 8);
     switch (p.dt) {
-        case KDType::F64: row_kernel<double><<<grid, 256, 0, s>>>(p); break;
-        case KDType::F32: row_kernel<float><<<grid, 256, 0, s>>>(p); break;
-        case KDType::BF16: row_kernel<bf16><<<grid, 256, 0, s>>>(p); break;
+        case KDType::F64: row_kernel<double><<<grid, 256, 0, s>>>(dp); break;
+        case KDType::F32: row_kernel<float><<<grid, 256, 0, s>>>(dp); break;
+        case KDType::BF16: row_kernel<bf16><<<grid, 256, 0, s>>>(dp); break;
         default: break;
     }
 }

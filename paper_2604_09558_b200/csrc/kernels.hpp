@@ -1,5 +1,10 @@
 // Kernel parameter blocks and host-side launchers (sm_100a).
 //
+// Parameter blocks live in device memory (uploaded once when a plan is
+// prepared); kernels receive one pointer.  Passing the multi-KB descriptor
+// blocks as __grid_constant__ launch parameters cost ~20 us of front-end time
+// per launch on B200 (measured with ncu), more than the kernels themselves.
+//
 // Every operand of every kernel is a VOperand: the lowered virtual-tensor map
 // plus host-derived facts about it along the kernel's fast (contiguous) axis.
 // Kernels evaluate the map at row / tile / vector origins and step with the
@@ -26,21 +31,35 @@ struct VOperand {
 };
 
 // ---- elementwise / copy --------------------------------------------------
-enum class EwOp : int32_t { Copy = 0, Add, Mul, SiLU, GELU, SiLUMul };
+enum class EwOp : int32_t { Copy = 0, Add, Mul, SiLU, GELU };
+
+// One step of a fused elementwise program: r[dst] = op(r[a], r[b]).
+// Registers 0..nin-1 hold the inputs; every result is rounded to the tensor
+// dtype, so a fused chain reproduces the unfused ops bit for bit.
+struct EwInstr {
+    EwOp op;
+    int8_t dst, a, b, pad;
+};
+constexpr int EW_MAX_IN = 4, EW_MAX_PROG = 8;
 
 struct EwParams {
-    VOperand out, a, b;
+    VOperand out;
+    VOperand in[EW_MAX_IN];
     int32_t rank;
     int32_t shape[VTC_MAX_RANK];   // iteration box extents
     int32_t origin[VTC_MAX_RANK];  // iteration box origin (virtual index of element 0)
-    int32_t vec;       // elements per thread-vector along the last axis
+    int32_t vec;                   // elements per thread-vector along the last axis
     int32_t nin;
-    int64_t nvec;      // number of vectors
-    EwOp op;
+    int32_t nprog;
+    int32_t result;                // register holding the output
+    EwInstr prog[EW_MAX_PROG];
+    int64_t nvec;                  // number of vectors
     KDType dt;
     int32_t esize;
+    int32_t copy_only;             // pure data movement: dtype-agnostic by element size
+    int32_t pad;
 };
-void launch_eltwise(const EwParams& p, cudaStream_t s);
+void launch_eltwise(const EwParams& p, const EwParams* dp, cudaStream_t s);
 
 // ---- generic batched matmul (any dtype, any maps) -----------------------
 struct MatmulParams {
@@ -54,7 +73,7 @@ struct MatmulParams {
     KDType dt;
     int32_t exact;  // f32/f64: unfused multiply-add, bit-identical to the CPU reference
 };
-void launch_matmul(const MatmulParams& p, cudaStream_t s);
+void launch_matmul(const MatmulParams& p, const MatmulParams* dp, cudaStream_t s);
 
 // ---- weight-streaming GEMV for bf16 decode (M <= 16) ----------------------
 // C[m,n] (+)= prologue(A)[m,:] . B[:,n] ; B is a physical (single-piece affine)
@@ -72,10 +91,16 @@ struct GemvParams {
     int32_t has_res;
     float eps;
     int32_t pad;
-    float* work;                    // [ksplit, M, N] partials
+    float* work;                    // [ksplit, M, N] partials   (TMA variant: [strips, max_contrib, M, 256])
     unsigned int* counters;         // [ceil(N / 256)] arrival counters (self-resetting)
+    // persistent TMA variant
+    int32_t stages, grid, max_contrib, tma;
+    const int32_t* strip_first;     // first CTA touching each 256-column strip
+    const int32_t* strip_count;     // number of CTAs touching it
 };
-void launch_gemv(const GemvParams& p, cudaStream_t s);
+void launch_gemv(const GemvParams& p, const GemvParams* dp, cudaStream_t s);
+void launch_gemv_tma(const GemvParams& p, const GemvParams* dp, cudaStream_t s);
+size_t gemv_tma_smem(int64_t M, int64_t K, int stages);
 
 // ---- row-wise normalisations / softmax -----------------------------------
 enum class RowOp : int32_t { RMSNorm = 0, LayerNorm, Softmax };
@@ -89,7 +114,7 @@ struct RowParams {
     KDType dt;
     int32_t pad;
 };
-void launch_rowop(const RowParams& p, cudaStream_t s);
+void launch_rowop(const RowParams& p, const RowParams* dp, cudaStream_t s);
 
 // ---- attention (split-KV flash decoding with GQA head grouping) ----------
 struct AttnParams {
@@ -106,6 +131,6 @@ struct AttnParams {
     float* part_o;                 // [Bt, H, Sq, splits, Dv]
     float* part_ml;                // [Bt, H, Sq, splits, 2]
 };
-void launch_attention(const AttnParams& p, cudaStream_t s);
+void launch_attention(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 
 }  // namespace vtc

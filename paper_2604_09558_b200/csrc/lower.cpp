@@ -23,23 +23,23 @@ bool digit_of(const Atom& a, vtc_digit& d) {
     d.group = -1;
     int ax = -1;
     switch (a.kind) {
-        case AtomKind::Axis: d.axis = a.axis; return true;
+        case AtomKind::Axis: d.axis = int8_t(a.axis); return true;
         case AtomKind::Div:
             if (!axis_only(a.arg, ax) || a.k > UINT32_MAX) return false;
-            d.axis = ax;
+            d.axis = int8_t(ax);
             d.div = uint32_t(a.k);
             return true;
         case AtomKind::Mod:
             if (a.k > UINT32_MAX) return false;
             if (axis_only(a.arg, ax)) {
-                d.axis = ax;
+                d.axis = int8_t(ax);
                 d.mod = uint32_t(a.k);
                 return true;
             }
             if (a.arg.c0 == 0 && a.arg.t.size() == 1 && a.arg.t[0].c == 1 && a.arg.t[0].a->kind == AtomKind::Div) {
                 const Atom& dv = *a.arg.t[0].a;
                 if (!axis_only(dv.arg, ax) || dv.k > UINT32_MAX) return false;
-                d.axis = ax;
+                d.axis = int8_t(ax);
                 d.div = uint32_t(dv.k);
                 d.mod = uint32_t(a.k);
                 return true;
@@ -110,7 +110,7 @@ bool lower_piece(const VPiece& p, vtc_piece& out, uint64_t& bad_axes) {
                 vtc_digit gd{};
                 if (!digit_of(*it.a, gd) || nd >= VTC_MAX_DIGITS) { gok = false; break; }
                 gd.coeff = it.c;
-                gd.group = ng;
+                gd.group = int8_t(ng);
                 out.dig[nd++] = gd;
             }
         }
@@ -126,6 +126,11 @@ bool lower_piece(const VPiece& p, vtc_piece& out, uint64_t& bad_axes) {
         g.m1 = m1;
         g.d = dv;
         g.m2 = m2;
+    }
+    for (int t = 0; t < nd; ++t) {
+        vtc_digit& d = out.dig[t];
+        d.div_shift = int8_t((d.div & (d.div - 1)) == 0 ? __builtin_ctz(d.div) : -1);
+        d.mod_shift = int8_t(d.mod && (d.mod & (d.mod - 1)) == 0 ? __builtin_ctz(d.mod) : -1);
     }
     out.ndigits = int16_t(nd);
     out.ngroups = int16_t(ng);

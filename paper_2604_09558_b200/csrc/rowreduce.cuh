@@ -30,6 +30,30 @@ __device__ __forceinline__ Acc block_sum_256(F f, int64_t D) {
     return r;
 }
 
+// Same arithmetic order as block_sum_256, for 256 consumer threads that sync
+// on named barrier 1 (a producer warp elsewhere in the CTA does not take part).
+template <typename Acc, class F>
+__device__ __forceinline__ Acc block_sum_256_bar1(F f, int64_t D) {
+    __shared__ Acc s_part[8];
+    __shared__ Acc s_total;
+    Acc s = Acc(0);
+    for (int64_t k = threadIdx.x; k < D; k += 256) s += f(k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = s;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (threadIdx.x == 0) {
+        Acc t = Acc(0);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += s_part[w];
+        s_total = t;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    Acc r = s_total;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    return r;
+}
+
 template <typename Acc, class F>
 __device__ __forceinline__ Acc block_max_256(F f, int64_t D) {
     __shared__ Acc s_part[8];

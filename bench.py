@@ -123,10 +123,13 @@ def time_steps(fn, steps, torch, stream, flush):
     """Per-step CUDA-event timing on `stream`; L2 flushed before each step, outside the events."""
     times = []
     for _ in range(steps):
-        flush()
+        torch.cuda.synchronize()
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
+        # the flush is queued ahead of the start event: the host enqueues the
+        # step while the device is still flushing, so the timed region starts
+        # when the flush ends and contains no host launch latency
+        flush()
         s.record(stream)
         fn()
         e.record(stream)
@@ -231,10 +234,15 @@ def run_vtc(args):
     read_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def flush():
-        # write a buffer larger than L2, then read another one so the dirty
-        # lines are written back here rather than inside the timed step
-        flush_buf.random_(0, 255)
-        read_buf.max()
+        if args.l2 == "flush":
+            # write a buffer larger than L2, then read another one so the dirty
+            # lines are written back here rather than inside the timed step
+            flush_buf.random_(0, 255)
+            read_buf.max()
+        else:
+            # inputs larger than L2: no flush; keep the device busy while the
+            # host enqueues the step so no launch gap lands inside the events
+            torch.cuda._sleep(50000)
 
     if args.config == "c1":
         return run_c1(args, torch, vtc, W, dev, stream, flush, hbm_peak, peak_src, world, rank)
@@ -269,6 +277,22 @@ def run_vtc(args):
         else:
             mean_ms, _ = time_steps(lambda: p.execute_graph(stream), args.steps, torch, stream, flush)
         results[name] = mean_ms
+
+    if os.environ.get("VTC_TRACE") == "1":
+        # device timeline of one graph replay (first-CTA entry / last-CTA exit per launch)
+        for name, p in plans.items():
+            p.trace()
+            flush()
+            p.execute_graph(stream)
+            torch.cuda.synchronize()
+            tr = p.trace().astype(np.int64)
+            t0 = tr[:, 0].min()
+            print(f"[trace {name}] total {(tr[:, 1].max() - t0) / 1e3:.1f} us", file=sys.stderr)
+            for l, row in zip(p.info()["launches"], tr):
+                a, z = row[0], row[1]
+                cps = " ".join(f"cp{k}={(row[k] - t0) / 1e3:.1f}" for k in range(2, 8) if row[k])
+                print(f"  {l['kernel']:<22} {(a - t0) / 1e3:8.1f} -> {(z - t0) / 1e3:8.1f}  ({(z - a) / 1e3:6.1f} us)  "
+                      f"{l['bytes'] / 1e6:8.2f} MB  {l['node'][:50]}  {cps}", file=sys.stderr)
 
     # per-launch device times (separate pass; same launches with events between them)
     launches = info["launches"]
@@ -397,6 +421,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="vtc", choices=["vtc", "reference"])
+    ap.add_argument("--l2", default="flush", choices=["flush", "none"],
+                    help="flush L2 between timed steps, or rely on the step's inputs exceeding L2")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

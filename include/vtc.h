@@ -70,7 +70,7 @@ enum vtc_plan_flags {
     VTC_FLAG_FAST_FP = 1u << 0,  /* generic f32/f64 MatMul with FMA instead of the bit-exact mul+add */
     VTC_FLAG_NO_GEMV = 1u << 1,  /* disable the weight-streaming decode kernel */
     VTC_FLAG_NO_FUSE = 1u << 2,  /* disable RMSNorm/SiLU*Mul/residual and elementwise-tree fusion */
-    VTC_FLAG_GEMV_TMA = 1u << 3  /* persistent bulk-copy (cp.async.bulk) GEMV instead of the LDG split-K GEMV */
+    VTC_FLAG_GEMV_LDG = 1u << 3  /* decode GEMV on the LDG split-K kernel instead of the persistent TMA-streamed one */
 };
 
 typedef struct vtc_graph vtc_graph;
@@ -104,6 +104,13 @@ int vtc_plan_num_launches(vtc_plan* p);
 /* Same launches with a CUDA event between each; ms[i] = device time of launch
  * record i (vtc_plan_info "launches" order).  For measurement only. */
 int vtc_execute_timed(vtc_plan* p, void* stream, float* ms, int32_t n);
+/* Device timeline of the launches when the plan was prepared with VTC_TRACE=1
+ * in the environment: out[8i] / out[8i+1] = first CTA entry / last CTA exit
+ * (globaltimer ns) of launch i, out[8i+2..8i+7] = kernel-specific checkpoints
+ * (latest CTA; 0 if unused), accumulated over executions since the last call
+ * (which resets it).  Returns the number of launches, 0 when tracing is
+ * off.  For measurement only. */
+int vtc_plan_trace(vtc_plan* p, uint64_t* out, int32_t n);
 
 /* Host evaluation (no GPU) of a tensor's resolved map over its whole index
  * space in row-major order: targets[i] = index into the sorted target list

@@ -22,7 +22,7 @@ namespace vtc {
 struct ExecOptions {
     bool exact_fp = true;     // generic f32/f64 MatMul: unfused mul+add (bit-exact vs CPU reference)
     bool use_gemv = true;     // bf16 decode projections on the weight-streaming kernel
-    bool gemv_tma = false;    // persistent cp.async.bulk-fed GEMV (M <= 4); default: the LDG split-K GEMV (faster today)
+    bool gemv_stream = true;  // persistent TMA-streamed GEMV for M <= 4 (else the LDG split-K GEMV)
     bool fuse = true;         // RMSNorm->MatMul, SiLU*Mul->MatMul, MatMul->Add(residual) fusion
     int attn_splits = 0;      // 0: automatic
 };
@@ -66,6 +66,10 @@ public:
     // Enqueue every launch with a CUDA event on each side; per-launch device
     // milliseconds are written to ms[0..n) after the stream drains.
     void run_timed(void* stream, float* ms, int n);
+    // VTC_TRACE=1 timeline: out[2i], out[2i+1] = globaltimer (ns) at entry / exit
+    // of launch i over the runs since the last read; returns the launch count.
+    int read_trace(unsigned long long* out, int n);
+    void reset_trace();
 
     void upload(const std::string& id, const void* host, int64_t bytes, void* stream);
     // Materialise any tensor (virtual or physical) into host memory.

@@ -10,6 +10,8 @@
  *          + sum_{groups g} coeff_g * ((((shift_g + sum_{digits in g} coeff*digit) % m1) / d) % m2)
  *   address = (char*)ptr + offset * elem_bytes
  *
+ * Pieces without any division, modulus or group carry affine = 1 and the
+ * per-axis strides aff[] (the same offset, evaluated without the digit walk).
  * mod == 0 / m1 == 0 / m2 == 0 mean "no modulus"; div/d == 1 mean "no
  * division".  All digit and group arguments are non-negative by
  * construction, so the device uses unsigned arithmetic.
@@ -53,6 +55,9 @@ typedef struct vtc_piece {
     int32_t target;    /* root index inside the owning plan */
     int16_t ndigits;
     int16_t ngroups;
+    int32_t affine;    /* 1: no div / mod / groups -- offset = base + sum_a aff[a] * I[a] */
+    int32_t pad2;
+    int64_t aff[VTC_MAX_RANK];
     vtc_digit dig[VTC_MAX_DIGITS];
     vtc_group grp[VTC_MAX_GROUPS];
 } vtc_piece;

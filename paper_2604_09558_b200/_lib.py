@@ -33,6 +33,7 @@ SIGNATURES = {
     "vtc_execute_graph": (C.c_int, [_VP, _VP]),
     "vtc_plan_num_launches": (C.c_int, [_VP]),
     "vtc_execute_timed": (C.c_int, [_VP, _VP, C.POINTER(C.c_float), C.c_int32]),
+    "vtc_plan_trace": (C.c_int, [_VP, C.POINTER(C.c_uint64), C.c_int32]),
     "vtc_map_eval": (C.c_int, [_VP, C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.c_int64]),
     "vtc_plan_map_json": (C.c_int, [_VP, C.c_char_p, C.POINTER(C.c_char_p)]),
     "vtc_launch_gather_copy": (C.c_int, [_VP, _VP, C.c_int32, _VP]),

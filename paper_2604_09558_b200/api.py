@@ -37,7 +37,7 @@ ERRORS = {code: type(name, (VtcError,), {"code": code}) for code, name in _ERROR
 globals().update({cls.__name__: cls for cls in ERRORS.values()})
 
 MATERIALIZE, SELECTED, MAX_ELIMINATION = 0, 1, 2
-FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE = 1, 2, 4
+FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE, FLAG_GEMV_LDG = 1, 2, 4, 8
 
 NP_DTYPES = {"f64": np.float64, "f32": np.float32, "i64": np.int64, "bf16": np.uint16}
 
@@ -163,6 +163,16 @@ class Plan:
         _check(_lib.load().vtc_execute_timed(self._h, _stream(stream), ms.ctypes.data_as(C.POINTER(C.c_float)),
                                              n_records))
         return ms
+
+    def trace(self) -> np.ndarray:
+        """[n_launches, 8] globaltimer (ns): entry, exit, kernel checkpoints per
+        launch since the last call (plans prepared with VTC_TRACE=1), else empty."""
+        n = max(1, self.num_launches())
+        buf = np.zeros(8 * n, np.uint64)
+        r = _lib.load().vtc_plan_trace(self._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), 8 * n)
+        if r < 0:
+            _check(-r)
+        return buf[: 8 * r].reshape(r, 8)
 
     def num_launches(self) -> int:
         return _lib.load().vtc_plan_num_launches(self._h)

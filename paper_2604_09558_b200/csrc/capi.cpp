@@ -154,7 +154,7 @@ int vtc_plan_create(vtc_graph* g, int mode, const int32_t* selected, int32_t n_s
         opt.exact_fp = !(flags & VTC_FLAG_FAST_FP);
         opt.use_gemv = !(flags & VTC_FLAG_NO_GEMV);
         opt.fuse = !(flags & VTC_FLAG_NO_FUSE);
-        opt.gemv_tma = (flags & VTC_FLAG_GEMV_TMA) != 0;
+        opt.gemv_stream = (flags & VTC_FLAG_GEMV_LDG) == 0;
         auto p = std::make_unique<vtc_plan>();
         p->graph = g;
         p->flags = flags;
@@ -237,6 +237,12 @@ int vtc_plan_num_launches(vtc_plan* p) { return p->exec->num_kernel_launches(); 
 
 int vtc_execute_timed(vtc_plan* p, void* stream, float* ms, int32_t n) {
     return guard([&] { p->exec->run_timed(stream, ms, n); });
+}
+
+int vtc_plan_trace(vtc_plan* p, uint64_t* out, int32_t n) {
+    int count = 0;
+    int st = guard([&] { count = p->exec->read_trace(reinterpret_cast<unsigned long long*>(out), n); });
+    return st == VTC_OK ? count : -st;
 }
 
 int vtc_map_eval(vtc_plan* p, const char* tensor, int lowered, int32_t* targets, int64_t* offsets, int64_t cap) {

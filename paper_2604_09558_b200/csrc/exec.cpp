@@ -2,6 +2,7 @@
 // Mirrors execute_detailed (proj/src/executor.cpp:448-498); see exec.hpp.
 #include "vtc/exec.hpp"
 
+#include <cstdlib>
 #include <algorithm>
 #include <climits>
 #include <cstring>
@@ -38,6 +39,7 @@ struct Launch {
     virtual size_t param_bytes() const = 0;
     virtual const void* host_params() const = 0;
     virtual void set_device_params(void* d) = 0;
+    virtual void set_trace(unsigned long long* t, int id) = 0;
 };
 
 // Host copy of the parameter block (for dispatch decisions) + its device copy
@@ -50,10 +52,14 @@ struct LaunchT : Launch {
     size_t param_bytes() const override { return sizeof(P); }
     const void* host_params() const override { return &p; }
     void set_device_params(void* d) override { dp = static_cast<const P*>(d); }
+    void set_trace(unsigned long long* t, int id) override {
+        p.head.trace = t;
+        p.head.id = id;
+    }
 };
 
 void launch_gemv_any(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
-    if (p.tma) launch_gemv_tma(p, dp, s);
+    if (p.stream) launch_gemv_stream(p, dp, s);
     else launch_gemv(p, dp, s);
 }
 
@@ -122,6 +128,7 @@ struct Executor::Impl {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t gexec = nullptr;
     cudaStream_t captured_on = nullptr;
+    unsigned long long* trace = nullptr;  // VTC_TRACE timeline buffer (2 per launch)
 
     void free_scratch() {
         for (void* p : scratch) cudaFree(p);
@@ -264,6 +271,66 @@ void Executor::prepare(bool dry) {
         li.bytes = group_bytes(l->node);
         infos_.push_back(li);
         impl_->launches.push_back(std::move(l));
+    };
+
+    // roots written by some node of the plan (weights that are not may be
+    // prefetched before the kernel's dependency on earlier launches resolves)
+    std::set<std::string> written_roots;
+    for (const auto& n : g_.nodes())
+        if (!elim.count(n.id))
+            for (const auto& o : n.outputs)
+                for (const auto& t : targets_of(map_of(o))) written_roots.insert(t);
+
+    // Configure the persistent TMA-streamed GEMV: balanced contiguous ranges of
+    // (256-column strip, 64-row k-tile) units, one CTA per SM.
+    auto stream_gemv = [&](GemvParams& p, uint64_t b_ptr, const std::string& b_root) -> bool {
+        const int64_t COLS = GEMV_STREAM_COLS, KT = GEMV_STREAM_KT;
+        int sms = 148;
+        if (!impl_->dry) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        int64_t strips0 = (p.N + COLS - 1) / COLS;
+        int64_t strips = strips0;  // (horizontal fusion adds the second matrix's strips)
+        int64_t kts = (p.K + KT - 1) / KT, units = strips * kts;
+        int grid = int(std::min<int64_t>(sms, units));
+        std::vector<int32_t> first(size_t(strips), -1), count(size_t(strips), 0);
+        int64_t maxrange = 0;
+        for (int c = 0; c < grid; ++c) {
+            int64_t ub = units * c / grid, ue = units * (c + 1) / grid;
+            maxrange = std::max(maxrange, ue - ub);
+            for (int64_t u = ub; u < ue; u = (u / kts + 1) * kts) {
+                int64_t s2 = u / kts;
+                if (first[size_t(s2)] < 0) first[size_t(s2)] = c;
+                ++count[size_t(s2)];
+            }
+        }
+        int a_tiles = int(std::min<int64_t>(kts, maxrange));
+        int stages = 0;
+        for (int st = 6; st >= 3 && !stages; --st)
+            if (gemv_stream_smem(p.M, a_tiles, st)) stages = st;
+        if (!stages) return false;
+        if (!impl_->dry && !encode_weight_tmap(p.tmap[0], reinterpret_cast<const void*>(b_ptr) , p.K, p.N, p.b_sk))
+            return false;
+        int maxc = *std::max_element(count.begin(), count.end());
+        p.stream = 1;
+        if (const char* dbg = std::getenv("VTC_GEMV_DBG")) p.pad = std::atoi(dbg);
+        p.nmat = 1;
+        p.n_mat[0] = p.N;
+        p.strips0 = int32_t(strips0);
+        p.stages = stages;
+        p.grid = grid;
+        p.max_contrib = maxc;
+        p.a_tiles = a_tiles;
+        p.b_static = written_roots.count(b_root) ? 0 : 1;
+        p.work = static_cast<float*>(impl_->alloc(size_t(strips * maxc * p.M * COLS) * sizeof(float), false));
+        p.counters = static_cast<unsigned*>(impl_->alloc(size_t(strips) * sizeof(unsigned), true));
+        auto* dfirst = static_cast<int32_t*>(impl_->alloc(size_t(strips) * 4, false));
+        auto* dcount = static_cast<int32_t*>(impl_->alloc(size_t(strips) * 4, false));
+        if (!impl_->dry) {
+            ck(cudaMemcpy(dfirst, first.data(), size_t(strips) * 4, cudaMemcpyHostToDevice), "H2D");
+            ck(cudaMemcpy(dcount, count.data(), size_t(strips) * 4, cudaMemcpyHostToDevice), "H2D");
+        }
+        p.strip_first = dfirst;
+        p.strip_count = dcount;
+        return true;
     };
 
     // ---- elementwise / copy launches over an output shape ----
@@ -681,43 +748,9 @@ void Executor::prepare(bool dry) {
                     TargetInfo bt = target(bp.target);
                     p.b_base = reinterpret_cast<const char*>(bt.ptr) + bp.off.c0 * es;
                     p.b_sk = *VMap::tile_stride(bp, 0, K);
-                    // persistent TMA-fed variant: one CTA per SM, balanced (strip, k-tile) ranges
-                    int tma_stages = 0;
-                    for (int st = 6; st >= 3; --st)
-                        if (gemv_tma_smem(M, K, st) <= 220 * 1024) {
-                            tma_stages = st;
-                            break;
-                        }
-                    if (M <= 4 && tma_stages > 0 && opt_.gemv_tma) {
-                        L->kernel = "gemv_tma_bf16";
-                        int sms = 148;
-                        if (!impl_->dry) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-                        int64_t strips = (N + 255) / 256, kts = (K + 63) / 64, units = strips * kts;
-                        int grid = int(std::min<int64_t>(sms, units));
-                        std::vector<int32_t> first(size_t(strips), -1), count(size_t(strips), 0);
-                        for (int c = 0; c < grid; ++c) {
-                            int64_t ub = units * c / grid, ue = units * (c + 1) / grid;
-                            for (int64_t u = ub; u < ue; u = (u / kts + 1) * kts) {
-                                int64_t s2 = u / kts;
-                                if (first[size_t(s2)] < 0) first[size_t(s2)] = c;
-                                ++count[size_t(s2)];
-                            }
-                        }
-                        int maxc = *std::max_element(count.begin(), count.end());
-                        p.tma = 1;
-                        p.stages = tma_stages;
-                        p.grid = grid;
-                        p.max_contrib = maxc;
-                        p.work = static_cast<float*>(impl_->alloc(size_t(strips * maxc * M * 256) * sizeof(float), false));
-                        p.counters = static_cast<unsigned*>(impl_->alloc(size_t(strips) * sizeof(unsigned), true));
-                        auto* dfirst = static_cast<int32_t*>(impl_->alloc(size_t(strips) * 4, false));
-                        auto* dcount = static_cast<int32_t*>(impl_->alloc(size_t(strips) * 4, false));
-                        if (!impl_->dry) {
-                            ck(cudaMemcpy(dfirst, first.data(), size_t(strips) * 4, cudaMemcpyHostToDevice), "H2D");
-                            ck(cudaMemcpy(dcount, count.data(), size_t(strips) * 4, cudaMemcpyHostToDevice), "H2D");
-                        }
-                        p.strip_first = dfirst;
-                        p.strip_count = dcount;
+                    // persistent TMA-streamed variant: one CTA per SM, balanced (strip, k-tile) ranges
+                    if (M <= 4 && opt_.gemv_stream && stream_gemv(p, reinterpret_cast<uint64_t>(p.b_base), bp.target)) {
+                        L->kernel = "gemv_stream_bf16";
                         push(std::move(L));
                         break;
                     }
@@ -815,18 +848,34 @@ void Executor::prepare(bool dry) {
                         break;
                     }
                 p.group = G;
-                int64_t qblocks = int64_t(p.Bt) * (p.H / G) * p.Sq;
+                // tensor-core decode path: K/V rows addressed as base + t * stride when
+                // the maps are single-piece affine along the key axis
+                p.fast = attn_decode_supported(p) ? 1 : 0;
+                if (p.fast && p.k.m.npieces == 1 && p.v.m.npieces == 1) {
+                    int64_t ks_ = desc_tile_stride(p.k.m.piece[0], rank - 2, p.Sk);
+                    int64_t vs_ = desc_tile_stride(p.v.m.piece[0], rank - 2, p.Sk);
+                    if (ks_ != INT64_MIN && vs_ != INT64_MIN) {
+                        p.kv_affine = 1;
+                        p.k_sstride = ks_;
+                        p.v_sstride = vs_;
+                    }
+                }
+                int64_t qblocks = int64_t(p.Bt) * (p.H / G) * (p.fast ? 1 : p.Sq);
                 int splits = opt_.attn_splits;
+                const int kgran = p.fast ? 64 : 32;  // keys per split granule (4 warps x 16 on the fast path)
                 if (splits <= 0) {
-                    splits = int((148 * 2 + qblocks - 1) / qblocks);
-                    splits = std::max(1, std::min(splits, (p.Sk + 31) / 32));
+                    int64_t target = p.fast ? 148 * 2 * 4 : 148 * 2;
+                    splits = int((target + qblocks - 1) / qblocks);
+                    splits = std::max(1, std::min(splits, (p.Sk + kgran - 1) / kgran));
                 }
                 int chunk = (p.Sk + splits - 1) / splits;
-                chunk = (chunk + 31) / 32 * 32;
+                chunk = (chunk + kgran - 1) / kgran * kgran;
                 splits = (p.Sk + chunk - 1) / chunk;
                 p.splits = splits;
                 p.chunk = chunk;
-                L->kernel = splits > 1 ? "attention_splitkv" : "attention";
+                L->kernel = p.fast ? (splits > 1 ? "attn_decode_tc_splitkv" : "attn_decode_tc") : (splits > 1 ? "attention_splitkv" : "attention");
+                if (splits > 1 && p.fast)
+                    p.counters = static_cast<unsigned*>(impl_->alloc(size_t(qblocks) * sizeof(unsigned), true));
                 if (splits > 1) {
                     int64_t rows = int64_t(p.Bt) * p.H * p.Sq;
                     p.part_o = static_cast<float*>(impl_->alloc(size_t(rows * splits * p.Dv) * sizeof(float), false));
@@ -838,6 +887,13 @@ void Executor::prepare(bool dry) {
             default:
                 throw UnsupportedError(std::string("no kernel for operator ") + to_string(n.kind));
         }
+    }
+    // optional device timeline (VTC_TRACE=1): [entry, exit] globaltimer per launch
+    impl_->trace = nullptr;
+    if (!dry && std::getenv("VTC_TRACE") && std::getenv("VTC_TRACE")[0] == '1') {
+        impl_->trace = static_cast<unsigned long long*>(impl_->alloc(impl_->launches.size() * 64, false));
+        for (size_t i = 0; i < impl_->launches.size(); ++i) impl_->launches[i]->set_trace(impl_->trace, int(i));
+        reset_trace();
     }
     // all parameter blocks in one device allocation, uploaded once
     if (!dry) {
@@ -881,6 +937,24 @@ void Executor::run_graph(void* stream) {
         ck(cudaGraphInstantiate(&impl_->gexec, impl_->graph, 0), "cudaGraphInstantiate");
     }
     ck(cudaGraphLaunch(impl_->gexec, s), "cudaGraphLaunch");
+}
+
+void Executor::reset_trace() {
+    if (!impl_->trace) return;
+    std::vector<unsigned long long> init(impl_->launches.size() * 8, 0ull);
+    for (size_t i = 0; i < impl_->launches.size(); ++i) init[8 * i] = ~0ull;
+    ck(cudaMemcpy(impl_->trace, init.data(), init.size() * 8, cudaMemcpyHostToDevice), "H2D(trace)");
+}
+
+int Executor::read_trace(unsigned long long* out, int n) {
+    if (!impl_->trace) return 0;
+    int L = int(impl_->launches.size());
+    std::vector<unsigned long long> buf(size_t(L) * 8);
+    ck(cudaDeviceSynchronize(), "sync");
+    ck(cudaMemcpy(buf.data(), impl_->trace, buf.size() * 8, cudaMemcpyDeviceToHost), "D2H(trace)");
+    for (int i = 0; i < 8 * L && i < n; ++i) out[i] = buf[size_t(i)];
+    reset_trace();
+    return L;
 }
 
 void Executor::run_timed(void* stream, float* ms, int n) {

@@ -15,6 +15,7 @@
 #include <cfloat>
 
 #include "device.cuh"
+#include "launch.cuh"
 
 namespace vtc {
 namespace {
@@ -28,7 +29,8 @@ __device__ __forceinline__ float ldf(const T* p) { return float(dev::to_acc<T>(*
 
 template <typename T>
 __global__ void __launch_bounds__(NT) attn_kernel(const AttnParams* __restrict__ pp) {
-    const AttnParams& p = *pp;
+    VTC_STAGE_PARAMS(AttnParams, pp);
+    dev::pdl_wait(); dev::pdl_launch_dependents();
     __shared__ float sQ[MAXG][MAXD];
     __shared__ float sP[MAXG][TK];
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -232,7 +234,8 @@ __global__ void __launch_bounds__(NT) attn_kernel(const AttnParams* __restrict__
 
 template <typename T>
 __global__ void __launch_bounds__(NT) combine_kernel(const AttnParams* __restrict__ pp) {
-    const AttnParams& p = *pp;
+    VTC_STAGE_PARAMS(AttnParams, pp);
+    dev::pdl_wait(); dev::pdl_launch_dependents();
     // one CTA per (lead, h, sq) row
     const int64_t row = blockIdx.x;
     const int r = p.rank;
@@ -270,12 +273,16 @@ __global__ void __launch_bounds__(NT) combine_kernel(const AttnParams* __restric
 
 template <typename T>
 void launch_t(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
-    int64_t qblocks = int64_t(p.Bt) * (p.H / p.group) * p.Sq;
-    dim3 grid(unsigned(qblocks), unsigned(p.splits));
-    size_t smem = size_t(TK) * size_t(p.D + 8 + p.Dv + 8) * sizeof(T);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(attn_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attn_kernel<T><<<grid, NT, smem, s>>>(dp);
-    if (p.splits > 1) combine_kernel<T><<<unsigned(int64_t(p.Bt) * p.H * p.Sq), NT, 0, s>>>(dp);
+    if (p.fast) {
+        launch_attn_decode(p, dp, s);
+    } else {
+        int64_t qblocks = int64_t(p.Bt) * (p.H / p.group) * p.Sq;
+        dim3 grid(unsigned(qblocks), unsigned(p.splits));
+        size_t smem = size_t(TK) * size_t(p.D + 8 + p.Dv + 8) * sizeof(T);
+        if (smem > 48 * 1024) cudaFuncSetAttribute(attn_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        launch_k(attn_kernel<T>, dim3(grid), dim3(NT), smem, s, dp);
+    }
+    if (p.splits > 1 && !p.fast) launch_k(combine_kernel<T>, dim3(unsigned(int64_t(p.Bt) * p.H * p.Sq)), dim3(NT), 0, s, dp);
 }
 
 }  // namespace

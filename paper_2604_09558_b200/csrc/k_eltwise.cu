@@ -12,6 +12,7 @@
 #include <cmath>
 
 #include "device.cuh"
+#include "launch.cuh"
 
 namespace vtc {
 namespace {
@@ -127,7 +128,8 @@ __device__ __forceinline__ T apply_op(EwOp op, T a, T b) {
 
 template <typename T, int VEC>
 __global__ void __launch_bounds__(256) ew_kernel(const EwParams* __restrict__ pp) {
-    const EwParams& p = *pp;
+    VTC_STAGE_PARAMS(EwParams, pp);
+    dev::pdl_wait(); dev::pdl_launch_dependents();
     const int last = p.rank - 1;
     const int nin = p.nin, nprog = p.nprog;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < p.nvec; v += (int64_t)gridDim.x * blockDim.x) {
@@ -135,9 +137,16 @@ __global__ void __launch_bounds__(256) ew_kernel(const EwParams* __restrict__ pp
         dev::unflatten(v * VEC, p.shape, p.rank, idx);
 #pragma unroll 1
         for (int a = 0; a < p.rank; ++a) idx[a] += p.origin[a];
+        // all input loads in flight at once (registers), then the program
+        T in[EW_MAX_IN][VEC];
+#pragma unroll
+        for (int i = 0; i < EW_MAX_IN; ++i)
+            if (i < nin) load_vec<T, VEC>(p.in[i], idx, last, in[i]);
         T r[EW_MAX_PROG + EW_MAX_IN][VEC];
-#pragma unroll 1
-        for (int i = 0; i < nin; ++i) load_vec<T, VEC>(p.in[i], idx, last, r[i]);
+#pragma unroll
+        for (int i = 0; i < EW_MAX_IN; ++i)
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) r[i][j] = in[i][j];
         if (nprog > 0) {
 #pragma unroll 1
             for (int s = 0; s < nprog; ++s) {
@@ -157,9 +166,9 @@ void launch_t(const EwParams& p, const EwParams* dp, cudaStream_t s) {
     int grid = int(blocks < 148 * 16 ? blocks : 148 * 16);
     if (grid < 1) grid = 1;
     if (p.vec == V)
-        ew_kernel<T, V><<<grid, 256, 0, s>>>(dp);
+        launch_k(ew_kernel<T, V>, dim3(grid), dim3(256), 0, s, dp);
     else
-        ew_kernel<T, 1><<<grid, 256, 0, s>>>(dp);
+        launch_k(ew_kernel<T, 1>, dim3(grid), dim3(256), 0, s, dp);
 }
 
 }  // namespace

@@ -10,6 +10,7 @@
 // Split-K partials are summed in split order by the last CTA to arrive, so the
 // result is deterministic and independent of the operand maps.
 #include "device.cuh"
+#include "launch.cuh"
 #include "rowreduce.cuh"
 
 namespace vtc {
@@ -18,11 +19,11 @@ namespace {
 using dev::bf16;
 constexpr int NT = 256, COLS = 256, WARPS = 8;
 
-__device__ __forceinline__ uint4 ld_stream(const void* p) {
+__device__ __forceinline__ uint4 ld_stream(const void* p, uint64_t policy) {
     uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
+                 : "l"(p), "l"(policy));
     return r;
 }
 
@@ -32,7 +33,8 @@ __device__ __forceinline__ float load_bf16_at(const VOperand& op, int32_t (&idx)
 
 template <int MT, int U>
 __global__ void __launch_bounds__(NT) gemv_kernel(const GemvParams* __restrict__ pp) {
-    const GemvParams& p = *pp;
+    VTC_STAGE_PARAMS(GemvParams, pp);
+    dev::pdl_wait(); dev::pdl_launch_dependents();
     extern __shared__ float sA[];  // [M][kchunk]
     __shared__ float red[WARPS][COLS];
     __shared__ float s_rs[16];
@@ -94,6 +96,7 @@ __global__ void __launch_bounds__(NT) gemv_kernel(const GemvParams* __restrict__
             sw = p.normw.fast_stride[l.piece];
             pw = dev::addr<bf16>(p.normw.m, l);
         }
+#pragma unroll 4
         for (int e = tid; e < klen; e += NT) {
             int64_t k = kb + e;
             float v = pa ? __bfloat162float(pa[e * sa]) : a_at(p.a, m, k);
@@ -126,12 +129,13 @@ __global__ void __launch_bounds__(NT) gemv_kernel(const GemvParams* __restrict__
     const int64_t col = n0 + lane * 8;
     const bool col_ok = col < p.N;
     const bf16* bcol = reinterpret_cast<const bf16*>(p.b_base) + col;
+    const uint64_t policy = dev::evict_first_policy();
     for (int base = 0; base < klen; base += WARPS * U) {
         uint4 w[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             int k = base + u * WARPS + warp;
-            if (k < klen && col_ok) w[u] = ld_stream(bcol + (kb + k) * p.b_sk);
+            if (k < klen && col_ok) w[u] = ld_stream(bcol + (kb + k) * p.b_sk, policy);
             else w[u] = make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
@@ -228,7 +232,7 @@ void launch_mt(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
     dim3 grid(unsigned((p.N + COLS - 1) / COLS), unsigned(p.ksplit));
     size_t smem = size_t(p.M) * size_t(p.kchunk) * sizeof(float);
     if (smem > 48 * 1024) cudaFuncSetAttribute(gemv_kernel<MT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    gemv_kernel<MT, U><<<grid, NT, smem, s>>>(dp);
+    launch_k(gemv_kernel<MT, U>, dim3(grid), dim3(NT), smem, s, dp);
 }
 
 }  // namespace

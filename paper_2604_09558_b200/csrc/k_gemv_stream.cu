@@ -1,0 +1,393 @@
+// Persistent TMA-streamed weight GEMV for bf16 decode (M <= 4 rows).
+//
+// C[m, n] (+)= prologue(A)[m, :] . B[:, n] -- the decode-step projections of a
+// VTC-planned decoder layer (the reference computes them with matmul_kernel,
+// proj/src/executor.cpp:230-249).  The step is bound by streaming the weights
+// once from HBM, so the kernel is organised around keeping HBM busy:
+//
+//   * one CTA per SM; the weight matrix is cut into units of one 64-row x
+//     256-column tile (32 KB) and each CTA owns a contiguous range of units in
+//     (strip, k-tile) order;
+//   * warp 8 is the producer: one elected thread issues one 2-D TMA load
+//     (cp.async.bulk.tensor) per unit into a STAGES-deep shared-memory ring,
+//     completion signalled through mbarrier transaction counts;
+//   * weights are static for the plan, so the producer starts streaming BEFORE
+//     griddepcontrol.wait: under programmatic dependent launch the first
+//     stages land while the previous kernel (attention, the previous GEMV)
+//     is still draining;
+//   * warps 0-7 wait for the previous kernel, stage their k-range of A through
+//     its VirtualTensor map (with the fused RMSNorm / SiLU*Mul prologue,
+//     rounding exactly like the unfused operators), then consume tiles with
+//     16-byte LDS (8 columns per lane, 8 rows per warp per tile);
+//   * a strip shared by several CTAs is reduced by the last CTA to finish it,
+//     in CTA order (deterministic), which applies the residual epilogue and
+//     stores C through its map.
+// Up to two weight matrices that share A (sibling MatMuls such as gate/up)
+// run as one launch.
+#include <cuda.h>
+
+#include <cstring>
+
+#include "device.cuh"
+#include "launch.cuh"
+#include "rowreduce.cuh"
+
+namespace vtc {
+namespace {
+
+using dev::bf16;
+constexpr int CONSUMERS = 8, NT = (CONSUMERS + 1) * 32, COLS = GEMV_STREAM_COLS, KT = GEMV_STREAM_KT;
+constexpr uint32_t TILE_BYTES = KT * COLS * sizeof(bf16);
+
+struct Tmaps {
+    CUtensorMap m[GEMV_MAX_MATS];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// Weights are read exactly once per step: stream them with an L2 evict-first
+// policy so they do not push code, parameters and activations out of L2.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint64_t* bar,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32) : "memory"); }
+
+template <int MT>
+__global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __restrict__ pp, const __grid_constant__ Tmaps tm) {
+    VTC_STAGE_PARAMS(GemvParams, pp);
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int stages = p.stages;
+    bf16* ring = reinterpret_cast<bf16*>(smem);
+    float* sA = reinterpret_cast<float*>(smem + size_t(stages) * TILE_BYTES);  // [M][a_tiles*KT]
+    float* red = sA + size_t(p.M) * p.a_tiles * KT;                              // [CONSUMERS][COLS]
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + CONSUMERS * COLS);
+    uint64_t* empty = full + stages;
+    __shared__ float s_rs[4];
+    __shared__ unsigned s_last;
+
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    const int M = int(p.M);
+    const int64_t ktiles = (p.K + KT - 1) / KT;
+    const int64_t strips1 = p.nmat > 1 ? (p.n_mat[1] + COLS - 1) / COLS : 0;
+    const int64_t units = (int64_t(p.strips0) + strips1) * ktiles;
+    const int64_t u_begin = units * blockIdx.x / gridDim.x;
+    const int64_t u_end = units * (blockIdx.x + 1) / gridDim.x;
+
+    if (tid == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CONSUMERS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    dev::pdl_launch_dependents();
+
+    if (warp == CONSUMERS) {
+        // ---------------- producer ----------------
+        if (lane != 0) return;
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.m[0])) : "memory");
+        const uint64_t policy = dev::evict_first_policy();
+        if (!p.b_static) dev::pdl_wait();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t u = u_begin; u < u_end; ++u) {
+            const int64_t strip = u / ktiles, kt = u % ktiles;
+            const int mat = strip < p.strips0 ? 0 : 1;
+            const int64_t n0 = (strip - (mat ? p.strips0 : 0)) * COLS;
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], TILE_BYTES);
+            tma_load_2d(ring + size_t(stage) * KT * COLS, &tm.m[mat], int32_t(n0), int32_t(kt * KT), &full[stage], policy);
+            if (++stage == stages) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers: A prologue (overlaps the first weight tiles) ----
+    if (tid == 0) dev::trace_point(p.head, 4);  // parameters staged, barriers ready
+    dev::pdl_wait();
+    if (tid == 0) dev::trace_point(p.head, 5);  // dependency resolved
+    const int ctid = tid;  // 0..255
+    const int64_t kt_first = u_begin % ktiles;
+    const int64_t a_cols = int64_t(p.a_tiles) * KT;
+    auto row_ptr = [&](const VOperand& op, int m, int64_t& stride) -> const bf16* {
+        int32_t idx[VTC_MAX_RANK] = {};
+        idx[0] = m;
+        dev::Loc l = dev::locate(op.m, idx);
+        stride = op.fast_stride[l.piece];
+        return dev::addr<bf16>(op.m, l);
+    };
+    auto elem = [&](const VOperand& op, int m, int64_t k) -> float {
+        int32_t idx[VTC_MAX_RANK] = {};
+        idx[0] = m;
+        idx[1] = int32_t(k);
+        return __bfloat162float(*dev::elem_ptr<bf16>(op.m, idx));
+    };
+    for (int m = 0; m < M; ++m) {
+        if (p.pad & 1) {  // DEBUG: skip the A prologue
+            for (int64_t e = ctid; e < a_cols; e += CONSUMERS * 32) sA[size_t(m) * a_cols + e] = 1.f;
+            continue;
+        }
+        int64_t sa = 0, sa2 = 0, sw = 0;
+        const bf16* pa = p.a.fast_ok ? row_ptr(p.a, m, sa) : nullptr;
+        const bf16* pa2 = (p.prologue == GemvPrologue::SiLUMul && p.a2.fast_ok) ? row_ptr(p.a2, m, sa2) : nullptr;
+        const bf16* pw = nullptr;
+        float rs = 0.f;
+        if (p.prologue == GemvPrologue::RMSNorm) {
+            if (p.normw.fast_ok) {
+                int32_t widx[VTC_MAX_RANK] = {};
+                dev::Loc l = dev::locate(p.normw.m, widx);
+                sw = p.normw.fast_stride[l.piece];
+                pw = dev::addr<bf16>(p.normw.m, l);
+            }
+            // the same 256-thread reduction order as the standalone RMSNorm kernel
+            float ss = block_sum_256_bar1<float>(
+                [&](int64_t k) {
+                    float v = pa ? __bfloat162float(pa[k * sa]) : elem(p.a, m, k);
+                    return v * v;
+                },
+                p.K);
+            if (ctid == 0) s_rs[m] = rsqrtf(ss / float(p.K) + p.eps);
+            if (ctid == 0) dev::trace_point(p.head, 6);  // norm reduction done
+            bar_consumers();
+            rs = s_rs[m];
+        }
+        // only the k-tiles this CTA's units touch: slot j <-> k-tile (kt_first + j) mod ktiles
+        // (unrolled so the loads of several elements are in flight together)
+#pragma unroll 4
+        for (int64_t e = ctid; e < a_cols; e += CONSUMERS * 32) {
+            const int64_t kt = (kt_first + e / KT) % ktiles;
+            const int64_t k = kt * KT + e % KT;
+            float v = 0.f;
+            if (k < p.K) {
+                v = pa ? __bfloat162float(pa[k * sa]) : elem(p.a, m, k);
+                if (p.prologue == GemvPrologue::SiLUMul) {
+                    float u = pa2 ? __bfloat162float(pa2[k * sa2]) : elem(p.a2, m, k);
+                    float sg = __bfloat162float(__float2bfloat16_rn(v / (1.0f + expf(-v))));
+                    v = __bfloat162float(__float2bfloat16_rn(sg * u));
+                } else if (p.prologue == GemvPrologue::RMSNorm) {
+                    float w;
+                    if (pw) {
+                        w = __bfloat162float(pw[k * sw]);
+                    } else {
+                        int32_t widx[VTC_MAX_RANK] = {};
+                        widx[0] = int32_t(k);
+                        w = __bfloat162float(*dev::elem_ptr<bf16>(p.normw.m, widx));
+                    }
+                    v = __bfloat162float(__float2bfloat16_rn(v * rs * w));
+                }
+            }
+            sA[size_t(m) * a_cols + e] = v;
+        }
+    }
+    bar_consumers();
+    if (ctid == 0) dev::trace_point(p.head, 2);  // A prologue done
+
+    // ---------------- consumers: stream tiles ----------------
+    float acc[MT][8];
+    auto zero = [&] {
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[m][j] = 0.f;
+    };
+    zero();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t u = u_begin; u < u_end; ++u) {
+        const int64_t strip = u / ktiles, kt = u % ktiles;
+        const int64_t slot = (kt - kt_first + ktiles) % ktiles;
+        const float* arow = sA + slot * KT;
+        mbar_wait(&full[stage], phase);
+        const bf16* tile = ring + size_t(stage) * KT * COLS;
+        uint4 w[KT / CONSUMERS];
+#pragma unroll
+        for (int i = 0; i < KT / CONSUMERS; ++i)
+            w[i] = *reinterpret_cast<const uint4*>(tile + (warp + i * CONSUMERS) * COLS + lane * 8);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);  // the tile is in registers: release the slot
+        if (++stage == stages) {
+            stage = 0;
+            phase ^= 1;
+        }
+#pragma unroll
+        for (int i = 0; i < KT / CONSUMERS; ++i) {
+            const int r = warp + i * CONSUMERS;
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+            float b[8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float2 f = __bfloat1622float2(h[j]);
+                b[2 * j] = f.x;
+                b[2 * j + 1] = f.y;
+            }
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                if (m < M) {
+                    const float a = arow[size_t(m) * a_cols + r];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[m][j] = fmaf(a, b[j], acc[m][j]);
+                }
+            }
+        }
+        const bool strip_end = (kt == ktiles - 1) || (u + 1 == u_end);
+        if (!strip_end) continue;
+        if (ctid == 0 && u + 1 == u_end) dev::trace_point(p.head, 3);  // last tile consumed
+
+        // ---- this CTA's part of the strip is done: reduce warps -> partial slot ----
+        const int mat = strip < p.strips0 ? 0 : 1;
+        const int64_t n0 = (strip - (mat ? p.strips0 : 0)) * COLS;
+        const int64_t Nl = p.n_mat[mat];
+        const int first = p.strip_first[strip];
+        const int ncontrib = p.strip_count[strip];
+        const int cslot = int(blockIdx.x) - first;
+        float outv[MT];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            outv[m] = 0.f;
+            if (m < M) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) red[warp * COLS + lane * 8 + j] = acc[m][j];
+                bar_consumers();
+                float v = 0.f;
+#pragma unroll
+                for (int w2 = 0; w2 < CONSUMERS; ++w2) v += red[w2 * COLS + ctid];
+                outv[m] = v;
+                bar_consumers();
+            }
+        }
+        zero();
+        const int64_t n = n0 + ctid;
+        bool last = true;
+        if (p.pad & 2) {  // DEBUG: no cross-CTA reduction
+            if (cslot == 0 && n < Nl) reinterpret_cast<bf16*>(p.work)[n] = __float2bfloat16_rn(outv[0]);
+            continue;
+        }
+        if (ncontrib > 1) {
+            for (int m = 0; m < M; ++m) p.work[((strip * p.max_contrib + cslot) * M + m) * COLS + ctid] = outv[m];
+            __threadfence();
+            bar_consumers();
+            if (ctid == 0) s_last = (atomicAdd(&p.counters[strip], 1u) == unsigned(ncontrib - 1));
+            bar_consumers();
+            last = s_last != 0;
+            if (last) {
+                __threadfence();
+                for (int m = 0; m < M; ++m) {
+                    float v = 0.f;
+                    for (int s2 = 0; s2 < ncontrib; ++s2)
+                        v += __ldcg(&p.work[((strip * p.max_contrib + s2) * M + m) * COLS + ctid]);
+                    outv[m] = v;
+                }
+                if (ctid == 0) p.counters[strip] = 0u;
+            }
+        }
+        if (!last || n >= Nl) continue;
+        const VOperand& cop = mat ? p.c2 : p.c;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            if (m >= M) continue;
+            int32_t idx[VTC_MAX_RANK] = {};
+            idx[0] = m;
+            idx[1] = int32_t(n0);
+            bf16 c = __float2bfloat16_rn(outv[m]);
+            if (p.has_res) {
+                float r;
+                if (p.res.fast_ok) {
+                    dev::Loc l = dev::locate(p.res.m, idx);
+                    r = __bfloat162float(dev::addr<bf16>(p.res.m, l)[int64_t(ctid) * p.res.fast_stride[l.piece]]);
+                } else {
+                    idx[1] = int32_t(n);
+                    r = __bfloat162float(*dev::elem_ptr<bf16>(p.res.m, idx));
+                    idx[1] = int32_t(n0);
+                }
+                c = __float2bfloat16_rn(__bfloat162float(c) + r);
+            }
+            if (cop.fast_ok) {
+                dev::Loc l = dev::locate(cop.m, idx);
+                dev::addr<bf16>(cop.m, l)[int64_t(ctid) * cop.fast_stride[l.piece]] = c;
+            } else {
+                idx[1] = int32_t(n);
+                *dev::elem_ptr<bf16>(cop.m, idx) = c;
+            }
+        }
+    }
+}
+
+template <int MT>
+void launch_mt(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
+    size_t smem = gemv_stream_smem(p.M, p.a_tiles, p.stages);
+    cudaFuncSetAttribute(gemv_stream_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    Tmaps tm;
+    std::memcpy(&tm, p.tmap, sizeof(tm));
+    launch_k(gemv_stream_kernel<MT>, dim3(p.grid), dim3(NT), smem, s, dp, tm);
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+}  // namespace
+
+size_t gemv_stream_smem(int64_t M, int a_tiles, int stages) {
+    size_t bytes = size_t(stages) * TILE_BYTES + size_t(M) * size_t(a_tiles) * KT * sizeof(float) +
+                   size_t(CONSUMERS) * COLS * sizeof(float) + 2 * size_t(stages) * sizeof(uint64_t);
+    // + the statically allocated parameter copy; 227 KB per CTA in total
+    return bytes + sizeof(GemvParams) + 4096 <= 227 * 1024 ? bytes : 0;
+}
+
+bool encode_weight_tmap(void* out128, const void* base, int64_t rows, int64_t cols, int64_t ld) {
+    static EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return EncodeFn(nullptr);
+        return reinterpret_cast<EncodeFn>(f);
+    }();
+    if (!fn || (reinterpret_cast<uintptr_t>(base) % 16) != 0 || (ld * 2) % 16 != 0) return false;
+    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
+    cuuint32_t box[2] = {COLS, KT};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(reinterpret_cast<CUtensorMap*>(out128), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+void launch_gemv_stream(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
+    if (p.M <= 1) launch_mt<1>(p, dp, s);
+    else if (p.M <= 2) launch_mt<2>(p, dp, s);
+    else launch_mt<4>(p, dp, s);
+}
+
+}  // namespace vtc

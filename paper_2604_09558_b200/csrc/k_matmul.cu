@@ -14,6 +14,7 @@
 #include <type_traits>
 
 #include "device.cuh"
+#include "launch.cuh"
 
 namespace vtc {
 namespace {
@@ -77,7 +78,8 @@ __device__ __forceinline__ A mac(A acc, A a, A b, bool exact) {
 
 template <typename T, bool EXACT>
 __global__ void __launch_bounds__(NT) mm_kernel(const MatmulParams* __restrict__ pp) {
-    const MatmulParams& p = *pp;
+    VTC_STAGE_PARAMS(MatmulParams, pp);
+    dev::pdl_wait();
     using A = typename dev::Acc<T>::type;
     __shared__ A As[2][BK][BM + 4];
     __shared__ A Bs[2][BK][BN + 4];
@@ -198,15 +200,15 @@ void launch_matmul(const MatmulParams& p, const MatmulParams* dp, cudaStream_t s
     const bool ex = p.exact != 0;
     switch (p.dt) {
         case KDType::F64:
-            if (ex) mm_kernel<double, true><<<grid, NT, 0, s>>>(dp);
-            else mm_kernel<double, false><<<grid, NT, 0, s>>>(dp);
+            if (ex) launch_k(mm_kernel<double, true>, dim3(grid), dim3(NT), 0, s, dp);
+            else launch_k(mm_kernel<double, false>, dim3(grid), dim3(NT), 0, s, dp);
             break;
         case KDType::F32:
-            if (ex) mm_kernel<float, true><<<grid, NT, 0, s>>>(dp);
-            else mm_kernel<float, false><<<grid, NT, 0, s>>>(dp);
+            if (ex) launch_k(mm_kernel<float, true>, dim3(grid), dim3(NT), 0, s, dp);
+            else launch_k(mm_kernel<float, false>, dim3(grid), dim3(NT), 0, s, dp);
             break;
-        case KDType::I64: mm_kernel<int64_t, true><<<grid, NT, 0, s>>>(dp); break;
-        case KDType::BF16: mm_kernel<bf16, false><<<grid, NT, 0, s>>>(dp); break;
+        case KDType::I64: launch_k(mm_kernel<int64_t, true>, dim3(grid), dim3(NT), 0, s, dp); break;
+        case KDType::BF16: launch_k(mm_kernel<bf16, false>, dim3(grid), dim3(NT), 0, s, dp); break;
     }
 }
 

@@ -9,6 +9,7 @@
 #include <type_traits>
 
 #include "device.cuh"
+#include "launch.cuh"
 #include "rowreduce.cuh"
 
 namespace vtc {
@@ -50,7 +51,8 @@ struct RowIO {
 
 template <typename T>
 __global__ void __launch_bounds__(256) row_kernel(const RowParams* __restrict__ pp) {
-    const RowParams& p = *pp;
+    VTC_STAGE_PARAMS(RowParams, pp);
+    dev::pdl_wait(); dev::pdl_launch_dependents();
     using A = std::conditional_t<std::is_same_v<T, double>, double, float>;
     const int last = p.rank - 1;
     for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
@@ -69,6 +71,7 @@ __global__ void __launch_bounds__(256) row_kernel(const RowParams* __restrict__ 
             A r;
             if constexpr (std::is_same_v<A, double>) r = 1.0 / sqrt(ss / double(p.D) + double(p.eps));
             else r = rsqrtf(ss / float(p.D) + p.eps);
+#pragma unroll 4
             for (int64_t k = threadIdx.x; k < p.D; k += 256)
                 *y.at(k) = dev::from_acc<T>((xv(k) * r) * A(dev::to_acc<T>(*w.at(k))));
         } else if (p.op == RowOp::LayerNorm) {
@@ -77,12 +80,14 @@ __global__ void __launch_bounds__(256) row_kernel(const RowParams* __restrict__ 
             A r;
             if constexpr (std::is_same_v<A, double>) r = 1.0 / sqrt(var + double(p.eps));
             else r = rsqrtf(var + p.eps);
+#pragma unroll 4
             for (int64_t k = threadIdx.x; k < p.D; k += 256)
                 *y.at(k) = dev::from_acc<T>(((xv(k) - mu) * r) * A(dev::to_acc<T>(*w.at(k))) +
                                             A(dev::to_acc<T>(*b.at(k))));
         } else {
             A mx = block_max_256<A>([&](int64_t k) { return xv(k); }, p.D);
             A s = block_sum_256<A>([&](int64_t k) { return A(exp(xv(k) - mx)); }, p.D);
+#pragma unroll 4
             for (int64_t k = threadIdx.x; k < p.D; k += 256) *y.at(k) = dev::from_acc<T>(A(exp(xv(k) - mx)) / s);
         }
     }
@@ -94,9 +99,9 @@ void launch_rowop(const RowParams& p, const RowParams* dp, cudaStream_t s) {
     if (p.rows == 0) return;
     int grid = int(p.rows < 148 * 8 ? p.rows : 148 * 8);
     switch (p.dt) {
-        case KDType::F64: row_kernel<double><<<grid, 256, 0, s>>>(dp); break;
-        case KDType::F32: row_kernel<float><<<grid, 256, 0, s>>>(dp); break;
-        case KDType::BF16: row_kernel<bf16><<<grid, 256, 0, s>>>(dp); break;
+        case KDType::F64: launch_k(row_kernel<double>, dim3(grid), dim3(256), 0, s, dp); break;
+        case KDType::F32: launch_k(row_kernel<float>, dim3(grid), dim3(256), 0, s, dp); break;
+        case KDType::BF16: launch_k(row_kernel<bf16>, dim3(grid), dim3(256), 0, s, dp); break;
         default: break;
     }
 }

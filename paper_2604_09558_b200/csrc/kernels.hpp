@@ -30,6 +30,15 @@ struct VOperand {
     int32_t pad;
 };
 
+// Common first member of every parameter block: optional device-side
+// timeline (VTC_TRACE=1): CTA 0..n thread 0 records globaltimer at kernel entry
+// (atomicMin into trace[2*id]) and exit (atomicMax into trace[2*id+1]).
+struct KHead {
+    unsigned long long* trace;
+    int32_t id;
+    int32_t pad;
+};
+
 // ---- elementwise / copy --------------------------------------------------
 enum class EwOp : int32_t { Copy = 0, Add, Mul, SiLU, GELU };
 
@@ -43,6 +52,7 @@ struct EwInstr {
 constexpr int EW_MAX_IN = 4, EW_MAX_PROG = 8;
 
 struct EwParams {
+    KHead head;
     VOperand out;
     VOperand in[EW_MAX_IN];
     int32_t rank;
@@ -63,6 +73,7 @@ void launch_eltwise(const EwParams& p, const EwParams* dp, cudaStream_t s);
 
 // ---- generic batched matmul (any dtype, any maps) -----------------------
 struct MatmulParams {
+    KHead head;
     VOperand a, b, c;  // a:[...,M,K] fast axis K, b:[...,K,N] fast axis N, c:[...,M,N] fast axis N
     int32_t rank;
     int32_t shape_c[VTC_MAX_RANK];
@@ -81,7 +92,9 @@ void launch_matmul(const MatmulParams& p, const MatmulParams* dp, cudaStream_t s
 // their VirtualTensor maps.  Split-K partials are reduced deterministically by
 // the last-arriving CTA of each N tile.
 enum class GemvPrologue : int32_t { None = 0, SiLUMul = 1, RMSNorm = 2 };
+constexpr int GEMV_MAX_MATS = 2;
 struct GemvParams {
+    KHead head;
     VOperand a, a2, normw, c, res;  // a:[M,K] (fast K); a2: second input of SiLUMul; normw: [K]
     const void* b_base;             // &B[0,0]
     int64_t b_sk;                   // element stride between rows k of B (columns contiguous)
@@ -91,20 +104,35 @@ struct GemvParams {
     int32_t has_res;
     float eps;
     int32_t pad;
-    float* work;                    // [ksplit, M, N] partials   (TMA variant: [strips, max_contrib, M, 256])
-    unsigned int* counters;         // [ceil(N / 256)] arrival counters (self-resetting)
-    // persistent TMA variant
-    int32_t stages, grid, max_contrib, tma;
+    float* work;                    // LDG variant: [ksplit, M, N] partials; stream variant: [strips, max_contrib, M, 256]
+    unsigned int* counters;         // per 256-column strip arrival counters (self-resetting)
+    // ---- persistent TMA-streamed variant (launch_gemv_stream) ----
+    // Up to two weight matrices sharing A and the prologue (horizontally fused
+    // sibling MatMuls, e.g. gate/up): strips [0, strips0) belong to matrix 0,
+    // the rest to matrix 1 (output map c2).
+    int32_t stream;                 // 1: use the streaming kernel
+    int32_t nmat;
+    int32_t stages, grid, max_contrib, a_tiles;  // a_tiles: k-tiles of A staged per CTA
+    int32_t strips0, b_static;      // b_static: weights never written by the plan (prefetch before pdl_wait)
+    int64_t n_mat[GEMV_MAX_MATS];
     const int32_t* strip_first;     // first CTA touching each 256-column strip
     const int32_t* strip_count;     // number of CTAs touching it
+    VOperand c2;
+    alignas(64) unsigned char tmap[GEMV_MAX_MATS][128];  // CUtensorMap per weight matrix (host-encoded)
 };
 void launch_gemv(const GemvParams& p, const GemvParams* dp, cudaStream_t s);
-void launch_gemv_tma(const GemvParams& p, const GemvParams* dp, cudaStream_t s);
-size_t gemv_tma_smem(int64_t M, int64_t K, int stages);
+void launch_gemv_stream(const GemvParams& p, const GemvParams* dp, cudaStream_t s);
+// dynamic shared memory of the streaming kernel; 0 if the configuration does not fit
+size_t gemv_stream_smem(int64_t M, int a_tiles, int stages);
+constexpr int GEMV_STREAM_COLS = 256, GEMV_STREAM_KT = 64;
+// Encode a 2-D TMA descriptor for a row-major bf16 [rows, cols] matrix with
+// row stride `ld` elements and a {256, 64} box; returns false if unsupported.
+bool encode_weight_tmap(void* out128, const void* base, int64_t rows, int64_t cols, int64_t ld);
 
 // ---- row-wise normalisations / softmax -----------------------------------
 enum class RowOp : int32_t { RMSNorm = 0, LayerNorm, Softmax };
 struct RowParams {
+    KHead head;
     VOperand x, w, bias, out;
     int32_t rank;
     int32_t shape[VTC_MAX_RANK];
@@ -118,6 +146,7 @@ void launch_rowop(const RowParams& p, const RowParams* dp, cudaStream_t s);
 
 // ---- attention (split-KV flash decoding with GQA head grouping) ----------
 struct AttnParams {
+    KHead head;
     VOperand q, k, v, o, bias;  // q:[..,H,Sq,d] k,v:[..,H,Sk,d] o:[..,H,Sq,dv]
     int32_t rank;
     int32_t has_bias;
@@ -130,7 +159,14 @@ struct AttnParams {
     KDType dt;
     float* part_o;                 // [Bt, H, Sq, splits, Dv]
     float* part_ml;                // [Bt, H, Sq, splits, 2]
+    // tensor-core decode path (k_attn_decode.cu)
+    int32_t fast;                  // 1: attn_decode_kernel
+    int32_t kv_affine;             // K/V maps affine along the key axis (single piece)
+    int64_t k_sstride, v_sstride;  // element stride between consecutive keys
+    unsigned int* counters;        // [Bt * H / group] split arrival counters (fused combine)
 };
 void launch_attention(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
+bool attn_decode_supported(const AttnParams& p);
+void launch_attn_decode(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 
 }  // namespace vtc

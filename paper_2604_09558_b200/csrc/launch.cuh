@@ -1,0 +1,41 @@
+// Host-side kernel launch with programmatic dependent launch (PDL).
+//
+// Every vtc kernel stages its parameter block, then calls dev::pdl_wait()
+// before touching data written by earlier kernels, and
+// dev::pdl_launch_dependents() once its own CTAs are resident.  Launching
+// with programmaticStreamSerialization lets the next kernel of the plan be
+// scheduled while the current one drains, so launch latency and parameter
+// staging overlap the previous kernel's tail (also inside CUDA graphs).
+// VTC_NO_PDL=1 in the environment launches with plain stream order (A/B).
+#pragma once
+
+#include <cstdlib>
+
+#include <cuda_runtime.h>
+
+namespace vtc {
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("VTC_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+}  // namespace vtc

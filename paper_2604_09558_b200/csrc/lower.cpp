@@ -134,6 +134,13 @@ bool lower_piece(const VPiece& p, vtc_piece& out, uint64_t& bad_axes) {
     }
     out.ndigits = int16_t(nd);
     out.ngroups = int16_t(ng);
+    out.affine = ng == 0 ? 1 : 0;
+    for (int a = 0; a < VTC_MAX_RANK; ++a) out.aff[a] = 0;
+    for (int t = 0; t < nd; ++t) {
+        const vtc_digit& d = out.dig[t];
+        if (d.div != 1 || d.mod != 0 || d.group >= 0) out.affine = 0;
+        else out.aff[d.axis] += d.coeff;
+    }
     return ok;
 }
 

@@ -13,6 +13,7 @@ __device__ __forceinline__ Acc block_sum_256(F f, int64_t D) {
     __shared__ Acc s_part[8];
     __shared__ Acc s_total;
     Acc s = Acc(0);
+#pragma unroll 8
     for (int64_t k = threadIdx.x; k < D; k += 256) s += f(k);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -37,6 +38,7 @@ __device__ __forceinline__ Acc block_sum_256_bar1(F f, int64_t D) {
     __shared__ Acc s_part[8];
     __shared__ Acc s_total;
     Acc s = Acc(0);
+#pragma unroll 8
     for (int64_t k = threadIdx.x; k < D; k += 256) s += f(k);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -59,6 +61,7 @@ __device__ __forceinline__ Acc block_max_256(F f, int64_t D) {
     __shared__ Acc s_part[8];
     __shared__ Acc s_total;
     Acc s = -INFINITY;
+#pragma unroll 8
     for (int64_t k = threadIdx.x; k < D; k += 256) s = max(s, f(k));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s = max(s, __shfl_xor_sync(0xffffffffu, s, o));

@@ -155,3 +155,50 @@ def test_llama_layer_c2_full_size(vtc, oracle):
     assert p.info()["data_movement_launches"] == 0
     err = _relerr(oracle.bf16_to_f32(got["y"]), oracle.bf16_to_f32(want))
     assert err < 2e-2, err
+
+
+def _gqa_attention_graph(B, Hq, Hkv, L, S, Sq, hd=128, causal=False, via_cache=True):
+    """Q [B,Hq,Sq,hd]; K/V through the decoder's virtual chain over a pos-major
+    cache [L,B,Hkv,hd]: Slice[0,S) -> Transpose -> Unsqueeze -> Expand(G) -> Reshape."""
+    import math
+    from paper_2604_09558_b200.workloads import GraphBuilder
+    G = Hq // Hkv
+    g = GraphBuilder("bf16")
+    g.input("q", [B, Hq, Sq, hd])
+    if via_cache:
+        for c in ("k", "v"):
+            g.input(f"{c}_cache", [L, B, Hkv, hd])
+            src = f"{c}_cache"
+            if S < L:
+                src = g.node(f"{c}_sl", "Slice", [src], f"{c}_s", {"axes": [0], "starts": [0], "ends": [S]})
+            g.node(f"{c}_t", "Transpose", [src], f"{c}_t", {"perm": [1, 2, 0, 3]})
+            g.node(f"{c}_u", "Unsqueeze", [f"{c}_t"], f"{c}_u", {"axis": 2})
+            g.node(f"{c}_e", "Expand", [f"{c}_u"], f"{c}_e", {"shape": [B, Hkv, G, S, hd]})
+            g.node(f"{c}_r", "Reshape", [f"{c}_e"], f"{c}_h", {"shape": [B, Hq, S, hd]})
+    else:
+        g.input("k_h", [B, Hq, S, hd])
+        g.input("v_h", [B, Hq, S, hd])
+    g.node("attn", "Attention", ["q", "k_h", "v_h"], "o", {"scale": 1.0 / math.sqrt(hd), "causal": causal},
+           out_kind="output")
+    return g.doc()
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(B=1, Hq=32, Hkv=8, L=2048, S=2048, Sq=1),          # C2 shape
+    dict(B=3, Hq=8, Hkv=2, L=300, S=257, Sq=1),             # ragged split / tile tails
+    dict(B=2, Hq=4, Hkv=4, L=64, S=64, Sq=1),               # no GQA sharing (G = 1)
+    dict(B=2, Hq=8, Hkv=2, L=96, S=90, Sq=4, causal=True),  # G*Sq = 16 query rows, causal
+    dict(B=2, Hq=8, Hkv=2, L=40, S=40, Sq=2, via_cache=False),  # physical K/V
+])
+def test_attention_tensor_core_path_matches_oracle(vtc, oracle, cfg):
+    doc = _gqa_attention_graph(**cfg)
+    x = oracle.random_inputs(doc, seed=9)
+    want = oracle.bf16_to_f32(oracle.execute(doc, x)["o"])
+    got, p = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
+    kinds = {l["kernel"] for l in p.info()["launches"]}
+    assert kinds & {"attn_decode_tc", "attn_decode_tc_splitkv"}, kinds
+    assert p.info()["data_movement_launches"] == 0
+    err = _relerr(oracle.bf16_to_f32(got["o"]), want)
+    assert err < 2e-2, err
+    got_m, _ = _run(vtc, doc, x, vtc.MATERIALIZE)
+    assert _relerr(oracle.bf16_to_f32(got_m["o"]), want) < 2e-2

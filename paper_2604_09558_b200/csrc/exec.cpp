@@ -304,7 +304,9 @@ void Executor::prepare(bool dry) {
         }
         int a_tiles = int(std::min<int64_t>(kts, maxrange));
         int stages = 0;
-        for (int st = 6; st >= 3 && !stages; --st)
+        int max_st = 3;
+        if (const char* e = std::getenv("VTC_GEMV_STAGES")) max_st = std::atoi(e);
+        for (int st = max_st; st >= 2 && !stages; --st)
             if (gemv_stream_smem(p.M, a_tiles, st)) stages = st;
         if (!stages) return false;
         if (!impl_->dry && !encode_weight_tmap(p.tmap[0], reinterpret_cast<const void*>(b_ptr) , p.K, p.N, p.b_sk))
@@ -320,6 +322,8 @@ void Executor::prepare(bool dry) {
         p.max_contrib = maxc;
         p.a_tiles = a_tiles;
         p.b_static = written_roots.count(b_root) ? 0 : 1;
+        p.pre_stages = 1;
+        if (const char* e = std::getenv("VTC_GEMV_PRE")) p.pre_stages = std::atoi(e);
         p.work = static_cast<float*>(impl_->alloc(size_t(strips * maxc * p.M * COLS) * sizeof(float), false));
         p.counters = static_cast<unsigned*>(impl_->alloc(size_t(strips) * sizeof(unsigned), true));
         auto* dfirst = static_cast<int32_t*>(impl_->alloc(size_t(strips) * 4, false));
@@ -864,7 +868,8 @@ void Executor::prepare(bool dry) {
                 int splits = opt_.attn_splits;
                 const int kgran = p.fast ? 64 : 32;  // keys per split granule (4 warps x 16 on the fast path)
                 if (splits <= 0) {
-                    int64_t target = p.fast ? 148 * 2 * 4 : 148 * 2;
+                    // fast path: one wave (2 CTAs per SM) when the KV is short, ~4 waves when long
+                    int64_t target = p.fast ? (int64_t(p.Sk) * qblocks >= 148 * 2 * 512 ? 148 * 2 * 4 : 148 * 2) : 148 * 2;
                     splits = int((target + qblocks - 1) / qblocks);
                     splits = std::max(1, std::min(splits, (p.Sk + kgran - 1) / kgran));
                 }
@@ -874,7 +879,7 @@ void Executor::prepare(bool dry) {
                 p.splits = splits;
                 p.chunk = chunk;
                 L->kernel = p.fast ? (splits > 1 ? "attn_decode_tc_splitkv" : "attn_decode_tc") : (splits > 1 ? "attention_splitkv" : "attention");
-                if (splits > 1 && p.fast)
+                if (splits > 1 && p.fast && std::getenv("VTC_ATTN_FUSED_COMBINE"))
                     p.counters = static_cast<unsigned*>(impl_->alloc(size_t(qblocks) * sizeof(unsigned), true));
                 if (splits > 1) {
                     int64_t rows = int64_t(p.Bt) * p.H * p.Sq;

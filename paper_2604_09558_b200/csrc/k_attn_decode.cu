@@ -32,7 +32,7 @@ namespace vtc {
 namespace {
 
 using dev::bf16;
-constexpr int WARPS = 4, NT = WARPS * 32, TK = 16, D = 128, STAGES = 3;
+constexpr int WARPS = 4, NT = WARPS * 32, TK = 16, D = 128, STAGES = 2;
 constexpr int ROWB = D * 2;                     // bytes per K/V row
 constexpr int TILEB = TK * ROWB;                // 4 KB per K (or V) tile
 constexpr int STAGEB = 2 * TILEB;               // K + V
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
             }
         }
     }
-    if (p.splits == 1) return;
+    if (p.splits == 1 || p.counters == nullptr) return;  // no counters: combine_fast_kernel merges
     if (tid == 0) dev::trace_point(p.head, 6);
 
     // ---- split-KV combine, fused: the last CTA of this query group to finish
@@ -402,6 +402,49 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
     }
 }
 
+// Split merge as a separate kernel: one CTA per (lead, h, sq) output row, all
+// split partials of the row loaded at once (one memory round trip).
+__global__ void __launch_bounds__(NT) combine_fast_kernel(const AttnParams* __restrict__ pp) {
+    VTC_STAGE_PARAMS(AttnParams, pp);
+    __shared__ float s_ml[2 * 256];
+    __shared__ bf16* s_out;
+    __shared__ int64_t s_ostride;
+    const int64_t row = blockIdx.x;  // (lead, h, sq)
+    const int S = p.splits;
+    if (threadIdx.x == 0) {
+        const int r = p.rank;
+        int64_t rr = row;
+        int32_t idx[VTC_MAX_RANK] = {};
+        idx[r - 2] = int32_t(rr % p.Sq);
+        rr /= p.Sq;
+        idx[r - 3] = int32_t(rr % p.H);
+        rr /= p.H;
+        for (int a = r - 4; a >= 0; --a) {
+            idx[a] = int32_t(rr % p.o.m.shape[a]);
+            rr /= p.o.m.shape[a];
+        }
+        dev::Loc l = dev::locate(p.o.m, idx);
+        s_out = dev::addr<bf16>(p.o.m, l);
+        s_ostride = p.o.fast_stride[l.piece];
+    }
+    dev::pdl_wait();
+    dev::pdl_launch_dependents();
+    for (int e = threadIdx.x; e < 2 * S; e += NT) s_ml[e] = __ldcg(&p.part_ml[row * S * 2 + e]);
+    __syncthreads();
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < S; ++s2) M = fmaxf(M, s_ml[2 * s2]);
+    const int d = threadIdx.x;
+    float L = 0.f, acc = 0.f;
+#pragma unroll 8
+    for (int s2 = 0; s2 < S; ++s2) {
+        const float m = s_ml[2 * s2];
+        const float f = m == -INFINITY ? 0.f : exp2f(m - M);
+        L += f * s_ml[2 * s2 + 1];
+        acc += f * __ldcg(&p.part_o[(row * S + s2) * D + d]);
+    }
+    s_out[int64_t(d) * s_ostride] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+}
+
 }  // namespace
 
 bool attn_decode_supported(const AttnParams& p) {
@@ -417,6 +460,8 @@ void launch_attn_decode(const AttnParams& p, const AttnParams* dp, cudaStream_t 
     size_t smem = attn_decode_smem();
     cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     launch_k(attn_decode_kernel, grid, dim3(NT), smem, s, dp);
+    if (p.splits > 1 && p.counters == nullptr)
+        launch_k(combine_fast_kernel, dim3(unsigned(int64_t(p.Bt) * p.H * p.Sq)), dim3(NT), 0, s, dp);
 }
 
 }  // namespace vtc

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(NT) gemv_kernel(const GemvParams* __restrict__
             if (p.a.fast_ok) {
                 int64_t st;
                 const bf16* b0 = row_ptr(p.a, m, 0, st);
-                ss = block_sum_256<float>([&](int64_t k) { float v = __bfloat162float(b0[k * st]); return v * v; }, p.K);
+                ss = block_sumsq_bf16_fast<false>(b0, st, p.K);
             } else {
                 ss = block_sumsq_row_bf16(p.a, m, p.K);
             }

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
     float* red = sA + size_t(p.M) * p.a_tiles * KT;                              // [CONSUMERS][COLS]
     uint64_t* full = reinterpret_cast<uint64_t*>(red + CONSUMERS * COLS);
     uint64_t* empty = full + stages;
+    __shared__ uint64_t go;  // consumers have issued their activation loads
     __shared__ float s_rs[4];
     __shared__ unsigned s_last;
 
@@ -104,6 +105,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], CONSUMERS);
         }
+        mbar_init(&go, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -117,7 +119,12 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
         if (!p.b_static) dev::pdl_wait();
         int stage = 0;
         uint32_t phase = 0;
+        // Only PRE tiles go out before the consumers have issued their
+        // activation loads: a full ring of weight requests queued ahead of
+        // them would put every activation load behind ~MBs of HBM traffic.
+        const int64_t u_pre = u_begin + (p.pre_stages < stages ? p.pre_stages : stages);
         for (int64_t u = u_begin; u < u_end; ++u) {
+            if (u == u_pre) mbar_wait(&go, 0);
             const int64_t strip = u / ktiles, kt = u % ktiles;
             const int mat = strip < p.strips0 ? 0 : 1;
             const int64_t n0 = (strip - (mat ? p.strips0 : 0)) * COLS;
@@ -152,38 +159,88 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
         idx[1] = int32_t(k);
         return __bfloat162float(*dev::elem_ptr<bf16>(op.m, idx));
     };
+    bool go_sent = false;
+    auto send_go = [&] {
+        if (go_sent) return;
+        go_sent = true;
+        bar_consumers();  // every consumer thread has issued its loads (they are in flight)
+        if (ctid == 0) mbar_arrive(&go);
+    };
+    constexpr int XR = 16, EV = 8;  // register budgets of the fast prologue
     for (int m = 0; m < M; ++m) {
-        if (p.pad & 1) {  // DEBUG: skip the A prologue
-            for (int64_t e = ctid; e < a_cols; e += CONSUMERS * 32) sA[size_t(m) * a_cols + e] = 1.f;
-            continue;
-        }
         int64_t sa = 0, sa2 = 0, sw = 0;
         const bf16* pa = p.a.fast_ok ? row_ptr(p.a, m, sa) : nullptr;
         const bf16* pa2 = (p.prologue == GemvPrologue::SiLUMul && p.a2.fast_ok) ? row_ptr(p.a2, m, sa2) : nullptr;
         const bf16* pw = nullptr;
+        if (p.prologue == GemvPrologue::RMSNorm && p.normw.fast_ok) {
+            int32_t widx[VTC_MAX_RANK] = {};
+            dev::Loc l = dev::locate(p.normw.m, widx);
+            sw = p.normw.fast_stride[l.piece];
+            pw = dev::addr<bf16>(p.normw.m, l);
+        }
+        if (ctid == 0) dev::trace_point(p.head, 7);  // operand rows located
+        const bool fast = pa && (p.prologue != GemvPrologue::SiLUMul || pa2) && (p.prologue != GemvPrologue::RMSNorm || pw);
+        const bool regs = fast && (p.prologue != GemvPrologue::RMSNorm || p.K <= XR * 256) && a_cols <= EV * 256;
         float rs = 0.f;
-        if (p.prologue == GemvPrologue::RMSNorm) {
-            if (p.normw.fast_ok) {
-                int32_t widx[VTC_MAX_RANK] = {};
-                dev::Loc l = dev::locate(p.normw.m, widx);
-                sw = p.normw.fast_stride[l.piece];
-                pw = dev::addr<bf16>(p.normw.m, l);
+        if (regs) {
+            // phase 1: issue every load of this row (registers), then let the producer go
+            float xr[XR], av[EV], a2v[EV], wv[EV];
+            if (p.prologue == GemvPrologue::RMSNorm) {
+#pragma unroll
+                for (int j = 0; j < XR; ++j) {
+                    const int64_t k = ctid + int64_t(j) * 256;
+                    xr[j] = k < p.K ? __bfloat162float(pa[k * sa]) : 0.f;
+                }
             }
+#pragma unroll
+            for (int i = 0; i < EV; ++i) {
+                const int64_t e = ctid + int64_t(i) * 256;
+                const int64_t k = ((kt_first + e / KT) % ktiles) * KT + e % KT;
+                const bool ok = e < a_cols && k < p.K;
+                av[i] = ok ? __bfloat162float(pa[k * sa]) : 0.f;
+                if (p.prologue == GemvPrologue::SiLUMul) a2v[i] = ok ? __bfloat162float(pa2[k * sa2]) : 0.f;
+                if (p.prologue == GemvPrologue::RMSNorm) wv[i] = ok ? __bfloat162float(pw[k * sw]) : 0.f;
+            }
+            send_go();
+            // phase 2: RMSNorm statistics in block_sum_256's exact order
+            if (p.prologue == GemvPrologue::RMSNorm) {
+                float s = 0.f;
+#pragma unroll
+                for (int j = 0; j < XR; ++j)
+                    if (ctid + int64_t(j) * 256 < p.K) s += xr[j] * xr[j];
+                const float ss = block_sum_regs_bar1(s);
+                rs = rsqrtf(ss / float(p.K) + p.eps);
+                if (ctid == 0) dev::trace_point(p.head, 6);  // norm reduction done
+            }
+#pragma unroll
+            for (int i = 0; i < EV; ++i) {
+                const int64_t e = ctid + int64_t(i) * 256;
+                if (e >= a_cols) continue;
+                float v = av[i];
+                if (p.prologue == GemvPrologue::SiLUMul) {
+                    const float sg = __bfloat162float(__float2bfloat16_rn(v / (1.0f + expf(-v))));
+                    v = __bfloat162float(__float2bfloat16_rn(sg * a2v[i]));
+                } else if (p.prologue == GemvPrologue::RMSNorm) {
+                    v = __bfloat162float(__float2bfloat16_rn(v * rs * wv[i]));
+                }
+                sA[size_t(m) * a_cols + e] = v;
+            }
+            continue;
+        }
+        send_go();
+        if (p.prologue == GemvPrologue::RMSNorm) {
             // the same 256-thread reduction order as the standalone RMSNorm kernel
-            float ss = block_sum_256_bar1<float>(
-                [&](int64_t k) {
-                    float v = pa ? __bfloat162float(pa[k * sa]) : elem(p.a, m, k);
-                    return v * v;
-                },
-                p.K);
+            float ss = pa ? block_sumsq_bf16_fast<true>(pa, sa, p.K)
+                          : block_sum_256_bar1<float>(
+                                [&](int64_t k) {
+                                    float v = elem(p.a, m, k);
+                                    return v * v;
+                                },
+                                p.K);
             if (ctid == 0) s_rs[m] = rsqrtf(ss / float(p.K) + p.eps);
-            if (ctid == 0) dev::trace_point(p.head, 6);  // norm reduction done
             bar_consumers();
             rs = s_rs[m];
         }
-        // only the k-tiles this CTA's units touch: slot j <-> k-tile (kt_first + j) mod ktiles
-        // (unrolled so the loads of several elements are in flight together)
-#pragma unroll 4
         for (int64_t e = ctid; e < a_cols; e += CONSUMERS * 32) {
             const int64_t kt = (kt_first + e / KT) % ktiles;
             const int64_t k = kt * KT + e % KT;
@@ -209,6 +266,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
             sA[size_t(m) * a_cols + e] = v;
         }
     }
+    send_go();
     bar_consumers();
     if (ctid == 0) dev::trace_point(p.head, 2);  // A prologue done
 

@@ -67,7 +67,13 @@ __global__ void __launch_bounds__(256) row_kernel(const RowParams* __restrict__ 
         if (p.op != RowOp::Softmax) w.init(p.w, z, 0);
         if (p.op == RowOp::LayerNorm) b.init(p.bias, z, 0);
         if (p.op == RowOp::RMSNorm) {
-            A ss = block_sum_256<A>([&](int64_t k) { A v = xv(k); return v * v; }, p.D);
+            A ss;
+            if constexpr (std::is_same_v<T, bf16>) {
+                if (x.fast) ss = block_sumsq_bf16_fast<false>(x.base, x.stride, p.D);
+                else ss = block_sum_256<A>([&](int64_t k) { A v = xv(k); return v * v; }, p.D);
+            } else {
+                ss = block_sum_256<A>([&](int64_t k) { A v = xv(k); return v * v; }, p.D);
+            }
             A r;
             if constexpr (std::is_same_v<A, double>) r = 1.0 / sqrt(ss / double(p.D) + double(p.eps));
             else r = rsqrtf(ss / float(p.D) + p.eps);

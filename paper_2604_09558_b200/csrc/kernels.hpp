@@ -114,6 +114,7 @@ struct GemvParams {
     int32_t nmat;
     int32_t stages, grid, max_contrib, a_tiles;  // a_tiles: k-tiles of A staged per CTA
     int32_t strips0, b_static;      // b_static: weights never written by the plan (prefetch before pdl_wait)
+    int32_t pre_stages, pad3;       // weight tiles issued before the activation loads
     int64_t n_mat[GEMV_MAX_MATS];
     const int32_t* strip_first;     // first CTA touching each 256-column strip
     const int32_t* strip_count;     // number of CTAs touching it

@@ -70,7 +70,8 @@ enum vtc_plan_flags {
     VTC_FLAG_FAST_FP = 1u << 0,  /* generic f32/f64 MatMul with FMA instead of the bit-exact mul+add */
     VTC_FLAG_NO_GEMV = 1u << 1,  /* disable the weight-streaming decode kernel */
     VTC_FLAG_NO_FUSE = 1u << 2,  /* disable RMSNorm/SiLU*Mul/residual and elementwise-tree fusion */
-    VTC_FLAG_GEMV_LDG = 1u << 3  /* decode GEMV on the LDG split-K kernel instead of the persistent TMA-streamed one */
+    VTC_FLAG_GEMV_LDG = 1u << 3, /* decode GEMV on the LDG split-K kernel instead of the persistent TMA-streamed one */
+    VTC_FLAG_NO_TC = 1u << 4     /* bf16 MatMul with M > 16 on the generic tiled kernel instead of tcgen05 */
 };
 
 typedef struct vtc_graph vtc_graph;

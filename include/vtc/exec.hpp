@@ -22,6 +22,7 @@ namespace vtc {
 struct ExecOptions {
     bool exact_fp = true;     // generic f32/f64 MatMul: unfused mul+add (bit-exact vs CPU reference)
     bool use_gemv = true;     // bf16 decode projections on the weight-streaming kernel
+    bool use_tc = true;       // bf16 MatMul with M > 16 on the tcgen05 GEMM
     bool gemv_stream = true;  // persistent TMA-streamed GEMV for M <= 4 (else the LDG split-K GEMV)
     bool fuse = true;         // RMSNorm->MatMul, SiLU*Mul->MatMul, MatMul->Add(residual) fusion
     int attn_splits = 0;      // 0: automatic

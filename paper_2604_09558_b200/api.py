@@ -37,7 +37,7 @@ ERRORS = {code: type(name, (VtcError,), {"code": code}) for code, name in _ERROR
 globals().update({cls.__name__: cls for cls in ERRORS.values()})
 
 MATERIALIZE, SELECTED, MAX_ELIMINATION = 0, 1, 2
-FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE, FLAG_GEMV_LDG = 1, 2, 4, 8
+FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE, FLAG_GEMV_LDG, FLAG_NO_TC = 1, 2, 4, 8, 16
 
 NP_DTYPES = {"f64": np.float64, "f32": np.float32, "i64": np.int64, "bf16": np.uint16}
 

@@ -155,6 +155,7 @@ int vtc_plan_create(vtc_graph* g, int mode, const int32_t* selected, int32_t n_s
         opt.use_gemv = !(flags & VTC_FLAG_NO_GEMV);
         opt.fuse = !(flags & VTC_FLAG_NO_FUSE);
         opt.gemv_stream = (flags & VTC_FLAG_GEMV_LDG) == 0;
+        opt.use_tc = (flags & VTC_FLAG_NO_TC) == 0;
         auto p = std::make_unique<vtc_plan>();
         p->graph = g;
         p->flags = flags;

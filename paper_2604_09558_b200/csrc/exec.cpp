@@ -535,11 +535,35 @@ void Executor::prepare(bool dry) {
         if (p.off.c0 % 8 != 0 || *sk % 8 != 0) return false;
         return true;
     };
+    // tcgen05 GEMM: bf16 2-D MatMul with M > 16, B physical (single affine piece, N unit
+    // stride), A a single affine piece with unit stride along K (TMA-readable)
+    auto affine2d = [&](const VMap& m, int64_t& ld, int64_t& c0) -> bool {
+        if (m.pieces().size() != 1) return false;
+        const VPiece& pc = m.pieces()[0];
+        for (const auto& tm : pc.off.t)
+            if (tm.a->kind != AtomKind::Axis) return false;
+        auto s0 = VMap::tile_stride(pc, 0, m.shape()[0]);
+        auto s1 = VMap::tile_stride(pc, 1, m.shape()[1]);
+        if (!s0 || !s1 || *s1 != 1) return false;
+        ld = *s0;
+        c0 = pc.off.c0;
+        return ld % 8 == 0 && c0 % 8 == 0;
+    };
+    auto tc_eligible = [&](const OpNode& n) {
+        if (n.kind != OpKind::MatMul || !opt_.use_tc || gemv_eligible(n)) return false;
+        const TensorSpec& A = g_.tensor(n.inputs[0]);
+        const TensorSpec& B = g_.tensor(n.inputs[1]);
+        if (A.dtype != DType::BF16 || A.shape.size() != 2 || A.shape[0] <= 16) return false;
+        int64_t ld, c0;
+        return affine2d(map_of(n.inputs[0]), ld, c0) && affine2d(map_of(n.inputs[1]), ld, c0) && B.shape[1] % 8 == 0 &&
+               A.shape[1] % 8 == 0;
+    };
     if (opt_.fuse) {
         for (const auto& n : g_.nodes()) {
-            if (!gemv_eligible(n)) continue;
+            const bool tc = tc_eligible(n);
+            if (!gemv_eligible(n) && !tc) continue;
             GemvFusion f;
-            const OpNode* pa = g_.producer(n.inputs[0]);
+            const OpNode* pa = tc ? nullptr : g_.producer(n.inputs[0]);  // TMA-fed A: no prologue fusion
             if (pa && pa->kind == OpKind::RMSNorm && g_.tensor(n.inputs[0]).kind == TensorKind::Intermediate &&
                 g_.tensor(pa->inputs[0]).shape.size() == 2) {
                 bool all = true;
@@ -775,6 +799,57 @@ void Executor::prepare(bool dry) {
                     }
                     push(std::move(L));
                     break;
+                }
+                if (tc_eligible(n)) {
+                    auto T = std::make_unique<LaunchT<GemmTcParams, launch_gemm_tc>>();
+                    T->node = n.id;
+                    T->kernel = "gemm_tc_bf16";
+                    GemmTcParams& p = T->p;
+                    std::memset(&p, 0, sizeof(p));
+                    p.M = M;
+                    p.N = N;
+                    p.K = K;
+                    GemvFusion f;
+                    auto fit = fusion.find(n.id);
+                    if (fit != fusion.end()) f = fit->second;
+                    const std::string& cout = f.add ? f.add->outputs[0] : n.outputs[0];
+                    p.bn = 256;
+                    p.c = operand(map_of(cout), 1, p.bn, es);
+                    if (!p.c.fast_ok || N % 256 != 0) {
+                        p.bn = 128;
+                        p.c = operand(map_of(cout), 1, p.bn, es);
+                    }
+                    bool ok = p.c.fast_ok != 0;
+                    if (f.add) {
+                        const std::string& other = f.add->inputs[0] == n.outputs[0] ? f.add->inputs[1] : f.add->inputs[0];
+                        p.has_res = 1;
+                        p.res = operand(map_of(other), 1, p.bn, es);
+                        ok = ok && p.res.fast_ok;
+                        T->node += "+" + f.add->id;
+                    }
+                    int64_t lda, ca, ldb, cb;
+                    affine2d(map_of(n.inputs[0]), lda, ca);
+                    affine2d(map_of(n.inputs[1]), ldb, cb);
+                    const VMap& am = map_of(n.inputs[0]);
+                    const VMap& bmm = map_of(n.inputs[1]);
+                    const char* abase = reinterpret_cast<const char*>(target(am.pieces()[0].target).ptr) + ca * es;
+                    const char* bbase = reinterpret_cast<const char*>(target(bmm.pieces()[0].target).ptr) + cb * es;
+                    if (ok && !impl_->dry) ok = gemm_tc_encode(p, abase, lda, bbase, ldb);
+                    if (ok) {
+                        int64_t tiles = (M + 127) / 128 * ((N + p.bn - 1) / p.bn);
+                        int64_t ktiles = (K + 63) / 64;
+                        int sms = 148;
+                        if (!impl_->dry) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+                        int64_t splits = tiles >= sms ? 1 : std::min<int64_t>(ktiles, std::max<int64_t>(1, sms / tiles));
+                        p.splits = int32_t(splits);
+                        if (splits > 1) {
+                            p.work = static_cast<float*>(impl_->alloc(size_t(tiles * splits * 128 * p.bn) * 4, false));
+                            p.counters = static_cast<unsigned*>(impl_->alloc(size_t(tiles) * 4, true));
+                        }
+                        push(std::move(T));
+                        break;
+                    }
+                    if (f.add) throw UnsupportedError("gemm_tc: fused residual without a tensor-core launch for " + n.id);
                 }
                 auto L = std::make_unique<LaunchT<MatmulParams, launch_matmul>>();
                 L->node = n.id;

@@ -1,0 +1,365 @@
+// bf16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// C[M, N] = A[M, K] . B[K, N] (+ residual), bf16 in, fp32 accumulation, the
+// reference's matmul_kernel (proj/src/executor.cpp:230-249) for the projection
+// GEMMs of a VTC-planned decoder at batch / prefill sizes (M > 16).
+//
+//   * A is read by TMA through its VirtualTensor map when the map is one
+//     affine piece with unit stride along K (the map's row stride becomes the
+//     TMA row pitch, its base the TMA origin -- a split / slice / reshape view
+//     of the producer's buffer costs nothing); K-major, 128-byte swizzle;
+//   * B (the weight, [K, N] row-major) is the MN-major UMMA operand: four
+//     64-column TMA boxes per stage, 128-byte swizzle;
+//   * one CTA per 128 x BN output tile (split along K when the tile grid is
+//     smaller than the SM count): warp 0 = TMA producer, warp 1 = MMA issuer
+//     (one thread issues tcgen05.mma M128 x N x K16 into a TMEM accumulator,
+//     tcgen05.commit releases the smem stage), warps 0-3 = epilogue
+//     (tcgen05.ld 32x32b -> registers -> bf16 -> the output map, with the
+//     optional fused residual Add rounded like the unfused operator);
+//   * K splits write fp32 partial tiles; the last CTA of a tile sums them in
+//     split order (deterministic) and runs the epilogue.
+#include <cuda.h>
+
+#include <cstring>
+
+#include "device.cuh"
+#include "launch.cuh"
+
+namespace vtc {
+namespace {
+
+using dev::bf16;
+constexpr int BM = 128, BK = 64, UK = 16, NTHREADS = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint64_t* bar,
+                                       uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// UMMA shared-memory matrix descriptor: start >> 4 [0,14), LBO >> 4 [16,30),
+// SBO >> 4 [32,46), version 1 [46,48), layout SWIZZLE_128B = 2 [61,64).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);
+    d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(2) << 61;
+    return d;
+}
+// kind::f16 instruction descriptor: D f32, A/B bf16, A K-major, B MN-major.
+__host__ __device__ constexpr uint32_t instr_desc(int m, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) | (uint32_t(n >> 3) << 17) |
+           (uint32_t(m >> 4) << 24);
+}
+
+struct Tmaps {
+    CUtensorMap a, b;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams* __restrict__ pp,
+                                                               const __grid_constant__ Tmaps tm) {
+    VTC_STAGE_PARAMS(GemmTcParams, pp);
+    constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[STAGES], empty[STAGES], done;
+    __shared__ uint32_t s_tmem;
+    __shared__ unsigned s_last;
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int tiles_n = int((p.N + BN - 1) / BN);
+    const int tile = blockIdx.x;
+    const int tm_ = tile / tiles_n, tn = tile % tiles_n;
+    const int64_t m0 = int64_t(tm_) * BM, n0 = int64_t(tn) * BN;
+    const int split = blockIdx.y;
+    const int ktiles = int((p.K + BK - 1) / BK);
+    const int kt0 = int(int64_t(ktiles) * split / p.splits), kt1 = int(int64_t(ktiles) * (split + 1) / p.splits);
+    const int nk = kt1 - kt0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {  // TMEM accumulator: 128 lanes x BN fp32 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                     "r"(BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s_tmem;
+    dev::pdl_launch_dependents();
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer ----------------
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.b)) : "memory");
+        const uint64_t pol_b = dev::evict_first_policy();  // weights: read once
+        const uint64_t pol_a = evict_last_policy();        // activations: re-read by every N tile
+        dev::pdl_wait();  // A is produced by earlier kernels
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % STAGES;
+            const uint32_t ph = uint32_t(i / STAGES) & 1u;
+            mbar_wait(&empty[s], ph ^ 1u);
+            mbar_expect_tx(&full[s], STAGE_BYTES);
+            unsigned char* sa = smem + size_t(s) * STAGE_BYTES;
+            unsigned char* sb = sa + A_BYTES;
+            const int32_t k0 = int32_t(kt0 + i) * BK;
+            tma_2d(sa, &tm.a, k0, int32_t(m0), &full[s], pol_a);
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+                tma_2d(sb + j * (BK * 128), &tm.b, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer ----------------
+        dev::pdl_wait();
+        constexpr uint32_t idesc = instr_desc(BM, BN);
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % STAGES;
+            const uint32_t ph = uint32_t(i / STAGES) & 1u;
+            mbar_wait(&full[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t sa = smem_u32(smem + size_t(s) * STAGE_BYTES);
+            const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / UK; ++k) {
+                // A: K-major SW128, +32 B per K16 step; B: MN-major SW128, +2 KB (16 rows) per step,
+                // 64-column chunks BK*128 B apart (LBO), 8-row groups 1 KB apart (SBO)
+                const uint64_t da = smem_desc(sa + k * 32, 16, 1024);
+                const uint64_t db = smem_desc(sb + k * 2048, BK * 128, 1024);
+                const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(&empty[s]))
+                         : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&done))
+                     : "memory");
+    }
+
+    // ---------------- epilogue: all 4 warps, thread = accumulator row ----------------
+    dev::pdl_wait();
+    __syncwarp();
+    mbar_wait(&done, 0);
+    __syncwarp();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = warp * 32 + lane;  // TMEM lane == tile row
+    const int64_t m = m0 + row;
+    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+
+    auto tmem_ld16 = [&](int c, float (&v)[16]) {
+        uint32_t r[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(trow + uint32_t(c)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+    };
+
+    bool do_epilogue = true;
+    float* wtile = nullptr;
+    if (p.splits > 1) {
+        // fp32 partial tile -> workspace [tile][split][BM][BN]; the last split reduces
+        wtile = p.work + (int64_t(tile) * p.splits) * BM * BN;
+        float* mine = wtile + int64_t(split) * BM * BN + int64_t(row) * BN;
+        for (int c = 0; c < BN; c += 16) {
+            float v[16];
+            if (nk > 0) tmem_ld16(c, v);
+            else
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(mine + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[tile], 1u) == unsigned(p.splits - 1) ? 1u : 0u;
+        __syncthreads();
+        do_epilogue = s_last != 0;
+        if (do_epilogue) {
+            __threadfence();
+            if (threadIdx.x == 0) p.counters[tile] = 0u;
+        }
+    }
+
+    if (do_epilogue) {
+        // tcgen05.ld is warp-collective: every lane loads, rows >= M only skip the stores
+        const bool live = m < p.M;
+        bf16* crow = nullptr;
+        int64_t cs = 0;
+        const bf16* rrow = nullptr;
+        int64_t rs = 0;
+        if (live) {
+            // output row through the C map (and the residual's), stepping along N with the piece stride
+            int32_t idx[VTC_MAX_RANK] = {};
+            idx[0] = int32_t(m);
+            idx[1] = int32_t(n0);
+            dev::Loc lc = dev::locate(p.c.m, idx);
+            crow = dev::addr<bf16>(p.c.m, lc);
+            cs = p.c.fast_stride[lc.piece];
+            if (p.has_res) {
+                dev::Loc lr = dev::locate(p.res.m, idx);
+                rrow = dev::addr<bf16>(p.res.m, lr);
+                rs = p.res.fast_stride[lr.piece];
+            }
+        }
+        const int ncols = int(p.N - n0 < BN ? p.N - n0 : BN);
+        for (int c = 0; c < ncols; c += 16) {
+            float v[16];
+            if (p.splits > 1) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 0.f;
+                if (live)
+                    for (int s2 = 0; s2 < p.splits; ++s2) {
+                        const float* src = wtile + int64_t(s2) * BM * BN + int64_t(row) * BN + c;
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4) {
+                            float4 t = __ldcg(reinterpret_cast<const float4*>(src + j));
+                            v[j] += t.x;
+                            v[j + 1] += t.y;
+                            v[j + 2] += t.z;
+                            v[j + 3] += t.w;
+                        }
+                    }
+            } else {
+                tmem_ld16(c, v);
+            }
+            if (!live) continue;
+            bf16 o[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                float f = __bfloat162float(__float2bfloat16_rn(v[j]));
+                if (rrow && c + j < ncols) f = __bfloat162float(rrow[int64_t(c + j) * rs]) + f;
+                o[j] = __float2bfloat16_rn(f);
+            }
+            bf16* dst = crow + int64_t(c) * cs;
+            if (cs == 1 && c + 16 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                reinterpret_cast<uint4*>(dst)[0] = *reinterpret_cast<const uint4*>(&o[0]);
+                reinterpret_cast<uint4*>(dst)[1] = *reinterpret_cast<const uint4*>(&o[8]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c + j < ncols) dst[int64_t(j) * cs] = o[j];
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encoder() {
+    static EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return EncodeFn(nullptr);
+        return reinterpret_cast<EncodeFn>(f);
+    }();
+    return fn;
+}
+
+template <int BN, int STAGES>
+constexpr size_t smem_bytes() {
+    return size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024;
+}
+
+}  // namespace
+
+bool gemm_tc_encode(GemmTcParams& p, const void* a_base, int64_t a_ld, const void* b_base, int64_t b_ld) {
+    EncodeFn fn = encoder();
+    if (!fn) return false;
+    if ((reinterpret_cast<uintptr_t>(a_base) % 16) || (reinterpret_cast<uintptr_t>(b_base) % 16)) return false;
+    if ((a_ld * 2) % 16 || (b_ld * 2) % 16) return false;
+    cuuint32_t es[2] = {1, 1};
+    {
+        cuuint64_t dims[2] = {cuuint64_t(p.K), cuuint64_t(p.M)};
+        cuuint64_t str[1] = {cuuint64_t(a_ld) * 2};
+        cuuint32_t box[2] = {BK, BM};
+        if (fn(reinterpret_cast<CUtensorMap*>(p.tmap_a), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a_base), dims,
+               str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    {
+        cuuint64_t dims[2] = {cuuint64_t(p.N), cuuint64_t(p.K)};
+        cuuint64_t str[1] = {cuuint64_t(b_ld) * 2};
+        cuuint32_t box[2] = {64, BK};
+        if (fn(reinterpret_cast<CUtensorMap*>(p.tmap_b), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(b_base), dims,
+               str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    return true;
+}
+
+void launch_gemm_tc(const GemmTcParams& p, const GemmTcParams* dp, cudaStream_t s) {
+    Tmaps tmaps;
+    std::memcpy(&tmaps.a, p.tmap_a, sizeof(CUtensorMap));
+    std::memcpy(&tmaps.b, p.tmap_b, sizeof(CUtensorMap));
+    const int tiles = int((p.M + BM - 1) / BM) * int((p.N + p.bn - 1) / p.bn);
+    dim3 grid(unsigned(tiles), unsigned(p.splits));
+    if (p.bn == 256) {
+        constexpr size_t sm = smem_bytes<256, 4>();
+        cudaFuncSetAttribute(gemm_tc_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        launch_k(gemm_tc_kernel<256, 4>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+    } else {
+        constexpr size_t sm = smem_bytes<128, 6>();
+        cudaFuncSetAttribute(gemm_tc_kernel<128, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        launch_k(gemm_tc_kernel<128, 6>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+    }
+}
+
+}  // namespace vtc

@@ -130,6 +130,25 @@ constexpr int GEMV_STREAM_COLS = 256, GEMV_STREAM_KT = 64;
 // row stride `ld` elements and a {256, 64} box; returns false if unsupported.
 bool encode_weight_tmap(void* out128, const void* base, int64_t rows, int64_t cols, int64_t ld);
 
+// ---- bf16 GEMM on tcgen05 tensor cores (M > 16) ---------------------------
+// C = A . B (+ residual); A [M, K] read by TMA through a single-piece affine
+// map (unit stride along K), B [K, N] physical row-major; C / residual through
+// their maps (affine along N per row).  K is split across `splits` CTAs per
+// tile when the tile grid alone would leave SMs idle.
+struct GemmTcParams {
+    KHead head;
+    VOperand c, res;
+    int64_t M, N, K;
+    int32_t bn, splits;   // N tile (128 / 256), K splits
+    int32_t has_res, pad;
+    float* work;          // [tiles, splits, 128, bn] fp32 partials (splits > 1)
+    unsigned int* counters;
+    alignas(64) unsigned char tmap_a[128];
+    alignas(64) unsigned char tmap_b[128];
+};
+bool gemm_tc_encode(GemmTcParams& p, const void* a_base, int64_t a_ld, const void* b_base, int64_t b_ld);
+void launch_gemm_tc(const GemmTcParams& p, const GemmTcParams* dp, cudaStream_t s);
+
 // ---- row-wise normalisations / softmax -----------------------------------
 enum class RowOp : int32_t { RMSNorm = 0, LayerNorm, Softmax };
 struct RowParams {

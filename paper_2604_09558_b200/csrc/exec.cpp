@@ -813,7 +813,8 @@ void Executor::prepare(bool dry) {
                     auto fit = fusion.find(n.id);
                     if (fit != fusion.end()) f = fit->second;
                     const std::string& cout = f.add ? f.add->outputs[0] : n.outputs[0];
-                    p.bn = 256;
+                    // small M: 128-column tiles so the K split (and its reduction) stays shallow
+                    p.bn = M <= 128 ? 128 : 256;
                     p.c = operand(map_of(cout), 1, p.bn, es);
                     if (!p.c.fast_ok || N % 256 != 0) {
                         p.bn = 128;

@@ -204,17 +204,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     bool do_epilogue = true;
     float* wtile = nullptr;
     if (p.splits > 1) {
-        // fp32 partial tile -> workspace [tile][split][BM][BN]; the last split reduces
+        // fp32 partial tile -> workspace [tile][split][BN][BM] (column-major: a warp's
+        // 32 rows of one column are one coalesced 128-byte store); warps whose rows
+        // are all >= M skip; the last split reduces
         wtile = p.work + (int64_t(tile) * p.splits) * BM * BN;
-        float* mine = wtile + int64_t(split) * BM * BN + int64_t(row) * BN;
-        for (int c = 0; c < BN; c += 16) {
-            float v[16];
-            if (nk > 0) tmem_ld16(c, v);
-            else
+        float* mine = wtile + int64_t(split) * BM * BN + row;
+        if (m0 + warp * 32 < p.M) {
+            for (int c = 0; c < BN; c += 16) {
+                float v[16];
+                if (nk > 0) tmem_ld16(c, v);
+                else
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = 0.f;
+                    for (int j = 0; j < 16; ++j) v[j] = 0.f;
 #pragma unroll
-            for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(mine + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                for (int j = 0; j < 16; ++j) mine[int64_t(c + j) * BM] = v[j];
+            }
         }
         __threadfence();
         __syncthreads();
@@ -254,18 +258,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             if (p.splits > 1) {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = 0.f;
-                if (live)
-                    for (int s2 = 0; s2 < p.splits; ++s2) {
-                        const float* src = wtile + int64_t(s2) * BM * BN + int64_t(row) * BN + c;
+                if (live) {
+                    // up to 4 splits' 16 columns in flight per round trip, summed in split order
+                    for (int s0 = 0; s0 < p.splits; s0 += 4) {
+                        float t[4][16];
 #pragma unroll
-                        for (int j = 0; j < 16; j += 4) {
-                            float4 t = __ldcg(reinterpret_cast<const float4*>(src + j));
-                            v[j] += t.x;
-                            v[j + 1] += t.y;
-                            v[j + 2] += t.z;
-                            v[j + 3] += t.w;
+                        for (int q = 0; q < 4; ++q) {
+                            const float* src = wtile + int64_t(s0 + q) * BM * BN + int64_t(c) * BM + row;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) t[q][j] = s0 + q < p.splits ? __ldcg(src + int64_t(j) * BM) : 0.f;
                         }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (s0 + q < p.splits)
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) v[j] += t[q][j];
                     }
+                }
             } else {
                 tmem_ld16(c, v);
             }

@@ -248,12 +248,24 @@ def run_vtc(args):
         return run_c1(args, torch, vtc, W, dev, stream, flush, hbm_peak, peak_src, world, rank)
 
     B, L = cfg["B"], cfg["L"]
-    doc = W.llama_decode_layer(B=B, L=L)
+    # N > 1: Megatron head sharding (each rank 32/N query heads, 8/N KV heads,
+    # F/N FFN columns, its shard of the KV cache) with two NCCL allreduces per
+    # layer; --replicas runs N independent full layers instead
+    tp = world if (world > 1 and not args.replicas) else 1
+    doc = W.llama_decode_layer(B=B, L=L, tp=tp)
     g = vtc.parse_graph(doc)
     dev_tensors, host = build_layer_inputs(doc, cfg, torch, dev)
+    comm = None
+    if tp > 1:
+        import torch.distributed as dist
+        uid = [vtc.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = vtc.Comm(uid[0], world, rank)
     plans = {}
     for name, mode in (("virtual", vtc.MAX_ELIMINATION), ("materialized", vtc.MATERIALIZE)):
         p = vtc.Plan(g, mode)
+        if comm is not None:
+            p.set_comm(comm)
         for tid, t in dev_tensors.items():
             p.bind_root(tid, t.data_ptr())
         for tid, t in host.items():
@@ -365,12 +377,13 @@ def run_vtc(args):
         "warmup": args.warmup,
         "ms_per_step": lat_ms,
         "higher_is_better": False,
-        "scaling": "weak",
+        "scaling": "strong" if tp > 1 else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights uniform(-1,1)/sqrt(fan_in), random KV cache)",
         "config": {"workload": cfg["workload"], "batch": B, "kv_len": L, "pos": L - 1,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
+                   "parallelism": (f"tp{tp} (head-sharded; 2 NCCL allreduce of [{B},4096] bf16 per layer)" if tp > 1
+                                   else f"replicas x{world}" if world > 1 else "single-gpu"),
                    "l2": ("inputs larger than L2: every step streams %.0f MB of weights + KV (> 126 MB L2), weights/KV "
                           "loaded with an L2 evict-first policy; no explicit flush" % (bytes_step / 1e6)
                           if args.l2 == "none" else
@@ -434,6 +447,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="vtc", choices=["vtc", "reference"])
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent full layers instead of head sharding")
     ap.add_argument("--l2", default="none", choices=["flush", "none"],
                     help="flush L2 between timed steps, or rely on the step's inputs exceeding L2")
     args = ap.parse_args()

@@ -76,6 +76,7 @@ enum vtc_plan_flags {
 
 typedef struct vtc_graph vtc_graph;
 typedef struct vtc_plan vtc_plan;
+typedef struct vtc_comm vtc_comm;
 
 const char* vtc_last_error(void);
 const char* vtc_version(void);
@@ -119,6 +120,17 @@ int vtc_plan_trace(vtc_plan* p, uint64_t* out, int32_t n);
  * evaluates the device descriptor instead of the symbolic map. */
 int vtc_map_eval(vtc_plan* p, const char* tensor, int lowered, int32_t* targets, int64_t* offsets, int64_t cap);
 int vtc_plan_map_json(vtc_plan* p, const char* tensor, const char** json_out);
+
+/* Tensor-parallel plans (SURVEY.md §8 e): one NCCL communicator per process /
+ * GPU.  Rank 0 creates the 128-byte unique id, the host side distributes it
+ * (any channel), every rank calls vtc_comm_init on its current CUDA device.
+ * The plan's AllReduce nodes then run ncclAllReduce(sum) on the plan's stream;
+ * without a communicator an AllReduce is the single-rank identity.  NCCL is
+ * resolved at run time (libnccl.so.2). */
+int vtc_comm_unique_id(void* out, int32_t bytes);
+int vtc_comm_init(const void* unique_id, int32_t bytes, int32_t nranks, int32_t rank, vtc_comm** out);
+void vtc_comm_free(vtc_comm* c);
+int vtc_plan_set_comm(vtc_plan* p, vtc_comm* c);
 
 /* Low-level kernel entry: dst[map_dst(I)] = src[map_src(I)] over dst->shape. */
 int vtc_launch_gather_copy(const vtc_map* dst, const vtc_map* src, int32_t elem_bytes, void* stream);

@@ -70,6 +70,8 @@ public:
     // VTC_TRACE=1 timeline: out[2i], out[2i+1] = globaltimer (ns) at entry / exit
     // of launch i over the runs since the last read; returns the launch count.
     int read_trace(unsigned long long* out, int n);
+    // Communicator for the plan's AllReduce nodes (nullptr: single rank).
+    void set_comm(class Comm* c);
     void reset_trace();
 
     void upload(const std::string& id, const void* host, int64_t bytes, void* stream);

@@ -207,8 +207,13 @@ def run_operator(n, ins, dt, out_shapes=None):
     raise ValueError(f"oracle: no semantics for operator {kind}")
 
 
-def execute(doc, inputs: Dict[str, np.ndarray], keep_all: bool = False) -> Dict[str, np.ndarray]:
-    """All-physical execution (reference `execute`, executor.cpp:500-506)."""
+def execute(doc, inputs: Dict[str, np.ndarray], keep_all: bool = False, allreduce=None) -> Dict[str, np.ndarray]:
+    """All-physical execution (reference `execute`, executor.cpp:500-506).
+
+    `allreduce(values_f32) -> summed_f32` performs a tensor-parallel AllReduce
+    across ranks (e.g. torch.distributed over gloo in the multi-process tests);
+    without it AllReduce is the single-rank identity.  bf16 partials are summed
+    in fp32 and rounded once, like ncclAllReduce(ncclBfloat16) with two ranks."""
     g = doc if isinstance(doc, Graph) else Graph(doc)
     env = {}
     for tid in g.inputs():
@@ -218,6 +223,11 @@ def execute(doc, inputs: Dict[str, np.ndarray], keep_all: bool = False) -> Dict[
     for i in g.order:
         n = g.nodes[i]
         dt = g.tensors[n["inputs"][0]]["dtype"]
+        if n["kind"] == "AllReduce" and allreduce is not None:
+            x = env[n["inputs"][0]]
+            s = np.asarray(allreduce(_to_compute(x, dt).astype(np.float32)))
+            env[n["outputs"][0]] = f32_to_bf16(s) if dt == "bf16" else s.astype(x.dtype)
+            continue
         outs = run_operator(n, [env[t] for t in n["inputs"]], dt)
         for name, val in zip(n["outputs"], outs):
             env[name] = val

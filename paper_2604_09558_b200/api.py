@@ -65,7 +65,10 @@ class CompGraph:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            _lib.load().vtc_graph_free(self._h)
+            try:
+                _lib.load().vtc_graph_free(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     def serialize(self) -> str:
@@ -99,6 +102,34 @@ def parse_graph(text) -> CompGraph:
     return CompGraph(h, text)
 
 
+class Comm:
+    """NCCL communicator for tensor-parallel plans (include/vtc.h vtc_comm_*):
+    rank 0 calls Comm.unique_id(), the id is shared over any host channel, every
+    rank constructs Comm(uid, nranks, rank) on its current CUDA device."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        _check(_lib.load().vtc_comm_unique_id(C.cast(buf, C.c_void_p), 128))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        assert len(uid) == 128
+        h = C.c_void_p()
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        _check(_lib.load().vtc_comm_init(C.cast(buf, C.c_void_p), 128, nranks, rank, C.byref(h)))
+        self._h = h
+        self.nranks, self.rank = nranks, rank
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                _lib.load().vtc_comm_free(self._h)
+            except Exception:  # interpreter shutdown
+                pass
+            self._h = None
+
+
 class Plan:
     """A points-to graph bound to the GPU executor (roots own device memory)."""
 
@@ -113,7 +144,10 @@ class Plan:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            _lib.load().vtc_plan_free(self._h)
+            try:
+                _lib.load().vtc_plan_free(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     def info(self, dry: bool = False) -> dict:
@@ -163,6 +197,11 @@ class Plan:
         _check(_lib.load().vtc_execute_timed(self._h, _stream(stream), ms.ctypes.data_as(C.POINTER(C.c_float)),
                                              n_records))
         return ms
+
+    def set_comm(self, comm: Optional["Comm"]) -> None:
+        """Run this plan's AllReduce nodes on `comm` (None: single rank)."""
+        self._comm = comm  # keep alive
+        _check(_lib.load().vtc_plan_set_comm(self._h, comm._h if comm is not None else None))
 
     def trace(self) -> np.ndarray:
         """[n_launches, 8] globaltimer (ns): entry, exit, kernel checkpoints per

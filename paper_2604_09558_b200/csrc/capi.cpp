@@ -10,11 +10,16 @@
 #include "kernels.hpp"
 #include "lower.hpp"
 #include "vtc.h"
+#include "comm.hpp"
 #include "vtc/exec.hpp"
 
 struct vtc_graph {
     vtc::CompGraph g;
     std::unique_ptr<vtc::Vtog> vtog;
+};
+
+struct vtc_comm {
+    std::unique_ptr<vtc::Comm> c;
 };
 
 struct vtc_plan {
@@ -220,6 +225,33 @@ int vtc_plan_upload(vtc_plan* p, const char* tensor, const void* host, int64_t b
 
 int vtc_plan_download(vtc_plan* p, const char* tensor, void* host, int64_t bytes, void* stream) {
     return guard([&] { p->exec->download(tensor, host, bytes, stream); });
+}
+
+int vtc_comm_unique_id(void* out, int32_t bytes) {
+    return guard([&] {
+        if (bytes < 128) throw vtc::ExecutionError("vtc_comm_unique_id: buffer must hold 128 bytes");
+        vtc::comm_unique_id(out);
+    });
+}
+
+int vtc_comm_init(const void* unique_id, int32_t bytes, int32_t nranks, int32_t rank, vtc_comm** out) {
+    return guard([&] {
+        if (bytes < 128) throw vtc::ExecutionError("vtc_comm_init: unique id must be 128 bytes");
+        auto* c = new vtc_comm;
+        try {
+            c->c = std::make_unique<vtc::Comm>(unique_id, nranks, rank);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+void vtc_comm_free(vtc_comm* c) { delete c; }
+
+int vtc_plan_set_comm(vtc_plan* p, vtc_comm* c) {
+    return guard([&] { p->exec->set_comm(c ? c->c.get() : nullptr); });
 }
 
 int vtc_plan_prepare(vtc_plan* p) {

@@ -11,6 +11,7 @@
 
 #include <cuda_runtime.h>
 
+#include "comm.hpp"
 #include "kernels.hpp"
 #include "lower.hpp"
 
@@ -56,6 +57,24 @@ struct LaunchT : Launch {
         p.head.trace = t;
         p.head.id = id;
     }
+};
+
+// AllReduce(sum) of a contiguous buffer over the plan's communicator; with no
+// communicator (single rank) the sum over one rank is the identity.
+struct AllReduceLaunch : Launch {
+    const void* src = nullptr;
+    void* dst = nullptr;
+    size_t count = 0, bytes = 0;
+    ncclDataType_t dt = ncclBfloat16;
+    Comm* const* comm = nullptr;
+    void run(cudaStream_t s) override {
+        if (*comm) (*comm)->all_reduce_sum(src, dst, count, dt, s);
+        else if (dst != src) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s), "D2D");
+    }
+    size_t param_bytes() const override { return 0; }
+    const void* host_params() const override { return nullptr; }
+    void set_device_params(void*) override {}
+    void set_trace(unsigned long long*, int) override {}
 };
 
 void launch_gemv_any(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
@@ -128,7 +147,8 @@ struct Executor::Impl {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t gexec = nullptr;
     cudaStream_t captured_on = nullptr;
-    unsigned long long* trace = nullptr;  // VTC_TRACE timeline buffer (2 per launch)
+    unsigned long long* trace = nullptr;  // VTC_TRACE timeline buffer (8 per launch)
+    Comm* comm = nullptr;                 // tensor-parallel communicator (AllReduce nodes)
 
     void free_scratch() {
         for (void* p : scratch) cudaFree(p);
@@ -699,10 +719,37 @@ void Executor::prepare(bool dry) {
                 eltwise(label, sp, dt, o0.shape, map_of(n.outputs[0]));
                 break;
             }
-            case OpKind::AllReduce:
-                // single-rank execution: the sum over one rank is the identity
-                copy_checked(n.id, dt, o0.shape, map_of(n.outputs[0]), map_of(n.inputs[0]));
+            case OpKind::AllReduce: {
+                // NCCL on contiguous views of roots (the tensor-parallel partial sums)
+                auto contiguous = [&](const VMap& m) -> const char* {
+                    if (m.pieces().size() != 1) return nullptr;
+                    const VPiece& pc = m.pieces()[0];
+                    for (const auto& tm : pc.off.t)
+                        if (tm.a->kind != AtomKind::Axis) return nullptr;
+                    int64_t want = 1;
+                    for (int a = int(m.rank()) - 1; a >= 0; --a) {
+                        auto st = VMap::tile_stride(pc, a, m.shape()[size_t(a)]);
+                        if (!st || (m.shape()[size_t(a)] > 1 && *st != want)) return nullptr;
+                        want *= m.shape()[size_t(a)];
+                    }
+                    return reinterpret_cast<const char*>(target(pc.target).ptr) + pc.off.c0 * es;
+                };
+                const char* src = contiguous(map_of(n.inputs[0]));
+                const char* dst = contiguous(map_of(n.outputs[0]));
+                if ((!src || !dst) && !impl_->dry)
+                    throw UnsupportedError("AllReduce " + n.id + " needs contiguous input / output views");
+                auto L = std::make_unique<AllReduceLaunch>();
+                L->node = n.id;
+                L->kernel = "allreduce_nccl";
+                L->src = src;
+                L->dst = const_cast<char*>(dst);
+                L->count = size_t(volume(o0.shape));
+                L->bytes = L->count * size_t(es);
+                L->dt = dt == DType::BF16 ? ncclBfloat16 : dt == DType::F32 ? ncclFloat32 : dt == DType::F64 ? ncclFloat64 : ncclInt64;
+                L->comm = &impl_->comm;
+                push(std::move(L));
                 break;
+            }
             case OpKind::RMSNorm:
             case OpKind::LayerNorm:
             case OpKind::Softmax: {
@@ -988,6 +1035,7 @@ void Executor::prepare(bool dry) {
             auto* base = static_cast<char*>(impl_->alloc(total, false));
             std::vector<char> host(total);
             for (size_t i = 0; i < impl_->launches.size(); ++i) {
+                if (impl_->launches[i]->param_bytes() == 0) continue;
                 std::memcpy(host.data() + offs[i], impl_->launches[i]->host_params(), impl_->launches[i]->param_bytes());
                 impl_->launches[i]->set_device_params(base + offs[i]);
             }
@@ -1018,6 +1066,11 @@ void Executor::run_graph(void* stream) {
         ck(cudaGraphInstantiate(&impl_->gexec, impl_->graph, 0), "cudaGraphInstantiate");
     }
     ck(cudaGraphLaunch(impl_->gexec, s), "cudaGraphLaunch");
+}
+
+void Executor::set_comm(Comm* c) {
+    impl_->comm = c;
+    impl_->free_graph();  // a captured graph holds the previous collective
 }
 
 void Executor::reset_trace() {

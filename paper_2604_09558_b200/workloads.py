@@ -69,7 +69,7 @@ def c1_chain(n: int = 1024, dtype: str = "f32") -> dict:
 
 def llama_decode_layer(B: int = 1, L: int = 2048, pos: Optional[int] = None, D: int = 4096, Hq: int = 32,
                        Hkv: int = 8, hd: int = 128, F: int = 14336, dtype: str = "bf16", eps: float = 1e-5,
-                       reference_ops_only: bool = False) -> dict:
+                       reference_ops_only: bool = False, tp: int = 1) -> dict:
     """One Llama-3 decoder layer, decode step (one new token per sequence).
 
     KV caches are pos-major [L, B, Hkv, hd] (the reference's ScatterND only
@@ -81,8 +81,16 @@ def llama_decode_layer(B: int = 1, L: int = 2048, pos: Optional[int] = None, D: 
     MatMul(q, k^T) * scale -> MatMul(., v) (no softmax): the same data
     movement and the same GEMM work in the reference's vocabulary, used for
     the timed reference CPU arm.
+
+    tp > 1 builds ONE rank's graph of a Megatron head-sharded layer
+    (SURVEY.md §8 e): Hq/tp query heads, Hkv/tp KV heads and F/tp FFN columns
+    are local (weights / caches are the rank's shards, see shard_llama_inputs),
+    and exactly two AllReduce(sum) nodes -- after O-proj and after FFN-down --
+    are the only exchange.  Every rank's graph is identical.
     """
     pos = L - 1 if pos is None else pos
+    assert Hq % tp == 0 and Hkv % tp == 0 and F % tp == 0, "heads / FFN must divide the TP degree"
+    Hq, Hkv, F = Hq // tp, Hkv // tp, F // tp
     G = Hq // Hkv
     half = hd // 2
     nq, nkv = Hq * hd, Hkv * hd
@@ -157,16 +165,47 @@ def llama_decode_layer(B: int = 1, L: int = 2048, pos: Optional[int] = None, D: 
     else:
         g.node("attn", "Attention", ["q4", "k_h", "v_h"], "o4", {"scale": scale, "causal": False})
     g.node("o_reshape", "Reshape", ["o4"], "o2", {"shape": [B, nq]})
-    g.node("o_proj", "MatMul", ["o2", "w_o"], "ao")
+    if tp > 1:
+        g.node("o_proj", "MatMul", ["o2", "w_o"], "ao_part")
+        g.node("o_allreduce", "AllReduce", ["ao_part"], "ao")
+    else:
+        g.node("o_proj", "MatMul", ["o2", "w_o"], "ao")
     g.node("res1", "Add", ["x", "ao"], "x2")
     norm("ln2", "x2", "w_ln2", "h2")
     g.node("gate_proj", "MatMul", ["h2", "w_gate"], "gt")
     g.node("up_proj", "MatMul", ["h2", "w_up"], "up")
     g.node("silu", "SiLU", ["gt"], "sg")
     g.node("gate_mul", "Mul", ["sg", "up"], "mm")
-    g.node("down_proj", "MatMul", ["mm", "w_down"], "dn")
+    if tp > 1:
+        g.node("down_proj", "MatMul", ["mm", "w_down"], "dn_part")
+        g.node("down_allreduce", "AllReduce", ["dn_part"], "dn")
+    else:
+        g.node("down_proj", "MatMul", ["mm", "w_down"], "dn")
     g.node("res2", "Add", ["x2", "dn"], "y", out_kind="output")
     return g.doc()
+
+
+def shard_llama_inputs(full: Dict, rank: int, tp: int, Hq: int = 32, Hkv: int = 8, hd: int = 128,
+                       F: int = 14336) -> Dict:
+    """Rank `rank`'s inputs of llama_decode_layer(tp=tp) from the full layer's
+    inputs: Q/K/V columns and O rows of the local heads, gate/up columns and
+    down rows of the local FFN slice, the local KV-cache heads; x, norms and
+    RoPE tables replicated."""
+    import numpy as np
+    hq, hk, f = Hq // tp, Hkv // tp, F // tp
+    nq, nkv = Hq * hd, Hkv * hd
+    q_cols = np.arange(rank * hq * hd, (rank + 1) * hq * hd)
+    k_cols = nq + np.arange(rank * hk * hd, (rank + 1) * hk * hd)
+    v_cols = nq + nkv + np.arange(rank * hk * hd, (rank + 1) * hk * hd)
+    out = dict(full)
+    out["w_qkv"] = np.ascontiguousarray(full["w_qkv"][:, np.concatenate([q_cols, k_cols, v_cols])])
+    out["w_o"] = np.ascontiguousarray(full["w_o"][q_cols, :])
+    out["w_gate"] = np.ascontiguousarray(full["w_gate"][:, rank * f:(rank + 1) * f])
+    out["w_up"] = np.ascontiguousarray(full["w_up"][:, rank * f:(rank + 1) * f])
+    out["w_down"] = np.ascontiguousarray(full["w_down"][rank * f:(rank + 1) * f, :])
+    for c in ("k_cache", "v_cache"):
+        out[c] = np.ascontiguousarray(full[c][:, :, rank * hk:(rank + 1) * hk, :])
+    return out
 
 
 def llama_weight_scales(D: int = 4096, F: int = 14336) -> Dict[str, float]:

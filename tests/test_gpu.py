@@ -264,3 +264,45 @@ def test_llama_layer_batch64_tensor_core_path(vtc, oracle):
     # split-KV partition differs: equal within tolerance, not bit for bit
     assert _relerr(oracle.bf16_to_f32(got_v["y"]), oracle.bf16_to_f32(got_m["y"])) < 2e-2
     assert _relerr(oracle.bf16_to_f32(got_v["y"]), oracle.bf16_to_f32(want)) < 2e-2
+
+
+def _tp_nccl_check():
+    import sys
+    sys.path.insert(0, ".")
+    sys.path.insert(0, "oracle")
+    import numpy as np
+    import vtc_oracle as oracle
+    import paper_2604_09558_b200 as vtc
+    from paper_2604_09558_b200 import workloads as W
+    cfg = dict(B=2, L=64, pos=40, D=256, Hq=4, Hkv=2, hd=128, F=512)
+    full_doc = W.llama_decode_layer(**cfg)
+    full = _llama_inputs(oracle, W, full_doc, cfg["B"], cfg["pos"], cfg["D"], cfg["F"], cfg["hd"])
+    doc = W.llama_decode_layer(**cfg, tp=2)
+    x = W.shard_llama_inputs(full, 0, 2, Hq=cfg["Hq"], Hkv=cfg["Hkv"], hd=cfg["hd"], F=cfg["F"])
+    want = oracle.bf16_to_f32(oracle.execute(doc, x)["y"])
+    comm = vtc.Comm(vtc.Comm.unique_id(), 1, 0)
+    g = vtc.parse_graph(doc)
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    p.set_comm(comm)
+    kinds = [l["kernel"] for l in p.info(dry=True)["launches"]]
+    assert kinds.count("allreduce_nccl") == 2
+    got = vtc.execute(g, p, x)["y"]
+    assert _relerr(oracle.bf16_to_f32(got), want) < 2e-2
+    p.execute_graph()
+    assert np.array_equal(p.download("y"), got)
+
+
+def test_tensor_parallel_plan_runs_nccl_allreduce():
+    """A head-sharded rank graph (tp = 2, rank 0's shards) executed with a real
+    NCCL communicator: ncclAllReduce runs inside the plan (and its CUDA graph);
+    with one rank in the communicator the sum is the rank's own partial, so the
+    result equals the oracle run of the same rank graph with identity AllReduce.
+    Runs in a fresh process (NCCL initialisation inside a process that already
+    holds many CUDA allocations is slow)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "-c", "import sys; sys.path.insert(0, 'tests'); import test_gpu; test_gpu._tp_nccl_check()"],
+                       cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr

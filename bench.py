@@ -34,6 +34,7 @@ CONFIGS = {
     "c2": dict(B=1, L=2048, workload="llama3-8b-decoder-layer-decode-b1-kv2048"),
     "c3": dict(B=64, L=8192, workload="llama3-8b-decoder-layer-decode-b64-kv8192"),
     "c1": dict(n=1024, workload="reshape-transpose-slice-fp32-matmul-1024"),
+    "c5": dict(B=8, S=4096, prefill=True, workload="llama3-8b-decoder-layer-prefill-b8-s4096"),
 }
 METRIC = "decoder-layer latency (us) & HBM GB/s as % roofline; DRAM bytes eliminated"
 
@@ -104,14 +105,21 @@ def build_layer_inputs(doc, cfg, torch, dev):
     g.manual_seed(1)
     dev_tensors = {}
     for tid in ("w_ln1", "w_qkv", "w_o", "w_ln2", "w_gate", "w_up", "w_down", "k_cache", "v_cache"):
+        if tid not in specs:
+            continue
         shape = specs[tid]["shape"]
         t = torch.empty(shape, dtype=torch.float32, device=dev).uniform_(-1.0, 1.0, generator=g)
         dev_tensors[tid] = (t * scales.get(tid, 1.0)).to(torch.bfloat16).contiguous()
     B = cfg["B"]
-    cos, sin = W.rope_tables(B, [cfg["L"] - 1] * B)
     rng = np.random.default_rng(2)
+    if cfg.get("prefill"):
+        cos, sin = W.rope_tables_prefill(B, cfg["S"])
+        rows = B * cfg["S"]
+    else:
+        cos, sin = W.rope_tables(B, [cfg["L"] - 1] * B)
+        rows = B
     host = {
-        "x": torch.from_numpy(rng.uniform(-1, 1, size=(B, 4096)).astype(np.float32)).to(torch.bfloat16),
+        "x": torch.from_numpy(rng.uniform(-1, 1, size=(rows, 4096)).astype(np.float32)).to(torch.bfloat16),
         "cos": torch.from_numpy(cos.astype(np.float32)).to(torch.bfloat16),
         "sin": torch.from_numpy(sin.astype(np.float32)).to(torch.bfloat16),
     }
@@ -247,12 +255,13 @@ def run_vtc(args):
     if args.config == "c1":
         return run_c1(args, torch, vtc, W, dev, stream, flush, hbm_peak, peak_src, world, rank)
 
-    B, L = cfg["B"], cfg["L"]
+    B, L = cfg["B"], cfg.get("L", cfg.get("S"))
     # N > 1: Megatron head sharding (each rank 32/N query heads, 8/N KV heads,
     # F/N FFN columns, its shard of the KV cache) with two NCCL allreduces per
     # layer; --replicas runs N independent full layers instead
     tp = world if (world > 1 and not args.replicas) else 1
-    doc = W.llama_decode_layer(B=B, L=L, tp=tp)
+    prefill = bool(cfg.get("prefill"))
+    doc = W.llama_prefill_layer(B=B, S=cfg["S"]) if prefill else W.llama_decode_layer(B=B, L=L, tp=tp)
     g = vtc.parse_graph(doc)
     dev_tensors, host = build_layer_inputs(doc, cfg, torch, dev)
     comm = None
@@ -332,6 +341,13 @@ def run_vtc(args):
         f["launches"] += 1
     dom = max(fam, key=lambda k: fam[k]["ms"])
     achieved = fam[dom]["bytes"] / (fam[dom]["ms"] * 1e-3) / 1e9
+    if prefill:
+        # tensor-bound: algorithmic FLOPs of the dominant family over its time
+        T, D, F, nq, nkv = B * cfg["S"], 4096, 14336, 4096, 1024
+        gemm_flops = 2 * T * D * (nq + 2 * nkv) + 2 * T * nq * D + 2 * 2 * T * D * F + 2 * T * F * D
+        attn_flops = 2 * 2 * B * 32 * cfg["S"] * (cfg["S"] + 1) // 2 * 128
+        fam_flops = {"gemm_tc_bf16": gemm_flops, "attn_prefill_tc": attn_flops}
+        achieved_tf = fam_flops.get(dom, 0) / (fam[dom]["ms"] * 1e-3) / 1e12
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
@@ -342,7 +358,7 @@ def run_vtc(args):
 
     # e2e through the C ABI with host buffers: H2D of the step's inputs, the layer, D2H of y
     pv = plans["virtual"]
-    y_host = torch.empty((B, 4096), dtype=torch.bfloat16).pin_memory()
+    y_host = torch.empty((B * cfg["S"] if prefill else B, 4096), dtype=torch.bfloat16).pin_memory()
 
     def e2e_step():
         for tid, t in host.items():
@@ -367,7 +383,7 @@ def run_vtc(args):
     if rank != 0:
         return
     bytes_step = sum(l["bytes"] for l in launches)
-    cpu = cpu_reference_layer(cfg) if world == 1 and not os.environ.get("BENCH_NO_CPU") else None
+    cpu = cpu_reference_layer(cfg) if world == 1 and not prefill and not os.environ.get("BENCH_NO_CPU") else None
     line = {
         "metric": METRIC,
         "value": lat_ms * 1e3,
@@ -381,7 +397,8 @@ def run_vtc(args):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights uniform(-1,1)/sqrt(fan_in), random KV cache)",
-        "config": {"workload": cfg["workload"], "batch": B, "kv_len": L, "pos": L - 1,
+        "config": {"workload": cfg["workload"], "batch": B, ("seq_len" if prefill else "kv_len"): L,
+                   "pos": None if prefill else L - 1,
                    "parallelism": (f"tp{tp} (head-sharded; 2 NCCL allreduce of [{B},4096] bf16 per layer)" if tp > 1
                                    else f"replicas x{world}" if world > 1 else "single-gpu"),
                    "l2": ("inputs larger than L2: every step streams %.0f MB of weights + KV (> 126 MB L2), weights/KV "
@@ -389,10 +406,14 @@ def run_vtc(args):
                           if args.l2 == "none" else
                           "flushed between timed steps (256 MiB write + 256 MiB read, outside the events)"),
                    "plan": "VTC max-elimination (all data-movement ops virtual)", "cuda_graph": True},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic, "kernel": dom,
-                     "kernel_launches_per_step": fam[dom]["launches"],
-                     "algorithmic_bytes_per_step": fam[dom]["bytes"], "peak_source": peak_src},
+        "roofline": ({"bound": "tensor", "achieved": achieved_tf, "peak": tf_peak, "unit": "TFLOP/s",
+                      "frac": achieved_tf / tf_peak, "traffic": traffic, "kernel": dom,
+                      "kernel_launches_per_step": fam[dom]["launches"], "peak_source": peak_src}
+                     if prefill else
+                     {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": achieved / hbm_peak, "traffic": traffic, "kernel": dom,
+                      "kernel_launches_per_step": fam[dom]["launches"],
+                      "algorithmic_bytes_per_step": fam[dom]["bytes"], "peak_source": peak_src}),
         "step_hbm_gbs": bytes_step / (lat_ms * 1e-3) / 1e9,
         "step_hbm_frac": bytes_step / (lat_ms * 1e-3) / 1e9 / hbm_peak,
         "bytes_per_step": bytes_step,

@@ -575,8 +575,18 @@ void Executor::prepare(bool dry) {
         const TensorSpec& B = g_.tensor(n.inputs[1]);
         if (A.dtype != DType::BF16 || A.shape.size() != 2 || A.shape[0] <= 16) return false;
         int64_t ld, c0;
-        return affine2d(map_of(n.inputs[0]), ld, c0) && affine2d(map_of(n.inputs[1]), ld, c0) && B.shape[1] % 8 == 0 &&
-               A.shape[1] % 8 == 0;
+        if (!affine2d(map_of(n.inputs[1]), ld, c0) || B.shape[1] % 8 != 0 || A.shape[1] % 8 != 0) return false;
+        // A: TMA-readable through its map (tile-aligned mixed-radix digits)
+        vtc_map am{};
+        try {
+            am = lower_map(map_of(n.inputs[0]), target);
+        } catch (const UnsupportedError&) {
+            return false;
+        }
+        GemmTcParams probe{};
+        int64_t dims[5], strides[5];
+        const void* base = nullptr;
+        return gemm_tc_a_dims(am, A.shape[0], A.shape[1], probe, dims, strides, &base);
     };
     if (opt_.fuse) {
         for (const auto& n : g_.nodes()) {
@@ -875,14 +885,14 @@ void Executor::prepare(bool dry) {
                         ok = ok && p.res.fast_ok;
                         T->node += "+" + f.add->id;
                     }
-                    int64_t lda, ca, ldb, cb;
-                    affine2d(map_of(n.inputs[0]), lda, ca);
+                    int64_t ldb, cb;
                     affine2d(map_of(n.inputs[1]), ldb, cb);
-                    const VMap& am = map_of(n.inputs[0]);
                     const VMap& bmm = map_of(n.inputs[1]);
-                    const char* abase = reinterpret_cast<const char*>(target(am.pieces()[0].target).ptr) + ca * es;
                     const char* bbase = reinterpret_cast<const char*>(target(bmm.pieces()[0].target).ptr) + cb * es;
-                    if (ok && !impl_->dry) ok = gemm_tc_encode(p, abase, lda, bbase, ldb);
+                    int64_t adims[5], astr[5];
+                    const void* abase = nullptr;
+                    ok = ok && gemm_tc_a_dims(lower_map(map_of(n.inputs[0]), target), M, K, p, adims, astr, &abase);
+                    if (ok && !impl_->dry) ok = gemm_tc_encode(p, abase, adims, astr, bbase, ldb);
                     if (ok) {
                         int64_t tiles = (M + 127) / 128 * ((N + p.bn - 1) / p.bn);
                         int64_t ktiles = (K + 63) / 64;
@@ -978,7 +988,7 @@ void Executor::prepare(bool dry) {
                 // tensor-core decode path: K/V rows addressed as base + t * stride when
                 // the maps are single-piece affine along the key axis
                 p.fast = attn_decode_supported(p) ? 1 : 0;
-                if (p.fast && p.k.m.npieces == 1 && p.v.m.npieces == 1) {
+                if (p.k.m.npieces == 1 && p.v.m.npieces == 1) {
                     int64_t ks_ = desc_tile_stride(p.k.m.piece[0], rank - 2, p.Sk);
                     int64_t vs_ = desc_tile_stride(p.v.m.piece[0], rank - 2, p.Sk);
                     if (ks_ != INT64_MIN && vs_ != INT64_MIN) {
@@ -986,6 +996,15 @@ void Executor::prepare(bool dry) {
                         p.k_sstride = ks_;
                         p.v_sstride = vs_;
                     }
+                }
+                // long query blocks (prefill): flash attention on tensor cores, no K split
+                if (!p.fast && attn_prefill_supported(p)) {
+                    p.fast = 2;
+                    p.splits = 1;
+                    p.chunk = p.Sk;
+                    L->kernel = "attn_prefill_tc";
+                    push(std::move(L));
+                    break;
                 }
                 int64_t qblocks = int64_t(p.Bt) * (p.H / G) * (p.fast ? 1 : p.Sq);
                 int splits = opt_.attn_splits;

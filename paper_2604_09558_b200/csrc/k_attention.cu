@@ -273,6 +273,10 @@ __global__ void __launch_bounds__(NT) combine_kernel(const AttnParams* __restric
 
 template <typename T>
 void launch_t(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
+    if (p.fast == 2) {
+        launch_attn_prefill(p, dp, s);
+        return;
+    }
     if (p.fast) {
         launch_attn_decode(p, dp, s);
     } else {

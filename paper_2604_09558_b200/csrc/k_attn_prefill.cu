@@ -1,0 +1,277 @@
+// Flash attention for long query blocks (prefill), bf16, head dim 128.
+//
+// softmax(scale * Q K^T [causal]) V with Q, K, V and O read / written through
+// their VirtualTensor maps: in a VTC-planned prefill the QKV split, the RoPE
+// output, the [B,S,H,d] -> [B,H,S,d] transposes and the GQA Expand/Reshape of
+// K/V are all views, so the kernel addresses the projection outputs directly
+// (per query row one map evaluation, per (batch, KV head) one base + key stride).
+//
+//   * CTA = 4 warps x 16 query rows of one (lead, head); K/V tiles of 64 keys
+//     shared by the 4 warps through a 2-stage cp.async ring (XOR-swizzled rows,
+//     ldmatrix / ldmatrix.trans), zero-filled past the end;
+//   * S = Q K^T and O += P V on mma.sync m16n8k16 (bf16, fp32 accumulate),
+//     online softmax in the log2 domain; causal query blocks stop at the
+//     diagonal key tile (masked inside it);
+//   * O / l rounded to bf16 and stored through the output map.
+// Attention is absent from the reference (SURVEY.md §8 a'); CPU restatement:
+// oracle/vtc_oracle.py (Attention).
+#include <cfloat>
+
+#include "device.cuh"
+#include "launch.cuh"
+
+namespace vtc {
+namespace {
+
+using dev::bf16;
+constexpr int WARPS = 4, NT = WARPS * 32, QR = 16 * WARPS, TK = 64, D = 128, STAGES = 2;
+constexpr int ROWB = D * 2, TILEB = TK * ROWB, STAGEB = 2 * TILEB;  // K + V per stage: 32 KB
+constexpr float LOG2E = 1.4426950408889634f;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t swz(int r, int c) { return uint32_t(r * ROWB + ((c ^ (r & 7)) << 4)); }
+
+__global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* __restrict__ pp) {
+    VTC_STAGE_PARAMS(AttnParams, pp);
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ const bf16* s_qrow[QR];
+    __shared__ bf16* s_orow[QR];
+    __shared__ int64_t s_qstr[QR], s_ostr[QR];
+
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    const int r = p.rank, ax_h = r - 3, ax_s = r - 2, ax_d = r - 1;
+    const int Sq = p.Sq, Sk = p.Sk;
+    const int q0 = blockIdx.x * QR;
+    int64_t bh = blockIdx.y;
+    const int h = int(bh % p.H);
+    bh /= p.H;
+    int32_t base_idx[VTC_MAX_RANK] = {};
+    for (int a = r - 4; a >= 0; --a) {
+        base_idx[a] = int32_t(bh % p.q.m.shape[a]);
+        bh /= p.q.m.shape[a];
+    }
+    // query rows: one map evaluation each
+    if (tid < QR) {
+        int32_t idx[VTC_MAX_RANK];
+#pragma unroll
+        for (int a = 0; a < VTC_MAX_RANK; ++a) idx[a] = base_idx[a];
+        idx[ax_h] = h;
+        idx[ax_s] = min(q0 + tid, Sq - 1);
+        idx[ax_d] = 0;
+        dev::Loc l = dev::locate(p.q.m, idx);
+        s_qrow[tid] = dev::addr<bf16>(p.q.m, l);
+        s_qstr[tid] = p.q.fast_stride[l.piece];
+        dev::Loc lo = dev::locate(p.o.m, idx);
+        s_orow[tid] = dev::addr<bf16>(p.o.m, lo);
+        s_ostr[tid] = p.o.fast_stride[lo.piece];
+    }
+    // K / V of this head: base at key 0 + key stride (host-proved affine)
+    const bf16* kb0;
+    const bf16* vb0;
+    {
+        int32_t idx[VTC_MAX_RANK];
+#pragma unroll
+        for (int a = 0; a < VTC_MAX_RANK; ++a) idx[a] = base_idx[a];
+        idx[ax_h] = h;
+        idx[ax_s] = 0;
+        idx[ax_d] = 0;
+        kb0 = dev::elem_ptr<bf16>(p.k.m, idx);
+        vb0 = dev::elem_ptr<bf16>(p.v.m, idx);
+    }
+    dev::pdl_wait();
+    dev::pdl_launch_dependents();
+    __syncthreads();
+
+    // causal: query row q sees keys t <= q + (Sk - Sq)
+    const int kend = p.causal ? min(Sk, q0 + QR - 1 + (Sk - Sq) + 1) : Sk;
+    const int ntiles = kend > 0 ? (kend + TK - 1) / TK : 0;
+    const uint32_t sbase = smem_u32(smem);
+    auto load_tile = [&](int j, int st) {
+        const int t0 = j * TK;
+        const uint32_t kd = sbase + st * STAGEB, vd = kd + TILEB;
+#pragma unroll
+        for (int i = 0; i < (TK * 16) / NT; ++i) {  // 16 chunks of 16 B per row
+            const int c = tid + i * NT;
+            const int row = c >> 4, ch = c & 15;
+            const int t = t0 + row;
+            const bool ok = t < kend;
+            const int tc = ok ? t : 0;
+            cp_async16(kd + swz(row, ch), kb0 + int64_t(tc) * p.k_sstride + ch * 8, ok);
+            cp_async16(vd + swz(row, ch), vb0 + int64_t(tc) * p.v_sstride + ch * 8, ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (ntiles > 0) load_tile(0, 0);
+
+    // Q fragments of this warp's 16 rows
+    const int rA = warp * 16 + lane / 4, rB = rA + 8, kc = (lane % 4) * 2;
+    uint32_t qa[D / 16][4];
+    {
+        auto qv = [&](int row, int d) -> float {
+            return q0 + row < Sq ? __bfloat162float(s_qrow[row][int64_t(d) * s_qstr[row]]) : 0.f;
+        };
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+            const int d0 = ks * 16 + kc;
+            qa[ks][0] = pack_bf16(qv(rA, d0), qv(rA, d0 + 1));
+            qa[ks][1] = pack_bf16(qv(rB, d0), qv(rB, d0 + 1));
+            qa[ks][2] = pack_bf16(qv(rA, d0 + 8), qv(rA, d0 + 9));
+            qa[ks][3] = pack_bf16(qv(rB, d0 + 8), qv(rB, d0 + 9));
+        }
+    }
+    const float qscale = p.scale * LOG2E;
+    const int limA = p.causal ? q0 + rA + (Sk - Sq) : INT32_MAX;
+    const int limB = p.causal ? q0 + rB + (Sk - Sq) : INT32_MAX;
+    float o[D / 8][4];
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
+
+    for (int j = 0; j < ntiles; ++j) {
+        const int st = j % STAGES;
+        if (j + 1 < ntiles) {
+            load_tile(j + 1, (j + 1) % STAGES);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const uint32_t kt = sbase + st * STAGEB, vt = kt + TILEB;
+        const int t0 = j * TK;
+        // S[16 x 64]: 8 n-tiles of 8 keys
+        float sc[TK / 8][4];
+#pragma unroll
+        for (int nt = 0; nt < TK / 8; ++nt) {
+            sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+            for (int kp = 0; kp < D / 32; ++kp) {
+                const int mi = lane / 8, rr = lane % 8;
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(kt + swz(nt * 8 + rr, kp * 4 + mi), b0, b1, b2, b3);
+                mma_bf16(sc[nt], qa[2 * kp], b0, b1);
+                mma_bf16(sc[nt], qa[2 * kp + 1], b2, b3);
+            }
+        }
+        float tmA = -INFINITY, tmB = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < TK / 8; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int t = t0 + nt * 8 + (lane % 4) * 2 + c;
+                float a = sc[nt][c] * qscale, b = sc[nt][2 + c] * qscale;
+                if (t >= kend || t > limA) a = -INFINITY;
+                if (t >= kend || t > limB) b = -INFINITY;
+                sc[nt][c] = a;
+                sc[nt][2 + c] = b;
+                tmA = fmaxf(tmA, a);
+                tmB = fmaxf(tmB, b);
+            }
+#pragma unroll
+        for (int off = 1; off < 4; off <<= 1) {
+            tmA = fmaxf(tmA, __shfl_xor_sync(0xffffffffu, tmA, off));
+            tmB = fmaxf(tmB, __shfl_xor_sync(0xffffffffu, tmB, off));
+        }
+        const float nmA = fmaxf(mA, tmA), nmB = fmaxf(mB, tmB);
+        const float cA = nmA == -INFINITY ? 1.f : exp2f(mA - nmA);
+        const float cB = nmB == -INFINITY ? 1.f : exp2f(mB - nmB);
+        float sA = 0.f, sB = 0.f;
+        uint32_t pa[TK / 16][4];
+#pragma unroll
+        for (int nt = 0; nt < TK / 8; ++nt) {
+            float e[4];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                e[c] = sc[nt][c] == -INFINITY ? 0.f : exp2f(sc[nt][c] - nmA);
+                e[2 + c] = sc[nt][2 + c] == -INFINITY ? 0.f : exp2f(sc[nt][2 + c] - nmB);
+                sA += e[c];
+                sB += e[2 + c];
+            }
+            // D-fragment of n-tile nt == half of the A-fragment of k-step nt/2
+            const int ks = nt / 2, hi = nt % 2;
+            pa[ks][hi * 2 + 0] = pack_bf16(e[0], e[1]);
+            pa[ks][hi * 2 + 1] = pack_bf16(e[2], e[3]);
+        }
+        lA = lA * cA + sA;
+        lB = lB * cB + sB;
+        mA = nmA;
+        mB = nmB;
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i) {
+            o[i][0] *= cA;
+            o[i][1] *= cA;
+            o[i][2] *= cB;
+            o[i][3] *= cB;
+        }
+#pragma unroll
+        for (int ks = 0; ks < TK / 16; ++ks)
+#pragma unroll
+            for (int np = 0; np < D / 16; ++np) {
+                const int mi = lane / 8, rr = lane % 8;
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(vt + swz(ks * 16 + (mi & 1) * 8 + rr, np * 2 + (mi >> 1)), b0, b1, b2, b3);
+                mma_bf16(o[2 * np], pa[ks], b0, b1);
+                mma_bf16(o[2 * np + 1], pa[ks], b2, b3);
+            }
+        __syncthreads();  // the stage is reloaded by the next iteration's prefetch
+    }
+#pragma unroll
+    for (int off = 1; off < 4; off <<= 1) {
+        lA += __shfl_xor_sync(0xffffffffu, lA, off);
+        lB += __shfl_xor_sync(0xffffffffu, lB, off);
+    }
+    const float iA = lA > 0.f ? 1.f / lA : 0.f, iB = lB > 0.f ? 1.f / lB : 0.f;
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+        const int d = i * 8 + (lane % 4) * 2;
+        if (q0 + rA < Sq) {
+            s_orow[rA][int64_t(d) * s_ostr[rA]] = __float2bfloat16_rn(o[i][0] * iA);
+            s_orow[rA][int64_t(d + 1) * s_ostr[rA]] = __float2bfloat16_rn(o[i][1] * iA);
+        }
+        if (q0 + rB < Sq) {
+            s_orow[rB][int64_t(d) * s_ostr[rB]] = __float2bfloat16_rn(o[i][2] * iB);
+            s_orow[rB][int64_t(d + 1) * s_ostr[rB]] = __float2bfloat16_rn(o[i][3] * iB);
+        }
+    }
+}
+
+}  // namespace
+
+bool attn_prefill_supported(const AttnParams& p) {
+    return p.dt == KDType::BF16 && p.D == D && p.Dv == D && !p.has_bias && p.kv_affine && p.k.vec_ok && p.v.vec_ok &&
+           p.q.fast_ok && p.o.fast_ok;
+}
+
+void launch_attn_prefill(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
+    dim3 grid(unsigned((p.Sq + QR - 1) / QR), unsigned(int64_t(p.Bt) * p.H));
+    const size_t smem = size_t(STAGES) * STAGEB;
+    cudaFuncSetAttribute(attn_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    launch_k(attn_prefill_kernel, grid, dim3(NT), smem, s, dp);
+}
+
+}  // namespace vtc

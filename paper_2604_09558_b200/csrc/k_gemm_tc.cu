@@ -20,6 +20,7 @@
 //     split order (deterministic) and runs the epilogue.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "device.cuh"
@@ -58,6 +59,38 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int32_
         "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
+}
+__device__ __forceinline__ void tma_nd(void* dst, const CUtensorMap* map, const int32_t (&c)[5], int nd, uint64_t* bar,
+                                       uint64_t policy) {
+    const uint32_t d = smem_u32(dst), b = smem_u32(bar);
+    const uint64_t m = reinterpret_cast<uint64_t>(map);
+    switch (nd) {
+        case 2:
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+                "{%2, %3}], [%4], %5;" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(b), "l"(policy)
+                : "memory");
+            break;
+        case 3:
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+                "{%2, %3, %4}], [%5], %6;" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b), "l"(policy)
+                : "memory");
+            break;
+        case 4:
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+                "{%2, %3, %4, %5}], [%6], %7;" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(b), "l"(policy)
+                : "memory");
+            break;
+        default:
+            asm volatile(
+                "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+                "{%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]),
+                "r"(b), "l"(policy)
+                : "memory");
+            break;
+    }
 }
 __device__ __forceinline__ uint64_t evict_last_policy() {
     uint64_t p;
@@ -141,7 +174,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             unsigned char* sa = smem + size_t(s) * STAGE_BYTES;
             unsigned char* sb = sa + A_BYTES;
             const int32_t k0 = int32_t(kt0 + i) * BK;
-            tma_2d(sa, &tm.a, k0, int32_t(m0), &full[s], pol_a);
+            int32_t ca[5];
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                int64_t v = (p.a_axis[j] ? int64_t(k0) : m0) / p.a_div[j];
+                ca[j] = int32_t(p.a_mod[j] ? v % p.a_mod[j] : v);
+            }
+            tma_nd(sa, &tm.a, ca, p.a_ndims, &full[s], pol_a);
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
                 tma_2d(sb + j * (BK * 128), &tm.b, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
@@ -327,18 +366,85 @@ constexpr size_t smem_bytes() {
 
 }  // namespace
 
-bool gemm_tc_encode(GemmTcParams& p, const void* a_base, int64_t a_ld, const void* b_base, int64_t b_ld) {
+bool gemm_tc_a_dims(const vtc_map& a, int64_t M, int64_t K, GemmTcParams& p, int64_t dims[5], int64_t strides[5],
+                    const void** base) {
+    if (a.npieces != 1 || a.rank != 2) return false;
+    const vtc_piece& pc = a.piece[0];
+    if (pc.ngroups != 0 || pc.ndigits < 1 || pc.ndigits > 5) return false;
+    struct Dg {
+        int axis;
+        int64_t div, mod, coeff;
+    };
+    Dg dg[VTC_MAX_DIGITS];
+    int n = 0;
+    for (int t = 0; t < pc.ndigits; ++t) {
+        const vtc_digit& d = pc.dig[t];
+        if (d.coeff <= 0 || d.group >= 0 || (d.axis != 0 && d.axis != 1)) return false;
+        dg[n++] = Dg{d.axis, int64_t(d.div), int64_t(d.mod), d.coeff};
+    }
+    std::sort(dg, dg + n, [](const Dg& x, const Dg& y) { return x.coeff < y.coeff; });
+    if (dg[0].axis != 1 || dg[0].div != 1 || dg[0].coeff != 1) return false;
+    bool have_m = false;
+    for (int j = 0; j < n; ++j) {
+        const int64_t ext_axis = dg[j].axis ? K : M;
+        const int64_t tile = dg[j].axis ? BK : BM;
+        const int64_t extent = dg[j].mod ? dg[j].mod : (ext_axis + dg[j].div - 1) / dg[j].div;
+        if (dg[j].div == 1) {
+            // the box dimension of this axis: the tile must not cross its modulus
+            if (dg[j].mod && dg[j].mod % tile != 0) return false;
+            if (dg[j].axis == 0) {
+                if (have_m) return false;
+                have_m = true;
+            } else if (j != 0) {
+                return false;
+            }
+        } else if (dg[j].div % tile != 0) {
+            return false;  // constant over a tile only when the divisor is tile-aligned
+        }
+        if (j > 0 && (dg[j].coeff * 2) % 16 != 0) return false;
+        p.a_axis[j] = dg[j].axis;
+        p.a_div[j] = dg[j].div;
+        p.a_mod[j] = dg[j].mod;
+        dims[j] = extent;
+        strides[j] = dg[j].coeff;
+    }
+    if (!have_m && M > 1) return false;
+    for (int j = n; j < 5; ++j) {
+        p.a_axis[j] = 0;
+        p.a_div[j] = 1;
+        p.a_mod[j] = 1;
+    }
+    p.a_ndims = n < 2 ? 2 : n;
+    if (n < 2) {  // M == 1 without an M digit: a unit second dimension
+        dims[1] = 1;
+        strides[1] = K;
+        p.a_axis[1] = 0;
+        p.a_div[1] = 1;
+        p.a_mod[1] = 1;
+    }
+    *base = reinterpret_cast<const char*>(pc.ptr) + pc.base * 2;
+    return (reinterpret_cast<uintptr_t>(*base) % 16) == 0;
+}
+
+bool gemm_tc_encode(GemmTcParams& p, const void* a_base, const int64_t* a_dims, const int64_t* a_strides,
+                    const void* b_base, int64_t b_ld) {
     EncodeFn fn = encoder();
     if (!fn) return false;
     if ((reinterpret_cast<uintptr_t>(a_base) % 16) || (reinterpret_cast<uintptr_t>(b_base) % 16)) return false;
-    if ((a_ld * 2) % 16 || (b_ld * 2) % 16) return false;
-    cuuint32_t es[2] = {1, 1};
+    if ((b_ld * 2) % 16) return false;
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
     {
-        cuuint64_t dims[2] = {cuuint64_t(p.K), cuuint64_t(p.M)};
-        cuuint64_t str[1] = {cuuint64_t(a_ld) * 2};
-        cuuint32_t box[2] = {BK, BM};
-        if (fn(reinterpret_cast<CUtensorMap*>(p.tmap_a), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a_base), dims,
-               str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        const int nd = p.a_ndims;
+        cuuint64_t dims[5], str[4];
+        cuuint32_t box[5];
+        for (int j = 0; j < nd; ++j) {
+            dims[j] = cuuint64_t(a_dims[j]);
+            if (j > 0) str[j - 1] = cuuint64_t(a_strides[j]) * 2;
+            const bool boxed = p.a_div[j] == 1 && (j == 0 || p.a_axis[j] == 0);
+            box[j] = boxed ? (p.a_axis[j] ? BK : BM) : 1;
+        }
+        if (fn(reinterpret_cast<CUtensorMap*>(p.tmap_a), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, cuuint32_t(nd), const_cast<void*>(a_base),
+               dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return false;
     }

@@ -143,10 +143,22 @@ struct GemmTcParams {
     int32_t has_res, pad;
     float* work;          // [tiles, splits, 128, bn] fp32 partials (splits > 1)
     unsigned int* counters;
+    // A's TMA tensor: up to 5 dimensions, one per digit of A's map
+    // ((idx[axis] / div) mod mod, axis 0 = M, 1 = K); coordinates of a tile at
+    // (m0, k0) are computed per dimension by the producer
+    int32_t a_ndims, a_pad;
+    int32_t a_axis[5];
+    int32_t a_pad2[3];
+    int64_t a_div[5], a_mod[5];
     alignas(64) unsigned char tmap_a[128];
     alignas(64) unsigned char tmap_b[128];
 };
-bool gemm_tc_encode(GemmTcParams& p, const void* a_base, int64_t a_ld, const void* b_base, int64_t b_ld);
+// Derive A's TMA dimensions from its lowered map (one piece, no groups, digits
+// forming tile-aligned mixed-radix coordinates; innermost = K with unit stride).
+bool gemm_tc_a_dims(const vtc_map& a, int64_t M, int64_t K, GemmTcParams& p, int64_t dims[5], int64_t strides[5],
+                    const void** base);
+bool gemm_tc_encode(GemmTcParams& p, const void* a_base, const int64_t* a_dims, const int64_t* a_strides,
+                    const void* b_base, int64_t b_ld);
 void launch_gemm_tc(const GemmTcParams& p, const GemmTcParams* dp, cudaStream_t s);
 
 // ---- row-wise normalisations / softmax -----------------------------------
@@ -180,13 +192,15 @@ struct AttnParams {
     float* part_o;                 // [Bt, H, Sq, splits, Dv]
     float* part_ml;                // [Bt, H, Sq, splits, 2]
     // tensor-core decode path (k_attn_decode.cu)
-    int32_t fast;                  // 1: attn_decode_kernel
+    int32_t fast;                  // 1: attn_decode_kernel, 2: attn_prefill_kernel
     int32_t kv_affine;             // K/V maps affine along the key axis (single piece)
     int64_t k_sstride, v_sstride;  // element stride between consecutive keys
     unsigned int* counters;        // [Bt * H / group] split arrival counters (fused combine)
 };
 void launch_attention(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 bool attn_decode_supported(const AttnParams& p);
+bool attn_prefill_supported(const AttnParams& p);
+void launch_attn_prefill(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 void launch_attn_decode(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 
 }  // namespace vtc

@@ -185,6 +185,81 @@ def llama_decode_layer(B: int = 1, L: int = 2048, pos: Optional[int] = None, D: 
     return g.doc()
 
 
+def llama_prefill_layer(B: int = 8, S: int = 4096, D: int = 4096, Hq: int = 32, Hkv: int = 8, hd: int = 128,
+                        F: int = 14336, dtype: str = "bf16", eps: float = 1e-5) -> dict:
+    """One Llama-3 decoder layer over a prefill of S tokens per sequence
+    (BASELINE configs[4]): T = B*S token rows, causal attention.  The QKV
+    split, the RoPE rotate-half, the [B,S,H,d] <-> [B,H,S,d] transposes and the
+    GQA Expand/Reshape of K/V are data-movement chains the planner turns into
+    maps; the roped K and the V projection rows ([B,S,Hkv,d], token-major) are
+    what a KV cache stores for these positions."""
+    G = Hq // Hkv
+    half = hd // 2
+    nq, nkv = Hq * hd, Hkv * hd
+    T = B * S
+    g = GraphBuilder(dtype)
+    g.input("x", [T, D])
+    g.input("w_ln1", [D])
+    g.input("w_qkv", [D, nq + 2 * nkv])
+    g.input("cos", [B, S, hd])
+    g.input("sin", [B, S, hd])
+    g.input("w_o", [nq, D])
+    g.input("w_ln2", [D])
+    g.input("w_gate", [D, F])
+    g.input("w_up", [D, F])
+    g.input("w_down", [F, D])
+    g.node("ln1", "RMSNorm", ["x", "w_ln1"], "h1", {"eps": eps})
+    g.node("qkv_proj", "MatMul", ["h1", "w_qkv"], "qkv")
+    g.node("qkv_split", "Split", ["qkv"], ["q2", "k2", "v2"], {"axis": 1, "sizes": [nq, nkv, nkv]})
+    g.node("q_reshape", "Reshape", ["q2"], "q3", {"shape": [B, S, Hq, hd]})
+    g.node("k_reshape", "Reshape", ["k2"], "k3", {"shape": [B, S, Hkv, hd]})
+    g.node("v_reshape", "Reshape", ["v2"], "v3", {"shape": [B, S, Hkv, hd]})
+
+    def rope(tag, x, H, out):
+        g.node(f"{tag}_lo", "Slice", [x], f"{tag}_lo", {"axes": [3], "starts": [0], "ends": [half]})
+        g.node(f"{tag}_hi", "Slice", [x], f"{tag}_hi", {"axes": [3], "starts": [half], "ends": [hd]})
+        g.node(f"{tag}_rot", "Concat", [f"{tag}_hi", f"{tag}_lo"], f"{tag}_rot", {"axis": 3})
+        for tab in ("cos", "sin"):
+            g.node(f"{tag}_{tab}_u", "Unsqueeze", [tab], f"{tag}_{tab}_1", {"axis": 2})
+            g.node(f"{tag}_{tab}_e", "Expand", [f"{tag}_{tab}_1"], f"{tag}_{tab}_b", {"shape": [B, S, H, hd]})
+        g.node(f"{tag}_mc", "Mul", [x, f"{tag}_cos_b"], f"{tag}_xc")
+        g.node(f"{tag}_ms", "Mul", [f"{tag}_rot", f"{tag}_sin_b"], f"{tag}_xs")
+        return g.node(f"{tag}_add", "Add", [f"{tag}_xc", f"{tag}_xs"], out)
+
+    rope("rq", "q3", Hq, "q_r")
+    rope("rk", "k3", Hkv, "k_r")
+    g.node("q_t", "Transpose", ["q_r"], "q4", {"perm": [0, 2, 1, 3]})
+
+    def kv(tag, src, out):
+        g.node(f"{tag}_t", "Transpose", [src], f"{tag}_t", {"perm": [0, 2, 1, 3]})           # [B,Hkv,S,hd]
+        g.node(f"{tag}_u", "Unsqueeze", [f"{tag}_t"], f"{tag}_u5", {"axis": 2})
+        g.node(f"{tag}_e", "Expand", [f"{tag}_u5"], f"{tag}_e", {"shape": [B, Hkv, G, S, hd]})
+        return g.node(f"{tag}_r", "Reshape", [f"{tag}_e"], out, {"shape": [B, Hq, S, hd]})
+
+    kv("kp", "k_r", "k_h")
+    kv("vp", "v3", "v_h")
+    g.node("attn", "Attention", ["q4", "k_h", "v_h"], "o4", {"scale": 1.0 / math.sqrt(hd), "causal": True})
+    g.node("o_t", "Transpose", ["o4"], "o5", {"perm": [0, 2, 1, 3]})
+    g.node("o_reshape", "Reshape", ["o5"], "o2", {"shape": [T, nq]})
+    g.node("o_proj", "MatMul", ["o2", "w_o"], "ao")
+    g.node("res1", "Add", ["x", "ao"], "x2")
+    g.node("ln2", "RMSNorm", ["x2", "w_ln2"], "h2", {"eps": eps})
+    g.node("gate_proj", "MatMul", ["h2", "w_gate"], "gt")
+    g.node("up_proj", "MatMul", ["h2", "w_up"], "up")
+    g.node("silu", "SiLU", ["gt"], "sg")
+    g.node("gate_mul", "Mul", ["sg", "up"], "mm")
+    g.node("down_proj", "MatMul", ["mm", "w_down"], "dn")
+    g.node("res2", "Add", ["x2", "dn"], "y", out_kind="output")
+    return g.doc()
+
+
+def rope_tables_prefill(B: int, S: int, hd: int = 128, theta: float = 500000.0):
+    """cos and sign-folded sin tables [B, S, hd] for positions 0..S-1."""
+    import numpy as np
+    cos, sin = rope_tables(S, list(range(S)), hd, theta)
+    return np.broadcast_to(cos, (B, S, hd)).copy(), np.broadcast_to(sin, (B, S, hd)).copy()
+
+
 def shard_llama_inputs(full: Dict, rank: int, tp: int, Hq: int = 32, Hkv: int = 8, hd: int = 128,
                        F: int = 14336) -> Dict:
     """Rank `rank`'s inputs of llama_decode_layer(tp=tp) from the full layer's

@@ -306,3 +306,44 @@ def test_tensor_parallel_plan_runs_nccl_allreduce():
     r = subprocess.run([sys.executable, "-c", "import sys; sys.path.insert(0, 'tests'); import test_gpu; test_gpu._tp_nccl_check()"],
                        cwd=root, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_gemm_tensor_core_reads_a_transposed_view_through_4d_tma(vtc, oracle):
+    """o2[t, h*d + j] = o4[b, h, s, j] (Transpose + Reshape of the attention
+    output): not a 2-D affine operand, but its map's div/mod digits become a
+    4-D TMA tensor (tile-aligned), so the GEMM reads the view with no copy."""
+    from paper_2604_09558_b200.workloads import GraphBuilder
+    B, H, S, hd, N = 2, 4, 256, 128, 384
+    g = GraphBuilder("bf16")
+    g.input("o4", [B, H, S, hd])
+    g.input("w", [H * hd, N])
+    g.node("t", "Transpose", ["o4"], "o5", {"perm": [0, 2, 1, 3]})
+    g.node("r", "Reshape", ["o5"], "o2", {"shape": [B * S, H * hd]})
+    g.node("mm", "MatMul", ["o2", "w"], "y", out_kind="output")
+    doc = g.doc()
+    x = oracle.random_inputs(doc, seed=21, scales={"w": 1.0 / np.sqrt(H * hd)})
+    got, p = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
+    assert [l["kernel"] for l in p.info()["launches"]] == ["gemm_tc_bf16"]
+    a = oracle.bf16_to_f32(x["o4"]).astype(np.float64).transpose(0, 2, 1, 3).reshape(B * S, H * hd)
+    want = a @ oracle.bf16_to_f32(x["w"]).astype(np.float64)
+    assert _relerr(oracle.bf16_to_f32(got["y"]), want) < 1e-2
+
+
+@pytest.mark.parametrize("cfg", [dict(B=2, S=128, D=256, Hq=4, Hkv=2, hd=128, F=512),
+                                 dict(B=1, S=192, D=512, Hq=8, Hkv=2, hd=128, F=1024)])
+def test_llama_prefill_layer_small(vtc, oracle, cfg):
+    """BASELINE configs[4] shape family at reduced size: causal flash attention
+    on tensor cores, projections on tcgen05 (o_proj reads the attention output
+    through a 4-D TMA view), zero data-movement kernels."""
+    from paper_2604_09558_b200 import workloads as W
+    doc = W.llama_prefill_layer(**cfg)
+    x = oracle.random_inputs(doc, seed=8, scales=W.llama_weight_scales(cfg["D"], cfg["F"]))
+    cos, sin = W.rope_tables_prefill(cfg["B"], cfg["S"], hd=cfg["hd"])
+    x["cos"] = oracle.f32_to_bf16(cos.astype(np.float32))
+    x["sin"] = oracle.f32_to_bf16(sin.astype(np.float32))
+    want = oracle.execute(doc, x)["y"]
+    got, p = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
+    kinds = [l["kernel"] for l in p.info()["launches"]]
+    assert "attn_prefill_tc" in kinds and kinds.count("gemm_tc_bf16") == 5, kinds
+    assert p.info()["data_movement_launches"] == 0
+    assert _relerr(oracle.bf16_to_f32(got["y"]), oracle.bf16_to_f32(want)) < 2e-2

@@ -320,7 +320,10 @@ def run_vtc(args):
             print(f"[trace {name}] total {(tr[:, 1].max() - t0) / 1e3:.1f} us", file=sys.stderr)
             for l, row in zip(p.info()["launches"], tr):
                 a, z = row[0], row[1]
-                cps = " ".join(f"cp{k}={(row[k] - t0) / 1e3:.1f}" for k in range(2, 8) if row[k])
+                if l["kernel"].startswith("gemm_tc") and row[4]:
+                    cps = f"avg mainloop {row[2] / row[4] / 1e3:.2f} us, avg epilogue {row[3] / row[4] / 1e3:.2f} us over {row[4]} CTAs"
+                else:
+                    cps = " ".join(f"cp{k}={(row[k] - t0) / 1e3:.1f}" for k in range(2, 8) if row[k])
                 print(f"  {l['kernel']:<22} {(a - t0) / 1e3:8.1f} -> {(z - t0) / 1e3:8.1f}  ({(z - a) / 1e3:6.1f} us)  "
                       f"{l['bytes'] / 1e6:8.2f} MB  {l['node'][:50]}  {cps}", file=sys.stderr)
 

@@ -333,7 +333,6 @@ void Executor::prepare(bool dry) {
             return false;
         int maxc = *std::max_element(count.begin(), count.end());
         p.stream = 1;
-        if (const char* dbg = std::getenv("VTC_GEMV_DBG")) p.pad = std::atoi(dbg);
         p.nmat = 1;
         p.n_mat[0] = p.N;
         p.strips0 = int32_t(strips0);

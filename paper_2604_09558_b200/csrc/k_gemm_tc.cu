@@ -132,8 +132,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int tiles_n = int((p.N + BN - 1) / BN);
+    const int tiles_m = int((p.M + BM - 1) / BM);
     const int tile = blockIdx.x;
-    const int tm_ = tile / tiles_n, tn = tile % tiles_n;
+    // grouped rasterisation: consecutive CTAs walk GROUP_M row tiles of one
+    // column tile, so the CTAs in flight share a few A row blocks and B column
+    // blocks through L2 (A and B are re-read by every tile of their row / column)
+    constexpr int GROUP_M = 16;
+    const int in_group = GROUP_M * tiles_n;
+    const int first_m = (tile / in_group) * GROUP_M;
+    const int gm = min(tiles_m - first_m, GROUP_M);
+    const int tm_ = first_m + (tile % in_group) % gm, tn = (tile % in_group) / gm;
     const int64_t m0 = int64_t(tm_) * BM, n0 = int64_t(tn) * BN;
     const int split = blockIdx.y;
     const int ktiles = int((p.K + BK - 1) / BK);
@@ -158,13 +166,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = s_tmem;
     dev::pdl_launch_dependents();
+    const unsigned long long t_start = dev::gtime();
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.b)) : "memory");
-        const uint64_t pol_b = dev::evict_first_policy();  // weights: read once
-        const uint64_t pol_a = evict_last_policy();        // activations: re-read by every N tile
+        // decode-sized M (one row tile): weights are read exactly once -> evict-first;
+        // prefill: every row tile re-reads them -> keep them in L2
+        const uint64_t pol_b = tiles_m == 1 ? dev::evict_first_policy() : evict_last_policy();
+        const uint64_t pol_a = evict_last_policy();  // activations: re-read by every N tile
         dev::pdl_wait();  // A is produced by earlier kernels
         for (int i = 0; i < nk; ++i) {
             const int s = i % STAGES;
@@ -224,6 +235,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     mbar_wait(&done, 0);
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned long long t_main = dev::gtime();
+    if (threadIdx.x == 0) {
+        dev::trace_add(p.head, 2, t_main - t_start);  // sum over CTAs: mainloop
+        dev::trace_add(p.head, 4, 1);                 // CTA count
+    }
     const int row = warp * 32 + lane;  // TMEM lane == tile row
     const int64_t m = m0 + row;
     const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
@@ -338,6 +354,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (threadIdx.x == 0) dev::trace_add(p.head, 3, dev::gtime() - t_main);  // sum over CTAs: epilogue
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));

@@ -346,10 +346,6 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
         zero();
         const int64_t n = n0 + ctid;
         bool last = true;
-        if (p.pad & 2) {  // DEBUG: no cross-CTA reduction
-            if (cslot == 0 && n < Nl) reinterpret_cast<bf16*>(p.work)[n] = __float2bfloat16_rn(outv[0]);
-            continue;
-        }
         if (ncontrib > 1) {
             for (int m = 0; m < M; ++m) p.work[((strip * p.max_contrib + cslot) * M + m) * COLS + ctid] = outv[m];
             __threadfence();

@@ -35,6 +35,7 @@ CONFIGS = {
     "c3": dict(B=64, L=8192, workload="llama3-8b-decoder-layer-decode-b64-kv8192"),
     "c1": dict(n=1024, workload="reshape-transpose-slice-fp32-matmul-1024"),
     "c5": dict(B=8, S=4096, prefill=True, workload="llama3-8b-decoder-layer-prefill-b8-s4096"),
+    "c4": dict(B=64, H=56, swin=True, workload="swin-t-stage1-shifted-window-block-b64-224"),
 }
 METRIC = "decoder-layer latency (us) & HBM GB/s as % roofline; DRAM bytes eliminated"
 
@@ -100,18 +101,26 @@ def build_layer_inputs(doc, cfg, torch, dev):
     """Random-init weights / caches directly on the device; per-step inputs on pinned host."""
     from paper_2604_09558_b200 import workloads as W
     specs = {t["id"]: t for t in doc["tensors"]}
-    scales = W.llama_weight_scales()
+    swin = bool(cfg.get("swin"))
+    scales = W.swin_weight_scales() if swin else W.llama_weight_scales()
+    host_ids = ("x",) if swin else ("x", "cos", "sin")
     g = torch.Generator(device=dev)
     g.manual_seed(1)
     dev_tensors = {}
-    for tid in ("w_ln1", "w_qkv", "w_o", "w_ln2", "w_gate", "w_up", "w_down", "k_cache", "v_cache"):
-        if tid not in specs:
+    for t in doc["tensors"]:
+        tid = t["id"]
+        if t["kind"] != "input" or tid in host_ids:
             continue
-        shape = specs[tid]["shape"]
-        t = torch.empty(shape, dtype=torch.float32, device=dev).uniform_(-1.0, 1.0, generator=g)
-        dev_tensors[tid] = (t * scales.get(tid, 1.0)).to(torch.bfloat16).contiguous()
+        if tid == "attn_bias":
+            dev_tensors[tid] = torch.from_numpy(W.swin_attn_bias()).to(dev).to(torch.bfloat16).contiguous()
+            continue
+        x = torch.empty(t["shape"], dtype=torch.float32, device=dev).uniform_(-1.0, 1.0, generator=g)
+        dev_tensors[tid] = (x * scales.get(tid, 1.0)).to(torch.bfloat16).contiguous()
     B = cfg["B"]
     rng = np.random.default_rng(2)
+    if swin:
+        host = {"x": torch.from_numpy(rng.uniform(-1, 1, size=specs["x"]["shape"]).astype(np.float32)).to(torch.bfloat16)}
+        return dev_tensors, {k: v.contiguous().pin_memory() for k, v in host.items()}
     if cfg.get("prefill"):
         cos, sin = W.rope_tables_prefill(B, cfg["S"])
         rows = B * cfg["S"]
@@ -255,13 +264,19 @@ def run_vtc(args):
     if args.config == "c1":
         return run_c1(args, torch, vtc, W, dev, stream, flush, hbm_peak, peak_src, world, rank)
 
-    B, L = cfg["B"], cfg.get("L", cfg.get("S"))
+    B, L = cfg["B"], cfg.get("L", cfg.get("S", cfg.get("H")))
+    swin = bool(cfg.get("swin"))
     # N > 1: Megatron head sharding (each rank 32/N query heads, 8/N KV heads,
     # F/N FFN columns, its shard of the KV cache) with two NCCL allreduces per
     # layer; --replicas runs N independent full layers instead
     tp = world if (world > 1 and not args.replicas) else 1
     prefill = bool(cfg.get("prefill"))
-    doc = W.llama_prefill_layer(B=B, S=cfg["S"]) if prefill else W.llama_decode_layer(B=B, L=L, tp=tp)
+    if swin:
+        doc = W.swin_block(B=B, H=cfg["H"])
+    elif prefill:
+        doc = W.llama_prefill_layer(B=B, S=cfg["S"])
+    else:
+        doc = W.llama_decode_layer(B=B, L=L, tp=tp)
     g = vtc.parse_graph(doc)
     dev_tensors, host = build_layer_inputs(doc, cfg, torch, dev)
     comm = None
@@ -361,7 +376,8 @@ def run_vtc(args):
 
     # e2e through the C ABI with host buffers: H2D of the step's inputs, the layer, D2H of y
     pv = plans["virtual"]
-    y_host = torch.empty((B * cfg["S"] if prefill else B, 4096), dtype=torch.bfloat16).pin_memory()
+    y_spec = [t for t in doc["tensors"] if t["id"] == "y"][0]
+    y_host = torch.empty(y_spec["shape"], dtype=torch.bfloat16).pin_memory()
 
     def e2e_step():
         for tid, t in host.items():
@@ -386,7 +402,8 @@ def run_vtc(args):
     if rank != 0:
         return
     bytes_step = sum(l["bytes"] for l in launches)
-    cpu = cpu_reference_layer(cfg) if world == 1 and not prefill and not os.environ.get("BENCH_NO_CPU") else None
+    cpu = (cpu_reference_layer(cfg) if world == 1 and not prefill and not swin and not os.environ.get("BENCH_NO_CPU")
+           else None)
     line = {
         "metric": METRIC,
         "value": lat_ms * 1e3,
@@ -400,8 +417,9 @@ def run_vtc(args):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights uniform(-1,1)/sqrt(fan_in), random KV cache)",
-        "config": {"workload": cfg["workload"], "batch": B, ("seq_len" if prefill else "kv_len"): L,
-                   "pos": None if prefill else L - 1,
+        "config": {"workload": cfg["workload"], "batch": B,
+                   **({"resolution": 224, "stage1_grid": L, "window": 7, "shift": 3} if swin else
+                      {("seq_len" if prefill else "kv_len"): L, "pos": None if prefill else L - 1}),
                    "parallelism": (f"tp{tp} (head-sharded; 2 NCCL allreduce of [{B},4096] bf16 per layer)" if tp > 1
                                    else f"replicas x{world}" if world > 1 else "single-gpu"),
                    "l2": ("inputs larger than L2: every step streams %.0f MB of weights + KV (> 126 MB L2), weights/KV "

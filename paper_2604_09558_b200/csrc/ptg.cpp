@@ -7,6 +7,9 @@
 #include "lower.hpp"
 #include "vtc/plan.hpp"
 
+#include "kernels.hpp"
+#include "lower.hpp"
+
 namespace vtc {
 
 std::vector<int> Vtog::out_edges(const std::string& node) const {
@@ -222,6 +225,7 @@ std::vector<int> plan_max_elimination(const Vtog& v) {
 
     std::vector<int> selected;
     std::set<std::string> assigned;
+    std::map<std::string, int> chosen;  // virtual tensor -> candidate
     auto try_select = [&](int c) -> bool {
         if (c < 0) return false;
         const std::string& virt = v.edges[size_t(cand_edges[c][0])].src;
@@ -238,7 +242,15 @@ std::vector<int> plan_max_elimination(const Vtog& v) {
         }
         selected = std::move(trial);
         assigned.insert(virt);
+        chosen[virt] = c;
         return true;
+    };
+    auto unselect = [&](const std::string& virt) {
+        auto it = chosen.find(virt);
+        if (it == chosen.end()) return;
+        for (int e : cand_edges[it->second]) selected.erase(std::remove(selected.begin(), selected.end(), e), selected.end());
+        assigned.erase(virt);
+        chosen.erase(it);
     };
 
     // Phase 1: write-side chains.  A ScatterND output aliases its data in place
@@ -280,6 +292,110 @@ std::vector<int> plan_max_elimination(const Vtog& v) {
             const std::string& x = n.inputs[0];
             const OpNode* px = g.producer(x);
             if (px && !is_data_movement(*px)) try_select(cand_of(x, VtDirection::InputOverOutput, n.id, ""));
+        }
+    }
+    // Phase 3: a data-movement op still left as a copy (its gather map composed
+    // with the upstream views does not lower, e.g. Roll after a window-reverse
+    // chain) -- re-plan its upstream single-input DM chain in the other
+    // direction: its output stays physical and the chain's tensors become
+    // views of it, so the compute producer writes straight through the
+    // composed (lowerable) inverse map.
+    for (int ni : g.topo_order()) {
+        const OpNode& n = g.nodes()[size_t(ni)];
+        if (!is_data_movement(n) || n.kind == OpKind::ScatterND || n.kind == OpKind::Concat || n.kind == OpKind::Split)
+            continue;
+        if (n.outputs.size() != 1 || assigned.count(n.outputs[0])) continue;
+        std::vector<std::string> chain;  // tensors upstream of n's output through single-input DM ops
+        std::string t = n.inputs[0];
+        const OpNode* p = &n;
+        while (true) {
+            chain.push_back(t);
+            const OpNode* q = g.producer(t);
+            if (!q || !is_data_movement(*q) || q->inputs.size() != 1 || q->outputs.size() != 1 ||
+                q->kind == OpKind::ScatterND || g.consumers(t).size() != 1)
+                break;
+            p = q;
+            t = q->inputs[0];
+        }
+        (void)p;
+        std::vector<int> saved = selected;
+        std::set<std::string> saved_assigned = assigned;
+        std::map<std::string, int> saved_chosen = chosen;
+        for (const auto& c : chain) unselect(c);
+        pull_back(n.outputs[0]);
+        // keep the re-plan only if it eliminated more operators
+        auto count_elim = [&](const std::vector<int>& sel) -> size_t {
+            try {
+                return validate_ptg(v, sel).eliminated_ops.size();
+            } catch (const Error&) {
+                return 0;
+            }
+        };
+        if (count_elim(selected) <= count_elim(saved)) {
+            selected = saved;
+            assigned = saved_assigned;
+            chosen = saved_chosen;
+        }
+    }
+    // Phase 4: a bf16 MatMul whose A operand is a view the tensor-core GEMM cannot
+    // read by TMA (e.g. Swin's roll + window partition, a head transpose whose
+    // K digits are narrower than a 64-wide K tile): make A physical instead and
+    // let the producer write through the inverse chain (LayerNorm / attention
+    // store through any map), when that eliminates as many operators.
+    auto count_elim = [&](const std::vector<int>& sel) -> size_t {
+        try {
+            return validate_ptg(v, sel).eliminated_ops.size();
+        } catch (const Error&) {
+            return 0;
+        }
+    };
+    auto tma_ok = [&](const std::string& a) -> bool {
+        try {
+            PointsToGraph p = validate_ptg(v, selected);
+            auto it = p.resolved.find(a);
+            if (it == p.resolved.end()) return true;  // physical
+            vtc_map d = lower_map(it->second, [](const std::string&) { return TargetInfo{0, 0}; });
+            const TensorSpec& t = g.tensor(a);
+            GemmTcParams probe{};
+            int64_t dims[5], strides[5];
+            const void* base = nullptr;
+            return gemm_tc_a_dims(d, t.shape[0], t.shape[1], probe, dims, strides, &base);
+        } catch (const Error&) {
+            return true;
+        }
+    };
+    for (int ni : g.topo_order()) {
+        const OpNode& n = g.nodes()[size_t(ni)];
+        if (n.kind != OpKind::MatMul) continue;
+        const std::string& a = n.inputs[0];
+        const TensorSpec& at = g.tensor(a);
+        if (at.dtype != DType::BF16 || at.shape.size() != 2 || at.shape[0] <= 16 || !assigned.count(a) || tma_ok(a))
+            continue;
+        std::vector<std::string> chain;
+        std::string t = a;
+        while (true) {
+            const OpNode* q = g.producer(t);
+            if (!q || !is_data_movement(*q) || q->inputs.size() != 1 || q->outputs.size() != 1 ||
+                q->kind == OpKind::ScatterND)
+                break;
+            chain.push_back(t);
+            t = q->inputs[0];
+            if (g.consumers(t).size() != 1) break;
+            if (!g.producer(t) || !is_data_movement(*g.producer(t))) {
+                chain.push_back(t);  // the compute producer's output becomes a view too
+                break;
+            }
+        }
+        std::vector<int> saved = selected;
+        std::set<std::string> saved_assigned = assigned;
+        std::map<std::string, int> saved_chosen = chosen;
+        size_t before = count_elim(selected);
+        for (const auto& c : chain) unselect(c);
+        pull_back(a);
+        if (count_elim(selected) < before || !tma_ok(a)) {
+            selected = saved;
+            assigned = saved_assigned;
+            chosen = saved_chosen;
         }
     }
     std::sort(selected.begin(), selected.end());

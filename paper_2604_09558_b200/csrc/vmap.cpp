@@ -11,6 +11,8 @@
 // until every box is carry-free; here div/mod atoms absorb the carries, and
 // boxes are split only at base-piece boundaries.
 #include <algorithm>
+#include <set>
+#include <functional>
 #include <cassert>
 #include <map>
 #include <mutex>
@@ -528,6 +530,53 @@ bool digit_structure(const VPiece& p, std::vector<std::pair<int64_t, int64_t>>& 
                     continue;
                 }
             }
+            // composite roll: ((sum_i c_i * digit_i + s) mod k) where the digits form an
+            // exact mixed-radix number x in [0, prod ext_i) <= k: x -> (x + s) mod k is a
+            // bijection, so the atom is one digit of extent k built from its constituents
+            // (Swin's roll after window partition: (7 * (t div 392 mod 8) + t div 7 mod 7 + 3) mod 56)
+            if (a.kind == AtomKind::Mod && !a.arg.t.empty()) {
+                struct Term {
+                    int64_t c, ext;
+                    Digit d;
+                };
+                std::vector<Term> ts;
+                bool ok = true;
+                for (const auto& at : a.arg.t) {
+                    auto sub = as_digit(*at.a);
+                    if (!sub || sub->shift != 0 || at.c <= 0) {
+                        ok = false;
+                        break;
+                    }
+                    Term t{at.c, at.a->hi - at.a->lo + 1, *sub};
+                    // c * x mod k only sees x mod (k / c): an unbounded digit is cut there
+                    if (a.k % at.c == 0 && t.ext > a.k / at.c) {
+                        t.ext = a.k / at.c;
+                        if (t.d.m == 0) t.d.m = t.ext;
+                        else if (t.d.m % t.ext == 0) t.d.m = t.ext;
+                        else {
+                            ok = false;
+                            break;
+                        }
+                    }
+                    ts.push_back(t);
+                }
+                if (ok) {
+                    std::sort(ts.begin(), ts.end(), [](const Term& x, const Term& y) { return x.c < y.c; });
+                    int64_t radix = 1;
+                    for (const auto& t : ts) {
+                        if (t.c != radix) {
+                            ok = false;
+                            break;
+                        }
+                        radix *= t.ext;
+                    }
+                    if (ok && radix <= a.k) {
+                        for (const auto& t : ts) per_axis[t.d.axis].push_back(t.d);
+                        out.emplace_back(std::llabs(tm.c), a.k);
+                        continue;
+                    }
+                }
+            }
             return false;
         }
         per_axis[dg->axis].push_back(*dg);
@@ -903,6 +952,64 @@ VMap VMap::compose(const std::function<const VMap*(const std::string&)>& base, i
     return m;
 }
 
+namespace {
+
+// Change of `l` when axis `ax` advances by P, if that change is the same for
+// every index (atoms see the shift only through whole periods); nullopt else.
+std::optional<int64_t> shift_delta(const Lin& l, int ax, int64_t P);
+
+std::optional<int64_t> atom_delta(const Atom& a, int ax, int64_t P) {
+    if (!(a.axes_mask & (uint64_t(1) << ax))) return 0;
+    if (a.kind == AtomKind::Axis) return a.axis == ax ? P : 0;
+    auto d = shift_delta(a.arg, ax, P);
+    if (!d) return std::nullopt;
+    if (a.kind == AtomKind::Div) {
+        if (*d % a.k != 0) return std::nullopt;
+        return *d / a.k;
+    }
+    if (*d % a.k != 0) return std::nullopt;  // Mod: whole periods only
+    return 0;
+}
+
+std::optional<int64_t> shift_delta(const Lin& l, int ax, int64_t P) {
+    int64_t s = 0;
+    for (const auto& tm : l.t) {
+        auto d = atom_delta(*tm.a, ax, P);
+        if (!d) return std::nullopt;
+        s += tm.c * *d;
+    }
+    return s;
+}
+
+// Smallest period P (a multiple of every divisor / modulus on the way to `ax`)
+// after which every atom of `l` changes by a constant; 0 if none is found.
+int64_t clean_period(const Lin& p, const Lin& q, int ax, int64_t extent) {
+    std::set<int64_t> ks;
+    std::function<void(const Lin&)> walk = [&](const Lin& l) {
+        for (const auto& tm : l.t) {
+            const Atom& a = *tm.a;
+            if (a.kind == AtomKind::Axis || !(a.axes_mask & (uint64_t(1) << ax))) continue;
+            ks.insert(a.k);
+            walk(a.arg);
+        }
+    };
+    walk(p);
+    walk(q);
+    int64_t P = 1;
+    for (int64_t k : ks) {
+        P = std::lcm(P, k);
+        if (P > extent) return 0;
+    }
+    // coefficients inside the atoms may need a multiple of the lcm
+    for (int64_t m = 1; m * P <= extent / 2; ++m) {
+        auto dp = shift_delta(p, ax, m * P), dq = shift_delta(q, ax, m * P);
+        if (dp && dq) return *dp == *dq ? m * P : -1;
+    }
+    return 0;
+}
+
+}  // namespace
+
 int64_t VMap::agree_volume(const VMap& other, int64_t exhaustive_limit) const {
     int64_t agree = 0;
     Index lo, hi;
@@ -919,10 +1026,37 @@ int64_t VMap::agree_volume(const VMap& other, int64_t exhaustive_limit) const {
                 agree += v;
                 continue;
             }
-            if (v > exhaustive_limit) continue;  // conservative: counted as disagreeing
-            for_each_in_box(lo, hi, [&](const Index& idx) {
-                if (p.off.eval(idx.data()) == q.off.eval(idx.data())) ++agree;
+            // Periodic reduction: when advancing an axis by a period P changes both
+            // offsets by the same constant, they agree on the box iff they agree on
+            // its first P slices along that axis (and disagreement repeats).
+            Index rhi = hi;
+            int64_t reps = 1;
+            bool differ_const = false;
+            for (size_t ax = 0; ax < lo.size() && volume([&] {
+                     Index e(lo.size());
+                     for (size_t i = 0; i < lo.size(); ++i) e[i] = rhi[i] - lo[i];
+                     return e;
+                 }()) > exhaustive_limit;
+                 ++ax) {
+                int64_t ext = rhi[ax] - lo[ax];
+                if (ext < 4 || (rhi[ax] - lo[ax]) != (hi[ax] - lo[ax])) continue;
+                int64_t P = clean_period(p.off, q.off, int(ax), ext);
+                if (P < 0) {
+                    differ_const = true;  // both periodic with different steps: disagree beyond the first period
+                    break;
+                }
+                if (P == 0 || ext % P != 0) continue;
+                reps *= ext / P;
+                rhi[ax] = lo[ax] + P;
+            }
+            int64_t rv = 1;
+            for (size_t i = 0; i < lo.size(); ++i) rv *= rhi[i] - lo[i];
+            if (differ_const || rv > exhaustive_limit) continue;  // conservative: counted as disagreeing
+            int64_t part = 0;
+            for_each_in_box(lo, rhi, [&](const Index& idx) {
+                if (p.off.eval(idx.data()) == q.off.eval(idx.data())) ++part;
             });
+            agree += part == rv ? v : (reps == 1 ? part : 0);
         }
     return agree;
 }

@@ -253,6 +253,93 @@ def llama_prefill_layer(B: int = 8, S: int = 4096, D: int = 4096, Hq: int = 32, 
     return g.doc()
 
 
+def swin_block(B: int = 64, H: int = 56, C: int = 96, heads: int = 3, win: int = 7, shift: int = 3,
+               mlp: int = 384, dtype: str = "bf16", eps: float = 1e-5) -> dict:
+    """Swin-T stage-1 shifted-window transformer block (BASELINE configs[3]):
+    x [B, H, H, C] -> LN -> cyclic Roll(-shift) -> window partition ->
+    QKV linear -> W-MSA (relative-position bias + shift mask, one additive
+    bias tensor per window) -> proj -> window reverse -> Roll(+shift) ->
+    residual -> LN -> MLP (GELU) -> residual.  Roll, the partition / reverse
+    reshapes and transposes, the QKV split and the per-window bias broadcast
+    are data movement; under a VTC plan they are maps ((i + 3) mod 56,
+    t div 7, t mod 7, ...) evaluated inside the LN / GEMM / attention kernels."""
+    nw = (H // win) ** 2
+    T = win * win
+    hd = C // heads
+    g = GraphBuilder(dtype)
+    g.input("x", [B, H, H, C])
+    g.input("ln1_g", [C])
+    g.input("ln1_b", [C])
+    g.input("w_qkv", [C, 3 * C])
+    g.input("attn_bias", [nw, heads, T, T])   # relative-position bias + shift mask, per window
+    g.input("w_proj", [C, C])
+    g.input("ln2_g", [C])
+    g.input("ln2_b", [C])
+    g.input("w_fc1", [C, mlp])
+    g.input("w_fc2", [mlp, C])
+    g.node("ln1", "LayerNorm", ["x", "ln1_g", "ln1_b"], "xn", {"eps": eps})
+    g.node("roll", "Roll", ["xn"], "xs", {"axes": [1, 2], "shifts": [-shift, -shift]})
+    # window partition: [B, H/w, w, H/w, w, C] -> [B, H/w, H/w, w, w, C] -> [B*nw*T, C]
+    g.node("part_r", "Reshape", ["xs"], "xp6", {"shape": [B, H // win, win, H // win, win, C]})
+    g.node("part_t", "Transpose", ["xp6"], "xw6", {"perm": [0, 1, 3, 2, 4, 5]})
+    g.node("part_f", "Reshape", ["xw6"], "xw", {"shape": [B * nw * T, C]})
+    g.node("qkv_proj", "MatMul", ["xw", "w_qkv"], "qkv")
+    g.node("qkv_r", "Reshape", ["qkv"], "qkv5", {"shape": [B * nw, T, 3, heads, hd]})
+    g.node("qkv_t", "Transpose", ["qkv5"], "qkvt", {"perm": [2, 0, 3, 1, 4]})      # [3, B*nw, heads, T, hd]
+    g.node("qkv_s", "Split", ["qkvt"], ["q5", "k5", "v5"], {"axis": 0, "sizes": [1, 1, 1]})
+    for c in ("q", "k", "v"):
+        g.node(f"{c}_r", "Reshape", [f"{c}5"], f"{c}4", {"shape": [B * nw, heads, T, hd]})
+    g.node("bias_u", "Unsqueeze", ["attn_bias"], "bias5", {"axis": 0})                  # [1, nw, heads, T, T]
+    g.node("bias_e", "Expand", ["bias5"], "bias_be", {"shape": [B, nw, heads, T, T]})
+    g.node("bias_r", "Reshape", ["bias_be"], "bias4", {"shape": [B * nw, heads, T, T]})
+    g.node("attn", "Attention", ["q4", "k4", "v4", "bias4"], "o4", {"scale": 1.0 / math.sqrt(hd), "causal": False})
+    g.node("o_t", "Transpose", ["o4"], "o5", {"perm": [0, 2, 1, 3]})                     # [B*nw, T, heads, hd]
+    g.node("o_r", "Reshape", ["o5"], "o2", {"shape": [B * nw * T, C]})
+    g.node("proj", "MatMul", ["o2", "w_proj"], "pw")
+    # window reverse + reverse roll
+    g.node("rev_r", "Reshape", ["pw"], "pr6", {"shape": [B, H // win, H // win, win, win, C]})
+    g.node("rev_t", "Transpose", ["pr6"], "pt6", {"perm": [0, 1, 3, 2, 4, 5]})
+    g.node("rev_f", "Reshape", ["pt6"], "ps", {"shape": [B, H, H, C]})
+    g.node("unroll", "Roll", ["ps"], "pu", {"axes": [1, 2], "shifts": [shift, shift]})
+    g.node("res1", "Add", ["x", "pu"], "x2")
+    g.node("ln2", "LayerNorm", ["x2", "ln2_g", "ln2_b"], "xn2", {"eps": eps})
+    g.node("mlp_f", "Reshape", ["xn2"], "xm", {"shape": [B * H * H, C]})
+    g.node("fc1", "MatMul", ["xm", "w_fc1"], "h1")
+    g.node("gelu", "GELU", ["h1"], "h1g")
+    g.node("fc2", "MatMul", ["h1g", "w_fc2"], "h2")
+    g.node("mlp_b", "Reshape", ["h2"], "h2r", {"shape": [B, H, H, C]})
+    g.node("res2", "Add", ["x2", "h2r"], "y", out_kind="output")
+    return g.doc()
+
+
+def swin_attn_bias(H: int = 56, heads: int = 3, win: int = 7, shift: int = 3, seed: int = 0):
+    """Per-window additive attention bias [nw, heads, T, T]: a random relative-
+    position bias table gathered by relative coordinates (as in Swin) plus the
+    -100 shift mask between tokens from different regions of a shifted window."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    table = rng.uniform(-0.1, 0.1, size=((2 * win - 1) ** 2, heads)).astype(np.float32)
+    coords = np.stack(np.meshgrid(np.arange(win), np.arange(win), indexing="ij")).reshape(2, -1)
+    rel = coords[:, :, None] - coords[:, None, :] + win - 1
+    idx = rel[0] * (2 * win - 1) + rel[1]
+    rpb = table[idx.reshape(-1)].reshape(win * win, win * win, heads).transpose(2, 0, 1)
+    img = np.zeros((H, H), np.int32)
+    cnt = 0
+    for hs in (slice(0, -win), slice(-win, -shift), slice(-shift, None)):
+        for ws in (slice(0, -win), slice(-win, -shift), slice(-shift, None)):
+            img[hs, ws] = cnt
+            cnt += 1
+    nwin = H // win
+    win_ids = img.reshape(nwin, win, nwin, win).transpose(0, 2, 1, 3).reshape(nwin * nwin, win * win)
+    mask = np.where(win_ids[:, :, None] != win_ids[:, None, :], -100.0, 0.0).astype(np.float32)
+    return (rpb[None, :, :, :] + mask[:, None, :, :]).astype(np.float32)
+
+
+def swin_weight_scales(C: int = 96, mlp: int = 384) -> Dict[str, float]:
+    return {"w_qkv": 1 / math.sqrt(C), "w_proj": 1 / math.sqrt(C), "w_fc1": 1 / math.sqrt(C),
+            "w_fc2": 1 / math.sqrt(mlp), "ln1_g": 1.0, "ln2_g": 1.0, "ln1_b": 0.1, "ln2_b": 0.1}
+
+
 def rope_tables_prefill(B: int, S: int, hd: int = 128, theta: float = 500000.0):
     """cos and sign-folded sin tables [B, S, hd] for positions 0..S-1."""
     import numpy as np

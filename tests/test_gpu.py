@@ -347,3 +347,22 @@ def test_llama_prefill_layer_small(vtc, oracle, cfg):
     assert "attn_prefill_tc" in kinds and kinds.count("gemm_tc_bf16") == 5, kinds
     assert p.info()["data_movement_launches"] == 0
     assert _relerr(oracle.bf16_to_f32(got["y"]), oracle.bf16_to_f32(want)) < 2e-2
+
+
+@pytest.mark.parametrize("cfg", [dict(B=2, H=14, C=24, heads=3, mlp=96), dict(B=1, H=28, C=96, heads=3, mlp=384)])
+def test_swin_block_small(vtc, oracle, cfg):
+    """BASELINE configs[3] family at reduced size: cyclic roll, window
+    partition / reverse, the QKV split and the per-window bias broadcast are
+    all maps (zero data-movement kernels); LayerNorm writes and the attention
+    stores go through inverse maps so the projections read physical operands."""
+    from paper_2604_09558_b200 import workloads as W
+    doc = W.swin_block(**cfg)
+    x = oracle.random_inputs(doc, seed=13, scales=W.swin_weight_scales(cfg["C"], cfg["mlp"]))
+    x["attn_bias"] = oracle.f32_to_bf16(W.swin_attn_bias(H=cfg["H"], heads=cfg["heads"]))
+    want = oracle.execute(doc, x)["y"]
+    got, p = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
+    assert p.info()["data_movement_launches"] == 0
+    assert _relerr(oracle.bf16_to_f32(got["y"]), oracle.bf16_to_f32(want)) < 2e-2
+    got_m, pm = _run(vtc, doc, x, vtc.MATERIALIZE)
+    assert pm.info()["data_movement_launches"] > 10
+    assert _relerr(oracle.bf16_to_f32(got_m["y"]), oracle.bf16_to_f32(want)) < 2e-2

@@ -376,8 +376,7 @@ def run_vtc(args):
 
     # e2e through the C ABI with host buffers: H2D of the step's inputs, the layer, D2H of y
     pv = plans["virtual"]
-    y_spec = [t for t in doc["tensors"] if t["id"] == "y"][0]
-    y_host = torch.empty(y_spec["shape"], dtype=torch.bfloat16).pin_memory()
+    y_host = torch.empty(g.tensors()["y"]["shape"], dtype=torch.bfloat16).pin_memory()
 
     def e2e_step():
         for tid, t in host.items():

@@ -585,7 +585,12 @@ void Executor::prepare(bool dry) {
         GemmTcParams probe{};
         int64_t dims[5], strides[5];
         const void* base = nullptr;
-        return gemm_tc_a_dims(am, A.shape[0], A.shape[1], probe, dims, strides, &base);
+        if (gemm_tc_a_dims(am, A.shape[0], A.shape[1], probe, dims, strides, &base)) return true;
+        // gather fallback: rows located through the map, unit stride + 16-B aligned along K
+        VOperand op{};
+        op.m = am;
+        finish_operand(op, 1, 64, 2);
+        return op.vec_ok != 0;
     };
     if (opt_.fuse) {
         for (const auto& n : g_.nodes()) {
@@ -890,7 +895,24 @@ void Executor::prepare(bool dry) {
                     const char* bbase = reinterpret_cast<const char*>(target(bmm.pieces()[0].target).ptr) + cb * es;
                     int64_t adims[5], astr[5];
                     const void* abase = nullptr;
-                    ok = ok && gemm_tc_a_dims(lower_map(map_of(n.inputs[0]), target), M, K, p, adims, astr, &abase);
+                    const vtc_map alow = lower_map(map_of(n.inputs[0]), target);
+                    if (ok && !gemm_tc_a_dims(alow, M, K, p, adims, astr, &abase)) {
+                        // A through 16-byte cp.async gathers (row bases from its map)
+                        p.a = operand(map_of(n.inputs[0]), 1, 64, es);
+                        ok = p.a.vec_ok != 0;
+                        p.a_gather = 1;
+                        p.a_ndims = 2;  // the (unused) A tensor map: a dummy over B
+                        adims[0] = K;
+                        adims[1] = 1;
+                        astr[1] = K;
+                        abase = bbase;
+                        for (int j = 0; j < 5; ++j) {
+                            p.a_axis[j] = j == 0 ? 1 : 0;
+                            p.a_div[j] = 1;
+                            p.a_mod[j] = 0;
+                        }
+                        if (ok) T->kernel = "gemm_tc_bf16_gather";
+                    }
                     if (ok && !impl_->dry) ok = gemm_tc_encode(p, abase, adims, astr, bbase, ldb);
                     if (ok) {
                         int64_t tiles = (M + 127) / 128 * ((N + p.bn - 1) / p.bn);

@@ -1,4 +1,5 @@
-// Flash attention for long query blocks (prefill), bf16, head dim 128.
+// Flash attention for long query blocks (prefill, windows), bf16, head dim 32 / 64 / 128,
+// optional additive bias through its own map (Swin relative-position bias + shift mask).
 //
 // softmax(scale * Q K^T [causal]) V with Q, K, V and O read / written through
 // their VirtualTensor maps: in a VTC-planned prefill the QKV split, the RoPE
@@ -24,8 +25,7 @@ namespace vtc {
 namespace {
 
 using dev::bf16;
-constexpr int WARPS = 4, NT = WARPS * 32, QR = 16 * WARPS, TK = 64, D = 128, STAGES = 2;
-constexpr int ROWB = D * 2, TILEB = TK * ROWB, STAGEB = 2 * TILEB;  // K + V per stage: 32 KB
+constexpr int WARPS = 4, NT = WARPS * 32, QR = 16 * WARPS, TK = 64, STAGES = 2;
 constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -55,14 +55,25 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&h);
 }
-__device__ __forceinline__ uint32_t swz(int r, int c) { return uint32_t(r * ROWB + ((c ^ (r & 7)) << 4)); }
+// byte offset of 16-byte chunk c of row r: rows of D/8 chunks, XOR-swizzled so
+// the 8 rows an ldmatrix reads land in 8 distinct 16-byte bank groups
+template <int D>
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+    constexpr int ROWB = D * 2;
+    if constexpr (D >= 64) return uint32_t(r * ROWB + ((c ^ (r & 7)) << 4));
+    else return uint32_t(r * ROWB + ((c ^ ((r >> 1) & 3)) << 4));
+}
 
+template <int D>
 __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* __restrict__ pp) {
+    constexpr int ROWB = D * 2, TILEB = TK * ROWB, STAGEB = 2 * TILEB;
     VTC_STAGE_PARAMS(AttnParams, pp);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ const bf16* s_qrow[QR];
     __shared__ bf16* s_orow[QR];
     __shared__ int64_t s_qstr[QR], s_ostr[QR];
+    __shared__ const bf16* s_brow[QR];
+    __shared__ int64_t s_bstr[QR];
 
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int r = p.rank, ax_h = r - 3, ax_s = r - 2, ax_d = r - 1;
@@ -90,6 +101,11 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
         dev::Loc lo = dev::locate(p.o.m, idx);
         s_orow[tid] = dev::addr<bf16>(p.o.m, lo);
         s_ostr[tid] = p.o.fast_stride[lo.piece];
+        if (p.has_bias) {  // additive bias row [.., h, sq, :] (e.g. Swin relative position + shift mask)
+            dev::Loc lb = dev::locate(p.bias.m, idx);
+            s_brow[tid] = dev::addr<bf16>(p.bias.m, lb);
+            s_bstr[tid] = p.bias.fast_stride[lb.piece];
+        }
     }
     // K / V of this head: base at key 0 + key stride (host-proved affine)
     const bf16* kb0;
@@ -115,15 +131,16 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
     auto load_tile = [&](int j, int st) {
         const int t0 = j * TK;
         const uint32_t kd = sbase + st * STAGEB, vd = kd + TILEB;
+        constexpr int CPR = D / 8;  // 16-byte chunks per row
 #pragma unroll
-        for (int i = 0; i < (TK * 16) / NT; ++i) {  // 16 chunks of 16 B per row
+        for (int i = 0; i < (TK * CPR) / NT; ++i) {
             const int c = tid + i * NT;
-            const int row = c >> 4, ch = c & 15;
+            const int row = c / CPR, ch = c % CPR;
             const int t = t0 + row;
             const bool ok = t < kend;
             const int tc = ok ? t : 0;
-            cp_async16(kd + swz(row, ch), kb0 + int64_t(tc) * p.k_sstride + ch * 8, ok);
-            cp_async16(vd + swz(row, ch), vb0 + int64_t(tc) * p.v_sstride + ch * 8, ok);
+            cp_async16(kd + swz<D>(row, ch), kb0 + int64_t(tc) * p.k_sstride + ch * 8, ok);
+            cp_async16(vd + swz<D>(row, ch), vb0 + int64_t(tc) * p.v_sstride + ch * 8, ok);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -173,7 +190,7 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
             for (int kp = 0; kp < D / 32; ++kp) {
                 const int mi = lane / 8, rr = lane % 8;
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4(kt + swz(nt * 8 + rr, kp * 4 + mi), b0, b1, b2, b3);
+                ldsm_x4(kt + swz<D>(nt * 8 + rr, kp * 4 + mi), b0, b1, b2, b3);
                 mma_bf16(sc[nt], qa[2 * kp], b0, b1);
                 mma_bf16(sc[nt], qa[2 * kp + 1], b2, b3);
             }
@@ -185,6 +202,10 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
             for (int c = 0; c < 2; ++c) {
                 const int t = t0 + nt * 8 + (lane % 4) * 2 + c;
                 float a = sc[nt][c] * qscale, b = sc[nt][2 + c] * qscale;
+                if (p.has_bias && t < kend) {
+                    if (q0 + rA < Sq) a += __bfloat162float(s_brow[rA][int64_t(t) * s_bstr[rA]]) * LOG2E;
+                    if (q0 + rB < Sq) b += __bfloat162float(s_brow[rB][int64_t(t) * s_bstr[rB]]) * LOG2E;
+                }
                 if (t >= kend || t > limA) a = -INFINITY;
                 if (t >= kend || t > limB) b = -INFINITY;
                 sc[nt][c] = a;
@@ -234,7 +255,7 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
             for (int np = 0; np < D / 16; ++np) {
                 const int mi = lane / 8, rr = lane % 8;
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(vt + swz(ks * 16 + (mi & 1) * 8 + rr, np * 2 + (mi >> 1)), b0, b1, b2, b3);
+                ldsm_x4_t(vt + swz<D>(ks * 16 + (mi & 1) * 8 + rr, np * 2 + (mi >> 1)), b0, b1, b2, b3);
                 mma_bf16(o[2 * np], pa[ks], b0, b1);
                 mma_bf16(o[2 * np + 1], pa[ks], b2, b3);
             }
@@ -263,15 +284,22 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
 }  // namespace
 
 bool attn_prefill_supported(const AttnParams& p) {
-    return p.dt == KDType::BF16 && p.D == D && p.Dv == D && !p.has_bias && p.kv_affine && p.k.vec_ok && p.v.vec_ok &&
-           p.q.fast_ok && p.o.fast_ok;
+    return p.dt == KDType::BF16 && p.D == p.Dv && (p.D == 32 || p.D == 64 || p.D == 128) && p.kv_affine &&
+           p.k.vec_ok && p.v.vec_ok && p.q.fast_ok && p.o.fast_ok && (!p.has_bias || p.bias.fast_ok);
+}
+
+template <int D>
+void launch_d(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
+    dim3 grid(unsigned((p.Sq + QR - 1) / QR), unsigned(int64_t(p.Bt) * p.H));
+    const size_t smem = size_t(STAGES) * 2 * TK * D * 2;
+    cudaFuncSetAttribute(attn_prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    launch_k(attn_prefill_kernel<D>, grid, dim3(NT), smem, s, dp);
 }
 
 void launch_attn_prefill(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
-    dim3 grid(unsigned((p.Sq + QR - 1) / QR), unsigned(int64_t(p.Bt) * p.H));
-    const size_t smem = size_t(STAGES) * STAGEB;
-    cudaFuncSetAttribute(attn_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    launch_k(attn_prefill_kernel, grid, dim3(NT), smem, s, dp);
+    if (p.D == 32) launch_d<32>(p, dp, s);
+    else if (p.D == 64) launch_d<64>(p, dp, s);
+    else launch_d<128>(p, dp, s);
 }
 
 }  // namespace vtc

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], p.a_gather ? 33 : 1);  // gather: + one arrival per loader lane
             mbar_init(&empty[s], 1);
         }
         mbar_init(&done, 1);
@@ -168,7 +168,57 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     dev::pdl_launch_dependents();
     const unsigned long long t_start = dev::gtime();
 
-    if (warp == 0 && lane == 0) {
+    if (warp == 0 && p.a_gather) {
+        // ---------------- gather producer (A not TMA-readable) ----------------
+        // A's rows are located once through its map (row base, unit stride
+        // along K); every k-tile is then 1024 16-byte cp.asyncs written in the
+        // 128-byte-swizzled layout TMA would produce.  B still comes by TMA.
+        __shared__ const bf16* s_arow[BM];
+        for (int r = lane; r < BM; r += 32) {
+            const int64_t m = m0 + r;
+            const bf16* rp = nullptr;
+            if (m < p.M) {
+                int32_t idx[VTC_MAX_RANK] = {};
+                idx[0] = int32_t(m);
+                rp = dev::elem_ptr<bf16>(p.a.m, idx);
+            }
+            s_arow[r] = rp;
+        }
+        const uint64_t pol_b = tiles_m == 1 ? dev::evict_first_policy() : evict_last_policy();
+        dev::pdl_wait();
+        __syncwarp();
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % STAGES;
+            const uint32_t ph = uint32_t(i / STAGES) & 1u;
+            mbar_wait(&empty[s], ph ^ 1u);
+            unsigned char* sa = smem + size_t(s) * STAGE_BYTES;
+            unsigned char* sb = sa + A_BYTES;
+            const int32_t k0 = int32_t(kt0 + i) * BK;
+            if (lane == 0) {
+                mbar_expect_tx(&full[s], B_BYTES);
+#pragma unroll
+                for (int j = 0; j < BN / 64; ++j)
+                    tma_2d(sb + j * (BK * 128), &tm.b, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
+            }
+            const uint32_t sa_u = smem_u32(sa);
+#pragma unroll 8
+            for (int j = 0; j < (BM * 8) / 32; ++j) {
+                const int c = lane + 32 * j;
+                const int row = c >> 3, ch = c & 7;
+                const bf16* rp = s_arow[row];
+                const int64_t k = int64_t(k0) + ch * 8;
+                const bool ok = rp != nullptr && k < p.K;
+                const void* src = ok ? static_cast<const void*>(rp + k) : static_cast<const void*>(s_arow);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa_u + row * 128 + ((ch ^ (row & 7)) << 4)),
+                             "l"(src), "r"(ok ? 16 : 0)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+            // generic-proxy smem writes must be visible to the tensor core's async proxy
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+        }
+    } else if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.b)) : "memory");

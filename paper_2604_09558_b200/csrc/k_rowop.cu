@@ -99,10 +99,110 @@ __global__ void __launch_bounds__(256) row_kernel(const RowParams* __restrict__ 
     }
 }
 
+// Short rows (bf16, D <= 256, every operand affine along the row): one warp
+// per row, the row's elements in registers (all loads in flight at once), warp
+// shuffle reductions -- Swin's LayerNorm over C = 96 has 200,704 such rows.
+template <int J>
+__global__ void __launch_bounds__(256) row_warp_kernel(const RowParams* __restrict__ pp) {
+    VTC_STAGE_PARAMS(RowParams, pp);
+    dev::pdl_wait();
+    dev::pdl_launch_dependents();
+    const int lane = threadIdx.x % 32;
+    const int D = int(p.D), last = p.rank - 1;
+    const int64_t nw = int64_t(gridDim.x) * 8;
+    // weights / bias once per warp
+    float wv[J], bv[J];
+    {
+        int32_t z[VTC_MAX_RANK] = {};
+        const bf16* w0 = nullptr;
+        const bf16* b0 = nullptr;
+        int64_t ws = 0, bs = 0;
+        if (p.op != RowOp::Softmax) {
+            dev::Loc l = dev::locate(p.w.m, z);
+            w0 = dev::addr<bf16>(p.w.m, l);
+            ws = p.w.fast_stride[l.piece];
+        }
+        if (p.op == RowOp::LayerNorm) {
+            dev::Loc l = dev::locate(p.bias.m, z);
+            b0 = dev::addr<bf16>(p.bias.m, l);
+            bs = p.bias.fast_stride[l.piece];
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int k = lane + 32 * j;
+            wv[j] = (w0 && k < D) ? __bfloat162float(w0[int64_t(k) * ws]) : 0.f;
+            bv[j] = (b0 && k < D) ? __bfloat162float(b0[int64_t(k) * bs]) : 0.f;
+        }
+    }
+    for (int64_t row = int64_t(blockIdx.x) * 8 + threadIdx.x / 32; row < p.rows; row += nw) {
+        int32_t idx[VTC_MAX_RANK];
+        dev::unflatten(row * p.D, p.shape, p.rank, idx);
+        idx[last] = 0;
+        dev::Loc lx = dev::locate(p.x.m, idx), ly = dev::locate(p.out.m, idx);
+        const bf16* xr = dev::addr<bf16>(p.x.m, lx);
+        bf16* yr = dev::addr<bf16>(p.out.m, ly);
+        const int64_t xs = p.x.fast_stride[lx.piece], ys = p.out.fast_stride[ly.piece];
+        float v[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int k = lane + 32 * j;
+            v[j] = k < D ? __bfloat162float(xr[int64_t(k) * xs]) : 0.f;
+        }
+        if (p.op == RowOp::Softmax) {
+            float mx = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+                if (lane + 32 * j < D) mx = fmaxf(mx, v[j]);
+            mx = dev::warp_max(mx);
+            float sum = 0.f;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                v[j] = lane + 32 * j < D ? expf(v[j] - mx) : 0.f;
+                sum += v[j];
+            }
+            sum = dev::warp_sum(sum);
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+                if (lane + 32 * j < D) yr[int64_t(lane + 32 * j) * ys] = __float2bfloat16_rn(v[j] / sum);
+            continue;
+        }
+        float mu = 0.f;
+        if (p.op == RowOp::LayerNorm) {
+            float s = 0.f;
+#pragma unroll
+            for (int j = 0; j < J; ++j) s += v[j];
+            mu = dev::warp_sum(s) / float(D);
+        }
+        float s2 = 0.f;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const float c = lane + 32 * j < D ? v[j] - mu : 0.f;
+            s2 += c * c;
+        }
+        const float r = rsqrtf(dev::warp_sum(s2) / float(D) + p.eps);
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int k = lane + 32 * j;
+            if (k >= D) continue;
+            const float o = p.op == RowOp::LayerNorm ? ((v[j] - mu) * r) * wv[j] + bv[j] : (v[j] * r) * wv[j];
+            yr[int64_t(k) * ys] = __float2bfloat16_rn(o);
+        }
+    }
+}
+
 }  // namespace
 
 void launch_rowop(const RowParams& p, const RowParams* dp, cudaStream_t s) {
     if (p.rows == 0) return;
+    const bool warp_rows = p.dt == KDType::BF16 && p.D <= 256 && p.x.fast_ok && p.out.fast_ok &&
+                           (p.op == RowOp::Softmax || p.w.fast_ok) && (p.op != RowOp::LayerNorm || p.bias.fast_ok);
+    if (warp_rows) {
+        int64_t blocks = (p.rows + 7) / 8;
+        int grid = int(blocks < 148 * 16 ? blocks : 148 * 16);
+        if (p.D <= 128) launch_k(row_warp_kernel<4>, dim3(grid), dim3(256), 0, s, dp);
+        else launch_k(row_warp_kernel<8>, dim3(grid), dim3(256), 0, s, dp);
+        return;
+    }
     int grid = int(p.rows < 148 * 8 ? p.rows : 148 * 8);
     switch (p.dt) {
         case KDType::F64: launch_k(row_kernel<double>, dim3(grid), dim3(256), 0, s, dp); break;

@@ -138,6 +138,9 @@ bool encode_weight_tmap(void* out128, const void* base, int64_t rows, int64_t co
 struct GemmTcParams {
     KHead head;
     VOperand c, res;
+    VOperand a;           // gather path only: A rows located through this map
+    int32_t a_gather;     // 1: A by cp.async gathers (map not TMA-readable), 0: A by TMA
+    int32_t a_pad0;
     int64_t M, N, K;
     int32_t bn, splits;   // N tile (128 / 256), K splits
     int32_t has_res, pad;

@@ -366,3 +366,23 @@ def test_swin_block_small(vtc, oracle, cfg):
     got_m, pm = _run(vtc, doc, x, vtc.MATERIALIZE)
     assert pm.info()["data_movement_launches"] > 10
     assert _relerr(oracle.bf16_to_f32(got_m["y"]), oracle.bf16_to_f32(want)) < 2e-2
+
+
+def test_gemm_tensor_core_gathers_a_through_a_roll_map(vtc, oracle):
+    """A = Roll(x) rows: ((i + s) mod n) is not TMA-expressible, so the GEMM's
+    loader warp gathers A rows (one map evaluation per row, 16-byte cp.async
+    into the 128-byte-swizzled tile) while B still arrives by TMA."""
+    from paper_2604_09558_b200.workloads import GraphBuilder
+    M, K, N = 300, 96, 288
+    g = GraphBuilder("bf16")
+    g.input("x", [M, K])
+    g.input("w", [K, N])
+    g.node("roll", "Roll", ["x"], "a", {"axes": [0], "shifts": [-37]})
+    g.node("mm", "MatMul", ["a", "w"], "y", out_kind="output")
+    doc = g.doc()
+    x = oracle.random_inputs(doc, seed=31, scales={"w": 1.0 / np.sqrt(K)})
+    got, p = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
+    assert [l["kernel"] for l in p.info()["launches"]] == ["gemm_tc_bf16_gather"]
+    a = np.roll(oracle.bf16_to_f32(x["x"]).astype(np.float64), -37, axis=0)
+    want = a @ oracle.bf16_to_f32(x["w"]).astype(np.float64)
+    assert _relerr(oracle.bf16_to_f32(got["y"]), want) < 1e-2

@@ -303,12 +303,17 @@ void Executor::prepare(bool dry) {
 
     // Configure the persistent TMA-streamed GEMV: balanced contiguous ranges of
     // (256-column strip, 64-row k-tile) units, one CTA per SM.
-    auto stream_gemv = [&](GemvParams& p, uint64_t b_ptr, const std::string& b_root) -> bool {
+    struct SecondMat {
+        uint64_t ptr = 0;
+        int64_t N = 0, ld = 0;
+        std::string root;
+    };
+    auto stream_gemv = [&](GemvParams& p, uint64_t b_ptr, const std::string& b_root, const SecondMat* m2) -> bool {
         const int64_t COLS = GEMV_STREAM_COLS, KT = GEMV_STREAM_KT;
         int sms = 148;
         if (!impl_->dry) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         int64_t strips0 = (p.N + COLS - 1) / COLS;
-        int64_t strips = strips0;  // (horizontal fusion adds the second matrix's strips)
+        int64_t strips = strips0 + (m2 ? (m2->N + COLS - 1) / COLS : 0);  // horizontal fusion: + the second matrix
         int64_t kts = (p.K + KT - 1) / KT, units = strips * kts;
         int grid = int(std::min<int64_t>(sms, units));
         std::vector<int32_t> first(size_t(strips), -1), count(size_t(strips), 0);
@@ -331,16 +336,19 @@ void Executor::prepare(bool dry) {
         if (!stages) return false;
         if (!impl_->dry && !encode_weight_tmap(p.tmap[0], reinterpret_cast<const void*>(b_ptr) , p.K, p.N, p.b_sk))
             return false;
+        if (m2 && !impl_->dry && !encode_weight_tmap(p.tmap[1], reinterpret_cast<const void*>(m2->ptr), p.K, m2->N, m2->ld))
+            return false;
         int maxc = *std::max_element(count.begin(), count.end());
         p.stream = 1;
-        p.nmat = 1;
+        p.nmat = m2 ? 2 : 1;
         p.n_mat[0] = p.N;
+        if (m2) p.n_mat[1] = m2->N;
         p.strips0 = int32_t(strips0);
         p.stages = stages;
         p.grid = grid;
         p.max_contrib = maxc;
         p.a_tiles = a_tiles;
-        p.b_static = written_roots.count(b_root) ? 0 : 1;
+        p.b_static = (written_roots.count(b_root) || (m2 && written_roots.count(m2->root))) ? 0 : 1;
         p.pre_stages = 1;
         if (const char* e = std::getenv("VTC_GEMV_PRE")) p.pre_stages = std::atoi(e);
         p.work = static_cast<float*>(impl_->alloc(size_t(strips * maxc * p.M * COLS) * sizeof(float), false));
@@ -530,6 +538,8 @@ void Executor::prepare(bool dry) {
         const OpNode* add = nullptr;
     };
     std::map<std::string, GemvFusion> fusion;
+    std::map<std::string, const OpNode*> hfuse;  // first MatMul -> its horizontally fused sibling
+    std::set<std::string> hpartner;
     std::set<std::string> absorbed;
     std::map<std::string, int> topo_pos;
     for (size_t i = 0; i < g_.topo_order().size(); ++i) topo_pos[g_.nodes()[size_t(g_.topo_order()[i])].id] = int(i);
@@ -622,6 +632,31 @@ void Executor::prepare(bool dry) {
                 if (!po || topo_pos[po->id] < topo_pos[n.id]) f.add = ad;
             }
             if (f.norm || f.silu || f.add) fusion[n.id] = f;
+        }
+        // horizontal fusion: two streamed GEMVs reading the same A with the same
+        // prologue (gate / up) run as one launch over both weight matrices
+        if (opt_.gemv_stream) {
+            std::vector<const OpNode*> cands;
+            for (const auto& n : g_.nodes())
+                if (gemv_eligible(n) && g_.tensor(n.inputs[0]).shape[0] <= 4) cands.push_back(&n);
+            for (size_t i = 0; i < cands.size(); ++i) {
+                const OpNode* a = cands[i];
+                if (hfuse.count(a->id) || hpartner.count(a->id)) continue;
+                for (size_t j = i + 1; j < cands.size(); ++j) {
+                    const OpNode* b = cands[j];
+                    if (hfuse.count(b->id) || hpartner.count(b->id) || b->inputs[0] != a->inputs[0]) continue;
+                    auto fa = fusion.find(a->id), fb = fusion.find(b->id);
+                    const OpNode* na = fa != fusion.end() ? fa->second.norm : nullptr;
+                    const OpNode* nb = fb != fusion.end() ? fb->second.norm : nullptr;
+                    bool other = (fa != fusion.end() && (fa->second.silu || fa->second.add)) ||
+                                 (fb != fusion.end() && (fb->second.silu || fb->second.add));
+                    if (other || na != nb) continue;
+                    hfuse[a->id] = b;
+                    hpartner.insert(b->id);
+                    break;
+                }
+            }
+            for (const auto& id : hpartner) absorbed.insert(id);
         }
         // a norm is absorbed only if every consumer MatMul fused it
         for (auto& [id, f] : fusion) {
@@ -838,11 +873,27 @@ void Executor::prepare(bool dry) {
                     p.b_base = reinterpret_cast<const char*>(bt.ptr) + bp.off.c0 * es;
                     p.b_sk = *VMap::tile_stride(bp, 0, K);
                     // persistent TMA-streamed variant: one CTA per SM, balanced (strip, k-tile) ranges
-                    if (M <= 4 && opt_.gemv_stream && stream_gemv(p, reinterpret_cast<uint64_t>(p.b_base), bp.target)) {
+                    SecondMat m2;
+                    const SecondMat* m2p = nullptr;
+                    auto hf = hfuse.find(n.id);
+                    if (hf != hfuse.end()) {
+                        const OpNode& n2 = *hf->second;
+                        const VPiece& bp2 = map_of(n2.inputs[1]).pieces()[0];
+                        TargetInfo bt2 = target(bp2.target);
+                        m2.ptr = reinterpret_cast<uint64_t>(reinterpret_cast<const char*>(bt2.ptr) + bp2.off.c0 * es);
+                        m2.N = g_.tensor(n2.inputs[1]).shape[1];
+                        m2.ld = *VMap::tile_stride(bp2, 0, K);
+                        m2.root = bp2.target;
+                        m2p = &m2;
+                        p.c2 = operand(map_of(n2.outputs[0]), 1, 256, es);
+                        L->node += "+" + n2.id;
+                    }
+                    if (M <= 4 && opt_.gemv_stream && stream_gemv(p, reinterpret_cast<uint64_t>(p.b_base), bp.target, m2p)) {
                         L->kernel = "gemv_stream_bf16";
                         push(std::move(L));
                         break;
                     }
+                    if (m2p) throw UnsupportedError("horizontally fused GEMV " + L->node + " needs the streaming kernel");
                     // grid: 256-column strips x K splits, ~3 CTAs per SM
                     int64_t ntiles = (N + 255) / 256;
                     int64_t want = (148 * 3 + ntiles - 1) / ntiles;

@@ -38,6 +38,7 @@ namespace {
 using dev::bf16;
 constexpr int CONSUMERS = 8, NT = (CONSUMERS + 1) * 32, COLS = GEMV_STREAM_COLS, KT = GEMV_STREAM_KT;
 constexpr uint32_t TILE_BYTES = KT * COLS * sizeof(bf16);
+static_assert(KT == 64, "a_col_to_k assumes 64-row k-tiles");
 
 struct Tmaps {
     CUtensorMap m[GEMV_MAX_MATS];
@@ -123,9 +124,13 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
         // activation loads: a full ring of weight requests queued ahead of
         // them would put every activation load behind ~MBs of HBM traffic.
         const int64_t u_pre = u_begin + (p.pre_stages < stages ? p.pre_stages : stages);
+        int64_t strip = u_begin / ktiles, kt = u_begin % ktiles;
         for (int64_t u = u_begin; u < u_end; ++u) {
             if (u == u_pre) mbar_wait(&go, 0);
-            const int64_t strip = u / ktiles, kt = u % ktiles;
+            if (u != u_begin && ++kt == ktiles) {
+                kt = 0;
+                ++strip;
+            }
             const int mat = strip < p.strips0 ? 0 : 1;
             const int64_t n0 = (strip - (mat ? p.strips0 : 0)) * COLS;
             mbar_wait(&empty[stage], phase ^ 1);
@@ -146,6 +151,15 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
     const int ctid = tid;  // 0..255
     const int64_t kt_first = u_begin % ktiles;
     const int64_t a_cols = int64_t(p.a_tiles) * KT;
+    // staged column e of A -> k: k-tile (kt_first + e / 64) mod ktiles, no 64-bit
+    // division in the prologue loops (a division call there serialises the loads)
+    const int kt_first32 = int(kt_first), ktiles32 = int(ktiles);
+    auto a_col_to_k = [&](int64_t e) -> int64_t {
+        const int ee = int(e);
+        int kt = kt_first32 + (ee >> 6);
+        if (kt >= ktiles32) kt -= ktiles32;
+        return int64_t(kt) * KT + (ee & (KT - 1));
+    };
     auto row_ptr = [&](const VOperand& op, int m, int64_t& stride) -> const bf16* {
         int32_t idx[VTC_MAX_RANK] = {};
         idx[0] = m;
@@ -182,6 +196,76 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
         const bool fast = pa && (p.prologue != GemvPrologue::SiLUMul || pa2) && (p.prologue != GemvPrologue::RMSNorm || pw);
         const bool regs = fast && (p.prologue != GemvPrologue::RMSNorm || p.K <= XR * 256) && a_cols <= EV * 256;
         float rs = 0.f;
+        // 16-byte path: unit-stride, 16-B aligned operands; 8 elements per load,
+        // every load of the row issued (as raw bits) before any is converted
+        const bool vec = fast && p.a.vec_ok && (p.prologue != GemvPrologue::SiLUMul || p.a2.vec_ok) &&
+                         (p.prologue != GemvPrologue::RMSNorm || (p.normw.vec_ok && p.K <= 4 * 2048)) &&
+                         a_cols <= 2 * 8 * 256 && p.K % 8 == 0;
+        if (vec) {
+            constexpr int XV = 4, AV = 2;
+            uint4 xq[XV], aq[AV], bq[AV];
+            const uint4 z4 = make_uint4(0, 0, 0, 0);
+            if (p.prologue == GemvPrologue::RMSNorm) {
+#pragma unroll
+                for (int j = 0; j < XV; ++j) {
+                    const int64_t k = (ctid + int64_t(j) * 256) * 8;
+                    xq[j] = k < p.K ? *reinterpret_cast<const uint4*>(pa + k) : z4;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < AV; ++i) {
+                const int64_t e = (ctid + int64_t(i) * 256) * 8;
+                const int64_t k = e < a_cols ? a_col_to_k(e) : p.K;
+                const bool ok = k < p.K;
+                aq[i] = ok ? *reinterpret_cast<const uint4*>(pa + k) : z4;
+                bq[i] = z4;
+                if (p.prologue == GemvPrologue::SiLUMul && ok) bq[i] = *reinterpret_cast<const uint4*>(pa2 + k);
+                if (p.prologue == GemvPrologue::RMSNorm && ok) bq[i] = *reinterpret_cast<const uint4*>(pw + k);
+            }
+            send_go();
+            auto unpack = [](const uint4& q, float (&f)[8]) {
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    float2 v2 = __bfloat1622float2(h[t]);
+                    f[2 * t] = v2.x;
+                    f[2 * t + 1] = v2.y;
+                }
+            };
+            if (p.prologue == GemvPrologue::RMSNorm) {
+                float s = 0.f;
+#pragma unroll
+                for (int j = 0; j < XV; ++j) {
+                    float f[8];
+                    unpack(xq[j], f);
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) s += f[t] * f[t];
+                }
+                rs = rsqrtf(block_sum_regs_bar1(s) / float(p.K) + p.eps);
+                if (ctid == 0) dev::trace_point(p.head, 6);  // norm reduction done
+            }
+#pragma unroll
+            for (int i = 0; i < AV; ++i) {
+                const int64_t e = (ctid + int64_t(i) * 256) * 8;
+                if (e >= a_cols) continue;
+                float v[8], u[8];
+                unpack(aq[i], v);
+                unpack(bq[i], u);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    if (p.prologue == GemvPrologue::SiLUMul) {
+                        const float sg = __bfloat162float(__float2bfloat16_rn(v[t] / (1.0f + expf(-v[t]))));
+                        v[t] = __bfloat162float(__float2bfloat16_rn(sg * u[t]));
+                    } else if (p.prologue == GemvPrologue::RMSNorm) {
+                        v[t] = __bfloat162float(__float2bfloat16_rn(v[t] * rs * u[t]));
+                    }
+                }
+                float4* dst = reinterpret_cast<float4*>(sA + size_t(m) * a_cols + e);
+                dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+                dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+            }
+            continue;
+        }
         if (regs) {
             // phase 1: issue every load of this row (registers), then let the producer go
             float xr[XR], av[EV], a2v[EV], wv[EV];
@@ -195,7 +279,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
 #pragma unroll
             for (int i = 0; i < EV; ++i) {
                 const int64_t e = ctid + int64_t(i) * 256;
-                const int64_t k = ((kt_first + e / KT) % ktiles) * KT + e % KT;
+                const int64_t k = a_col_to_k(e);
                 const bool ok = e < a_cols && k < p.K;
                 av[i] = ok ? __bfloat162float(pa[k * sa]) : 0.f;
                 if (p.prologue == GemvPrologue::SiLUMul) a2v[i] = ok ? __bfloat162float(pa2[k * sa2]) : 0.f;
@@ -228,6 +312,41 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
             continue;
         }
         send_go();
+        if (fast) {
+            // long k-ranges (e.g. gate+up: ~3K columns per CTA): batches of 8
+            // elements per thread with every load of a batch in flight together
+            if (p.prologue == GemvPrologue::RMSNorm) {
+                const float ss = block_sumsq_bf16_fast<true>(pa, sa, p.K);
+                rs = rsqrtf(ss / float(p.K) + p.eps);
+            }
+            for (int64_t e0 = ctid; e0 < a_cols; e0 += 8 * CONSUMERS * 32) {
+                float v[8], u[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int64_t e = e0 + int64_t(j) * CONSUMERS * 32;
+                    const int64_t k = a_col_to_k(e);
+                    const bool ok = e < a_cols && k < p.K;
+                    v[j] = ok ? __bfloat162float(pa[k * sa]) : 0.f;
+                    u[j] = 0.f;
+                    if (p.prologue == GemvPrologue::SiLUMul) u[j] = ok ? __bfloat162float(pa2[k * sa2]) : 0.f;
+                    if (p.prologue == GemvPrologue::RMSNorm) u[j] = ok ? __bfloat162float(pw[k * sw]) : 0.f;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int64_t e = e0 + int64_t(j) * CONSUMERS * 32;
+                    if (e >= a_cols) continue;
+                    float x = v[j];
+                    if (p.prologue == GemvPrologue::SiLUMul) {
+                        const float sg = __bfloat162float(__float2bfloat16_rn(x / (1.0f + expf(-x))));
+                        x = __bfloat162float(__float2bfloat16_rn(sg * u[j]));
+                    } else if (p.prologue == GemvPrologue::RMSNorm) {
+                        x = __bfloat162float(__float2bfloat16_rn(x * rs * u[j]));
+                    }
+                    sA[size_t(m) * a_cols + e] = x;
+                }
+            }
+            continue;
+        }
         if (p.prologue == GemvPrologue::RMSNorm) {
             // the same 256-thread reduction order as the standalone RMSNorm kernel
             float ss = pa ? block_sumsq_bf16_fast<true>(pa, sa, p.K)
@@ -242,8 +361,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
             rs = s_rs[m];
         }
         for (int64_t e = ctid; e < a_cols; e += CONSUMERS * 32) {
-            const int64_t kt = (kt_first + e / KT) % ktiles;
-            const int64_t k = kt * KT + e % KT;
+            const int64_t k = a_col_to_k(e);
             float v = 0.f;
             if (k < p.K) {
                 v = pa ? __bfloat162float(pa[k * sa]) : elem(p.a, m, k);
@@ -281,9 +399,13 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
     zero();
     int stage = 0;
     uint32_t phase = 0;
+    int64_t strip = u_begin / ktiles, kt = u_begin % ktiles, slot = -1;
     for (int64_t u = u_begin; u < u_end; ++u) {
-        const int64_t strip = u / ktiles, kt = u % ktiles;
-        const int64_t slot = (kt - kt_first + ktiles) % ktiles;
+        if (++slot == ktiles) slot = 0;  // slot = (kt - kt_first) mod ktiles
+        if (u != u_begin && ++kt == ktiles) {
+            kt = 0;
+            ++strip;
+        }
         const float* arow = sA + slot * KT;
         mbar_wait(&full[stage], phase);
         const bf16* tile = ring + size_t(stage) * KT * COLS;

@@ -43,6 +43,16 @@ struct Launch {
     virtual void set_trace(unsigned long long* t, int id) = 0;
 };
 
+template <class P>
+void set_head(P& p, unsigned long long* t, int id) {
+    p.head.trace = t;
+    p.head.id = id;
+}
+inline void set_head(EwPair& p, unsigned long long* t, int id) {
+    set_head(p.a, t, id);
+    set_head(p.b, t, id);
+}
+
 // Host copy of the parameter block (for dispatch decisions) + its device copy
 // (what the kernel reads).
 template <class P, void (*F)(const P&, const P*, cudaStream_t)>
@@ -53,10 +63,7 @@ struct LaunchT : Launch {
     size_t param_bytes() const override { return sizeof(P); }
     const void* host_params() const override { return &p; }
     void set_device_params(void* d) override { dp = static_cast<const P*>(d); }
-    void set_trace(unsigned long long* t, int id) override {
-        p.head.trace = t;
-        p.head.id = id;
-    }
+    void set_trace(unsigned long long* t, int id) override { set_head(p, t, id); }
 };
 
 // AllReduce(sum) of a contiguous buffer over the plan's communicator; with no
@@ -1106,6 +1113,48 @@ void Executor::prepare(bool dry) {
             default:
                 throw UnsupportedError(std::string("no kernel for operator ") + to_string(n.kind));
         }
+    }
+    // horizontal fusion of adjacent independent elementwise launches (e.g. the Q
+    // and K RoPE trees): one launch, CTAs split between the two programs
+    if (opt_.fuse) {
+        using EwL = LaunchT<EwParams, launch_eltwise>;
+        auto roots_of = [](const vtc_map& m, std::set<int>& out) {
+            for (int i = 0; i < m.npieces; ++i) out.insert(m.piece[i].target);
+        };
+        std::vector<std::unique_ptr<Launch>> merged;
+        std::vector<LaunchInfo> minfos;
+        for (size_t i = 0; i < impl_->launches.size(); ++i) {
+            auto* a = dynamic_cast<EwL*>(impl_->launches[i].get());
+            auto* b = i + 1 < impl_->launches.size() ? dynamic_cast<EwL*>(impl_->launches[i + 1].get()) : nullptr;
+            if (a && b && eltwise_pair_compatible(a->p, b->p)) {
+                std::set<int> wa, rb, wb, ra;
+                roots_of(a->p.out.m, wa);
+                roots_of(b->p.out.m, wb);
+                for (int k = 0; k < b->p.nin; ++k) roots_of(b->p.in[k].m, rb);
+                for (int k = 0; k < a->p.nin; ++k) roots_of(a->p.in[k].m, ra);
+                bool dep = false;
+                for (int t : wa) dep |= rb.count(t) > 0 || wb.count(t) > 0;
+                for (int t : wb) dep |= ra.count(t) > 0;
+                if (!dep) {
+                    auto P = std::make_unique<LaunchT<EwPair, launch_eltwise_pair>>();
+                    P->node = a->node + "|" + b->node;
+                    P->kernel = "eltwise";
+                    P->p.a = a->p;
+                    P->p.b = b->p;
+                    LaunchInfo li = infos_[i];
+                    li.node = P->node;
+                    li.bytes += infos_[i + 1].bytes;
+                    merged.push_back(std::move(P));
+                    minfos.push_back(li);
+                    ++i;
+                    continue;
+                }
+            }
+            merged.push_back(std::move(impl_->launches[i]));
+            minfos.push_back(infos_[i]);
+        }
+        impl_->launches = std::move(merged);
+        infos_ = std::move(minfos);
     }
     // optional device timeline (VTC_TRACE=1): [entry, exit] globaltimer per launch
     impl_->trace = nullptr;

@@ -406,7 +406,6 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
 // split partials of the row loaded at once (one memory round trip).
 __global__ void __launch_bounds__(NT) combine_fast_kernel(const AttnParams* __restrict__ pp) {
     VTC_STAGE_PARAMS(AttnParams, pp);
-    __shared__ float s_ml[2 * 256];
     __shared__ bf16* s_out;
     __shared__ int64_t s_ostride;
     const int64_t row = blockIdx.x;  // (lead, h, sq)
@@ -429,18 +428,34 @@ __global__ void __launch_bounds__(NT) combine_fast_kernel(const AttnParams* __re
     }
     dev::pdl_wait();
     dev::pdl_launch_dependents();
-    for (int e = threadIdx.x; e < 2 * S; e += NT) s_ml[e] = __ldcg(&p.part_ml[row * S * 2 + e]);
-    __syncthreads();
-    float M = -INFINITY;
-    for (int s2 = 0; s2 < S; ++s2) M = fmaxf(M, s_ml[2 * s2]);
+    __syncthreads();  // s_out / s_ostride
+    // every load of the row in flight at once: (m, l) pairs and this thread's
+    // column of the partial outputs (32 splits per batch)
     const int d = threadIdx.x;
-    float L = 0.f, acc = 0.f;
-#pragma unroll 8
-    for (int s2 = 0; s2 < S; ++s2) {
-        const float m = s_ml[2 * s2];
-        const float f = m == -INFINITY ? 0.f : exp2f(m - M);
-        L += f * s_ml[2 * s2 + 1];
-        acc += f * __ldcg(&p.part_o[(row * S + s2) * D + d]);
+    float L = 0.f, acc = 0.f, M = -INFINITY;
+    for (int s0 = 0; s0 < S; s0 += 32) {
+        float mv[32], lv[32], ov[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int s2 = s0 + j;
+            mv[j] = s2 < S ? __ldcg(&p.part_ml[(row * S + s2) * 2]) : -INFINITY;
+            lv[j] = s2 < S ? __ldcg(&p.part_ml[(row * S + s2) * 2 + 1]) : 0.f;
+            ov[j] = s2 < S ? __ldcg(&p.part_o[(row * S + s2) * D + d]) : 0.f;
+        }
+        float Mb = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) Mb = fmaxf(Mb, mv[j]);
+        const float Mn = fmaxf(M, Mb);
+        const float c = M == -INFINITY ? 0.f : exp2f(M - Mn);
+        L *= c;
+        acc *= c;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float f = mv[j] == -INFINITY ? 0.f : exp2f(mv[j] - Mn);
+            L += f * lv[j];
+            acc += f * ov[j];
+        }
+        M = Mn;
     }
     s_out[int64_t(d) * s_ostride] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
 }

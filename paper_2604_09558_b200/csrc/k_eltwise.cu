@@ -126,13 +126,19 @@ __device__ __forceinline__ T apply_op(EwOp op, T a, T b) {
     }
 }
 
+// pp1 != nullptr: CTAs [0, blocks0) run program pp0, the rest program pp1.
 template <typename T, int VEC>
-__global__ void __launch_bounds__(256) ew_kernel(const EwParams* __restrict__ pp) {
+__global__ void __launch_bounds__(256) ew_kernel(const EwParams* __restrict__ pp0, const EwParams* __restrict__ pp1,
+                                                 int blocks0) {
+    const bool second = pp1 != nullptr && int(blockIdx.x) >= blocks0;
+    const EwParams* __restrict__ pp = second ? pp1 : pp0;
+    const int64_t bid = second ? int64_t(blockIdx.x) - blocks0 : int64_t(blockIdx.x);
+    const int64_t nblk = pp1 == nullptr ? int64_t(gridDim.x) : (second ? int64_t(gridDim.x) - blocks0 : int64_t(blocks0));
     VTC_STAGE_PARAMS(EwParams, pp);
     dev::pdl_wait(); dev::pdl_launch_dependents();
     const int last = p.rank - 1;
     const int nin = p.nin, nprog = p.nprog;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < p.nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t v = bid * (int64_t)blockDim.x + threadIdx.x; v < p.nvec; v += nblk * blockDim.x) {
         int32_t idx[VTC_MAX_RANK];
         dev::unflatten(v * VEC, p.shape, p.rank, idx);
 #pragma unroll 1
@@ -159,19 +165,47 @@ __global__ void __launch_bounds__(256) ew_kernel(const EwParams* __restrict__ pp
     }
 }
 
+int ew_grid(const EwParams& p) {
+    int64_t blocks = (p.nvec + 255) / 256;
+    int grid = int(blocks < 148 * 16 ? blocks : 148 * 16);
+    return grid < 1 ? 1 : grid;
+}
+
 template <typename T>
 void launch_t(const EwParams& p, const EwParams* dp, cudaStream_t s) {
     constexpr int V = 16 / sizeof(T);
-    int64_t blocks = (p.nvec + 255) / 256;
-    int grid = int(blocks < 148 * 16 ? blocks : 148 * 16);
-    if (grid < 1) grid = 1;
+    const int grid = ew_grid(p);
+    const EwParams* none = nullptr;
     if (p.vec == V)
-        launch_k(ew_kernel<T, V>, dim3(grid), dim3(256), 0, s, dp);
+        launch_k(ew_kernel<T, V>, dim3(grid), dim3(256), 0, s, dp, none, grid);
     else
-        launch_k(ew_kernel<T, 1>, dim3(grid), dim3(256), 0, s, dp);
+        launch_k(ew_kernel<T, 1>, dim3(grid), dim3(256), 0, s, dp, none, grid);
+}
+
+template <typename T>
+void launch_pair_t(const EwPair& p, const EwPair* dp, cudaStream_t s) {
+    constexpr int V = 16 / sizeof(T);
+    const int g0 = ew_grid(p.a), g1 = ew_grid(p.b);
+    if (p.a.vec == V)
+        launch_k(ew_kernel<T, V>, dim3(g0 + g1), dim3(256), 0, s, &dp->a, &dp->b, g0);
+    else
+        launch_k(ew_kernel<T, 1>, dim3(g0 + g1), dim3(256), 0, s, &dp->a, &dp->b, g0);
 }
 
 }  // namespace
+
+bool eltwise_pair_compatible(const EwParams& a, const EwParams& b) {
+    return a.nvec > 0 && b.nvec > 0 && !a.copy_only && !b.copy_only && a.dt == b.dt && a.vec == b.vec;
+}
+
+void launch_eltwise_pair(const EwPair& p, const EwPair* dp, cudaStream_t s) {
+    switch (p.a.dt) {
+        case KDType::F64: launch_pair_t<double>(p, dp, s); break;
+        case KDType::F32: launch_pair_t<float>(p, dp, s); break;
+        case KDType::I64: launch_pair_t<int64_t>(p, dp, s); break;
+        case KDType::BF16: launch_pair_t<bf16>(p, dp, s); break;
+    }
+}
 
 void launch_eltwise(const EwParams& p, const EwParams* dp, cudaStream_t s) {
     if (p.nvec == 0) return;

@@ -70,6 +70,14 @@ struct EwParams {
     int32_t pad;
 };
 void launch_eltwise(const EwParams& p, const EwParams* dp, cudaStream_t s);
+// Two independent elementwise programs of the same element type in one launch
+// (horizontal fusion of small launches, e.g. the Q and K RoPE trees).
+struct EwPair {
+    alignas(16) EwParams a;  // kernels stage parameter blocks with 16-byte loads
+    alignas(16) EwParams b;
+};
+bool eltwise_pair_compatible(const EwParams& a, const EwParams& b);
+void launch_eltwise_pair(const EwPair& p, const EwPair* dp, cudaStream_t s);
 
 // ---- generic batched matmul (any dtype, any maps) -----------------------
 struct MatmulParams {

@@ -1091,6 +1091,7 @@ void Executor::prepare(bool dry) {
                 if (splits <= 0) {
                     // fast path: one wave (2 CTAs per SM) when the KV is short, ~4 waves when long
                     int64_t target = p.fast ? (int64_t(p.Sk) * qblocks >= 148 * 2 * 512 ? 148 * 2 * 4 : 148 * 2) : 148 * 2;
+                    if (const char* ev = std::getenv("VTC_ATTN_CTAS")) target = std::atoll(ev);
                     splits = int((target + qblocks - 1) / qblocks);
                     splits = std::max(1, std::min(splits, (p.Sk + kgran - 1) / kgran));
                 }
@@ -1100,7 +1101,9 @@ void Executor::prepare(bool dry) {
                 p.splits = splits;
                 p.chunk = chunk;
                 L->kernel = p.fast ? (splits > 1 ? "attn_decode_tc_splitkv" : "attn_decode_tc") : (splits > 1 ? "attention_splitkv" : "attention");
-                if (splits > 1 && p.fast && std::getenv("VTC_ATTN_FUSED_COMBINE"))
+                // cooperative in-kernel split combine when every CTA fits on the GPU at once
+                if (splits > 1 && p.fast == 1 && !impl_->dry && !std::getenv("VTC_ATTN_SEPARATE_COMBINE") &&
+                    qblocks * splits <= attn_decode_capacity())
                     p.counters = static_cast<unsigned*>(impl_->alloc(size_t(qblocks) * sizeof(unsigned), true));
                 if (splits > 1) {
                     int64_t rows = int64_t(p.Bt) * p.H * p.Sq;

@@ -191,18 +191,33 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
             s_ostr[tid] = p.o.fast_stride[lo.piece];
         }
         __syncthreads();
+        // stage the R query rows in shared memory with 16-byte loads (zero rows >= R)
+        __shared__ __align__(16) bf16 s_q[16][D];
+        for (int c = tid; c < 16 * (D / 8); c += NT) {
+            const int row = c / (D / 8), ch = c % (D / 8);
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (row < R) {
+                if (s_qstr[row] == 1 && (reinterpret_cast<uintptr_t>(s_qrow[row]) & 15) == 0) {
+                    v = *reinterpret_cast<const uint4*>(s_qrow[row] + ch * 8);
+                } else {
+                    bf16 t[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) t[j] = s_qrow[row][int64_t(ch * 8 + j) * s_qstr[row]];
+                    v = *reinterpret_cast<const uint4*>(t);
+                }
+            }
+            *reinterpret_cast<uint4*>(&s_q[row][ch * 8]) = v;
+        }
+        __syncthreads();
         const int rA = lane / 4, rB = lane / 4 + 8, kc = (lane % 4) * 2;
-        auto qv = [&](int row, int d) -> float {
-            if (row >= R) return 0.f;
-            return __bfloat162float(s_qrow[row][int64_t(d) * s_qstr[row]]);
-        };
+        auto qp = [&](int row, int d) -> uint32_t { return *reinterpret_cast<const uint32_t*>(&s_q[row][d]); };
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
             const int d0 = ks * 16 + kc;
-            qa[ks][0] = pack_bf16(qv(rA, d0), qv(rA, d0 + 1));
-            qa[ks][1] = pack_bf16(qv(rB, d0), qv(rB, d0 + 1));
-            qa[ks][2] = pack_bf16(qv(rA, d0 + 8), qv(rA, d0 + 9));
-            qa[ks][3] = pack_bf16(qv(rB, d0 + 8), qv(rB, d0 + 9));
+            qa[ks][0] = qp(rA, d0);
+            qa[ks][1] = qp(rB, d0);
+            qa[ks][2] = qp(rA, d0 + 8);
+            qa[ks][3] = qp(rB, d0 + 8);
         }
     }
     if (tid == 0) dev::trace_point(p.head, 4);
@@ -355,48 +370,56 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
     if (p.splits == 1 || p.counters == nullptr) return;  // no counters: combine_fast_kernel merges
     if (tid == 0) dev::trace_point(p.head, 6);
 
-    // ---- split-KV combine, fused: the last CTA of this query group to finish
-    //      merges every split in split order (deterministic) ----
-    __shared__ unsigned s_last;
+    // ---- split-KV combine, cooperative: every split CTA of the group waits
+    //      until all S partials are written (all CTAs are co-resident -- the
+    //      host enables this only when the grid fits the GPU at once), then
+    //      merges a 1/S slice of the group's R x D outputs in split order ----
+    __shared__ unsigned s_target;
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&p.counters[blockIdx.x], 1u) == unsigned(p.splits - 1) ? 1u : 0u;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (tid == 0) p.counters[blockIdx.x] = 0u;  // self-resetting for the next execution
     const int S = p.splits;
-    const int64_t orow0 = (int64_t(blockIdx.x) / HG) * p.H + h0;  // (lead, h0) row; rows (g, sq) follow
-    // stage every split's (m, l) and O rows of the group in shared memory (one round trip)
-    float* sml = reinterpret_cast<float*>(smem);          // [R][S][2]
-    float* spo = sml + ((R * S * 2 + 3) / 4) * 4;         // [R][S][D]
-    const bool staged = size_t(R) * S * (D + 2) * 4 + 16 <= size_t(WARPS) * WARPB;
-#pragma unroll 4
-    for (int e = tid; e < R * S * 2; e += NT) {
-        const int row = e / (S * 2), rest = e % (S * 2);
-        sml[e] = __ldcg(&p.part_ml[((orow0 * Sq + row) * S) * 2 + rest]);
-    }
-    if (staged) {
-        const int n4 = R * S * D / 4;
-#pragma unroll 8
-        for (int e = tid; e < n4; e += NT) {
-            const int row = (e * 4) / (S * D), rest = (e * 4) % (S * D);
-            reinterpret_cast<float4*>(spo)[e] =
-                __ldcg(reinterpret_cast<const float4*>(&p.part_o[(orow0 * Sq + row) * S * D + rest]));
-        }
+    if (tid == 0) {
+        // tickets grow monotonically across executions: no reset needed
+        const unsigned ticket = atomicAdd(&p.counters[blockIdx.x], 1u);
+        const unsigned target = (ticket / unsigned(S) + 1u) * unsigned(S);
+        unsigned seen;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(&p.counters[blockIdx.x]) : "memory");
+            if (int(seen - target) < 0) __nanosleep(64);
+        } while (int(seen - target) < 0);
+        s_target = target;
     }
     __syncthreads();
-    for (int e = tid; e < R * D; e += NT) {
+    const int64_t orow0 = (int64_t(blockIdx.x) / HG) * p.H + h0;  // (lead, h0): rows (g, sq) follow
+    const int per = (R * D + S - 1) / S;
+    const int e = split * per + tid;
+    if (tid < per && e < R * D) {
         const int row = e / D, d = e % D;
-        const float* ml = sml + row * S * 2;
-        float M = -INFINITY;
-        for (int s2 = 0; s2 < S; ++s2) M = fmaxf(M, ml[2 * s2]);
-        float L = 0.f, acc = 0.f;
-        for (int s2 = 0; s2 < S; ++s2) {
-            if (ml[2 * s2] == -INFINITY) continue;
-            const float f = exp2f(ml[2 * s2] - M);
-            L += f * ml[2 * s2 + 1];
-            acc += f * (staged ? spo[(row * S + s2) * D + d] : __ldcg(&p.part_o[((orow0 * Sq + row) * S + s2) * D + d]));
+        const int64_t base = (orow0 * Sq + row) * S;
+        float L = 0.f, acc = 0.f, M = -INFINITY;
+        for (int s0 = 0; s0 < S; s0 += 32) {
+            float mv[32], lv[32], ov[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int s2 = s0 + j;
+                mv[j] = s2 < S ? __ldcg(&p.part_ml[(base + s2) * 2]) : -INFINITY;
+                lv[j] = s2 < S ? __ldcg(&p.part_ml[(base + s2) * 2 + 1]) : 0.f;
+                ov[j] = s2 < S ? __ldcg(&p.part_o[(base + s2) * D + d]) : 0.f;
+            }
+            float Mb = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) Mb = fmaxf(Mb, mv[j]);
+            const float Mn = fmaxf(M, Mb);
+            const float c = M == -INFINITY ? 0.f : exp2f(M - Mn);
+            L *= c;
+            acc *= c;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float f = mv[j] == -INFINITY ? 0.f : exp2f(mv[j] - Mn);
+                L += f * lv[j];
+                acc += f * ov[j];
+            }
+            M = Mn;
         }
         s_orow[row][int64_t(d) * s_ostr[row]] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
     }
@@ -468,6 +491,17 @@ bool attn_decode_supported(const AttnParams& p) {
 }
 
 size_t attn_decode_smem() { return size_t(WARPS) * WARPB; }
+
+// CTAs of attn_decode_kernel resident at once on the whole GPU (the cooperative
+// split combine spins on its group's arrivals, so every CTA must be resident).
+int64_t attn_decode_capacity() {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_decode_smem()));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attn_decode_kernel, NT, attn_decode_smem());
+    return int64_t(sms) * per;
+}
 
 void launch_attn_decode(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
     int64_t qblocks = int64_t(p.Bt) * (p.H / p.group);

@@ -210,6 +210,7 @@ struct AttnParams {
 };
 void launch_attention(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 bool attn_decode_supported(const AttnParams& p);
+int64_t attn_decode_capacity();
 bool attn_prefill_supported(const AttnParams& p);
 void launch_attn_prefill(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 void launch_attn_decode(const AttnParams& p, const AttnParams* dp, cudaStream_t s);

@@ -973,10 +973,16 @@ void Executor::prepare(bool dry) {
                     }
                     if (ok && !impl_->dry) ok = gemm_tc_encode(p, abase, adims, astr, bbase, ldb);
                     if (ok) {
-                        int64_t tiles = (M + 127) / 128 * ((N + p.bn - 1) / p.bn);
+                        // prefill-sized M: 256-row tiles (two M=128 MMAs per B stage)
+                        p.mt = (!p.a_gather && p.bn == 256 && M >= 4096) ? 2 : 1;
+                        int64_t tiles = (M + 128 * p.mt - 1) / (128 * p.mt) * ((N + p.bn - 1) / p.bn);
                         int64_t ktiles = (K + 63) / 64;
                         int sms = 148;
                         if (!impl_->dry) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+                        if (p.mt == 2 && tiles < sms) {  // not enough 256-row tiles: back to 128 rows
+                            p.mt = 1;
+                            tiles = (M + 127) / 128 * ((N + p.bn - 1) / p.bn);
+                        }
                         int64_t splits = tiles >= sms ? 1 : std::min<int64_t>(ktiles, std::max<int64_t>(1, sms / tiles));
                         p.splits = int32_t(splits);
                         if (splits > 1) {

@@ -119,11 +119,14 @@ struct Tmaps {
     CUtensorMap a, b;
 };
 
-template <int BN, int STAGES>
+// MT = 128-row sub-tiles per CTA (2: a 256 x BN tile whose two M=128 MMAs
+// share each B stage -- half the B traffic per FLOP for prefill-sized M)
+template <int BN, int STAGES, int MT>
 __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams* __restrict__ pp,
                                                                const __grid_constant__ Tmaps tm) {
     VTC_STAGE_PARAMS(GemmTcParams, pp);
-    constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+    constexpr int TM = BM * MT;
+    constexpr uint32_t A_SUB = BM * BK * 2, A_BYTES = A_SUB * MT, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t full[STAGES], empty[STAGES], done;
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int tiles_n = int((p.N + BN - 1) / BN);
-    const int tiles_m = int((p.M + BM - 1) / BM);
+    const int tiles_m = int((p.M + TM - 1) / TM);
     const int tile = blockIdx.x;
     // grouped rasterisation: consecutive CTAs walk GROUP_M row tiles of one
     // column tile, so the CTAs in flight share a few A row blocks and B column
@@ -142,11 +145,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     const int first_m = (tile / in_group) * GROUP_M;
     const int gm = min(tiles_m - first_m, GROUP_M);
     const int tm_ = first_m + (tile % in_group) % gm, tn = (tile % in_group) / gm;
-    const int64_t m0 = int64_t(tm_) * BM, n0 = int64_t(tn) * BN;
+    const int64_t m0 = int64_t(tm_) * TM, n0 = int64_t(tn) * BN;
     const int split = blockIdx.y;
     const int ktiles = int((p.K + BK - 1) / BK);
     const int kt0 = int(int64_t(ktiles) * split / p.splits), kt1 = int(int64_t(ktiles) * (split + 1) / p.splits);
     const int nk = kt1 - kt0;
+    // stagger the k order across tiles: CTAs in flight that share an A row
+    // block or a B column block then request different lines of it at a time
+    const int krot = (p.splits == 1 && nk > 0) ? int((tm_ * 7 + tn * 3) % nk) : 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -158,7 +164,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     }
     if (warp == 0) {  // TMEM accumulator: 128 lanes x BN fp32 columns
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                     "r"(BN));
+                     "r"(BN * MT));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             mbar_wait(&empty[s], ph ^ 1u);
             unsigned char* sa = smem + size_t(s) * STAGE_BYTES;
             unsigned char* sb = sa + A_BYTES;
-            const int32_t k0 = int32_t(kt0 + i) * BK;
+            const int32_t k0 = int32_t(kt0 + (i + krot) % nk) * BK;
             if (lane == 0) {
                 mbar_expect_tx(&full[s], B_BYTES);
 #pragma unroll
@@ -234,14 +240,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             mbar_expect_tx(&full[s], STAGE_BYTES);
             unsigned char* sa = smem + size_t(s) * STAGE_BYTES;
             unsigned char* sb = sa + A_BYTES;
-            const int32_t k0 = int32_t(kt0 + i) * BK;
-            int32_t ca[5];
+            const int32_t k0 = int32_t(kt0 + (i + krot) % nk) * BK;
 #pragma unroll
-            for (int j = 0; j < 5; ++j) {
-                int64_t v = (p.a_axis[j] ? int64_t(k0) : m0) / p.a_div[j];
-                ca[j] = int32_t(p.a_mod[j] ? v % p.a_mod[j] : v);
+            for (int t = 0; t < MT; ++t) {
+                int32_t ca[5];
+#pragma unroll
+                for (int j = 0; j < 5; ++j) {
+                    int64_t v = (p.a_axis[j] ? int64_t(k0) : m0 + t * BM) / p.a_div[j];
+                    ca[j] = int32_t(p.a_mod[j] ? v % p.a_mod[j] : v);
+                }
+                tma_nd(sa + t * A_SUB, &tm.a, ca, p.a_ndims, &full[s], pol_a);
             }
-            tma_nd(sa, &tm.a, ca, p.a_ndims, &full[s], pol_a);
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
                 tma_2d(sb + j * (BK * 128), &tm.b, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
@@ -261,14 +270,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             for (int k = 0; k < BK / UK; ++k) {
                 // A: K-major SW128, +32 B per K16 step; B: MN-major SW128, +2 KB (16 rows) per step,
                 // 64-column chunks BK*128 B apart (LBO), 8-row groups 1 KB apart (SBO)
-                const uint64_t da = smem_desc(sa + k * 32, 16, 1024);
                 const uint64_t db = smem_desc(sb + k * 2048, BK * 128, 1024);
                 const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-                asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                    "l"(da), "l"(db), "r"(idesc), "r"(acc)
-                    : "memory");
+#pragma unroll
+                for (int t = 0; t < MT; ++t) {  // sub-tile t -> TMEM columns [t*BN, (t+1)*BN)
+                    const uint64_t da = smem_desc(sa + t * A_SUB + k * 32, 16, 1024);
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + uint32_t(t * BN)),
+                        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                        : "memory");
+                }
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                              smem_u32(&empty[s]))
@@ -290,9 +302,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
         dev::trace_add(p.head, 2, t_main - t_start);  // sum over CTAs: mainloop
         dev::trace_add(p.head, 4, 1);                 // CTA count
     }
-    const int row = warp * 32 + lane;  // TMEM lane == tile row
-    const int64_t m = m0 + row;
-    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+    for (int t = 0; t < MT; ++t) {
+    const int row = warp * 32 + lane;  // TMEM lane == tile row (of sub-tile t)
+    const int64_t m = m0 + t * BM + row;
+    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16) + uint32_t(t * BN);
 
     auto tmem_ld16 = [&](int c, float (&v)[16]) {
         uint32_t r[16];
@@ -402,12 +415,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             }
         }
     }
+    }  // sub-tiles
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) dev::trace_add(p.head, 3, dev::gtime() - t_main);  // sum over CTAs: epilogue
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN * MT));
     }
 }
 
@@ -426,9 +440,9 @@ EncodeFn encoder() {
     return fn;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int MT>
 constexpr size_t smem_bytes() {
-    return size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024;
+    return size_t(STAGES) * (MT * BM * BK * 2 + BN * BK * 2) + 1024;
 }
 
 }  // namespace
@@ -531,16 +545,21 @@ void launch_gemm_tc(const GemmTcParams& p, const GemmTcParams* dp, cudaStream_t 
     Tmaps tmaps;
     std::memcpy(&tmaps.a, p.tmap_a, sizeof(CUtensorMap));
     std::memcpy(&tmaps.b, p.tmap_b, sizeof(CUtensorMap));
-    const int tiles = int((p.M + BM - 1) / BM) * int((p.N + p.bn - 1) / p.bn);
+    const int tm = p.mt == 2 ? 2 * BM : BM;
+    const int tiles = int((p.M + tm - 1) / tm) * int((p.N + p.bn - 1) / p.bn);
     dim3 grid(unsigned(tiles), unsigned(p.splits));
-    if (p.bn == 256) {
-        constexpr size_t sm = smem_bytes<256, 4>();
-        cudaFuncSetAttribute(gemm_tc_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        launch_k(gemm_tc_kernel<256, 4>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+    if (p.mt == 2) {
+        constexpr size_t sm = smem_bytes<256, 3, 2>();
+        cudaFuncSetAttribute(gemm_tc_kernel<256, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        launch_k(gemm_tc_kernel<256, 3, 2>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+    } else if (p.bn == 256) {
+        constexpr size_t sm = smem_bytes<256, 4, 1>();
+        cudaFuncSetAttribute(gemm_tc_kernel<256, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        launch_k(gemm_tc_kernel<256, 4, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
     } else {
-        constexpr size_t sm = smem_bytes<128, 6>();
-        cudaFuncSetAttribute(gemm_tc_kernel<128, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        launch_k(gemm_tc_kernel<128, 6>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+        constexpr size_t sm = smem_bytes<128, 6, 1>();
+        cudaFuncSetAttribute(gemm_tc_kernel<128, 6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        launch_k(gemm_tc_kernel<128, 6, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
     }
 }
 

@@ -204,7 +204,8 @@ def test_attention_tensor_core_path_matches_oracle(vtc, oracle, cfg):
     assert _relerr(oracle.bf16_to_f32(got_m["o"]), want) < 2e-2
 
 
-@pytest.mark.parametrize("M,K,N", [(64, 4096, 6144), (200, 256, 384), (1000, 512, 256), (17, 64, 128), (130, 4096, 4096)])
+@pytest.mark.parametrize("M,K,N", [(64, 4096, 6144), (200, 256, 384), (1000, 512, 256), (17, 64, 128), (130, 4096, 4096),
+                                   (8192, 512, 2560), (4200, 256, 4096)])
 def test_gemm_tensor_core_matches_fp32_reference(vtc, oracle, M, K, N):
     """tcgen05 GEMM (bf16 in, fp32 accumulate) against a float64 reference of
     the same bf16 inputs; the only error is the final bf16 rounding plus

@@ -392,8 +392,9 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
     __syncthreads();
     const int64_t orow0 = (int64_t(blockIdx.x) / HG) * p.H + h0;  // (lead, h0): rows (g, sq) follow
     const int per = (R * D + S - 1) / S;
-    const int e = split * per + tid;
-    if (tid < per && e < R * D) {
+    for (int i = tid; i < per; i += NT) {
+        const int e = split * per + i;
+        if (e >= R * D) break;
         const int row = e / D, d = e % D;
         const int64_t base = (orow0 * Sq + row) * S;
         float L = 0.f, acc = 0.f, M = -INFINITY;

@@ -387,3 +387,30 @@ def test_gemm_tensor_core_gathers_a_through_a_roll_map(vtc, oracle):
     a = np.roll(oracle.bf16_to_f32(x["x"]).astype(np.float64), -37, axis=0)
     want = a @ oracle.bf16_to_f32(x["w"]).astype(np.float64)
     assert _relerr(oracle.bf16_to_f32(got["y"]), want) < 1e-2
+
+
+def test_cuda_path_matches_reference_golden_vectors(vtc):
+    """The CUDA path (VTC plan and materialising plan) against outputs of the
+    reference itself (tests/golden/, generated from oracle/_ref): bit-exact."""
+    import test_golden as G
+    for name, doc, ins, outs in G.CASES:
+        for mode in (vtc.MAX_ELIMINATION, vtc.MATERIALIZE):
+            got, _ = _run(vtc, doc, ins, mode)
+            for k, want in outs.items():
+                assert np.array_equal(_bits(got[k]), _bits(want)), (name, mode, k)
+
+
+def test_c1_full_size_digest_matches_reference(vtc, ref):
+    """BASELINE configs[0] at full size with the reference's own seeded inputs
+    (make_random_inputs, seed 1): the GPU output's FNV-1a digest equals the
+    reference executor's (tests/golden/ref_digests.json, = SURVEY.md §8 c)."""
+    import json
+    from pathlib import Path
+    import test_golden as G
+    from paper_2604_09558_b200 import workloads as W
+    doc = W.c1_chain(1024)
+    x = ref.RefGraph(doc).inputs_random(1)
+    got, p = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
+    assert p.info()["data_movement_launches"] == 0
+    dig = json.loads((Path(G.GOLD) / "ref_digests.json").read_text())["c1_chain_1024_f32_seed1"]["y"]
+    assert format(G.fnv1a64(got["y"]), "016x") == dig

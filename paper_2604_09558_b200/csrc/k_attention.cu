@@ -283,7 +283,7 @@ void launch_t(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
         int64_t qblocks = int64_t(p.Bt) * (p.H / p.group) * p.Sq;
         dim3 grid(unsigned(qblocks), unsigned(p.splits));
         size_t smem = size_t(TK) * size_t(p.D + 8 + p.Dv + 8) * sizeof(T);
-        if (smem > 48 * 1024) cudaFuncSetAttribute(attn_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (smem > 48 * 1024) allow_max_smem(attn_kernel<T>);
         launch_k(attn_kernel<T>, dim3(grid), dim3(NT), smem, s, dp);
     }
     if (p.splits > 1 && !p.fast) launch_k(combine_kernel<T>, dim3(unsigned(int64_t(p.Bt) * p.H * p.Sq)), dim3(NT), 0, s, dp);

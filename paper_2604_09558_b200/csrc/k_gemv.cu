@@ -231,7 +231,7 @@ template <int MT, int U>
 void launch_mt(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
     dim3 grid(unsigned((p.N + COLS - 1) / COLS), unsigned(p.ksplit));
     size_t smem = size_t(p.M) * size_t(p.kchunk) * sizeof(float);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(gemv_kernel<MT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (smem > 48 * 1024) allow_max_smem(gemv_kernel<MT, U>);
     launch_k(gemv_kernel<MT, U>, dim3(grid), dim3(NT), smem, s, dp);
 }
 

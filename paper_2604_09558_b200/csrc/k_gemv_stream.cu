@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
 template <int MT>
 void launch_mt(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
     size_t smem = gemv_stream_smem(p.M, p.a_tiles, p.stages);
-    cudaFuncSetAttribute(gemv_stream_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    allow_max_smem(gemv_stream_kernel<MT>);
     Tmaps tm;
     std::memcpy(&tm, p.tmap, sizeof(tm));
     launch_k(gemv_stream_kernel<MT>, dim3(p.grid), dim3(NT), smem, s, dp, tm);
@@ -537,7 +537,7 @@ size_t gemv_stream_smem(int64_t M, int a_tiles, int stages) {
     size_t bytes = size_t(stages) * TILE_BYTES + size_t(M) * size_t(a_tiles) * KT * sizeof(float) +
                    size_t(CONSUMERS) * COLS * sizeof(float) + 2 * size_t(stages) * sizeof(uint64_t);
     // + the statically allocated parameter copy; 227 KB per CTA in total
-    return bytes + sizeof(GemvParams) + 4096 <= 227 * 1024 ? bytes : 0;
+    return bytes + sizeof(GemvParams) + 12 * 1024 <= 227 * 1024 ? bytes : 0;
 }
 
 bool encode_weight_tmap(void* out128, const void* base, int64_t rows, int64_t cols, int64_t ld) {

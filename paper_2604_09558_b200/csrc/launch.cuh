@@ -23,6 +23,24 @@ inline bool pdl_enabled() {
     return on;
 }
 
+// Opt a kernel into the largest dynamic shared memory it can use, once.
+// (Setting the attribute per launch to that launch's size is wrong under CUDA
+// graphs: the attribute is read at replay, after a later capture may have
+// lowered it for a launch with a smaller footprint.)
+template <typename... KArgs>
+inline void allow_max_smem(void (*kern)(KArgs...)) {
+    static const bool done = [kern] {
+        cudaFuncAttributes a{};
+        cudaFuncGetAttributes(&a, kern);
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - int(a.sharedSizeBytes));
+        return true;
+    }();
+    (void)done;
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg = {};

@@ -1,12 +1,16 @@
 #!/bin/bash
-# Round profile pass (one GPU): ncu launch lists (per-launch device time + DRAM bytes)
-# of the C2 / C3 decode steps and one --set full capture of the dominant kernel.
+# Round profile pass (one GPU): ncu launch lists (per-launch device time; DRAM
+# bytes in a second pass) of the C2 / C3 decode steps and --set full captures.
 # Outputs under gpurun_out/; scripts/summarize_profiles.py turns them into profiles/.
 export BENCH_NO_CPU=1
-M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+# ncu serialises kernels anyway; plain stream order avoids a replay failure of a
+# programmatic-dependent graph node under the profiler
+export VTC_NO_PDL=1
 for cfg in c2 c3; do
-  timeout 600 ncu --metrics $M --clock-control none -c 400 --csv --log-file gpurun_out/launches_$cfg.csv \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$cfg.csv \
      python bench.py --config $cfg --steps 2 --warmup 1 > gpurun_out/ncu_launch_$cfg.log 2>&1; echo launch_$cfg=$?
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
+     --log-file gpurun_out/dram_$cfg.csv python bench.py --config $cfg --steps 2 --warmup 1 > gpurun_out/ncu_dram_$cfg.log 2>&1; echo dram_$cfg=$?
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_stream -s 4 -c 4 \
    -o gpurun_out/full_gemv_stream python bench.py --steps 2 --warmup 1 > gpurun_out/ncu_full.log 2>&1; echo full=$?

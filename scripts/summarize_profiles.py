@@ -26,15 +26,25 @@ def family(name):
 
 
 def launches(cfg):
-    rows = list(csv.reader(open(OUT / f"launches_{cfg}.csv")))
-    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
-    h = rows[hi]
-    ii, ki, mi, vi = h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
     d = defaultdict(dict)
     names = {}
-    for r in rows[hi + 1:]:
-        d[int(r[ii])][r[mi]] = float(r[vi].replace(",", ""))
-        names[int(r[ii])] = r[ki]
+    for fn in (f"launches_{cfg}.csv", f"dram_{cfg}.csv"):  # time pass, DRAM-bytes pass (same launch ids)
+        if not (OUT / fn).exists():
+            continue
+        rows = list(csv.reader(open(OUT / fn)))
+        hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+        h = rows[hi]
+        ii, ki, mi, vi = h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+        ui = h.index("Metric Unit") if "Metric Unit" in h else None
+        for r in rows[hi + 1:]:
+            v = float(r[vi].replace(",", ""))
+            unit = r[ui] if ui is not None else ""
+            v *= {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e3, "msecond": 1e6}.get(unit, 1.0)
+            d[int(r[ii])][r[mi]] = v
+            names[int(r[ii])] = r[ki]
+    for i in d:
+        d[i].setdefault("dram__bytes_read.sum", 0.0)
+        d[i].setdefault("dram__bytes_write.sum", 0.0)
     out = []
     for i in sorted(d):
         fam = family(names[i])

@@ -150,9 +150,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     const int ktiles = int((p.K + BK - 1) / BK);
     const int kt0 = int(int64_t(ktiles) * split / p.splits), kt1 = int(int64_t(ktiles) * (split + 1) / p.splits);
     const int nk = kt1 - kt0;
-    // stagger the k order across tiles: CTAs in flight that share an A row
-    // block or a B column block then request different lines of it at a time
-    const int krot = (p.splits == 1 && nk > 0) ? int((tm_ * 7 + tn * 3) % nk) : 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -199,7 +196,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             mbar_wait(&empty[s], ph ^ 1u);
             unsigned char* sa = smem + size_t(s) * STAGE_BYTES;
             unsigned char* sb = sa + A_BYTES;
-            const int32_t k0 = int32_t(kt0 + (i + krot) % nk) * BK;
+            const int32_t k0 = int32_t(kt0 + i) * BK;  // all CTAs walk K in step: weight rows stream DRAM page by page
             if (lane == 0) {
                 mbar_expect_tx(&full[s], B_BYTES);
 #pragma unroll
@@ -232,6 +229,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
         // prefill: every row tile re-reads them -> keep them in L2
         const uint64_t pol_b = tiles_m == 1 ? dev::evict_first_policy() : evict_last_policy();
         const uint64_t pol_a = evict_last_policy();  // activations: re-read by every N tile
+        // A's TMA coordinates: M dimensions are fixed for the CTA; K dimensions
+        // advance incrementally by one 64-wide k-tile per stage (no division in the loop)
+        int32_t cm[MT][5], ck[5], sub[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+#pragma unroll
+            for (int t = 0; t < MT; ++t) {
+                const uint32_t v = uint32_t(m0 + t * BM) / uint32_t(p.a_div[j]);
+                cm[t][j] = int32_t(p.a_mod[j] ? v % uint32_t(p.a_mod[j]) : v);
+            }
+            const uint32_t kb = uint32_t(kt0) * BK, dv = uint32_t(p.a_div[j]);
+            const uint32_t v = kb / dv;
+            ck[j] = int32_t(p.a_mod[j] ? v % uint32_t(p.a_mod[j]) : v);
+            sub[j] = int32_t(kb % dv);
+        }
         dev::pdl_wait();  // A is produced by earlier kernels
         for (int i = 0; i < nk; ++i) {
             const int s = i % STAGES;
@@ -240,16 +252,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             mbar_expect_tx(&full[s], STAGE_BYTES);
             unsigned char* sa = smem + size_t(s) * STAGE_BYTES;
             unsigned char* sb = sa + A_BYTES;
-            const int32_t k0 = int32_t(kt0 + (i + krot) % nk) * BK;
+            const int32_t k0 = int32_t(kt0 + i) * BK;  // all CTAs walk K in step: weight rows stream DRAM page by page
 #pragma unroll
             for (int t = 0; t < MT; ++t) {
                 int32_t ca[5];
 #pragma unroll
-                for (int j = 0; j < 5; ++j) {
-                    int64_t v = (p.a_axis[j] ? int64_t(k0) : m0 + t * BM) / p.a_div[j];
-                    ca[j] = int32_t(p.a_mod[j] ? v % p.a_mod[j] : v);
-                }
+                for (int j = 0; j < 5; ++j) ca[j] = p.a_axis[j] ? ck[j] : cm[t][j];
                 tma_nd(sa + t * A_SUB, &tm.a, ca, p.a_ndims, &full[s], pol_a);
+            }
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {  // advance the K coordinates by one k-tile
+                if (!p.a_axis[j]) continue;
+                if (p.a_div[j] == 1) {
+                    ck[j] += BK;
+                    if (p.a_mod[j] && ck[j] >= p.a_mod[j]) ck[j] -= int32_t(p.a_mod[j]);
+                } else if ((sub[j] += BK) >= p.a_div[j]) {
+                    sub[j] = 0;
+                    if (++ck[j] == p.a_mod[j]) ck[j] = 0;
+                }
             }
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)

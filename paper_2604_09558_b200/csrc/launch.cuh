@@ -10,6 +10,8 @@
 #pragma once
 
 #include <cstdlib>
+#include <mutex>
+#include <set>
 
 #include <cuda_runtime.h>
 
@@ -29,16 +31,18 @@ inline bool pdl_enabled() {
 // lowered it for a launch with a smaller footprint.)
 template <typename... KArgs>
 inline void allow_max_smem(void (*kern)(KArgs...)) {
-    static const bool done = [kern] {
-        cudaFuncAttributes a{};
-        cudaFuncGetAttributes(&a, kern);
-        int dev = 0, optin = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - int(a.sharedSizeBytes));
-        return true;
-    }();
-    (void)done;
+    // once per kernel function (a function-local static would be shared by every
+    // kernel with the same signature)
+    static std::mutex mu;
+    static std::set<const void*> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!done.insert(reinterpret_cast<const void*>(kern)).second) return;
+    cudaFuncAttributes a{};
+    cudaFuncGetAttributes(&a, kern);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - int(a.sharedSizeBytes));
 }
 
 template <typename... KArgs, typename... Args>

@@ -733,6 +733,76 @@ void Executor::prepare(bool dry) {
                 if (m != root) absorbed.insert(m);
     }
 
+    // ---- elementwise trees folded into a streamed GEMV's epilogue: trees whose
+    //      operands are strip-local views of the GEMV output (e.g. Q/K RoPE with
+    //      its rotate-half) are evaluated by the GEMV's last-CTA epilogue; the
+    //      intermediate roots they would have read are never written ----
+    std::map<std::string, std::vector<std::string>> epi_trees;  // gemv node -> tree roots
+    std::map<std::string, std::set<std::string>> epi_roots;     // gemv node -> exclusive roots
+    if (opt_.fuse && opt_.gemv_stream && !std::getenv("VTC_NO_EPI_FUSION")) {
+        std::set<std::string> graph_io;
+        for (const auto& t : g_.graph_inputs()) graph_io.insert(t);
+        for (const auto& t : g_.graph_outputs()) graph_io.insert(t);
+        std::map<std::string, std::string> tree_of_input;  // tensor -> tree root (first)
+        for (const auto& [root, t] : ew_trees)
+            for (const auto& in : t.in_names) tree_of_input.emplace(in, root);
+        for (const auto& n : g_.nodes()) {
+            if (!gemv_eligible(n) || g_.tensor(n.inputs[0]).shape[0] > 4 || hfuse.count(n.id) || hpartner.count(n.id))
+                continue;
+            auto fit = fusion.find(n.id);
+            if (fit != fusion.end() && fit->second.add) continue;
+            const std::string& C = n.outputs[0];
+            if (g_.tensor(C).kind != TensorKind::Intermediate) continue;
+            std::set<std::string> excl;
+            for (const auto& r : targets_of(map_of(C)))
+                if (!graph_io.count(r) && r != C) excl.insert(r);
+            // an exclusive root is read only through views that feed ew trees, and
+            // written only by this GEMV
+            std::set<std::string> trees;
+            for (const auto& [tid, m] : ptg_.resolved) {
+                if (tid == C) continue;
+                bool hits = false;
+                for (const auto& r : m.targets()) hits |= excl.count(r) > 0;
+                if (!hits) continue;
+                auto it = tree_of_input.find(tid);
+                bool consumed_by_tree = it != tree_of_input.end();
+                bool other_consumer = false;
+                for (const OpNode* c : g_.consumers(tid)) {
+                    if (is_data_movement(*c) && elim.count(c->id)) continue;
+                    bool in_tree = false;
+                    for (const auto& [root, t] : ew_trees)
+                        if (std::find(t.members.begin(), t.members.end(), c->id) != t.members.end()) in_tree = true;
+                    if (!in_tree) other_consumer = true;
+                }
+                if (!consumed_by_tree && !other_consumer) continue;  // a pure intermediate view
+                if (!consumed_by_tree || other_consumer) {
+                    for (const auto& r : m.targets()) excl.erase(r);
+                    continue;
+                }
+                trees.insert(it->second);
+            }
+            for (const auto& r : excl)
+                for (const OpNode* c : g_.consumers(r))
+                    if (!(is_data_movement(*c) && elim.count(c->id))) excl.erase(r);
+            if (excl.empty() || trees.empty() || trees.size() > size_t(EPI_MAX_TREES)) continue;
+            bool ok = true;
+            for (const auto& root : trees) {
+                const EwTree& t = ew_trees.at(root);
+                if (t.in_names.size() > size_t(EPI_MAX_IN) || absorbed.count(root)) ok = false;
+                for (const auto& in : t.in_names) {  // each operand: all C-derived or none
+                    int hit = 0, miss = 0;
+                    for (const auto& r : map_of(in).targets()) (excl.count(r) ? hit : miss)++;
+                    if (hit && miss) ok = false;
+                }
+            }
+            if (!ok) continue;
+            epi_trees[n.id] = std::vector<std::string>(trees.begin(), trees.end());
+            epi_roots[n.id] = excl;
+            for (const auto& root : trees)
+                for (const auto& m : ew_trees.at(root).members) absorbed.insert(m);
+        }
+    }
+
     for (int ni : g_.topo_order()) {
         const OpNode& n = g_.nodes()[size_t(ni)];
         if (absorbed.count(n.id)) continue;
@@ -895,11 +965,81 @@ void Executor::prepare(bool dry) {
                         p.c2 = operand(map_of(n2.outputs[0]), 1, 256, es);
                         L->node += "+" + n2.id;
                     }
+                    auto ef = epi_trees.find(n.id);
+                    if (ef != epi_trees.end()) {
+                        // the fused-epilogue table: one entry per output element (m, col)
+                        const std::string& C = n.outputs[0];
+                        const VMap& cm = map_of(C);
+                        const std::set<std::string>& excl = epi_roots.at(n.id);
+                        std::map<std::pair<std::string, int64_t>, int64_t> inv;  // (root, offset) -> m * N + col
+                        for (int64_t m = 0; m < M; ++m)
+                            for (int64_t c = 0; c < N; ++c) {
+                                auto te = cm.eval(Index{m, c});
+                                if (excl.count(te.first)) inv[te] = m * N + c;
+                            }
+                        std::vector<EpiEntry> tab(size_t(M * N));
+                        for (auto& x : tab) {
+                            std::memset(&x, 0, sizeof(x));
+                            x.tree = -1;
+                        }
+                        auto addr_of = [&](const std::pair<std::string, int64_t>& te) -> uint64_t {
+                            return target(te.first).ptr + uint64_t(te.second * es);
+                        };
+                        for (size_t ti = 0; ti < ef->second.size(); ++ti) {
+                            const std::string& root = ef->second[ti];
+                            const EwTree& t = ew_trees.at(root);
+                            const OpNode* rn = g_.node(root);
+                            const VMap& om = map_of(rn->outputs[0]);
+                            EpiTree& et = p.epi_tree[ti];
+                            et.nin = int32_t(t.in_names.size());
+                            et.nprog = int32_t(t.spec.prog.size());
+                            et.result = t.reg;
+                            for (size_t k2 = 0; k2 < t.spec.prog.size(); ++k2) et.prog[k2] = t.spec.prog[k2];
+                            const Index& shp = g_.tensor(rn->outputs[0]).shape;
+                            Index idx(shp.size(), 0);
+                            for (int64_t f = 0; f < volume(shp); ++f) {
+                                int64_t r = f;
+                                for (int a = int(shp.size()) - 1; a >= 0; --a) {
+                                    idx[size_t(a)] = r % shp[size_t(a)];
+                                    r /= shp[size_t(a)];
+                                }
+                                EpiEntry ent{};
+                                ent.tree = int32_t(ti);
+                                ent.out = addr_of(om.eval(idx));
+                                int64_t anchor = -1;
+                                for (size_t j = 0; j < t.in_names.size(); ++j) {
+                                    auto te = map_of(t.in_names[j]).eval(idx);
+                                    if (excl.count(te.first)) {
+                                        auto it = inv.find(te);
+                                        if (it == inv.end()) throw UnsupportedError("fused epilogue: operand outside the GEMV output");
+                                        if (anchor < 0) anchor = it->second;
+                                        if (it->second / N != anchor / N ||
+                                            (it->second % N) / GEMV_STREAM_COLS != (anchor % N) / GEMV_STREAM_COLS)
+                                            throw UnsupportedError("fused epilogue: operand crosses a 256-column strip");
+                                        ent.in[j] = uint64_t(it->second % N);
+                                        ent.cmask |= 1u << j;
+                                    } else {
+                                        ent.in[j] = addr_of(te);
+                                    }
+                                }
+                                if (anchor < 0 || tab[size_t(anchor)].tree >= 0)
+                                    throw UnsupportedError("fused epilogue: tree element without a unique anchor");
+                                tab[size_t(anchor)] = ent;
+                            }
+                            for (const auto& m : t.members) L->node += "+" + m;
+                        }
+                        auto* dtab = static_cast<EpiEntry*>(impl_->alloc(tab.size() * sizeof(EpiEntry), false));
+                        if (!impl_->dry)
+                            ck(cudaMemcpy(dtab, tab.data(), tab.size() * sizeof(EpiEntry), cudaMemcpyHostToDevice), "H2D(epi)");
+                        p.has_epi = 1;
+                        p.epi = dtab;
+                    }
                     if (M <= 4 && opt_.gemv_stream && stream_gemv(p, reinterpret_cast<uint64_t>(p.b_base), bp.target, m2p)) {
                         L->kernel = "gemv_stream_bf16";
                         push(std::move(L));
                         break;
                     }
+                    if (p.has_epi) throw UnsupportedError("fused GEMV epilogue " + L->node + " needs the streaming kernel");
                     if (m2p) throw UnsupportedError("horizontally fused GEMV " + L->node + " needs the streaming kernel");
                     // grid: 256-column strips x K splits, ~3 CTAs per SM
                     int64_t ntiles = (N + 255) / 256;

@@ -486,7 +486,50 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
                 if (ctid == 0) p.counters[strip] = 0u;
             }
         }
-        if (!last || n >= Nl) continue;
+        if (!last) continue;
+        if (p.has_epi) {
+            // fused elementwise trees: the strip's bf16 outputs in shared memory,
+            // then every element either evaluates its tree or is stored plainly
+            float* sC = red;  // [M][COLS] (the warp-reduction buffer is free again)
+            for (int m = 0; m < M; ++m) sC[m * COLS + ctid] = __bfloat162float(__float2bfloat16_rn(outv[m]));
+            bar_consumers();
+            if (n < Nl)
+                for (int m = 0; m < M; ++m) {
+                    const EpiEntry& e = p.epi[int64_t(m) * Nl + n];
+                    if (e.tree < 0) {
+                        int32_t idx[VTC_MAX_RANK] = {};
+                        idx[0] = m;
+                        idx[1] = int32_t(n);
+                        *dev::elem_ptr<bf16>(p.c.m, idx) = __float2bfloat16_rn(sC[m * COLS + ctid]);
+                        continue;
+                    }
+                    const EpiTree& t = p.epi_tree[e.tree];
+                    float r[EW_MAX_IN + EW_MAX_PROG];
+#pragma unroll
+                    for (int j = 0; j < EPI_MAX_IN; ++j) {
+                        if (j >= t.nin) break;
+                        r[j] = (e.cmask >> j) & 1u ? sC[m * COLS + int(int64_t(e.in[j]) - n0)]
+                                                   : __bfloat162float(*reinterpret_cast<const bf16*>(e.in[j]));
+                    }
+                    for (int s2 = 0; s2 < t.nprog; ++s2) {
+                        const EwInstr ins = t.prog[s2];
+                        const float a = r[ins.a], b = r[ins.b];
+                        float v;
+                        switch (ins.op) {  // bf16 rounding after every op, as the unfused kernel
+                            case EwOp::Add: v = a + b; break;
+                            case EwOp::Mul: v = a * b; break;
+                            case EwOp::SiLU: v = a / (1.0f + expf(-a)); break;
+                            case EwOp::GELU: v = 0.5f * a * (1.0f + erff(a * 0.70710678f)); break;
+                            default: v = a; break;
+                        }
+                        r[ins.dst] = __bfloat162float(__float2bfloat16_rn(v));
+                    }
+                    *reinterpret_cast<bf16*>(e.out) = __float2bfloat16_rn(r[t.result]);
+                }
+            bar_consumers();  // sC is the reduction buffer of the next strip
+            continue;
+        }
+        if (n >= Nl) continue;
         const VOperand& cop = mat ? p.c2 : p.c;
 #pragma unroll
         for (int m = 0; m < MT; ++m) {

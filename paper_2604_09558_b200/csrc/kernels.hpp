@@ -101,6 +101,23 @@ void launch_matmul(const MatmulParams& p, const MatmulParams* dp, cudaStream_t s
 // the last-arriving CTA of each N tile.
 enum class GemvPrologue : int32_t { None = 0, SiLUMul = 1, RMSNorm = 2 };
 constexpr int GEMV_MAX_MATS = 2;
+// Elementwise trees fused into the GEMV epilogue (e.g. RoPE on the Q / K
+// columns of the QKV projection): the tree's operands that are the GEMV output
+// itself are read from the strip in shared memory (strip-local permutations
+// such as the rotate-half), the others from memory; the intermediate root the
+// GEMV would have written is never materialised.
+constexpr int EPI_MAX_TREES = 2, EPI_MAX_IN = 4;
+struct EpiTree {
+    int32_t nin, nprog, result, pad;
+    EwInstr prog[EW_MAX_PROG];
+};
+struct EpiEntry {            // one GEMV output element (m, n)
+    uint64_t out;            // tree output address (bf16)
+    uint64_t in[EPI_MAX_IN]; // C column (C-derived input) or element address (external input)
+    int32_t tree;            // -1: plain output element, stored through the C map
+    uint32_t cmask;          // bit j: input j is C-derived
+};
+
 struct GemvParams {
     KHead head;
     VOperand a, a2, normw, c, res;  // a:[M,K] (fast K); a2: second input of SiLUMul; normw: [K]
@@ -127,6 +144,10 @@ struct GemvParams {
     const int32_t* strip_first;     // first CTA touching each 256-column strip
     const int32_t* strip_count;     // number of CTAs touching it
     VOperand c2;
+    // fused epilogue trees (has_epi): table [M * N] of EpiEntry
+    int32_t has_epi, pad4;
+    const EpiEntry* epi;
+    EpiTree epi_tree[EPI_MAX_TREES];
     alignas(64) unsigned char tmap[GEMV_MAX_MATS][128];  // CUtensorMap per weight matrix (host-encoded)
 };
 void launch_gemv(const GemvParams& p, const GemvParams* dp, cudaStream_t s);

@@ -99,6 +99,14 @@ int vtc_plan_bind_root(vtc_plan* p, const char* tensor, void* dev_ptr);
 int vtc_plan_root_ptr(vtc_plan* p, const char* tensor, void** dev_ptr);
 int vtc_plan_upload(vtc_plan* p, const char* tensor, const void* host, int64_t bytes, void* stream);
 int vtc_plan_download(vtc_plan* p, const char* tensor, void* host, int64_t bytes, void* stream);
+/* One step from host buffers -- the drop-in for the reference's
+ * execute(g, ptg, inputs) (proj/include/vtelim/executor.hpp:77-83): every
+ * input lands in its root with ONE H2D copy (the inputs' roots share a device
+ * arena staged through pinned memory), the plan runs as a CUDA-graph replay,
+ * each output (physical or virtual) is copied back, and the stream is
+ * synchronised before returning.  Inputs not named keep their device contents. */
+int vtc_run(vtc_plan* p, int32_t n_in, const char* const* in_ids, const void* const* in_host, const int64_t* in_bytes,
+            int32_t n_out, const char* const* out_ids, void* const* out_host, const int64_t* out_bytes, void* stream);
 int vtc_plan_prepare(vtc_plan* p);
 int vtc_execute(vtc_plan* p, void* stream);        /* async launches on `stream` (cudaStream_t) */
 int vtc_execute_graph(vtc_plan* p, void* stream);  /* CUDA-graph replay of the same launches */

@@ -78,6 +78,22 @@ public:
     // Materialise any tensor (virtual or physical) into host memory.
     void download(const std::string& id, void* host, int64_t bytes, void* stream);
 
+    // One call per step from host buffers (the reference's execute(g, ptg, inputs),
+    // proj/include/vtelim/executor.hpp:77): the inputs' roots live in one device
+    // arena filled by a single H2D copy from a pinned staging buffer, then the
+    // CUDA-graph replay, then one D2H per output and a stream synchronisation.
+    struct HostIn {
+        std::string id;
+        const void* ptr;
+        int64_t bytes;
+    };
+    struct HostOut {
+        std::string id;
+        void* ptr;
+        int64_t bytes;
+    };
+    void run_host(const std::vector<HostIn>& ins, const std::vector<HostOut>& outs, void* stream);
+
     const std::vector<LaunchInfo>& launches() const { return infos_; }
     int num_kernel_launches() const;
 
@@ -91,6 +107,12 @@ private:
     std::vector<LaunchInfo> infos_;
     std::unique_ptr<Impl> impl_;
     bool prepared_ = false;
+    // run_host staging: device arena holding the per-step input roots + pinned mirror
+    std::string arena_key_;
+    void* arena_dev_ = nullptr;
+    void* arena_host_ = nullptr;
+    int64_t arena_bytes_ = 0;
+    std::vector<int64_t> arena_off_;
 };
 
 }  // namespace vtc

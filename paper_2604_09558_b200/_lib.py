@@ -28,6 +28,8 @@ SIGNATURES = {
     "vtc_plan_root_ptr": (C.c_int, [_VP, C.c_char_p, C.POINTER(_VP)]),
     "vtc_plan_upload": (C.c_int, [_VP, C.c_char_p, _VP, C.c_int64, _VP]),
     "vtc_plan_download": (C.c_int, [_VP, C.c_char_p, _VP, C.c_int64, _VP]),
+    "vtc_run": (C.c_int, [_VP, C.c_int32, C.POINTER(C.c_char_p), C.POINTER(_VP), C.POINTER(C.c_int64),
+                          C.c_int32, C.POINTER(C.c_char_p), C.POINTER(_VP), C.POINTER(C.c_int64), _VP]),
     "vtc_plan_prepare": (C.c_int, [_VP]),
     "vtc_execute": (C.c_int, [_VP, _VP]),
     "vtc_execute_graph": (C.c_int, [_VP, _VP]),

@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json
-from typing import Dict, Iterable, Optional
+from typing import Dict, Iterable, Optional, Sequence
 
 import numpy as np
 
@@ -182,6 +182,44 @@ class Plan:
         _check(_lib.load().vtc_plan_download(self._h, tensor.encode(), out.ctypes.data_as(C.c_void_p),
                                              out.nbytes, _stream(stream)))
         return out
+
+    def host_step(self, inputs, outputs, stream=None):
+        """A bound vtc_run call for repeated steps from fixed host buffers:
+        `inputs` / `outputs` are lists of (tensor id, host pointer, nbytes).
+        The ctypes argument arrays are built once; calling the returned
+        function runs one step (one H2D, graph replay, D2H, stream sync).
+        Pinned host buffers make the copies asynchronous DMA."""
+        ni, no = len(inputs), len(outputs)
+        args = (self._h, ni,
+                (C.c_char_p * max(ni, 1))(*[t.encode() for t, _, _ in inputs]),
+                (C.c_void_p * max(ni, 1))(*[C.c_void_p(p) for _, p, _ in inputs]),
+                (C.c_int64 * max(ni, 1))(*[n for _, _, n in inputs]),
+                no,
+                (C.c_char_p * max(no, 1))(*[t.encode() for t, _, _ in outputs]),
+                (C.c_void_p * max(no, 1))(*[C.c_void_p(p) for _, p, _ in outputs]),
+                (C.c_int64 * max(no, 1))(*[n for _, _, n in outputs]),
+                _stream(stream))
+        fn = _lib.load().vtc_run
+
+        def step():
+            rc = fn(*args)
+            if rc:
+                _check(rc)
+        step._keep = (self, args)  # noqa: SLF001 -- keep the plan and buffers alive
+        return step
+
+    def run_ptrs(self, inputs, outputs, stream=None) -> None:
+        """One step from host memory through vtc_run (see host_step)."""
+        self.host_step(inputs, outputs, stream)()
+
+    def run(self, inputs: Dict[str, np.ndarray], outputs: Sequence[str], stream=None) -> Dict[str, np.ndarray]:
+        """execute(g, ptg, inputs) for one step: upload `inputs`, run, return `outputs`."""
+        arrs = {k: np.ascontiguousarray(v) for k, v in inputs.items()}
+        tens = self.graph.tensors()
+        res = {o: np.empty(tens[o]["shape"], dtype=NP_DTYPES[tens[o]["dtype"]]) for o in outputs}
+        self.run_ptrs([(k, a.ctypes.data, a.nbytes) for k, a in arrs.items()],
+                      [(k, a.ctypes.data, a.nbytes) for k, a in res.items()], stream)
+        return res
 
     def prepare(self) -> None:
         _check(_lib.load().vtc_plan_prepare(self._h))

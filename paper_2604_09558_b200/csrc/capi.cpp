@@ -227,6 +227,17 @@ int vtc_plan_download(vtc_plan* p, const char* tensor, void* host, int64_t bytes
     return guard([&] { p->exec->download(tensor, host, bytes, stream); });
 }
 
+int vtc_run(vtc_plan* p, int32_t n_in, const char* const* in_ids, const void* const* in_host, const int64_t* in_bytes,
+            int32_t n_out, const char* const* out_ids, void* const* out_host, const int64_t* out_bytes, void* stream) {
+    return guard([&] {
+        std::vector<vtc::Executor::HostIn> ins;
+        std::vector<vtc::Executor::HostOut> outs;
+        for (int32_t i = 0; i < n_in; ++i) ins.push_back({in_ids[i], in_host[i], in_bytes[i]});
+        for (int32_t i = 0; i < n_out; ++i) outs.push_back({out_ids[i], out_host[i], out_bytes[i]});
+        p->exec->run_host(ins, outs, stream);
+    });
+}
+
 int vtc_comm_unique_id(void* out, int32_t bytes) {
     return guard([&] {
         if (bytes < 128) throw vtc::ExecutionError("vtc_comm_unique_id: buffer must hold 128 bytes");

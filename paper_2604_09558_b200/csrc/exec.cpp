@@ -161,11 +161,23 @@ struct Executor::Impl {
         for (void* p : scratch) cudaFree(p);
         scratch.clear();
     }
+    // run_host graph: H2D of the input arena -> launches -> D2H of the outputs
+    cudaGraphExec_t hexec = nullptr;
+    std::string hkey;
+    void* out_host = nullptr;  // pinned output staging
+    size_t out_host_bytes = 0;
+    std::vector<std::pair<std::string, int64_t>> sig_in, sig_out;  // the call hexec was built for
+    std::vector<size_t> out_off;
+    bool fast_all_physical = false;
+    cudaStream_t fast_stream = nullptr;
     void free_graph() {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);
+        if (hexec) cudaGraphExecDestroy(hexec);
         gexec = nullptr;
         graph = nullptr;
+        hexec = nullptr;
+        hkey.clear();
     }
     bool dry = false;
     void* alloc(size_t bytes, bool zero) {
@@ -197,6 +209,9 @@ Executor::~Executor() {
     impl_->free_scratch();
     for (auto& r : roots_)
         if (r.owned && r.ptr) cudaFree(r.ptr);
+    if (arena_dev_) cudaFree(arena_dev_);
+    if (arena_host_) cudaFreeHost(arena_host_);
+    if (impl_->out_host) cudaFreeHost(impl_->out_host);
 }
 
 void Executor::bind_root(const std::string& id, void* dev_ptr) {
@@ -358,6 +373,8 @@ void Executor::prepare(bool dry) {
         p.b_static = (written_roots.count(b_root) || (m2 && written_roots.count(m2->root))) ? 0 : 1;
         p.pre_stages = 1;
         if (const char* e = std::getenv("VTC_GEMV_PRE")) p.pre_stages = std::atoi(e);
+        p.l2_prefetch = 0;
+        if (const char* e = std::getenv("VTC_GEMV_L2PF")) p.l2_prefetch = std::atoi(e);
         p.work = static_cast<float*>(impl_->alloc(size_t(strips * maxc * p.M * COLS) * sizeof(float), false));
         p.counters = static_cast<unsigned*>(impl_->alloc(size_t(strips) * sizeof(unsigned), true));
         auto* dfirst = static_cast<int32_t*>(impl_->alloc(size_t(strips) * 4, false));
@@ -1417,6 +1434,144 @@ void Executor::upload(const std::string& id, const void* host, int64_t bytes, vo
     if (bytes != r.bytes) throw ShapeMismatchError("upload of " + id + ": byte count mismatch");
     void* d = root_ptr(id);
     ck(cudaMemcpyAsync(d, host, size_t(bytes), cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)), "H2D");
+}
+
+void Executor::run_host(const std::vector<HostIn>& ins, const std::vector<HostOut>& outs, void* stream) {
+    auto s = static_cast<cudaStream_t>(stream);
+    // steady state: same inputs / outputs as the call that built the host graph
+    // (any rebind or re-prepare drops hexec) -> copies, one graph launch, sync
+    Impl& I = *impl_;
+    bool same = I.hexec && I.fast_all_physical && ins.size() == I.sig_in.size() && outs.size() == I.sig_out.size() &&
+                I.fast_stream == s;
+    for (size_t i = 0; same && i < ins.size(); ++i) same = ins[i].bytes == I.sig_in[i].second && ins[i].id == I.sig_in[i].first;
+    for (size_t i = 0; same && i < outs.size(); ++i)
+        same = outs[i].bytes == I.sig_out[i].second && outs[i].id == I.sig_out[i].first;
+    if (same) {
+        for (size_t i = 0; i < ins.size(); ++i)
+            if (ins[i].bytes) std::memcpy(static_cast<char*>(arena_host_) + arena_off_[i], ins[i].ptr, size_t(ins[i].bytes));
+        ck(cudaGraphLaunch(I.hexec, s), "cudaGraphLaunch(host graph)");
+        ck(cudaStreamSynchronize(s), "sync");
+        for (size_t i = 0; i < outs.size(); ++i)
+            std::memcpy(outs[i].ptr, static_cast<char*>(I.out_host) + I.out_off[i], size_t(outs[i].bytes));
+        return;
+    }
+    I.sig_in.clear();
+    I.sig_out.clear();
+    std::string key;
+    std::vector<int> idx;
+    for (const auto& in : ins) {
+        auto it = root_index_.find(in.id);
+        if (it == root_index_.end()) throw ExecutionError("input " + in.id + " is not a physical root");
+        if (in.bytes != roots_[size_t(it->second)].bytes)
+            throw ShapeMismatchError("input " + in.id + ": byte count mismatch");
+        idx.push_back(it->second);
+        key += in.id;
+        key += '\n';
+    }
+    // (re)build the arena when the input set changed or a root was rebound since
+    bool ok = key == arena_key_ && arena_dev_;
+    for (size_t i = 0; ok && i < ins.size(); ++i)
+        ok = roots_[size_t(idx[i])].ptr == static_cast<char*>(arena_dev_) + arena_off_[i];
+    if (!ok) {
+        if (arena_dev_) ck(cudaFree(arena_dev_), "cudaFree(arena)");
+        if (arena_host_) ck(cudaFreeHost(arena_host_), "cudaFreeHost(arena)");
+        arena_dev_ = arena_host_ = nullptr;
+        arena_off_.clear();
+        int64_t total = 0;
+        for (const auto& in : ins) {
+            arena_off_.push_back(total);
+            total += (std::max<int64_t>(in.bytes, 16) + 255) / 256 * 256;
+        }
+        arena_bytes_ = total;
+        if (total) {
+            ck(cudaMalloc(&arena_dev_, size_t(total)), "cudaMalloc(arena)");
+            ck(cudaHostAlloc(&arena_host_, size_t(total), cudaHostAllocMapped | cudaHostAllocPortable),
+               "cudaHostAlloc(arena)");
+            for (size_t i = 0; i < ins.size(); ++i) bind_root(ins[i].id, static_cast<char*>(arena_dev_) + arena_off_[i]);
+        }
+        arena_key_ = key;
+    }
+    for (size_t i = 0; i < ins.size(); ++i)
+        if (ins[i].bytes) std::memcpy(static_cast<char*>(arena_host_) + arena_off_[i], ins[i].ptr, size_t(ins[i].bytes));
+    // physical outputs come back inside the graph (into pinned staging); virtual
+    // ones are materialised through their maps afterwards
+    std::vector<size_t> out_off(outs.size(), SIZE_MAX);
+    size_t out_total = 0;
+    std::string hkey = key + "|";
+    for (size_t i = 0; i < outs.size(); ++i) {
+        const HostOut& o = outs[i];
+        if (o.bytes != g_.tensor(o.id).bytes()) throw ShapeMismatchError("output " + o.id + ": byte count mismatch");
+        if (root_index_.count(o.id) && ptg_.map_of(o.id).is_identity_of(o.id)) {
+            out_off[i] = out_total;
+            out_total += (size_t(o.bytes) + 255) / 256 * 256;
+            hkey += o.id;
+            hkey += '\n';
+        }
+    }
+    if (!prepared_) prepare();
+    if (!impl_->hexec || impl_->hkey != hkey) {
+        if (impl_->hexec) cudaGraphExecDestroy(impl_->hexec);
+        impl_->hexec = nullptr;
+        if (out_total > impl_->out_host_bytes) {
+            if (impl_->out_host) ck(cudaFreeHost(impl_->out_host), "cudaFreeHost(out)");
+            impl_->out_host = nullptr;
+            ck(cudaHostAlloc(&impl_->out_host, out_total, cudaHostAllocMapped | cudaHostAllocPortable),
+               "cudaHostAlloc(out)");
+            impl_->out_host_bytes = out_total;
+        }
+        std::vector<void*> out_dev(outs.size(), nullptr);
+        for (size_t i = 0; i < outs.size(); ++i)
+            if (out_off[i] != SIZE_MAX) out_dev[i] = root_ptr(outs[i].id);
+        void *arena_host_dev = nullptr, *out_host_dev = nullptr;  // device views of the pinned buffers
+        if (arena_host_) ck(cudaHostGetDevicePointer(&arena_host_dev, arena_host_, 0), "cudaHostGetDevicePointer");
+        if (impl_->out_host) ck(cudaHostGetDevicePointer(&out_host_dev, impl_->out_host, 0), "cudaHostGetDevicePointer");
+        cudaStream_t cap;
+        cudaGraph_t hg = nullptr;
+        ck(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        // small transfers: a host-link copy kernel (pinned memory is device-addressable);
+        // large ones: DMA memcpy nodes
+        const bool dma = std::getenv("VTC_HOST_DMA") != nullptr;
+        constexpr int64_t kLinkMax = 1 << 20;
+        if (arena_bytes_) {
+            if (!dma && arena_bytes_ <= kLinkMax)
+                launch_host_link_copy(arena_host_dev, arena_dev_, arena_bytes_, cap);
+            else
+                cudaMemcpyAsync(arena_dev_, arena_host_, size_t(arena_bytes_), cudaMemcpyHostToDevice, cap);
+        }
+        for (auto& l : impl_->launches) l->run(cap);
+        for (size_t i = 0; i < outs.size(); ++i) {
+            if (out_off[i] == SIZE_MAX) continue;
+            void* dst = static_cast<char*>(impl_->out_host) + out_off[i];
+            if (!dma && outs[i].bytes <= kLinkMax && outs[i].bytes % 16 == 0 &&
+                reinterpret_cast<uintptr_t>(out_dev[i]) % 16 == 0)
+                launch_host_link_copy(out_dev[i], static_cast<char*>(out_host_dev) + out_off[i], outs[i].bytes, cap);
+            else
+                cudaMemcpyAsync(dst, out_dev[i], size_t(outs[i].bytes), cudaMemcpyDeviceToHost, cap);
+        }
+        cudaError_t e = cudaStreamEndCapture(cap, &hg);
+        cudaStreamDestroy(cap);
+        ck(e, "cudaStreamEndCapture(host graph)");
+        e = cudaGraphInstantiate(&impl_->hexec, hg, 0);
+        cudaGraphDestroy(hg);
+        ck(e, "cudaGraphInstantiate(host graph)");
+        impl_->hkey = hkey;
+    }
+    ck(cudaGraphLaunch(impl_->hexec, s), "cudaGraphLaunch(host graph)");
+    I.fast_all_physical = true;
+    for (size_t i = 0; i < outs.size(); ++i)
+        if (out_off[i] == SIZE_MAX) {
+            I.fast_all_physical = false;
+            download(outs[i].id, outs[i].ptr, outs[i].bytes, stream);
+        }
+    for (const auto& in : ins) I.sig_in.emplace_back(in.id, in.bytes);
+    for (const auto& o : outs) I.sig_out.emplace_back(o.id, o.bytes);
+    I.out_off = out_off;
+    I.fast_stream = s;
+    ck(cudaStreamSynchronize(s), "sync");
+    for (size_t i = 0; i < outs.size(); ++i)
+        if (out_off[i] != SIZE_MAX)
+            std::memcpy(outs[i].ptr, static_cast<char*>(impl_->out_host) + out_off[i], size_t(outs[i].bytes));
 }
 
 void Executor::download(const std::string& id, void* host, int64_t bytes, void* stream) {

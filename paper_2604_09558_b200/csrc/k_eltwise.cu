@@ -225,4 +225,40 @@ void launch_eltwise(const EwParams& p, const EwParams* dp, cudaStream_t s) {
     }
 }
 
+
+// ---- host-link copies of run_host (vtc_run) --------------------------------
+// Pinned host buffers are device-addressable under UVA: one small kernel reads
+// the pinned input arena over the host link (or writes the outputs into pinned
+// staging with posted stores) instead of a DMA memcpy node, whose fixed cost
+// (~4.5 us per node on B200) exceeds the transfer of a decode step's few KB.
+// Launched with PDL like every other kernel, so the next launch's static
+// weight prefetch overlaps the copy-in and the copy-out overlaps the last
+// kernel's tail up to its dependency wait.
+namespace {
+__global__ void __launch_bounds__(256) host_link_copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                            int64_t n16) {
+    dev::pdl_wait();
+    dev::pdl_launch_dependents();
+    constexpr int U = 4;  // every load of a thread in flight before its stores
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n16; i0 += U * stride) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * stride < n16) v[u] = src[i0 + u * stride];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * stride < n16) dst[i0 + u * stride] = v[u];
+    }
+}
+}  // namespace
+
+void launch_host_link_copy(const void* src, void* dst, int64_t bytes, cudaStream_t s) {
+    const int64_t n16 = (bytes + 15) / 16;
+    if (n16 == 0) return;
+    const int64_t per_cta = 256 * 4;
+    const unsigned grid = unsigned(std::min<int64_t>((n16 + per_cta - 1) / per_cta, 148));
+    launch_k(host_link_copy_kernel, dim3(grid), dim3(256), 0, s, static_cast<const uint4*>(src), static_cast<uint4*>(dst), n16);
+}
+
 }  // namespace vtc

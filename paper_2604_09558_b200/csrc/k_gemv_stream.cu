@@ -77,6 +77,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
 __device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32) : "memory"); }
 
 template <int MT>
@@ -117,7 +122,24 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
         if (lane != 0) return;
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.m[0])) : "memory");
         const uint64_t policy = dev::evict_first_policy();
-        if (!p.b_static) dev::pdl_wait();
+        if (p.b_static) {
+            // the weights do not depend on earlier launches: pull this CTA's
+            // first tiles into L2 while the previous (often latency-bound)
+            // launch is still running, so HBM is busy during its tail
+            const int64_t pf_end = u_begin + p.l2_prefetch < u_end ? u_begin + p.l2_prefetch : u_end;
+            int64_t strip = u_begin / ktiles, kt = u_begin % ktiles;
+            for (int64_t u = u_begin; u < pf_end; ++u) {
+                if (u != u_begin && ++kt == ktiles) {
+                    kt = 0;
+                    ++strip;
+                }
+                const int mat = strip < p.strips0 ? 0 : 1;
+                const int64_t n0 = (strip - (mat ? p.strips0 : 0)) * COLS;
+                if (u >= u_begin + p.pre_stages) tma_prefetch_2d(&tm.m[mat], int32_t(n0), int32_t(kt * KT));
+            }
+        } else {
+            dev::pdl_wait();
+        }
         int stage = 0;
         uint32_t phase = 0;
         // Only PRE tiles go out before the consumers have issued their

@@ -78,6 +78,8 @@ struct EwPair {
 };
 bool eltwise_pair_compatible(const EwParams& a, const EwParams& b);
 void launch_eltwise_pair(const EwPair& p, const EwPair* dp, cudaStream_t s);
+// 16-byte-granular copy between UVA-addressable buffers (pinned host <-> device)
+void launch_host_link_copy(const void* src, void* dst, int64_t bytes, cudaStream_t s);
 
 // ---- generic batched matmul (any dtype, any maps) -----------------------
 struct MatmulParams {
@@ -139,7 +141,8 @@ struct GemvParams {
     int32_t nmat;
     int32_t stages, grid, max_contrib, a_tiles;  // a_tiles: k-tiles of A staged per CTA
     int32_t strips0, b_static;      // b_static: weights never written by the plan (prefetch before pdl_wait)
-    int32_t pre_stages, pad3;       // weight tiles issued before the activation loads
+    int32_t pre_stages, l2_prefetch;  // weight tiles issued before the activation loads; tiles
+                                     // prefetched into L2 while the previous launch finishes
     int64_t n_mat[GEMV_MAX_MATS];
     const int32_t* strip_first;     // first CTA touching each 256-column strip
     const int32_t* strip_count;     // number of CTAs touching it

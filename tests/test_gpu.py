@@ -414,3 +414,28 @@ def test_c1_full_size_digest_matches_reference(vtc, ref):
     assert p.info()["data_movement_launches"] == 0
     dig = json.loads((Path(G.GOLD) / "ref_digests.json").read_text())["c1_chain_1024_f32_seed1"]["y"]
     assert format(G.fnv1a64(got["y"]), "016x") == dig
+
+
+def test_vtc_run_single_call_matches_upload_execute_download(vtc, oracle):
+    """vtc_run (one H2D through the input arena, graph replay, D2H, sync) gives
+    the same bits as per-tensor upload + execute + download, over several steps
+    with changing inputs, and across a rebind of an arena root."""
+    from paper_2604_09558_b200 import workloads as W
+    cfg = dict(B=2, L=64, pos=40, D=256, Hq=4, Hkv=2, hd=64, F=512)
+    doc = W.llama_decode_layer(**cfg)
+    g = vtc.parse_graph(doc)
+    p1 = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    p2 = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    x = _llama_inputs(oracle, W, doc, cfg["B"], cfg["pos"], cfg["D"], cfg["F"], cfg["hd"])
+    for k, v in x.items():
+        p2.upload(k, v)
+    rng = np.random.default_rng(3)
+    for step in range(3):
+        xs = oracle.f32_to_bf16(rng.uniform(-1, 1, size=x["x"].shape).astype(np.float32))
+        x1 = dict(x, x=xs)
+        want = vtc.execute(g, p1, x1)["y"]
+        got = p2.run({"x": xs}, ["y", "k_cache"])
+        assert np.array_equal(got["y"], want), step
+        assert np.array_equal(got["k_cache"][cfg["pos"]], p1.download("k_cache")[cfg["pos"]])
+    with pytest.raises(vtc.api.ERRORS[15]):  # ShapeMismatchError
+        p2.run({"x": xs[:1]}, ["y"])

@@ -84,6 +84,20 @@ struct AllReduceLaunch : Launch {
     void set_trace(unsigned long long*, int) override {}
 };
 
+// Consecutive streamed GEMVs as the stages of one persistent launch.
+struct GemvChainLaunch : Launch {
+    std::vector<GemvParams> ps;
+    GemvChainArgs ca{};
+    const GemvParams* dp = nullptr;
+    void run(cudaStream_t s) override { launch_gemv_chain(ca, dp, ps[0].M, ps[0].grid, s); }
+    size_t param_bytes() const override { return ps.size() * sizeof(GemvParams); }
+    const void* host_params() const override { return ps.data(); }
+    void set_device_params(void* d) override { dp = static_cast<const GemvParams*>(d); }
+    void set_trace(unsigned long long* t, int id) override {
+        for (auto& p : ps) set_head(p, t, id);
+    }
+};
+
 void launch_gemv_any(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
     if (p.stream) launch_gemv_stream(p, dp, s);
     else launch_gemv(p, dp, s);
@@ -363,6 +377,27 @@ void Executor::prepare(bool dry) {
         int maxc = *std::max_element(count.begin(), count.end());
         p.stream = 1;
         p.nmat = m2 ? 2 : 1;
+        {
+            // rows of the prologue operands resolved here (the kernel's row_ptr, on the host)
+            auto row = [&](const VOperand& op, int64_t m, const void*& ptr, int64_t& st) {
+                if (!op.fast_ok) return false;
+                int64_t idx[VTC_MAX_RANK] = {};
+                idx[0] = m;
+                int pc = -1;
+                const int64_t off = desc_eval(op.m, idx, &pc);
+                if (pc < 0) return false;
+                ptr = reinterpret_cast<const void*>(op.m.piece[pc].ptr + uint64_t(off) * 2);
+                st = op.fast_stride[pc];
+                return true;
+            };
+            bool ok = p.M <= 4;
+            for (int64_t m = 0; ok && m < p.M; ++m) {
+                ok = row(p.a, m, p.arow[m], p.sa[m]);
+                if (ok && p.prologue == GemvPrologue::SiLUMul) ok = row(p.a2, m, p.a2row[m], p.sa2[m]);
+            }
+            if (ok && p.prologue == GemvPrologue::RMSNorm) ok = row(p.normw, 0, p.wrow, p.sw);
+            p.rows_ok = ok ? 1 : 0;
+        }
         p.n_mat[0] = p.N;
         if (m2) p.n_mat[1] = m2->N;
         p.strips0 = int32_t(strips0);
@@ -1318,6 +1353,137 @@ void Executor::prepare(bool dry) {
             }
             merged.push_back(std::move(impl_->launches[i]));
             minfos.push_back(infos_[i]);
+        }
+        impl_->launches = std::move(merged);
+        infos_ = std::move(minfos);
+    }
+    // chain consecutive streamed GEMVs (o_proj -> gate/up -> down) into one
+    // persistent launch with per-strip dependencies.  Opt-in (VTC_CHAIN=1):
+    // on C2 it measured equal to separate launches (113.6 vs 113.6 us) because
+    // every strip of a split-K stage completes at the stage's end, so the next
+    // stage cannot start early; kept for multi-layer chains.
+    if (opt_.fuse && std::getenv("VTC_CHAIN") && std::getenv("VTC_CHAIN")[0] == '1') {
+        using GL = LaunchT<GemvParams, launch_gemv_any>;
+        auto roots_of = [](const VOperand& op, std::set<int>& out) {
+            for (int i = 0; i < op.m.npieces; ++i) out.insert(op.m.piece[i].target);
+        };
+        auto reads_of = [&](const GemvParams& p) {
+            std::set<int> r;
+            roots_of(p.a, r);
+            if (p.prologue == GemvPrologue::SiLUMul) roots_of(p.a2, r);
+            if (p.prologue == GemvPrologue::RMSNorm) roots_of(p.normw, r);
+            if (p.has_res) roots_of(p.res, r);
+            return r;
+        };
+        auto writes_of = [&](const GemvParams& p) {
+            std::set<int> w;
+            roots_of(p.c, w);
+            if (p.nmat > 1) roots_of(p.c2, w);
+            return w;
+        };
+        auto chainable = [](const GemvParams& p) { return p.stream == 1 && p.has_epi == 0 && p.b_static == 1; };
+        auto same_map = [](const VOperand& x, const VOperand& y) { return std::memcmp(&x.m, &y.m, sizeof(vtc_map)) == 0; };
+        std::vector<std::unique_ptr<Launch>> merged;
+        std::vector<LaunchInfo> minfos;
+        size_t i = 0;
+        while (i < impl_->launches.size()) {
+            auto* a = dynamic_cast<GL*>(impl_->launches[i].get());
+            if (!a || !chainable(a->p)) {
+                merged.push_back(std::move(impl_->launches[i]));
+                minfos.push_back(infos_[i]);
+                ++i;
+                continue;
+            }
+            std::vector<GemvParams> run{a->p};
+            std::vector<GemvChainStage> hs(1);
+            std::set<int> rd = reads_of(a->p), wr = writes_of(a->p);
+            std::vector<std::set<int>> wr_st{writes_of(a->p)};
+            int64_t sA = a->p.M * int64_t(a->p.a_tiles) * GEMV_STREAM_KT;
+            size_t j = i + 1;
+            for (; j < impl_->launches.size() && run.size() < size_t(GEMV_MAX_CHAIN); ++j) {
+                auto* b = dynamic_cast<GL*>(impl_->launches[j].get());
+                if (!b || !chainable(b->p) || b->p.M != a->p.M || b->p.grid != a->p.grid) break;
+                const GemvParams& q = b->p;
+                std::set<int> rq = reads_of(q), wq = writes_of(q);
+                bool hazard = false;  // WAR / WAW against earlier stages
+                for (int t : wq) hazard |= rd.count(t) > 0 || wr.count(t) > 0;
+                if (hazard) break;
+                int64_t sAq = std::max<int64_t>(sA, q.M * int64_t(q.a_tiles) * GEMV_STREAM_KT);
+                if (gemv_chain_smem(sAq, 2) + sizeof(GemvParams) + 12 * 1024 > 227 * 1024) break;
+                GemvChainStage h{};
+                const GemvParams& pv = run.back();
+                const size_t k = run.size();
+                for (size_t t = 0; t < k; ++t) {
+                    bool touches = false;
+                    for (int r : rq) touches |= wr_st[t].count(r) > 0;
+                    if (touches) h.dep_all |= 1u << t;
+                }
+                // A exactly the previous stage's output columns: wait per strip
+                if ((h.dep_all >> (k - 1)) & 1u) {
+                    std::set<int> rest;
+                    if (q.prologue == GemvPrologue::RMSNorm) roots_of(q.normw, rest);
+                    if (q.has_res) roots_of(q.res, rest);
+                    bool other = false;
+                    for (int r : rest) other |= wr_st[k - 1].count(r) > 0;
+                    const bool a_ok = same_map(q.a, pv.c);
+                    const bool a2_ok = q.prologue != GemvPrologue::SiLUMul || (pv.nmat > 1 && same_map(q.a2, pv.c2));
+                    if (!other && a_ok && a2_ok && q.prologue != GemvPrologue::RMSNorm) {
+                        h.dep_all &= ~(1u << (k - 1));
+                        h.dep_range = 1;
+                        h.dep_a2 = q.prologue == GemvPrologue::SiLUMul ? 1 : 0;
+                    }
+                }
+                run.push_back(q);
+                hs.push_back(h);
+                rd.insert(rq.begin(), rq.end());
+                wr.insert(wq.begin(), wq.end());
+                wr_st.push_back(wq);
+                sA = sAq;
+            }
+            if (run.size() < 2) {
+                merged.push_back(std::move(impl_->launches[i]));
+                minfos.push_back(infos_[i]);
+                ++i;
+                continue;
+            }
+            auto C = std::make_unique<GemvChainLaunch>();
+            C->kernel = a->kernel;
+            LaunchInfo li = infos_[i];
+            int max_strips = 0;
+            for (size_t t = 0; t < run.size(); ++t) {
+                const GemvParams& p = run[t];
+                GemvChainStage& h = hs[t];
+                h.K = p.K;
+                h.n0 = p.n_mat[0];
+                h.n1 = p.nmat > 1 ? p.n_mat[1] : 0;
+                h.nmat = p.nmat;
+                h.strips0 = p.strips0;
+                h.b_static = p.b_static;
+                h.pre_stages = p.pre_stages;
+                h.l2_prefetch = p.l2_prefetch;
+                if (t) {
+                    h.l2_prefetch = 8;
+                    if (const char* e = std::getenv("VTC_CHAIN_L2PF")) h.l2_prefetch = std::atoi(e);
+                }
+                C->ca.st[t] = h;
+                std::memcpy(C->ca.tmap[t], p.tmap, sizeof(p.tmap));
+                const int ns = p.strips0 + (p.nmat > 1 ? int((p.n_mat[1] + GEMV_STREAM_COLS - 1) / GEMV_STREAM_COLS) : 0);
+                max_strips = std::max(max_strips, ns);
+                if (t) {
+                    li.node += "|" + infos_[i + t].node;
+                    li.bytes += infos_[i + t].bytes;
+                }
+            }
+            C->node = li.node;
+            C->ps = run;
+            C->ca.nst = int32_t(run.size());
+            C->ca.ring = gemv_chain_smem(sA, 3) + sizeof(GemvParams) + 12 * 1024 <= 227 * 1024 ? 3 : 2;
+            C->ca.max_strips = max_strips;
+            C->ca.sA_floats = sA;
+            C->ca.sync = static_cast<unsigned*>(impl_->alloc(size_t(2 + run.size() * max_strips) * 4, true));
+            merged.push_back(std::move(C));
+            minfos.push_back(li);
+            i = j;
         }
         impl_->launches = std::move(merged);
         infos_ = std::move(minfos);

@@ -40,10 +40,6 @@ constexpr int CONSUMERS = 8, NT = (CONSUMERS + 1) * 32, COLS = GEMV_STREAM_COLS,
 constexpr uint32_t TILE_BYTES = KT * COLS * sizeof(bf16);
 static_assert(KT == 64, "a_col_to_k assumes 64-row k-tiles");
 
-struct Tmaps {
-    CUtensorMap m[GEMV_MAX_MATS];
-};
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -85,26 +81,21 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t 
 __device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32) : "memory"); }
 
 template <int MT>
-__global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __restrict__ pp, const __grid_constant__ Tmaps tm) {
+__global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __restrict__ pp,
+                                                             const __grid_constant__ GemvChainArgs ca) {
     VTC_STAGE_PARAMS(GemvParams, pp);
     extern __shared__ __align__(1024) unsigned char smem[];
-    const int stages = p.stages;
+    const int stages = ca.ring;
     bf16* ring = reinterpret_cast<bf16*>(smem);
-    float* sA = reinterpret_cast<float*>(smem + size_t(stages) * TILE_BYTES);  // [M][a_tiles*KT]
-    float* red = sA + size_t(p.M) * p.a_tiles * KT;                              // [CONSUMERS][COLS]
+    float* sA = reinterpret_cast<float*>(smem + size_t(stages) * TILE_BYTES);  // [M][a_tiles*KT] (max over stages)
+    float* red = sA + ca.sA_floats;                                              // [CONSUMERS][COLS]
     uint64_t* full = reinterpret_cast<uint64_t*>(red + CONSUMERS * COLS);
     uint64_t* empty = full + stages;
     __shared__ uint64_t go;  // consumers have issued their activation loads
     __shared__ float s_rs[4];
-    __shared__ unsigned s_last;
+    __shared__ unsigned s_last, s_gen;
 
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-    const int M = int(p.M);
-    const int64_t ktiles = (p.K + KT - 1) / KT;
-    const int64_t strips1 = p.nmat > 1 ? (p.n_mat[1] + COLS - 1) / COLS : 0;
-    const int64_t units = (int64_t(p.strips0) + strips1) * ktiles;
-    const int64_t u_begin = units * blockIdx.x / gridDim.x;
-    const int64_t u_end = units * (blockIdx.x + 1) / gridDim.x;
 
     if (tid == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -120,57 +111,149 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
     if (warp == CONSUMERS) {
         // ---------------- producer ----------------
         if (lane != 0) return;
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.m[0])) : "memory");
         const uint64_t policy = dev::evict_first_policy();
-        if (p.b_static) {
-            // the weights do not depend on earlier launches: pull this CTA's
-            // first tiles into L2 while the previous (often latency-bound)
-            // launch is still running, so HBM is busy during its tail
-            const int64_t pf_end = u_begin + p.l2_prefetch < u_end ? u_begin + p.l2_prefetch : u_end;
+        int stage = 0;
+        uint32_t phase = 0;
+        // one continuous ring over every chained stage: weights are static, so
+        // the next stage's first tiles stream while this CTA still waits for
+        // the previous stage's outputs
+        for (int cs = 0; cs < ca.nst; ++cs) {
+            const GemvChainStage& h = ca.st[cs];
+            const CUtensorMap* tmc = reinterpret_cast<const CUtensorMap*>(ca.tmap[cs][0]);
+            for (int mt = 0; mt < h.nmat; ++mt)
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmc[mt])) : "memory");
+            const int64_t ktiles = (h.K + KT - 1) / KT;
+            const int64_t strips1 = h.nmat > 1 ? (h.n1 + COLS - 1) / COLS : 0;
+            const int64_t units = (int64_t(h.strips0) + strips1) * ktiles;
+            const int64_t u_begin = units * blockIdx.x / gridDim.x;
+            const int64_t u_end = units * (blockIdx.x + 1) / gridDim.x;
+            int64_t u_pre = INT64_MAX;
+            if (cs == 0) {
+                if (h.b_static) {
+                    // the weights do not depend on earlier launches: pull this CTA's
+                    // first tiles into L2 while the previous launch is still running
+                    const int64_t pf_end = u_begin + h.l2_prefetch < u_end ? u_begin + h.l2_prefetch : u_end;
+                    int64_t strip = u_begin / ktiles, kt = u_begin % ktiles;
+                    for (int64_t u = u_begin; u < pf_end; ++u) {
+                        if (u != u_begin && ++kt == ktiles) {
+                            kt = 0;
+                            ++strip;
+                        }
+                        const int mat = strip < h.strips0 ? 0 : 1;
+                        const int64_t n0 = (strip - (mat ? h.strips0 : 0)) * COLS;
+                        if (u >= u_begin + h.pre_stages) tma_prefetch_2d(&tmc[mat], int32_t(n0), int32_t(kt * KT));
+                    }
+                } else {
+                    dev::pdl_wait();
+                }
+                // Only PRE tiles go out before the consumers have issued their
+                // activation loads: a full ring of weight requests queued ahead of
+                // them would put every activation load behind ~MBs of HBM traffic.
+                u_pre = u_begin + (h.pre_stages < stages ? h.pre_stages : stages);
+            } else if (h.l2_prefetch > 0) {
+                // chained stage: while the previous stage drains (epilogue, this
+                // stage's dependency wait and prologue), pull the tiles just past
+                // the ring into L2 so HBM stays busy across the boundary
+                const int64_t pf_beg = u_begin + stages < u_end ? u_begin + stages : u_end;
+                const int64_t pf_end = pf_beg + h.l2_prefetch < u_end ? pf_beg + h.l2_prefetch : u_end;
+                for (int64_t u = pf_beg; u < pf_end; ++u) {
+                    const int64_t strip = u / ktiles, kt = u % ktiles;
+                    const int mat = strip < h.strips0 ? 0 : 1;
+                    const int64_t n0 = (strip - (mat ? h.strips0 : 0)) * COLS;
+                    tma_prefetch_2d(&tmc[mat], int32_t(n0), int32_t(kt * KT));
+                }
+            }
             int64_t strip = u_begin / ktiles, kt = u_begin % ktiles;
-            for (int64_t u = u_begin; u < pf_end; ++u) {
+            for (int64_t u = u_begin; u < u_end; ++u) {
+                if (u == u_pre) mbar_wait(&go, 0);
                 if (u != u_begin && ++kt == ktiles) {
                     kt = 0;
                     ++strip;
                 }
-                const int mat = strip < p.strips0 ? 0 : 1;
-                const int64_t n0 = (strip - (mat ? p.strips0 : 0)) * COLS;
-                if (u >= u_begin + p.pre_stages) tma_prefetch_2d(&tm.m[mat], int32_t(n0), int32_t(kt * KT));
-            }
-        } else {
-            dev::pdl_wait();
-        }
-        int stage = 0;
-        uint32_t phase = 0;
-        // Only PRE tiles go out before the consumers have issued their
-        // activation loads: a full ring of weight requests queued ahead of
-        // them would put every activation load behind ~MBs of HBM traffic.
-        const int64_t u_pre = u_begin + (p.pre_stages < stages ? p.pre_stages : stages);
-        int64_t strip = u_begin / ktiles, kt = u_begin % ktiles;
-        for (int64_t u = u_begin; u < u_end; ++u) {
-            if (u == u_pre) mbar_wait(&go, 0);
-            if (u != u_begin && ++kt == ktiles) {
-                kt = 0;
-                ++strip;
-            }
-            const int mat = strip < p.strips0 ? 0 : 1;
-            const int64_t n0 = (strip - (mat ? p.strips0 : 0)) * COLS;
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], TILE_BYTES);
-            tma_load_2d(ring + size_t(stage) * KT * COLS, &tm.m[mat], int32_t(n0), int32_t(kt * KT), &full[stage], policy);
-            if (++stage == stages) {
-                stage = 0;
-                phase ^= 1;
+                const int mat = strip < h.strips0 ? 0 : 1;
+                const int64_t n0 = (strip - (mat ? h.strips0 : 0)) * COLS;
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_expect_tx(&full[stage], TILE_BYTES);
+                tma_load_2d(ring + size_t(stage) * KT * COLS, &tmc[mat], int32_t(n0), int32_t(kt * KT), &full[stage], policy);
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
             }
         }
         return;
     }
 
-    // ---------------- consumers: A prologue (overlaps the first weight tiles) ----
-    if (tid == 0) dev::trace_point(p.head, 4);  // parameters staged, barriers ready
-    dev::pdl_wait();
-    if (tid == 0) dev::trace_point(p.head, 5);  // dependency resolved
+    // consumers: the ring position carries across chained stages
+    int stage = 0;
+    uint32_t phase = 0;
     const int ctid = tid;  // 0..255
+    for (int cs = 0; cs < ca.nst; ++cs) {
+    if (cs > 0) {
+        // next stage: its parameter block replaces the previous one (consumers only)
+        bar_consumers();
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(pp + cs);
+            uint4* dst = reinterpret_cast<uint4*>(s_params_);
+            constexpr int n = int((sizeof(GemvParams) + 15) / 16);
+            for (int i = ctid; i < n; i += CONSUMERS * 32) dst[i] = __ldg(src + i);
+        }
+        // wait until what this stage reads from earlier stages is published
+        if (ctid == 0) {
+            const GemvChainStage& h = ca.st[cs];
+            const unsigned target = s_gen + 1u;
+            auto wait_flag = [&](const unsigned* f) {
+                unsigned v;
+                long long spins = 0;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                    if (int(v - target) >= 0) break;
+                    __nanosleep(20);
+                    if (++spins > (1ll << 27)) __trap();  // a lost dependency: fail loudly, never hang
+                }
+            };
+            for (int j = 0; j < cs; ++j) {
+                if (!((h.dep_all >> j) & 1u)) continue;
+                const GemvChainStage& hj = ca.st[j];
+                const int ns = hj.strips0 + (hj.nmat > 1 ? int((hj.n1 + COLS - 1) / COLS) : 0);
+                for (int t = 0; t < ns; ++t) wait_flag(ca.sync + 2 + int64_t(j) * ca.max_strips + t);
+            }
+            if (h.dep_range) {
+                // k-tiles this CTA stages: (kt_first + i) mod ktiles, i < its unit count
+                const GemvChainStage& hp = ca.st[cs - 1];
+                const int64_t ktiles = (h.K + KT - 1) / KT;
+                const int64_t strips1 = h.nmat > 1 ? (h.n1 + COLS - 1) / COLS : 0;
+                const int64_t units = (int64_t(h.strips0) + strips1) * ktiles;
+                const int64_t u_begin = units * blockIdx.x / gridDim.x;
+                const int64_t u_end = units * (blockIdx.x + 1) / gridDim.x;
+                const int64_t nk = u_end - u_begin < ktiles ? u_end - u_begin : ktiles;
+                int last_strip = -1;
+                for (int64_t i = 0; i < nk; ++i) {
+                    const int64_t kt = (u_begin % ktiles + i) % ktiles;
+                    const int ps = int(kt * KT / COLS);  // producing strip of matrix 0
+                    if (ps == last_strip) continue;
+                    last_strip = ps;
+                    wait_flag(ca.sync + 2 + int64_t(cs - 1) * ca.max_strips + ps);
+                    if (h.dep_a2) wait_flag(ca.sync + 2 + int64_t(cs - 1) * ca.max_strips + hp.strips0 + ps);
+                }
+            }
+        }
+        bar_consumers();
+    }
+    const int M = int(p.M);
+    const int64_t ktiles = (p.K + KT - 1) / KT;
+    const int64_t strips1 = p.nmat > 1 ? (p.n_mat[1] + COLS - 1) / COLS : 0;
+    const int64_t units = (int64_t(p.strips0) + strips1) * ktiles;
+    const int64_t u_begin = units * blockIdx.x / gridDim.x;
+    const int64_t u_end = units * (blockIdx.x + 1) / gridDim.x;
+
+    // ---------------- consumers: A prologue (overlaps the first weight tiles) ----
+    if (cs == 0) {
+        if (tid == 0) dev::trace_point(p.head, 4);  // parameters staged, barriers ready
+        dev::pdl_wait();
+        if (tid == 0) dev::trace_point(p.head, 5);  // dependency resolved
+        if (ctid == 0 && ca.nst > 1) s_gen = *reinterpret_cast<volatile unsigned*>(ca.sync);
+    }
     const int64_t kt_first = u_begin % ktiles;
     const int64_t a_cols = int64_t(p.a_tiles) * KT;
     // staged column e of A -> k: k-tile (kt_first + e / 64) mod ktiles, no 64-bit
@@ -195,7 +278,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
         idx[1] = int32_t(k);
         return __bfloat162float(*dev::elem_ptr<bf16>(op.m, idx));
     };
-    bool go_sent = false;
+    bool go_sent = cs > 0;  // chained stages: the producer does not wait for `go`
     auto send_go = [&] {
         if (go_sent) return;
         go_sent = true;
@@ -205,14 +288,27 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
     constexpr int XR = 16, EV = 8;  // register budgets of the fast prologue
     for (int m = 0; m < M; ++m) {
         int64_t sa = 0, sa2 = 0, sw = 0;
-        const bf16* pa = p.a.fast_ok ? row_ptr(p.a, m, sa) : nullptr;
-        const bf16* pa2 = (p.prologue == GemvPrologue::SiLUMul && p.a2.fast_ok) ? row_ptr(p.a2, m, sa2) : nullptr;
-        const bf16* pw = nullptr;
+        const bf16 *pa = nullptr, *pa2 = nullptr, *pw = nullptr;
+        if (p.rows_ok) {
+            pa = static_cast<const bf16*>(p.arow[m]);
+            sa = p.sa[m];
+            if (p.prologue == GemvPrologue::SiLUMul) {
+                pa2 = static_cast<const bf16*>(p.a2row[m]);
+                sa2 = p.sa2[m];
+            }
+            if (p.prologue == GemvPrologue::RMSNorm) {
+                pw = static_cast<const bf16*>(p.wrow);
+                sw = p.sw;
+            }
+        } else {
+        pa = p.a.fast_ok ? row_ptr(p.a, m, sa) : nullptr;
+        pa2 = (p.prologue == GemvPrologue::SiLUMul && p.a2.fast_ok) ? row_ptr(p.a2, m, sa2) : nullptr;
         if (p.prologue == GemvPrologue::RMSNorm && p.normw.fast_ok) {
             int32_t widx[VTC_MAX_RANK] = {};
             dev::Loc l = dev::locate(p.normw.m, widx);
             sw = p.normw.fast_stride[l.piece];
             pw = dev::addr<bf16>(p.normw.m, l);
+        }
         }
         if (ctid == 0) dev::trace_point(p.head, 7);  // operand rows located
         const bool fast = pa && (p.prologue != GemvPrologue::SiLUMul || pa2) && (p.prologue != GemvPrologue::RMSNorm || pw);
@@ -419,8 +515,92 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
             for (int j = 0; j < 8; ++j) acc[m][j] = 0.f;
     };
     zero();
-    int stage = 0;
-    uint32_t phase = 0;
+    // publish a finished strip of a chained stage (its outputs are stored)
+    auto strip_done = [&](int64_t strip) {
+        if (ca.nst <= 1) return;
+        __threadfence();
+        bar_consumers();
+        if (ctid == 0) atomicAdd(ca.sync + 2 + int64_t(cs) * ca.max_strips + strip, 1u);
+    };
+    // store a finished strip: fused trees or residual epilogue, through C's map
+    auto finish_strip = [&](int64_t strip, const float (&outv)[MT]) {
+        const int mat = strip < p.strips0 ? 0 : 1;
+        const int64_t n0 = (strip - (mat ? p.strips0 : 0)) * COLS;
+        const int64_t Nl = p.n_mat[mat];
+        const int64_t n = n0 + ctid;
+        if (p.has_epi) {
+            // fused elementwise trees: the strip's bf16 outputs in shared memory,
+            // then every element either evaluates its tree or is stored plainly
+            float* sC = red;  // [M][COLS] (the warp-reduction buffer is free again)
+            for (int m = 0; m < M; ++m) sC[m * COLS + ctid] = __bfloat162float(__float2bfloat16_rn(outv[m]));
+            bar_consumers();
+            if (n < Nl)
+                for (int m = 0; m < M; ++m) {
+                    const EpiEntry& e = p.epi[int64_t(m) * Nl + n];
+                    if (e.tree < 0) {
+                        int32_t idx[VTC_MAX_RANK] = {};
+                        idx[0] = m;
+                        idx[1] = int32_t(n);
+                        *dev::elem_ptr<bf16>(p.c.m, idx) = __float2bfloat16_rn(sC[m * COLS + ctid]);
+                        continue;
+                    }
+                    const EpiTree& t = p.epi_tree[e.tree];
+                    float r[EW_MAX_IN + EW_MAX_PROG];
+#pragma unroll
+                    for (int j = 0; j < EPI_MAX_IN; ++j) {
+                        if (j >= t.nin) break;
+                        r[j] = (e.cmask >> j) & 1u ? sC[m * COLS + int(int64_t(e.in[j]) - n0)]
+                                                   : __bfloat162float(*reinterpret_cast<const bf16*>(e.in[j]));
+                    }
+                    for (int s2 = 0; s2 < t.nprog; ++s2) {
+                        const EwInstr ins = t.prog[s2];
+                        const float a = r[ins.a], b = r[ins.b];
+                        float v;
+                        switch (ins.op) {  // bf16 rounding after every op, as the unfused kernel
+                            case EwOp::Add: v = a + b; break;
+                            case EwOp::Mul: v = a * b; break;
+                            case EwOp::SiLU: v = a / (1.0f + expf(-a)); break;
+                            case EwOp::GELU: v = 0.5f * a * (1.0f + erff(a * 0.70710678f)); break;
+                            default: v = a; break;
+                        }
+                        r[ins.dst] = __bfloat162float(__float2bfloat16_rn(v));
+                    }
+                    *reinterpret_cast<bf16*>(e.out) = __float2bfloat16_rn(r[t.result]);
+                }
+            bar_consumers();  // sC is the reduction buffer of the next strip
+            strip_done(strip);
+            return;
+        }
+        const VOperand& cop = mat ? p.c2 : p.c;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            if (m >= M || n >= Nl) continue;
+            int32_t idx[VTC_MAX_RANK] = {};
+            idx[0] = m;
+            idx[1] = int32_t(n0);
+            bf16 c = __float2bfloat16_rn(outv[m]);
+            if (p.has_res) {
+                float r;
+                if (p.res.fast_ok) {
+                    dev::Loc l = dev::locate(p.res.m, idx);
+                    r = __bfloat162float(dev::addr<bf16>(p.res.m, l)[int64_t(ctid) * p.res.fast_stride[l.piece]]);
+                } else {
+                    idx[1] = int32_t(n);
+                    r = __bfloat162float(*dev::elem_ptr<bf16>(p.res.m, idx));
+                    idx[1] = int32_t(n0);
+                }
+                c = __float2bfloat16_rn(__bfloat162float(c) + r);
+            }
+            if (cop.fast_ok) {
+                dev::Loc l = dev::locate(cop.m, idx);
+                dev::addr<bf16>(cop.m, l)[int64_t(ctid) * cop.fast_stride[l.piece]] = c;
+            } else {
+                idx[1] = int32_t(n);
+                *dev::elem_ptr<bf16>(cop.m, idx) = c;
+            }
+        }
+        strip_done(strip);
+    };
     int64_t strip = u_begin / ktiles, kt = u_begin % ktiles, slot = -1;
     for (int64_t u = u_begin; u < u_end; ++u) {
         if (++slot == ktiles) slot = 0;  // slot = (kt - kt_first) mod ktiles
@@ -465,13 +645,9 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
         if (!strip_end) continue;
         if (ctid == 0 && u + 1 == u_end) dev::trace_point(p.head, 3);  // last tile consumed
 
-        // ---- this CTA's part of the strip is done: reduce warps -> partial slot ----
-        const int mat = strip < p.strips0 ? 0 : 1;
-        const int64_t n0 = (strip - (mat ? p.strips0 : 0)) * COLS;
-        const int64_t Nl = p.n_mat[mat];
-        const int first = p.strip_first[strip];
+        // ---- this CTA's part of the strip is done: reduce warps ----
         const int ncontrib = p.strip_count[strip];
-        const int cslot = int(blockIdx.x) - first;
+        const int cslot = int(blockIdx.x) - p.strip_first[strip];
         float outv[MT];
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
@@ -488,108 +664,46 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
             }
         }
         zero();
-        const int64_t n = n0 + ctid;
-        bool last = true;
         if (ncontrib > 1) {
+            // shared strip: the last contributor to arrive sums every slot in CTA order
             for (int m = 0; m < M; ++m) p.work[((strip * p.max_contrib + cslot) * M + m) * COLS + ctid] = outv[m];
             __threadfence();
             bar_consumers();
             if (ctid == 0) s_last = (atomicAdd(&p.counters[strip], 1u) == unsigned(ncontrib - 1));
             bar_consumers();
-            last = s_last != 0;
-            if (last) {
-                __threadfence();
-                for (int m = 0; m < M; ++m) {
-                    float v = 0.f;
+            if (!s_last) continue;
+            __threadfence();
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                float v = 0.f;
+                if (m < M)
                     for (int s2 = 0; s2 < ncontrib; ++s2)
                         v += __ldcg(&p.work[((strip * p.max_contrib + s2) * M + m) * COLS + ctid]);
-                    outv[m] = v;
-                }
-                if (ctid == 0) p.counters[strip] = 0u;
+                outv[m] = v;
             }
+            if (ctid == 0) p.counters[strip] = 0u;
         }
-        if (!last) continue;
-        if (p.has_epi) {
-            // fused elementwise trees: the strip's bf16 outputs in shared memory,
-            // then every element either evaluates its tree or is stored plainly
-            float* sC = red;  // [M][COLS] (the warp-reduction buffer is free again)
-            for (int m = 0; m < M; ++m) sC[m * COLS + ctid] = __bfloat162float(__float2bfloat16_rn(outv[m]));
-            bar_consumers();
-            if (n < Nl)
-                for (int m = 0; m < M; ++m) {
-                    const EpiEntry& e = p.epi[int64_t(m) * Nl + n];
-                    if (e.tree < 0) {
-                        int32_t idx[VTC_MAX_RANK] = {};
-                        idx[0] = m;
-                        idx[1] = int32_t(n);
-                        *dev::elem_ptr<bf16>(p.c.m, idx) = __float2bfloat16_rn(sC[m * COLS + ctid]);
-                        continue;
-                    }
-                    const EpiTree& t = p.epi_tree[e.tree];
-                    float r[EW_MAX_IN + EW_MAX_PROG];
-#pragma unroll
-                    for (int j = 0; j < EPI_MAX_IN; ++j) {
-                        if (j >= t.nin) break;
-                        r[j] = (e.cmask >> j) & 1u ? sC[m * COLS + int(int64_t(e.in[j]) - n0)]
-                                                   : __bfloat162float(*reinterpret_cast<const bf16*>(e.in[j]));
-                    }
-                    for (int s2 = 0; s2 < t.nprog; ++s2) {
-                        const EwInstr ins = t.prog[s2];
-                        const float a = r[ins.a], b = r[ins.b];
-                        float v;
-                        switch (ins.op) {  // bf16 rounding after every op, as the unfused kernel
-                            case EwOp::Add: v = a + b; break;
-                            case EwOp::Mul: v = a * b; break;
-                            case EwOp::SiLU: v = a / (1.0f + expf(-a)); break;
-                            case EwOp::GELU: v = 0.5f * a * (1.0f + erff(a * 0.70710678f)); break;
-                            default: v = a; break;
-                        }
-                        r[ins.dst] = __bfloat162float(__float2bfloat16_rn(v));
-                    }
-                    *reinterpret_cast<bf16*>(e.out) = __float2bfloat16_rn(r[t.result]);
-                }
-            bar_consumers();  // sC is the reduction buffer of the next strip
-            continue;
-        }
-        if (n >= Nl) continue;
-        const VOperand& cop = mat ? p.c2 : p.c;
-#pragma unroll
-        for (int m = 0; m < MT; ++m) {
-            if (m >= M) continue;
-            int32_t idx[VTC_MAX_RANK] = {};
-            idx[0] = m;
-            idx[1] = int32_t(n0);
-            bf16 c = __float2bfloat16_rn(outv[m]);
-            if (p.has_res) {
-                float r;
-                if (p.res.fast_ok) {
-                    dev::Loc l = dev::locate(p.res.m, idx);
-                    r = __bfloat162float(dev::addr<bf16>(p.res.m, l)[int64_t(ctid) * p.res.fast_stride[l.piece]]);
-                } else {
-                    idx[1] = int32_t(n);
-                    r = __bfloat162float(*dev::elem_ptr<bf16>(p.res.m, idx));
-                    idx[1] = int32_t(n0);
-                }
-                c = __float2bfloat16_rn(__bfloat162float(c) + r);
-            }
-            if (cop.fast_ok) {
-                dev::Loc l = dev::locate(cop.m, idx);
-                dev::addr<bf16>(cop.m, l)[int64_t(ctid) * cop.fast_stride[l.piece]] = c;
-            } else {
-                idx[1] = int32_t(n);
-                *dev::elem_ptr<bf16>(cop.m, idx) = c;
+        finish_strip(strip, outv);
+    }
+    }  // chained stages
+    if (ca.nst > 1) {
+        // the last CTA out advances the launch generation the flags are compared against
+        bar_consumers();
+        if (ctid == 0) {
+            __threadfence();
+            if (atomicAdd(ca.sync + 1, 1u) == gridDim.x - 1) {
+                ca.sync[1] = 0u;
+                __threadfence();
+                atomicAdd(ca.sync, 1u);
             }
         }
     }
 }
 
 template <int MT>
-void launch_mt(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
-    size_t smem = gemv_stream_smem(p.M, p.a_tiles, p.stages);
+void launch_mt(const GemvChainArgs& ca, const GemvParams* dp, int grid, cudaStream_t s) {
     allow_max_smem(gemv_stream_kernel<MT>);
-    Tmaps tm;
-    std::memcpy(&tm, p.tmap, sizeof(tm));
-    launch_k(gemv_stream_kernel<MT>, dim3(p.grid), dim3(NT), smem, s, dp, tm);
+    launch_k(gemv_stream_kernel<MT>, dim3(grid), dim3(NT), gemv_chain_smem(ca.sA_floats, ca.ring), s, dp, ca);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -625,10 +739,33 @@ bool encode_weight_tmap(void* out128, const void* base, int64_t rows, int64_t co
     return r == CUDA_SUCCESS;
 }
 
+size_t gemv_chain_smem(int64_t sA_floats, int ring) {
+    return size_t(ring) * TILE_BYTES + size_t(sA_floats) * sizeof(float) + size_t(CONSUMERS) * COLS * sizeof(float) +
+           2 * size_t(ring) * sizeof(uint64_t);
+}
+
+void launch_gemv_chain(const GemvChainArgs& ca, const GemvParams* dp, int64_t M, int grid, cudaStream_t s) {
+    if (M <= 1) launch_mt<1>(ca, dp, grid, s);
+    else if (M <= 2) launch_mt<2>(ca, dp, grid, s);
+    else launch_mt<4>(ca, dp, grid, s);
+}
+
 void launch_gemv_stream(const GemvParams& p, const GemvParams* dp, cudaStream_t s) {
-    if (p.M <= 1) launch_mt<1>(p, dp, s);
-    else if (p.M <= 2) launch_mt<2>(p, dp, s);
-    else launch_mt<4>(p, dp, s);
+    GemvChainArgs ca{};
+    std::memcpy(ca.tmap[0], p.tmap, sizeof(p.tmap));
+    GemvChainStage& h = ca.st[0];
+    h.K = p.K;
+    h.n0 = p.n_mat[0];
+    h.n1 = p.nmat > 1 ? p.n_mat[1] : 0;
+    h.nmat = p.nmat;
+    h.strips0 = p.strips0;
+    h.b_static = p.b_static;
+    h.pre_stages = p.pre_stages;
+    h.l2_prefetch = p.l2_prefetch;
+    ca.nst = 1;
+    ca.ring = p.stages;
+    ca.sA_floats = p.M * int64_t(p.a_tiles) * KT;
+    launch_gemv_chain(ca, dp, p.M, p.grid, s);
 }
 
 }  // namespace vtc

@@ -147,6 +147,15 @@ struct GemvParams {
     const int32_t* strip_first;     // first CTA touching each 256-column strip
     const int32_t* strip_count;     // number of CTAs touching it
     VOperand c2;
+    // host-resolved row addressing of the prologue operands (rows_ok): the
+    // element pointer of A[m, 0] / A2[m, 0] / normw[0] and the stride along K,
+    // so the kernel does no map evaluation between its dependency wait and
+    // its activation loads
+    int32_t rows_ok, pad5;
+    const void* arow[4];
+    const void* a2row[4];
+    const void* wrow;
+    int64_t sa[4], sa2[4], sw;
     // fused epilogue trees (has_epi): table [M * N] of EpiEntry
     int32_t has_epi, pad4;
     const EpiEntry* epi;
@@ -155,6 +164,32 @@ struct GemvParams {
 };
 void launch_gemv(const GemvParams& p, const GemvParams* dp, cudaStream_t s);
 void launch_gemv_stream(const GemvParams& p, const GemvParams* dp, cudaStream_t s);
+
+// ---- chained streaming GEMVs: one persistent launch, device-side dependencies ----
+// Consecutive streamed GEMVs (o_proj -> gate/up -> down) run as stages of ONE
+// launch: the producer keeps streaming weights across stage boundaries (they are
+// static), and each CTA starts a stage as soon as the strips of the previous
+// stage it reads are published (per-strip flags), instead of at a grid boundary.
+constexpr int GEMV_MAX_CHAIN = 4;
+struct GemvChainStage {
+    int64_t K, n0, n1;               // reduction length; columns of matrix 0 / 1
+    int32_t nmat, strips0, b_static, pre_stages;
+    int32_t l2_prefetch;
+    int32_t dep_range;               // 1: wait only for the previous stage's strips this CTA's k-range reads
+    int32_t dep_a2;                  //    ... also the matching strips of its second matrix (SiLU*Mul a2)
+    uint32_t dep_all;                // bitmask of earlier stages to wait for completely
+};
+struct GemvChainArgs {
+    alignas(64) unsigned char tmap[GEMV_MAX_CHAIN][GEMV_MAX_MATS][128];
+    GemvChainStage st[GEMV_MAX_CHAIN];
+    int32_t nst, ring;               // stages; weight-ring depth
+    int32_t max_strips, pad;
+    int64_t sA_floats;               // A staging area (max over stages)
+    unsigned* sync;                  // [0] launch generation, [1] exit count, [2 + st * max_strips + strip] flags
+};
+// dp: nst consecutive GemvParams (one per stage, same M and grid)
+void launch_gemv_chain(const GemvChainArgs& ca, const GemvParams* dp, int64_t M, int grid, cudaStream_t s);
+size_t gemv_chain_smem(int64_t sA_floats, int ring);
 // dynamic shared memory of the streaming kernel; 0 if the configuration does not fit
 size_t gemv_stream_smem(int64_t M, int a_tiles, int stages);
 constexpr int GEMV_STREAM_COLS = 256, GEMV_STREAM_KT = 64;

@@ -439,3 +439,20 @@ def test_vtc_run_single_call_matches_upload_execute_download(vtc, oracle):
         assert np.array_equal(got["k_cache"][cfg["pos"]], p1.download("k_cache")[cfg["pos"]])
     with pytest.raises(vtc.api.ERRORS[15]):  # ShapeMismatchError
         p2.run({"x": xs[:1]}, ["y"])
+
+
+def test_chained_gemv_stages_match_separate_launches(vtc, oracle, monkeypatch):
+    """VTC_CHAIN=1: o_proj -> gate/up -> down as one persistent launch with
+    per-strip dependency flags gives the same bits as three launches, over
+    repeated executions (the flags are generation-counted, never reset)."""
+    from paper_2604_09558_b200 import workloads as W
+    doc = W.llama_decode_layer(B=1, L=256)
+    x = _llama_inputs(oracle, W, doc, 1, 255, 4096, 14336, 128)
+    g = vtc.parse_graph(doc)
+    want = vtc.execute(g, vtc.Plan(g, vtc.MAX_ELIMINATION), x)["y"]
+    monkeypatch.setenv("VTC_CHAIN", "1")
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert len([l for l in p.info(dry=True)["launches"] if l["node"].count("|") == 2]) == 1
+    for _ in range(3):
+        got = vtc.execute(g, p, x)["y"]
+        assert np.array_equal(got, want)

@@ -145,6 +145,23 @@ void finish_operand(VOperand& op, int fast_axis, int64_t tile, int64_t esize) {
     op.vec_ok = vok ? 1 : 0;
 }
 
+}  // namespace
+
+bool map_flat_linear(const vtc_map& m, int rank, const int32_t* shape) {
+    if (m.npieces != 1 || m.rank != rank) return false;
+    const vtc_piece& p = m.piece[0];
+    if (!p.affine) return false;
+    int64_t st = 1;
+    for (int a = rank - 1; a >= 0; --a) {
+        if (m.shape[a] != shape[a] || p.lo[a] > 0 || p.hi[a] < shape[a]) return false;
+        if (shape[a] > 1 && p.aff[a] != st) return false;
+        st *= shape[a];
+    }
+    return true;
+}
+
+namespace {
+
 // Heads sharing identical K/V addresses: the map ignores (h mod G).
 bool ignores_mod(const vtc_map& d, int axis, int G) {
     for (int pi = 0; pi < d.npieces; ++pi) {
@@ -510,6 +527,30 @@ void Executor::prepare(bool dry) {
             finish_operand(op2, rank - 1, vec, es);
             (k == 0 ? p.out : p.in[k - 1]) = op2;
         }
+        // streaming fast path: bf16, every operand a plain row-major buffer of the
+        // box, and the program one op (GELU, residual adds) or SiLU(in0) * in1
+        // (registers: inputs 0..nin-1, op s writes EW_MAX_IN + s; Add / Mul commute exactly)
+        int pat = 0;
+        if (dt == DType::BF16 && vec == 8 && !spec.copy) {
+            const EwInstr* q = p.prog;
+            if (p.nprog == 1 && p.result == q[0].dst && q[0].op != EwOp::Copy &&
+                (p.nin == 1 ? q[0].a == 0 && (q[0].op == EwOp::SiLU || q[0].op == EwOp::GELU)
+                            : p.nin == 2 && q[0].a + q[0].b == 1 && q[0].a != q[0].b &&
+                                  (q[0].op == EwOp::Add || q[0].op == EwOp::Mul)))
+                pat = 1;
+            if (p.nprog == 2 && p.nin == 2 && q[0].op == EwOp::SiLU && q[0].a == 0 && q[1].op == EwOp::Mul &&
+                p.result == q[1].dst &&
+                ((q[1].a == q[0].dst && q[1].b == 1) || (q[1].b == q[0].dst && q[1].a == 1)))
+                pat = 2;
+        }
+        bool flat = pat != 0;
+        for (int i = 0; i < rank && flat; ++i) flat = p.origin[i] == 0;
+        for (int k = 0; k <= p.nin && flat; ++k) {
+            const vtc_map& m = k == 0 ? p.out.m : p.in[k - 1].m;
+            flat = map_flat_linear(m, rank, p.shape) && (m.piece[0].base * es) % 16 == 0 && m.piece[0].ptr % 16 == 0;
+        }
+        p.flat = flat ? pat : 0;
+        if (flat) L->kernel = "eltwise_flat";
         push(std::move(L));
     };
     auto eltwise = [&](const std::string& node, const EwSpec& spec, DType dt, const Index& shape, const VMap& out) {
@@ -950,6 +991,7 @@ void Executor::prepare(bool dry) {
                 p.out = operand(map_of(n.outputs[0]), rank - 1, p.D, es);
                 if (n.kind != OpKind::Softmax) p.w = operand(map_of(n.inputs[1]), 0, p.D, es);
                 if (n.kind == OpKind::LayerNorm) p.bias = operand(map_of(n.inputs[2]), 0, p.D, es);
+                p.linear = map_flat_linear(p.x.m, rank, p.shape) && map_flat_linear(p.out.m, rank, p.shape) ? 1 : 0;
                 push(std::move(L));
                 break;
             }

@@ -391,8 +391,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             }
         }
         const int ncols = int(p.N - n0 < BN ? p.N - n0 : BN);
+        // shallow-K variants (epilogue-bound): 64 accumulator columns per TMEM
+        // round trip (4 loads, one wait); deep-K variants keep 16 per trip
+        constexpr bool kBatch = MT == 1 && STAGES <= 3;
+        float v64[kBatch ? 64 : 1];
         for (int c = 0; c < ncols; c += 16) {
             float v[16];
+            if (kBatch && p.splits == 1 && (c & 63) == 0) {
+                uint32_t r[64];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t addr = trow + uint32_t(c + 16 * q < BN ? c + 16 * q : c);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                        : "=r"(r[16 * q + 0]), "=r"(r[16 * q + 1]), "=r"(r[16 * q + 2]), "=r"(r[16 * q + 3]),
+                          "=r"(r[16 * q + 4]), "=r"(r[16 * q + 5]), "=r"(r[16 * q + 6]), "=r"(r[16 * q + 7]),
+                          "=r"(r[16 * q + 8]), "=r"(r[16 * q + 9]), "=r"(r[16 * q + 10]), "=r"(r[16 * q + 11]),
+                          "=r"(r[16 * q + 12]), "=r"(r[16 * q + 13]), "=r"(r[16 * q + 14]), "=r"(r[16 * q + 15])
+                        : "r"(addr));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 64; ++j) v64[kBatch ? j : 0] = __uint_as_float(r[j]);
+            }
             if (p.splits > 1) {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = 0.f;
@@ -413,6 +434,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                                 for (int j = 0; j < 16; ++j) v[j] += t[q][j];
                     }
                 }
+            } else if (kBatch) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = v64[kBatch ? (c & 48) + j : 0];
             } else {
                 tmem_ld16(c, v);
             }
@@ -567,15 +591,30 @@ void launch_gemm_tc(const GemmTcParams& p, const GemmTcParams* dp, cudaStream_t 
     std::memcpy(&tmaps.b, p.tmap_b, sizeof(CUtensorMap));
     const int tm = p.mt == 2 ? 2 * BM : BM;
     const int tiles = int((p.M + tm - 1) / tm) * int((p.N + p.bn - 1) / p.bn);
+    const int64_t ktiles = (p.K + BK - 1) / BK;
     dim3 grid(unsigned(tiles), unsigned(p.splits));
     if (p.mt == 2) {
         constexpr size_t sm = smem_bytes<256, 3, 2>();
         cudaFuncSetAttribute(gemm_tc_kernel<256, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         launch_k(gemm_tc_kernel<256, 3, 2>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+    } else if (p.bn == 256 && ktiles <= 2 && p.splits == 1) {
+        // shallow K (e.g. Swin's K = 96): a 2-stage ring, two CTAs per SM, so one
+        // CTA's epilogue overlaps the other's loads and MMAs
+        constexpr size_t sm = smem_bytes<256, 2, 1>();
+        cudaFuncSetAttribute(gemm_tc_kernel<256, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        launch_k(gemm_tc_kernel<256, 2, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
     } else if (p.bn == 256) {
         constexpr size_t sm = smem_bytes<256, 4, 1>();
         cudaFuncSetAttribute(gemm_tc_kernel<256, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         launch_k(gemm_tc_kernel<256, 4, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+    } else if (ktiles <= 2 && p.splits == 1) {
+        constexpr size_t sm = smem_bytes<128, 2, 1>();  // three CTAs per SM
+        cudaFuncSetAttribute(gemm_tc_kernel<128, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        launch_k(gemm_tc_kernel<128, 2, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+    } else if (ktiles <= 6 && p.splits == 1) {
+        constexpr size_t sm = smem_bytes<128, 3, 1>();  // two CTAs per SM
+        cudaFuncSetAttribute(gemm_tc_kernel<128, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        launch_k(gemm_tc_kernel<128, 3, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
     } else {
         constexpr size_t sm = smem_bytes<128, 6, 1>();
         cudaFuncSetAttribute(gemm_tc_kernel<128, 6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));

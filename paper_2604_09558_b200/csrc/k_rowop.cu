@@ -134,19 +134,50 @@ __global__ void __launch_bounds__(256) row_warp_kernel(const RowParams* __restri
             bv[j] = (b0 && k < D) ? __bfloat162float(b0[int64_t(k) * bs]) : 0.f;
         }
     }
-    for (int64_t row = int64_t(blockIdx.x) * 8 + threadIdx.x / 32; row < p.rows; row += nw) {
+    // row r -> (x row, y row, strides): flat-linear operands (host-proved) need
+    // no index arithmetic; otherwise unflatten + locate through the maps
+    auto row_at = [&](int64_t row, const bf16*& xr, bf16*& yr, int64_t& xs, int64_t& ys) {
+        if (p.linear) {
+            xr = reinterpret_cast<const bf16*>(p.x.m.piece[0].ptr) + p.x.m.piece[0].base + row * p.D;
+            yr = reinterpret_cast<bf16*>(p.out.m.piece[0].ptr) + p.out.m.piece[0].base + row * p.D;
+            xs = ys = 1;
+            return;
+        }
         int32_t idx[VTC_MAX_RANK];
         dev::unflatten(row * p.D, p.shape, p.rank, idx);
         idx[last] = 0;
         dev::Loc lx = dev::locate(p.x.m, idx), ly = dev::locate(p.out.m, idx);
-        const bf16* xr = dev::addr<bf16>(p.x.m, lx);
-        bf16* yr = dev::addr<bf16>(p.out.m, ly);
-        const int64_t xs = p.x.fast_stride[lx.piece], ys = p.out.fast_stride[ly.piece];
-        float v[J];
+        xr = dev::addr<bf16>(p.x.m, lx);
+        yr = dev::addr<bf16>(p.out.m, ly);
+        xs = p.x.fast_stride[lx.piece];
+        ys = p.out.fast_stride[ly.piece];
+    };
+    auto load_row = [&](const bf16* xr, int64_t xs, float (&v)[J]) {
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const int k = lane + 32 * j;
             v[j] = k < D ? __bfloat162float(xr[int64_t(k) * xs]) : 0.f;
+        }
+    };
+    // the next row's loads are issued before this row's reductions
+    int64_t row = int64_t(blockIdx.x) * 8 + threadIdx.x / 32;
+    const bf16* nxr = nullptr;
+    bf16* nyr = nullptr;
+    int64_t nxs = 0, nys = 0;
+    float nv[J];
+    if (row < p.rows) {
+        row_at(row, nxr, nyr, nxs, nys);
+        load_row(nxr, nxs, nv);
+    }
+    for (; row < p.rows; row += nw) {
+        bf16* yr = nyr;
+        const int64_t ys = nys;
+        float v[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) v[j] = nv[j];
+        if (row + nw < p.rows) {
+            row_at(row + nw, nxr, nyr, nxs, nys);
+            load_row(nxr, nxs, nv);
         }
         if (p.op == RowOp::Softmax) {
             float mx = -INFINITY;

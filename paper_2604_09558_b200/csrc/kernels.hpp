@@ -67,9 +67,12 @@ struct EwParams {
     KDType dt;
     int32_t esize;
     int32_t copy_only;             // pure data movement: dtype-agnostic by element size
-    int32_t pad;
+    int32_t flat;                  // host-proved plain operands: 1 one-op program, 2 SiLU(in0) * in1
 };
 void launch_eltwise(const EwParams& p, const EwParams* dp, cudaStream_t s);
+// Host check: the map addresses element I of an iteration box of `shape` (origin 0)
+// at piece[0].ptr + piece[0].base + flat(I) (one affine piece, row-major, unit stride).
+bool map_flat_linear(const vtc_map& m, int rank, const int32_t* shape);
 // Two independent elementwise programs of the same element type in one launch
 // (horizontal fusion of small launches, e.g. the Q and K RoPE trees).
 struct EwPair {
@@ -242,7 +245,7 @@ struct RowParams {
     float eps;
     RowOp op;
     KDType dt;
-    int32_t pad;
+    int32_t linear;  // host-proved: x and out are flat-linear (row r at base + r * D)
 };
 void launch_rowop(const RowParams& p, const RowParams* dp, cudaStream_t s);
 

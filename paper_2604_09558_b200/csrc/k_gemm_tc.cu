@@ -391,56 +391,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             }
         }
         const int ncols = int(p.N - n0 < BN ? p.N - n0 : BN);
-        // shallow-K variants (epilogue-bound): 64 accumulator columns per TMEM
-        // round trip (4 loads, one wait); deep-K variants keep 16 per trip
-        constexpr bool kBatch = MT == 1 && STAGES <= 3;
-        float v64[kBatch ? 64 : 1];
-        for (int c = 0; c < ncols; c += 16) {
-            float v[16];
-            if (kBatch && p.splits == 1 && (c & 63) == 0) {
-                uint32_t r[64];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t addr = trow + uint32_t(c + 16 * q < BN ? c + 16 * q : c);
-                    asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                        : "=r"(r[16 * q + 0]), "=r"(r[16 * q + 1]), "=r"(r[16 * q + 2]), "=r"(r[16 * q + 3]),
-                          "=r"(r[16 * q + 4]), "=r"(r[16 * q + 5]), "=r"(r[16 * q + 6]), "=r"(r[16 * q + 7]),
-                          "=r"(r[16 * q + 8]), "=r"(r[16 * q + 9]), "=r"(r[16 * q + 10]), "=r"(r[16 * q + 11]),
-                          "=r"(r[16 * q + 12]), "=r"(r[16 * q + 13]), "=r"(r[16 * q + 14]), "=r"(r[16 * q + 15])
-                        : "r"(addr));
-                }
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                for (int j = 0; j < 64; ++j) v64[kBatch ? j : 0] = __uint_as_float(r[j]);
-            }
-            if (p.splits > 1) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = 0.f;
-                if (live) {
-                    // up to 4 splits' 16 columns in flight per round trip, summed in split order
-                    for (int s0 = 0; s0 < p.splits; s0 += 4) {
-                        float t[4][16];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const float* src = wtile + int64_t(s0 + q) * BM * BN + int64_t(c) * BM + row;
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) t[q][j] = s0 + q < p.splits ? __ldcg(src + int64_t(j) * BM) : 0.f;
-                        }
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            if (s0 + q < p.splits)
-#pragma unroll
-                                for (int j = 0; j < 16; ++j) v[j] += t[q][j];
-                    }
-                }
-            } else if (kBatch) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = v64[kBatch ? (c & 48) + j : 0];
-            } else {
-                tmem_ld16(c, v);
-            }
-            if (!live) continue;
+        // 16 finished columns c..c+15 of this row: round, residual, store through C's map
+        auto emit = [&](int c, const float (&v)[16]) {
             bf16 o[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -456,6 +408,65 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
                     if (c + j < ncols) dst[int64_t(j) * cs] = o[j];
+            }
+        };
+        // shallow-K variants (epilogue-bound): 64 accumulator columns per TMEM
+        // round trip (4 loads, one wait), indices static so they stay in registers
+        constexpr bool kBatch = MT == 1 && STAGES <= 3;
+        if (kBatch && p.splits == 1) {
+            for (int c0 = 0; c0 < ncols; c0 += 64) {
+                uint32_t r[64];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t addr = trow + uint32_t(c0 + 16 * q < BN ? c0 + 16 * q : c0);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                        : "=r"(r[16 * q + 0]), "=r"(r[16 * q + 1]), "=r"(r[16 * q + 2]), "=r"(r[16 * q + 3]),
+                          "=r"(r[16 * q + 4]), "=r"(r[16 * q + 5]), "=r"(r[16 * q + 6]), "=r"(r[16 * q + 7]),
+                          "=r"(r[16 * q + 8]), "=r"(r[16 * q + 9]), "=r"(r[16 * q + 10]), "=r"(r[16 * q + 11]),
+                          "=r"(r[16 * q + 12]), "=r"(r[16 * q + 13]), "=r"(r[16 * q + 14]), "=r"(r[16 * q + 15])
+                        : "r"(addr));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (!live) continue;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (c0 + 16 * q >= ncols) break;
+                    float v[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[16 * q + j]);
+                    emit(c0 + 16 * q, v);
+                }
+            }
+        } else {
+            for (int c = 0; c < ncols; c += 16) {
+                float v[16];
+                if (p.splits > 1) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = 0.f;
+                    if (live) {
+                        // up to 4 splits' 16 columns in flight per round trip, summed in split order
+                        for (int s0 = 0; s0 < p.splits; s0 += 4) {
+                            float t[4][16];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float* src = wtile + int64_t(s0 + q) * BM * BN + int64_t(c) * BM + row;
+#pragma unroll
+                                for (int j = 0; j < 16; ++j)
+                                    t[q][j] = s0 + q < p.splits ? __ldcg(src + int64_t(j) * BM) : 0.f;
+                            }
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                if (s0 + q < p.splits)
+#pragma unroll
+                                    for (int j = 0; j < 16; ++j) v[j] += t[q][j];
+                        }
+                    }
+                } else {
+                    tmem_ld16(c, v);
+                }
+                if (!live) continue;
+                emit(c, v);
             }
         }
     }

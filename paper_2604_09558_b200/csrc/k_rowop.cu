@@ -221,10 +221,242 @@ __global__ void __launch_bounds__(256) row_warp_kernel(const RowParams* __restri
     }
 }
 
+// Plain row-major bf16 rows of D = 32 U (p.linear; RMSNorm / LayerNorm):
+// four lanes per row, eight rows per warp, 16-byte loads and stores (chunk
+// q + 4 u of 8 elements per lane), reductions over the four lanes.
+template <int U>
+__global__ void __launch_bounds__(256) row_vec_kernel(const RowParams* __restrict__ pp) {
+    VTC_STAGE_PARAMS(RowParams, pp);
+    dev::pdl_wait();
+    dev::pdl_launch_dependents();
+    const int lane = threadIdx.x % 32, q = lane % 4;
+    const int D = 32 * U;
+    const bool ln = p.op == RowOp::LayerNorm;
+    auto unpack = [](const uint4& u, float (&f)[8]) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const float2 v = __bfloat1622float2(h[t]);
+            f[2 * t] = v.x;
+            f[2 * t + 1] = v.y;
+        }
+    };
+    // weight / bias of the row in shared memory (fp32), read back per chunk
+    __shared__ __align__(16) float sw[128], sb[128];
+    {
+        int32_t z[VTC_MAX_RANK] = {};
+        dev::Loc lw = dev::locate(p.w.m, z);
+        const bf16* w0 = dev::addr<bf16>(p.w.m, lw);
+        const int64_t ws = p.w.fast_stride[lw.piece];
+        const bf16* b0 = nullptr;
+        int64_t bs = 0;
+        if (ln) {
+            dev::Loc lb = dev::locate(p.bias.m, z);
+            b0 = dev::addr<bf16>(p.bias.m, lb);
+            bs = p.bias.fast_stride[lb.piece];
+        }
+        for (int k = threadIdx.x; k < D; k += blockDim.x) {
+            sw[k] = __bfloat162float(w0[int64_t(k) * ws]);
+            sb[k] = ln ? __bfloat162float(b0[int64_t(k) * bs]) : 0.f;
+        }
+        __syncthreads();
+    }
+    const bf16* xb = reinterpret_cast<const bf16*>(p.x.m.piece[0].ptr) + p.x.m.piece[0].base;
+    bf16* yb = reinterpret_cast<bf16*>(p.out.m.piece[0].ptr) + p.out.m.piece[0].base;
+    const int64_t nrw = int64_t(gridDim.x) * 64;  // rows per grid step
+    for (int64_t row = int64_t(blockIdx.x) * 64 + threadIdx.x / 4; row < p.rows; row += nrw) {
+        const uint4* xr = reinterpret_cast<const uint4*>(xb + row * D);
+        float x[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) unpack(__ldcs(xr + q + 4 * u), x[u]);
+        float mu = 0.f;
+        if (ln) {
+            float sm = 0.f;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int t = 0; t < 8; ++t) sm += x[u][t];
+            sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+            sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+            mu = sm / float(D);
+        }
+        float s2 = 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const float c = x[u][t] - mu;
+                s2 += c * c;
+            }
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+        const float r = rsqrtf(s2 / float(D) + p.eps);
+        uint4* yr = reinterpret_cast<uint4*>(yb + row * D);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float4* w4 = reinterpret_cast<const float4*>(sw + (q + 4 * u) * 8);
+            const float4* b4 = reinterpret_cast<const float4*>(sb + (q + 4 * u) * 8);
+            const float4 wa = w4[0], wb = w4[1], ba = b4[0], bb = b4[1];
+            const float w[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+            const float b[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+            uint4 o;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                float o0, o1;
+                if (ln) {
+                    o0 = ((x[u][2 * t] - mu) * r) * w[2 * t] + b[2 * t];
+                    o1 = ((x[u][2 * t + 1] - mu) * r) * w[2 * t + 1] + b[2 * t + 1];
+                } else {
+                    o0 = (x[u][2 * t] * r) * w[2 * t];
+                    o1 = (x[u][2 * t + 1] * r) * w[2 * t + 1];
+                }
+                h[t] = __floats2bfloat162_rn(o0, o1);
+            }
+            __stcs(yr + q + 4 * u, o);
+        }
+    }
+}
+
+// Long plain bf16 rows (p.linear, D = 2048 V, RMSNorm / LayerNorm): one CTA
+// per row, each thread holds V 16-byte chunks (chunk i = tid + 256 v) in
+// registers, together with the matching weight / bias chunks loaded once.
+template <int V>
+__global__ void __launch_bounds__(256) row_long_kernel(const RowParams* __restrict__ pp) {
+    VTC_STAGE_PARAMS(RowParams, pp);
+    dev::pdl_wait();
+    dev::pdl_launch_dependents();
+    const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+    const int D = int(p.D);
+    const bool ln = p.op == RowOp::LayerNorm;
+    __shared__ float s_red[2][8];
+    auto unpack = [](const uint4& u, float (&f)[8]) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const float2 v = __bfloat1622float2(h[t]);
+            f[2 * t] = v.x;
+            f[2 * t + 1] = v.y;
+        }
+    };
+    auto block_sum = [&](float v, int slot) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s_red[slot][warp] = v;
+        __syncthreads();
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += s_red[slot][w];
+        return t;
+    };
+    // weight / bias chunks of this thread (the same columns for every row)
+    uint4 wq[V], bq[V];
+    {
+        int32_t z[VTC_MAX_RANK] = {};
+        const bf16* w0 = dev::elem_ptr<bf16>(p.w.m, z);
+        const bf16* b0 = ln ? dev::elem_ptr<bf16>(p.bias.m, z) : w0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int c = tid + 256 * v;
+            wq[v] = c * 8 < D ? *reinterpret_cast<const uint4*>(w0 + c * 8) : make_uint4(0, 0, 0, 0);
+            bq[v] = (ln && c * 8 < D) ? *reinterpret_cast<const uint4*>(b0 + c * 8) : make_uint4(0, 0, 0, 0);
+        }
+    }
+    const bf16* xb = reinterpret_cast<const bf16*>(p.x.m.piece[0].ptr) + p.x.m.piece[0].base;
+    bf16* yb = reinterpret_cast<bf16*>(p.out.m.piece[0].ptr) + p.out.m.piece[0].base;
+    int parity = 0;
+    for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+        const uint4* xr = reinterpret_cast<const uint4*>(xb + row * D);
+        float x[V][8];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int c = tid + 256 * v;
+            if (c * 8 < D) unpack(__ldcs(xr + c), x[v]);
+            else
+#pragma unroll
+                for (int t = 0; t < 8; ++t) x[v][t] = 0.f;
+        }
+        float mu = 0.f;
+        if (ln) {
+            float sm = 0.f;
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+#pragma unroll
+                for (int t = 0; t < 8; ++t) sm += x[v][t];
+            mu = block_sum(sm, parity) / float(D);
+            parity ^= 1;
+        }
+        float s2 = 0.f;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const bool ok = (tid + 256 * v) * 8 < D;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const float c = ok ? x[v][t] - mu : 0.f;
+                s2 += c * c;
+            }
+        }
+        const float r = rsqrtf(block_sum(s2, parity) / float(D) + p.eps);
+        parity ^= 1;
+        uint4* yr = reinterpret_cast<uint4*>(yb + row * D);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int c = tid + 256 * v;
+            if (c * 8 >= D) continue;
+            float w[8], b[8];
+            unpack(wq[v], w);
+            unpack(bq[v], b);
+            uint4 o;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                float o0, o1;
+                if (ln) {
+                    o0 = ((x[v][2 * t] - mu) * r) * w[2 * t] + b[2 * t];
+                    o1 = ((x[v][2 * t + 1] - mu) * r) * w[2 * t + 1] + b[2 * t + 1];
+                } else {
+                    o0 = (x[v][2 * t] * r) * w[2 * t];
+                    o1 = (x[v][2 * t + 1] * r) * w[2 * t + 1];
+                }
+                h[t] = __floats2bfloat162_rn(o0, o1);
+            }
+            __stcs(yr + c, o);
+        }
+    }
+}
+
 }  // namespace
 
 void launch_rowop(const RowParams& p, const RowParams* dp, cudaStream_t s) {
     if (p.rows == 0) return;
+    const bool long_rows = p.dt == KDType::BF16 && p.linear && p.op != RowOp::Softmax && p.D % 8 == 0 &&
+                           p.D > 128 && p.D <= 8192 && p.w.vec_ok && p.w.fast_ok &&
+                           (p.op != RowOp::LayerNorm || (p.bias.vec_ok && p.bias.fast_ok)) &&
+                           p.x.m.piece[0].base % 8 == 0 && p.x.m.piece[0].ptr % 16 == 0 &&
+                           p.out.m.piece[0].base % 8 == 0 && p.out.m.piece[0].ptr % 16 == 0;
+    if (long_rows) {
+        const int grid = int(p.rows < 148 * 8 ? p.rows : 148 * 8);
+        const int64_t v = (p.D / 8 + 255) / 256;
+        if (v <= 1) launch_k(row_long_kernel<1>, dim3(grid), dim3(256), 0, s, dp);
+        else if (v <= 2) launch_k(row_long_kernel<2>, dim3(grid), dim3(256), 0, s, dp);
+        else launch_k(row_long_kernel<4>, dim3(grid), dim3(256), 0, s, dp);
+        return;
+    }
+    const bool vec_rows = p.dt == KDType::BF16 && p.linear && p.op != RowOp::Softmax && p.D % 32 == 0 && p.D <= 128 &&
+                          p.w.fast_ok && (p.op != RowOp::LayerNorm || p.bias.fast_ok) &&
+                          p.x.m.piece[0].base % 8 == 0 && p.x.m.piece[0].ptr % 16 == 0 &&
+                          p.out.m.piece[0].base % 8 == 0 && p.out.m.piece[0].ptr % 16 == 0;
+    if (vec_rows) {
+        const int64_t blocks = (p.rows + 63) / 64;
+        const int grid = int(blocks < 148 * 8 ? blocks : 148 * 8);
+        switch (p.D / 32) {
+            case 1: launch_k(row_vec_kernel<1>, dim3(grid), dim3(256), 0, s, dp); break;
+            case 2: launch_k(row_vec_kernel<2>, dim3(grid), dim3(256), 0, s, dp); break;
+            case 3: launch_k(row_vec_kernel<3>, dim3(grid), dim3(256), 0, s, dp); break;
+            default: launch_k(row_vec_kernel<4>, dim3(grid), dim3(256), 0, s, dp); break;
+        }
+        return;
+    }
     const bool warp_rows = p.dt == KDType::BF16 && p.D <= 256 && p.x.fast_ok && p.out.fast_ok &&
                            (p.op == RowOp::Softmax || p.w.fast_ok) && (p.op != RowOp::LayerNorm || p.bias.fast_ok);
     if (warp_rows) {

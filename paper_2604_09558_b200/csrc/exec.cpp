@@ -199,7 +199,9 @@ struct Executor::Impl {
     size_t out_host_bytes = 0;
     std::vector<std::pair<std::string, int64_t>> sig_in, sig_out;  // the call hexec was built for
     std::vector<size_t> out_off;
-    bool fast_all_physical = false;
+    std::vector<int> out_kind;  // 0: staged in the graph, 1: DMA after the launch, 2: virtual (download)
+    std::vector<int> in_slot;   // arena slot of a staged input, -1: DMA before the launch
+    std::vector<void*> in_dev, out_dev;
     cudaStream_t fast_stream = nullptr;
     void free_graph() {
         if (gexec) cudaGraphExecDestroy(gexec);
@@ -1645,141 +1647,141 @@ void Executor::upload(const std::string& id, const void* host, int64_t bytes, vo
 }
 
 void Executor::run_host(const std::vector<HostIn>& ins, const std::vector<HostOut>& outs, void* stream) {
+    // Small transfers (a decode step's activations) go through pinned staging and
+    // host-link copy kernels captured in the host graph -- a DMA node costs more
+    // than moving a few KB.  Large ones (prefill activations) are DMA'd straight
+    // between the caller's buffer and the root around the graph launch.
+    int64_t kLinkMax = 1 << 20;
+    if (const char* e = std::getenv("VTC_HOST_LINK_MAX")) kLinkMax = std::atoll(e);  // tests: force either path
     auto s = static_cast<cudaStream_t>(stream);
-    // steady state: same inputs / outputs as the call that built the host graph
-    // (any rebind or re-prepare drops hexec) -> copies, one graph launch, sync
     Impl& I = *impl_;
-    bool same = I.hexec && I.fast_all_physical && ins.size() == I.sig_in.size() && outs.size() == I.sig_out.size() &&
-                I.fast_stream == s;
+    bool same = I.hexec && ins.size() == I.sig_in.size() && outs.size() == I.sig_out.size() && I.fast_stream == s;
     for (size_t i = 0; same && i < ins.size(); ++i) same = ins[i].bytes == I.sig_in[i].second && ins[i].id == I.sig_in[i].first;
     for (size_t i = 0; same && i < outs.size(); ++i)
         same = outs[i].bytes == I.sig_out[i].second && outs[i].id == I.sig_out[i].first;
-    if (same) {
-        for (size_t i = 0; i < ins.size(); ++i)
-            if (ins[i].bytes) std::memcpy(static_cast<char*>(arena_host_) + arena_off_[i], ins[i].ptr, size_t(ins[i].bytes));
-        ck(cudaGraphLaunch(I.hexec, s), "cudaGraphLaunch(host graph)");
-        ck(cudaStreamSynchronize(s), "sync");
-        for (size_t i = 0; i < outs.size(); ++i)
-            std::memcpy(outs[i].ptr, static_cast<char*>(I.out_host) + I.out_off[i], size_t(outs[i].bytes));
-        return;
-    }
-    I.sig_in.clear();
-    I.sig_out.clear();
-    std::string key;
-    std::vector<int> idx;
-    for (const auto& in : ins) {
-        auto it = root_index_.find(in.id);
-        if (it == root_index_.end()) throw ExecutionError("input " + in.id + " is not a physical root");
-        if (in.bytes != roots_[size_t(it->second)].bytes)
-            throw ShapeMismatchError("input " + in.id + ": byte count mismatch");
-        idx.push_back(it->second);
-        key += in.id;
-        key += '\n';
-    }
-    // (re)build the arena when the input set changed or a root was rebound since
-    bool ok = key == arena_key_ && arena_dev_;
-    for (size_t i = 0; ok && i < ins.size(); ++i)
-        ok = roots_[size_t(idx[i])].ptr == static_cast<char*>(arena_dev_) + arena_off_[i];
-    if (!ok) {
-        if (arena_dev_) ck(cudaFree(arena_dev_), "cudaFree(arena)");
-        if (arena_host_) ck(cudaFreeHost(arena_host_), "cudaFreeHost(arena)");
-        arena_dev_ = arena_host_ = nullptr;
-        arena_off_.clear();
-        int64_t total = 0;
-        for (const auto& in : ins) {
-            arena_off_.push_back(total);
-            total += (std::max<int64_t>(in.bytes, 16) + 255) / 256 * 256;
+    if (!same) {
+        I.sig_in.clear();
+        I.sig_out.clear();
+        if (I.hexec) cudaGraphExecDestroy(I.hexec);
+        I.hexec = nullptr;
+        // inputs: validate, pick the staged (small) ones, (re)build their arena
+        std::string key;
+        std::vector<int> small;
+        for (size_t i = 0; i < ins.size(); ++i) {
+            auto it = root_index_.find(ins[i].id);
+            if (it == root_index_.end()) throw ExecutionError("input " + ins[i].id + " is not a physical root");
+            if (ins[i].bytes != roots_[size_t(it->second)].bytes)
+                throw ShapeMismatchError("input " + ins[i].id + ": byte count mismatch");
+            if (ins[i].bytes <= kLinkMax) {
+                small.push_back(int(i));
+                key += ins[i].id;
+                key += '\n';
+            }
         }
-        arena_bytes_ = total;
-        if (total) {
-            ck(cudaMalloc(&arena_dev_, size_t(total)), "cudaMalloc(arena)");
-            ck(cudaHostAlloc(&arena_host_, size_t(total), cudaHostAllocMapped | cudaHostAllocPortable),
-               "cudaHostAlloc(arena)");
-            for (size_t i = 0; i < ins.size(); ++i) bind_root(ins[i].id, static_cast<char*>(arena_dev_) + arena_off_[i]);
+        bool ok = key == arena_key_ && (arena_dev_ || small.empty());
+        for (size_t j = 0; ok && j < small.size(); ++j)
+            ok = root_ptr(ins[size_t(small[j])].id) == static_cast<char*>(arena_dev_) + arena_off_[j];
+        if (!ok) {
+            if (arena_dev_) ck(cudaFree(arena_dev_), "cudaFree(arena)");
+            if (arena_host_) ck(cudaFreeHost(arena_host_), "cudaFreeHost(arena)");
+            arena_dev_ = arena_host_ = nullptr;
+            arena_off_.clear();
+            int64_t total = 0;
+            for (int i : small) {
+                arena_off_.push_back(total);
+                total += (std::max<int64_t>(ins[size_t(i)].bytes, 16) + 255) / 256 * 256;
+            }
+            arena_bytes_ = total;
+            if (total) {
+                ck(cudaMalloc(&arena_dev_, size_t(total)), "cudaMalloc(arena)");
+                ck(cudaHostAlloc(&arena_host_, size_t(total), cudaHostAllocMapped | cudaHostAllocPortable),
+                   "cudaHostAlloc(arena)");
+                for (size_t j = 0; j < small.size(); ++j)
+                    bind_root(ins[size_t(small[j])].id, static_cast<char*>(arena_dev_) + arena_off_[j]);
+            }
+            arena_key_ = key;
         }
-        arena_key_ = key;
-    }
-    for (size_t i = 0; i < ins.size(); ++i)
-        if (ins[i].bytes) std::memcpy(static_cast<char*>(arena_host_) + arena_off_[i], ins[i].ptr, size_t(ins[i].bytes));
-    // physical outputs come back inside the graph (into pinned staging); virtual
-    // ones are materialised through their maps afterwards
-    std::vector<size_t> out_off(outs.size(), SIZE_MAX);
-    size_t out_total = 0;
-    std::string hkey = key + "|";
-    for (size_t i = 0; i < outs.size(); ++i) {
-        const HostOut& o = outs[i];
-        if (o.bytes != g_.tensor(o.id).bytes()) throw ShapeMismatchError("output " + o.id + ": byte count mismatch");
-        if (root_index_.count(o.id) && ptg_.map_of(o.id).is_identity_of(o.id)) {
-            out_off[i] = out_total;
-            out_total += (size_t(o.bytes) + 255) / 256 * 256;
-            hkey += o.id;
-            hkey += '\n';
+        I.in_slot.assign(ins.size(), -1);
+        for (size_t j = 0; j < small.size(); ++j) I.in_slot[size_t(small[j])] = int(j);
+        // outputs: small physical -> staged in the graph; large physical -> DMA; virtual -> download
+        I.out_off.assign(outs.size(), SIZE_MAX);
+        I.out_kind.assign(outs.size(), 2);
+        size_t out_total = 0;
+        for (size_t i = 0; i < outs.size(); ++i) {
+            const HostOut& o = outs[i];
+            if (o.bytes != g_.tensor(o.id).bytes()) throw ShapeMismatchError("output " + o.id + ": byte count mismatch");
+            if (root_index_.count(o.id) && ptg_.map_of(o.id).is_identity_of(o.id)) {
+                const bool link = o.bytes <= kLinkMax && o.bytes % 16 == 0;
+                I.out_kind[i] = link ? 0 : 1;
+                if (link) {
+                    I.out_off[i] = out_total;
+                    out_total += (size_t(o.bytes) + 255) / 256 * 256;
+                }
+            }
         }
-    }
-    if (!prepared_) prepare();
-    if (!impl_->hexec || impl_->hkey != hkey) {
-        if (impl_->hexec) cudaGraphExecDestroy(impl_->hexec);
-        impl_->hexec = nullptr;
-        if (out_total > impl_->out_host_bytes) {
-            if (impl_->out_host) ck(cudaFreeHost(impl_->out_host), "cudaFreeHost(out)");
-            impl_->out_host = nullptr;
-            ck(cudaHostAlloc(&impl_->out_host, out_total, cudaHostAllocMapped | cudaHostAllocPortable),
-               "cudaHostAlloc(out)");
-            impl_->out_host_bytes = out_total;
+        if (!prepared_) prepare();
+        if (out_total > I.out_host_bytes) {
+            if (I.out_host) ck(cudaFreeHost(I.out_host), "cudaFreeHost(out)");
+            I.out_host = nullptr;
+            ck(cudaHostAlloc(&I.out_host, out_total, cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc(out)");
+            I.out_host_bytes = out_total;
         }
         std::vector<void*> out_dev(outs.size(), nullptr);
         for (size_t i = 0; i < outs.size(); ++i)
-            if (out_off[i] != SIZE_MAX) out_dev[i] = root_ptr(outs[i].id);
+            if (I.out_kind[i] != 2) out_dev[i] = root_ptr(outs[i].id);
         void *arena_host_dev = nullptr, *out_host_dev = nullptr;  // device views of the pinned buffers
         if (arena_host_) ck(cudaHostGetDevicePointer(&arena_host_dev, arena_host_, 0), "cudaHostGetDevicePointer");
-        if (impl_->out_host) ck(cudaHostGetDevicePointer(&out_host_dev, impl_->out_host, 0), "cudaHostGetDevicePointer");
+        if (I.out_host) ck(cudaHostGetDevicePointer(&out_host_dev, I.out_host, 0), "cudaHostGetDevicePointer");
+        const bool dma = std::getenv("VTC_HOST_DMA") != nullptr;  // A/B: DMA nodes for the small copies too
         cudaStream_t cap;
         cudaGraph_t hg = nullptr;
         ck(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
-        // small transfers: a host-link copy kernel (pinned memory is device-addressable);
-        // large ones: DMA memcpy nodes
-        const bool dma = std::getenv("VTC_HOST_DMA") != nullptr;
-        constexpr int64_t kLinkMax = 1 << 20;
         if (arena_bytes_) {
-            if (!dma && arena_bytes_ <= kLinkMax)
-                launch_host_link_copy(arena_host_dev, arena_dev_, arena_bytes_, cap);
-            else
-                cudaMemcpyAsync(arena_dev_, arena_host_, size_t(arena_bytes_), cudaMemcpyHostToDevice, cap);
+            if (!dma) launch_host_link_copy(arena_host_dev, arena_dev_, arena_bytes_, cap);
+            else cudaMemcpyAsync(arena_dev_, arena_host_, size_t(arena_bytes_), cudaMemcpyHostToDevice, cap);
         }
-        for (auto& l : impl_->launches) l->run(cap);
+        for (auto& l : I.launches) l->run(cap);
         for (size_t i = 0; i < outs.size(); ++i) {
-            if (out_off[i] == SIZE_MAX) continue;
-            void* dst = static_cast<char*>(impl_->out_host) + out_off[i];
-            if (!dma && outs[i].bytes <= kLinkMax && outs[i].bytes % 16 == 0 &&
-                reinterpret_cast<uintptr_t>(out_dev[i]) % 16 == 0)
-                launch_host_link_copy(out_dev[i], static_cast<char*>(out_host_dev) + out_off[i], outs[i].bytes, cap);
+            if (I.out_kind[i] != 0) continue;
+            if (!dma)
+                launch_host_link_copy(out_dev[i], static_cast<char*>(out_host_dev) + I.out_off[i], outs[i].bytes, cap);
             else
-                cudaMemcpyAsync(dst, out_dev[i], size_t(outs[i].bytes), cudaMemcpyDeviceToHost, cap);
+                cudaMemcpyAsync(static_cast<char*>(I.out_host) + I.out_off[i], out_dev[i], size_t(outs[i].bytes),
+                                cudaMemcpyDeviceToHost, cap);
         }
         cudaError_t e = cudaStreamEndCapture(cap, &hg);
         cudaStreamDestroy(cap);
         ck(e, "cudaStreamEndCapture(host graph)");
-        e = cudaGraphInstantiate(&impl_->hexec, hg, 0);
+        e = cudaGraphInstantiate(&I.hexec, hg, 0);
         cudaGraphDestroy(hg);
         ck(e, "cudaGraphInstantiate(host graph)");
-        impl_->hkey = hkey;
+        I.out_dev = out_dev;
+        I.in_dev.assign(ins.size(), nullptr);
+        for (size_t i = 0; i < ins.size(); ++i)
+            if (I.in_slot[i] < 0) I.in_dev[i] = root_ptr(ins[i].id);
+        for (const auto& in : ins) I.sig_in.emplace_back(in.id, in.bytes);
+        for (const auto& o : outs) I.sig_out.emplace_back(o.id, o.bytes);
+        I.fast_stream = s;
     }
-    ck(cudaGraphLaunch(impl_->hexec, s), "cudaGraphLaunch(host graph)");
-    I.fast_all_physical = true;
-    for (size_t i = 0; i < outs.size(); ++i)
-        if (out_off[i] == SIZE_MAX) {
-            I.fast_all_physical = false;
-            download(outs[i].id, outs[i].ptr, outs[i].bytes, stream);
-        }
-    for (const auto& in : ins) I.sig_in.emplace_back(in.id, in.bytes);
-    for (const auto& o : outs) I.sig_out.emplace_back(o.id, o.bytes);
-    I.out_off = out_off;
-    I.fast_stream = s;
+    for (size_t i = 0; i < ins.size(); ++i) {
+        if (!ins[i].bytes) continue;
+        if (I.in_slot[i] >= 0)
+            std::memcpy(static_cast<char*>(arena_host_) + arena_off_[size_t(I.in_slot[i])], ins[i].ptr, size_t(ins[i].bytes));
+        else
+            ck(cudaMemcpyAsync(I.in_dev[i], ins[i].ptr, size_t(ins[i].bytes), cudaMemcpyHostToDevice, s), "H2D");
+    }
+    ck(cudaGraphLaunch(I.hexec, s), "cudaGraphLaunch(host graph)");
+    for (size_t i = 0; i < outs.size(); ++i) {
+        if (I.out_kind[i] == 1)
+            ck(cudaMemcpyAsync(outs[i].ptr, I.out_dev[i], size_t(outs[i].bytes), cudaMemcpyDeviceToHost, s), "D2H");
+        else if (I.out_kind[i] == 2)
+            download(outs[i].id, outs[i].ptr, outs[i].bytes, stream);  // virtual: materialised through its map
+    }
     ck(cudaStreamSynchronize(s), "sync");
     for (size_t i = 0; i < outs.size(); ++i)
-        if (out_off[i] != SIZE_MAX)
-            std::memcpy(outs[i].ptr, static_cast<char*>(impl_->out_host) + out_off[i], size_t(outs[i].bytes));
+        if (I.out_kind[i] == 0)
+            std::memcpy(outs[i].ptr, static_cast<char*>(I.out_host) + I.out_off[i], size_t(outs[i].bytes));
 }
 
 void Executor::download(const std::string& id, void* host, int64_t bytes, void* stream) {

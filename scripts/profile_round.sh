@@ -6,7 +6,7 @@ export BENCH_NO_CPU=1
 # ncu serialises kernels anyway; plain stream order avoids a replay failure of a
 # programmatic-dependent graph node under the profiler
 export VTC_NO_PDL=1
-for cfg in c2 c3; do
+for cfg in c2 c3 c4; do
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$cfg.csv \
      python bench.py --config $cfg --steps 2 --warmup 1 > gpurun_out/ncu_launch_$cfg.log 2>&1; echo launch_$cfg=$?
   timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \

@@ -416,11 +416,14 @@ def test_c1_full_size_digest_matches_reference(vtc, ref):
     assert format(G.fnv1a64(got["y"]), "016x") == dig
 
 
-def test_vtc_run_single_call_matches_upload_execute_download(vtc, oracle):
+@pytest.mark.parametrize("link_max", [None, "0"])
+def test_vtc_run_single_call_matches_upload_execute_download(vtc, oracle, monkeypatch, link_max):
     """vtc_run (one H2D through the input arena, graph replay, D2H, sync) gives
     the same bits as per-tensor upload + execute + download, over several steps
     with changing inputs, and across a rebind of an arena root."""
     from paper_2604_09558_b200 import workloads as W
+    if link_max is not None:  # every transfer as a DMA around the graph instead of staged link copies
+        monkeypatch.setenv("VTC_HOST_LINK_MAX", link_max)
     cfg = dict(B=2, L=64, pos=40, D=256, Hq=4, Hkv=2, hd=64, F=512)
     doc = W.llama_decode_layer(**cfg)
     g = vtc.parse_graph(doc)

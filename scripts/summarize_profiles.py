@@ -14,8 +14,10 @@ OUT = ROOT / "gpurun_out"
 PROF = ROOT / "profiles"
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r1"
 FAMILY = {"gemv_stream_kernel": "gemv_stream_bf16", "gemv_kernel": "gemv_bf16", "attn_decode_kernel": "attn_decode_tc_splitkv",
-          "combine_fast_kernel": "attn_decode_tc_splitkv", "ew_kernel": "eltwise", "row_kernel": "rowop",
-          "gemm_tc_kernel": "gemm_tc_bf16", "mm_kernel": "matmul_tiled", "attn_kernel": "attention"}
+          "combine_fast_kernel": "attn_decode_tc_splitkv", "ew_flat_kernel": "eltwise_flat", "ew_kernel": "eltwise",
+          "row_kernel": "rowop", "row_warp_kernel": "rowop", "row_vec_kernel": "rowop", "row_long_kernel": "rowop",
+          "gemm_tc_kernel": "gemm_tc_bf16", "mm_kernel": "matmul_tiled", "attn_prefill_kernel": "attn_prefill_tc",
+          "attn_kernel": "attention", "host_link_copy_kernel": "host_link_copy"}
 
 
 def family(name):
@@ -77,9 +79,14 @@ def c3_start(ls, k):  # ln1 (rowop) followed by the QKV GEMM opens a C3 step
         45 < ls[k + 1]["read_MB"] < 60
 
 
+def c4_start(ls, k):  # ln1 (rowop) followed by the QKV GEMM opens a C4 (Swin) step
+    return ls[k]["family"] == "rowop" and k + 2 < len(ls) and ls[k + 1]["family"] == "gemm_tc_bf16" and \
+        ls[k + 2]["family"] == "attn_prefill_tc"
+
+
 traffic = {}
 md = [f"# Round {TAG[1:]} ncu summaries (B200, `--clock-control none`, serialized cold-cache launches)\n"]
-for cfg, first in (("c2", c2_start), ("c3", c3_start)):
+for cfg, first in (("c2", c2_start), ("c3", c3_start), ("c4", c4_start)):
     p = OUT / f"launches_{cfg}.csv"
     if not p.exists():
         continue

@@ -165,6 +165,46 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
         }
     };
 
+    // Q first: its row loads go out ahead of the K/V prologue (which requests a
+    // large share of the KV cache at once), then the K/V cp.asyncs, then Q is
+    // written to shared memory and turned into fragments
+    uint32_t qa[D / 16][4];
+    __shared__ __align__(16) bf16 s_q[16][D];
+    if (tid < R) {
+        int32_t idx[VTC_MAX_RANK];
+#pragma unroll
+        for (int a = 0; a < VTC_MAX_RANK; ++a) idx[a] = base_idx[a];
+        idx[ax_h] = h0 + tid / Sq;
+        idx[ax_s] = tid % Sq;
+        idx[ax_d] = 0;
+        dev::Loc l = dev::locate(p.q.m, idx);
+        s_qrow[tid] = dev::addr<bf16>(p.q.m, l);
+        s_qstr[tid] = p.q.fast_stride[l.piece];
+        dev::Loc lo = dev::locate(p.o.m, idx);
+        s_orow[tid] = dev::addr<bf16>(p.o.m, lo);
+        s_ostr[tid] = p.o.fast_stride[lo.piece];
+    }
+    __syncthreads();
+    constexpr int QCH = 16 * (D / 8) / NT;  // 16-byte chunks of the 16 x D query block per thread
+    uint4 qv[QCH];
+#pragma unroll
+    for (int i = 0; i < QCH; ++i) {
+        const int c = tid + i * NT;
+        const int row = c / (D / 8), ch = c % (D / 8);
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row < R) {
+            if (s_qstr[row] == 1 && (reinterpret_cast<uintptr_t>(s_qrow[row]) & 15) == 0) {
+                v = *reinterpret_cast<const uint4*>(s_qrow[row] + ch * 8);
+            } else {
+                bf16 t[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) t[j] = s_qrow[row][int64_t(ch * 8 + j) * s_qstr[row]];
+                v = *reinterpret_cast<const uint4*>(t);
+            }
+        }
+        qv[i] = v;
+    }
+
     const int my_tiles = ntiles > warp ? (ntiles - warp + WARPS - 1) / WARPS : 0;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -172,41 +212,11 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
         cp_async_commit();
     }
 
-    // Q fragments (rows = g*Sq + sq, unscaled bf16; rows >= R are zero).  One
-    // map evaluation per query row (row base + d * stride along the head dim).
-    uint32_t qa[D / 16][4];
     {
-        if (tid < R) {
-            int32_t idx[VTC_MAX_RANK];
 #pragma unroll
-            for (int a = 0; a < VTC_MAX_RANK; ++a) idx[a] = base_idx[a];
-            idx[ax_h] = h0 + tid / Sq;
-            idx[ax_s] = tid % Sq;
-            idx[ax_d] = 0;
-            dev::Loc l = dev::locate(p.q.m, idx);
-            s_qrow[tid] = dev::addr<bf16>(p.q.m, l);
-            s_qstr[tid] = p.q.fast_stride[l.piece];
-            dev::Loc lo = dev::locate(p.o.m, idx);
-            s_orow[tid] = dev::addr<bf16>(p.o.m, lo);
-            s_ostr[tid] = p.o.fast_stride[lo.piece];
-        }
-        __syncthreads();
-        // stage the R query rows in shared memory with 16-byte loads (zero rows >= R)
-        __shared__ __align__(16) bf16 s_q[16][D];
-        for (int c = tid; c < 16 * (D / 8); c += NT) {
-            const int row = c / (D / 8), ch = c % (D / 8);
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (row < R) {
-                if (s_qstr[row] == 1 && (reinterpret_cast<uintptr_t>(s_qrow[row]) & 15) == 0) {
-                    v = *reinterpret_cast<const uint4*>(s_qrow[row] + ch * 8);
-                } else {
-                    bf16 t[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) t[j] = s_qrow[row][int64_t(ch * 8 + j) * s_qstr[row]];
-                    v = *reinterpret_cast<const uint4*>(t);
-                }
-            }
-            *reinterpret_cast<uint4*>(&s_q[row][ch * 8]) = v;
+        for (int i = 0; i < QCH; ++i) {
+            const int c = tid + i * NT;
+            *reinterpret_cast<uint4*>(&s_q[c / (D / 8)][(c % (D / 8)) * 8]) = qv[i];
         }
         __syncthreads();
         const int rA = lane / 4, rB = lane / 4 + 8, kc = (lane % 4) * 2;

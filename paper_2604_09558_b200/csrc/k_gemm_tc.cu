@@ -370,8 +370,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     }
 
     if (do_epilogue) {
+        // split-K reduction (partials from global, no TMEM): short tiles (decode M)
+        // spread each row's columns over several threads so all 128 reduce
+        int erow = row, part = 0, nparts = 1;
+        if (p.splits > 1) {
+            const int64_t rows_live = p.M - (m0 + int64_t(t) * BM);
+            const int rp = rows_live <= 32 ? 32 : rows_live <= 64 ? 64 : 128;
+            erow = int(threadIdx.x) % rp;
+            part = int(threadIdx.x) / rp;
+            nparts = 128 / rp;
+        }
+        const int64_t em = m0 + int64_t(t) * BM + erow;
         // tcgen05.ld is warp-collective: every lane loads, rows >= M only skip the stores
-        const bool live = m < p.M;
+        const bool live = em < p.M;
         bf16* crow = nullptr;
         int64_t cs = 0;
         const bf16* rrow = nullptr;
@@ -379,7 +390,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
         if (live) {
             // output row through the C map (and the residual's), stepping along N with the piece stride
             int32_t idx[VTC_MAX_RANK] = {};
-            idx[0] = int32_t(m);
+            idx[0] = int32_t(em);
             idx[1] = int32_t(n0);
             dev::Loc lc = dev::locate(p.c.m, idx);
             crow = dev::addr<bf16>(p.c.m, lc);
@@ -412,7 +423,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
         };
         // shallow-K variants (epilogue-bound): 64 accumulator columns per TMEM
         // round trip (4 loads, one wait), indices static so they stay in registers
-        constexpr bool kBatch = MT == 1 && STAGES <= 3;
+        constexpr bool kBatch = MT == 1;
         if (kBatch && p.splits == 1) {
             for (int c0 = 0; c0 < ncols; c0 += 64) {
                 uint32_t r[64];
@@ -439,7 +450,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                 }
             }
         } else {
-            for (int c = 0; c < ncols; c += 16) {
+            const int cpart = (BN / nparts + 15) / 16 * 16;  // this thread's columns [c_lo, c_hi)
+            const int c_lo = part * cpart, c_hi = min(ncols, c_lo + cpart);
+            for (int c = c_lo; c < c_hi; c += 16) {
                 float v[16];
                 if (p.splits > 1) {
 #pragma unroll
@@ -450,7 +463,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                             float t[4][16];
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                const float* src = wtile + int64_t(s0 + q) * BM * BN + int64_t(c) * BM + row;
+                                const float* src = wtile + int64_t(s0 + q) * BM * BN + int64_t(c) * BM + erow;
 #pragma unroll
                                 for (int j = 0; j < 16; ++j)
                                     t[q][j] = s0 + q < p.splits ? __ldcg(src + int64_t(j) * BM) : 0.f;

@@ -77,6 +77,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // byte offset of 16-byte chunk c of row r inside a tile (XOR swizzle on the low 3 bits)
 __device__ __forceinline__ uint32_t swz(int r, int c) { return uint32_t(r * ROWB + ((c ^ (r & 7)) << 4)); }
 
+// KVA: K/V rows affine along the key axis (host-proved p.kv_affine) -- the
+// per-row map evaluation path is compiled out, which keeps the hot loop's code
+// (and its instruction-cache footprint) small.
+template <bool KVA>
 __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __restrict__ pp) {
     VTC_STAGE_PARAMS(AttnParams, pp);
     extern __shared__ __align__(128) unsigned char smem[];
@@ -91,16 +95,18 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
     const int G = p.group, HG = p.H / G, Sq = p.Sq, R = G * Sq;  // R query rows (<= 16)
     const int r = p.rank, ax_h = r - 3, ax_s = r - 2, ax_d = r - 1;
 
-    int64_t qb = blockIdx.x;
-    const int hg = int(qb % HG);
-    qb /= HG;
+    // 32-bit index arithmetic (grid dimensions fit): no 64-bit division calls
+    const uint32_t qlead = blockIdx.x / uint32_t(HG);
+    const int hg = int(blockIdx.x - qlead * uint32_t(HG));
+    uint32_t qb = qlead;
     int32_t base_idx[VTC_MAX_RANK] = {};
     {
-        int64_t b = qb;
+        uint32_t b = qb;
         for (int a = r - 4; a >= 0; --a) {
             int32_t ext = p.q.m.shape[a];
-            base_idx[a] = int32_t(b % ext);
-            b /= ext;
+            const uint32_t nb = b / uint32_t(ext);
+            base_idx[a] = int32_t(b - nb * uint32_t(ext));
+            b = nb;
         }
     }
     const int h0 = hg * G;
@@ -113,7 +119,7 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
     // K/V row addressing: affine along the key axis (host-proved) or per-row map evaluation
     const bf16* kb0 = nullptr;
     const bf16* vb0 = nullptr;
-    if (p.kv_affine) {
+    if (KVA) {
         int32_t idx[VTC_MAX_RANK];
 #pragma unroll
         for (int a = 0; a < VTC_MAX_RANK; ++a) idx[a] = base_idx[a];
@@ -136,7 +142,7 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
     auto load_tile = [&](int j, int st) {
         const int tile = warp + j * WARPS;
         const int t0 = kbeg + tile * TK;
-        if (!p.kv_affine) {
+        if (!KVA) {
             if (lane < TK) {
                 int t = min(t0 + lane, kend - 1);
                 int32_t idx[VTC_MAX_RANK];
@@ -158,8 +164,8 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
             const int t = t0 + row;
             const bool ok = t < kend;
             const int tc = ok ? t : kbeg;
-            const bf16* ks = p.kv_affine ? kb0 + int64_t(tc) * p.k_sstride : s_krow[warp][row];
-            const bf16* vs = p.kv_affine ? vb0 + int64_t(tc) * p.v_sstride : s_vrow[warp][row];
+            const bf16* ks = KVA ? kb0 + int64_t(tc) * p.k_sstride : s_krow[warp][row];
+            const bf16* vs = KVA ? vb0 + int64_t(tc) * p.v_sstride : s_vrow[warp][row];
             cp_async16(kdst + swz(row, ch), ks + ch * 8, ok, policy);
             cp_async16(vdst + swz(row, ch), vs + ch * 8, ok, policy);
         }
@@ -369,7 +375,7 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
         if (p.splits == 1) {
             s_orow[row][int64_t(d) * s_ostr[row]] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
         } else {
-            const int64_t orow = ((int64_t(blockIdx.x) / HG) * p.H + h) * Sq + sq;
+            const int64_t orow = (int64_t(qlead) * p.H + h) * Sq + sq;
             p.part_o[(orow * p.splits + split) * D + d] = acc;
             if (d == 0) {
                 p.part_ml[(orow * p.splits + split) * 2] = M;
@@ -400,7 +406,7 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
         s_target = target;
     }
     __syncthreads();
-    const int64_t orow0 = (int64_t(blockIdx.x) / HG) * p.H + h0;  // (lead, h0): rows (g, sq) follow
+    const int64_t orow0 = int64_t(qlead) * p.H + h0;  // (lead, h0): rows (g, sq) follow
     const int per = (R * D + S - 1) / S;
     for (int i = tid; i < per; i += NT) {
         const int e = split * per + i;
@@ -509,8 +515,8 @@ int64_t attn_decode_capacity() {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_decode_smem()));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attn_decode_kernel, NT, attn_decode_smem());
+    cudaFuncSetAttribute(attn_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_decode_smem()));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attn_decode_kernel<true>, NT, attn_decode_smem());
     return int64_t(sms) * per;
 }
 
@@ -518,8 +524,13 @@ void launch_attn_decode(const AttnParams& p, const AttnParams* dp, cudaStream_t 
     int64_t qblocks = int64_t(p.Bt) * (p.H / p.group);
     dim3 grid(unsigned(qblocks), unsigned(p.splits));
     size_t smem = attn_decode_smem();
-    cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    launch_k(attn_decode_kernel, grid, dim3(NT), smem, s, dp);
+    if (p.kv_affine) {
+        cudaFuncSetAttribute(attn_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        launch_k(attn_decode_kernel<true>, grid, dim3(NT), smem, s, dp);
+    } else {
+        cudaFuncSetAttribute(attn_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        launch_k(attn_decode_kernel<false>, grid, dim3(NT), smem, s, dp);
+    }
     if (p.splits > 1 && p.counters == nullptr)
         launch_k(combine_fast_kernel, dim3(unsigned(int64_t(p.Bt) * p.H * p.Sq)), dim3(NT), 0, s, dp);
 }

@@ -523,7 +523,9 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
         if (ctid == 0) atomicAdd(ca.sync + 2 + int64_t(cs) * ca.max_strips + strip, 1u);
     };
     // store a finished strip: fused trees or residual epilogue, through C's map
-    auto finish_strip = [&](int64_t strip, const float (&outv)[MT]) {
+    // pe0 / pin0: row 0's epilogue entry and its external inputs, loaded before the
+    // split-K exchange so the tail has no dependent table / input round trips
+    auto finish_strip = [&](int64_t strip, const float (&outv)[MT], const EpiEntry* pe0, const float* pin0) {
         const int mat = strip < p.strips0 ? 0 : 1;
         const int64_t n0 = (strip - (mat ? p.strips0 : 0)) * COLS;
         const int64_t Nl = p.n_mat[mat];
@@ -536,7 +538,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
             bar_consumers();
             if (n < Nl)
                 for (int m = 0; m < M; ++m) {
-                    const EpiEntry& e = p.epi[int64_t(m) * Nl + n];
+                    const EpiEntry& e = (m == 0 && pe0) ? *pe0 : p.epi[int64_t(m) * Nl + n];
                     if (e.tree < 0) {
                         int32_t idx[VTC_MAX_RANK] = {};
                         idx[0] = m;
@@ -550,7 +552,8 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
                     for (int j = 0; j < EPI_MAX_IN; ++j) {
                         if (j >= t.nin) break;
                         r[j] = (e.cmask >> j) & 1u ? sC[m * COLS + int(int64_t(e.in[j]) - n0)]
-                                                   : __bfloat162float(*reinterpret_cast<const bf16*>(e.in[j]));
+                               : (m == 0 && pe0) ? pin0[j]
+                                                 : __bfloat162float(*reinterpret_cast<const bf16*>(e.in[j]));
                     }
                     for (int s2 = 0; s2 < t.nprog; ++s2) {
                         const EwInstr ins = t.prog[s2];
@@ -664,6 +667,25 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
             }
         }
         zero();
+        EpiEntry pe0;
+        float pin0[EPI_MAX_IN];
+        bool have0 = false;
+        if (p.has_epi) {
+            const int mat = strip < p.strips0 ? 0 : 1;
+            const int64_t n = (strip - (mat ? p.strips0 : 0)) * COLS + ctid;
+            if (n < p.n_mat[mat]) {
+                pe0 = p.epi[n];
+                if (pe0.tree >= 0) {
+                    const EpiTree& t = p.epi_tree[pe0.tree];
+#pragma unroll
+                    for (int j = 0; j < EPI_MAX_IN; ++j)
+                        pin0[j] = (j < t.nin && !((pe0.cmask >> j) & 1u))
+                                      ? __bfloat162float(*reinterpret_cast<const bf16*>(pe0.in[j]))
+                                      : 0.f;
+                }
+                have0 = true;
+            }
+        }
         if (ncontrib > 1) {
             // shared strip: the last contributor to arrive sums every slot in CTA order
             for (int m = 0; m < M; ++m) p.work[((strip * p.max_contrib + cslot) * M + m) * COLS + ctid] = outv[m];
@@ -683,7 +705,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
             }
             if (ctid == 0) p.counters[strip] = 0u;
         }
-        finish_strip(strip, outv);
+        finish_strip(strip, outv, have0 ? &pe0 : nullptr, pin0);
     }
     }  // chained stages
     if (ca.nst > 1) {

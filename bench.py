@@ -337,6 +337,8 @@ def run_vtc(args):
                 a, z = row[0], row[1]
                 if l["kernel"].startswith("gemm_tc") and row[4]:
                     cps = f"avg mainloop {row[2] / row[4] / 1e3:.2f} us, avg epilogue {row[3] / row[4] / 1e3:.2f} us over {row[4]} CTAs"
+                    if row[5] or row[6]:
+                        cps += f"; gather: rows located {row[5] / row[4] / 1e3:.2f} us, k-tiles {row[6] / row[4] / 1e3:.2f} us"
                 else:
                     cps = " ".join(f"cp{k}={(row[k] - t0) / 1e3:.1f}" for k in range(2, 8) if row[k])
                 print(f"  {l['kernel']:<22} {(a - t0) / 1e3:8.1f} -> {(z - t0) / 1e3:8.1f}  ({(z - a) / 1e3:6.1f} us)  "

@@ -181,15 +181,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             const int64_t m = m0 + r;
             const bf16* rp = nullptr;
             if (m < p.M) {
-                int32_t idx[VTC_MAX_RANK] = {};
-                idx[0] = int32_t(m);
-                rp = dev::elem_ptr<bf16>(p.a.m, idx);
+                if (p.a_rows) {
+                    rp = reinterpret_cast<const bf16*>(p.a_rows[m]);
+                } else {
+                    int32_t idx[VTC_MAX_RANK] = {};
+                    idx[0] = int32_t(m);
+                    rp = dev::elem_ptr<bf16>(p.a.m, idx);
+                }
             }
             s_arow[r] = rp;
         }
         const uint64_t pol_b = tiles_m == 1 ? dev::evict_first_policy() : evict_last_policy();
+        if (lane == 0) dev::trace_add(p.head, 5, dev::gtime() - t_start);  // sum over CTAs: rows located
         dev::pdl_wait();
         __syncwarp();
+        const unsigned long long t_rows = dev::gtime();
         for (int i = 0; i < nk; ++i) {
             const int s = i % STAGES;
             const uint32_t ph = uint32_t(i / STAGES) & 1u;
@@ -216,11 +222,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                              "l"(src), "r"(ok ? 16 : 0)
                              : "memory");
             }
-            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-            // generic-proxy smem writes must be visible to the tensor core's async proxy
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            if (i > 0) {
+                // k-tile i-1 has landed (one group stays in flight: consecutive k-tiles' gathers overlap)
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+                // generic-proxy smem writes must be visible to the tensor core's async proxy
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[(i - 1) % STAGES])) : "memory");
+            }
         }
+        if (nk > 0) {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[(nk - 1) % STAGES])) : "memory");
+        }
+        if (lane == 0) dev::trace_add(p.head, 6, dev::gtime() - t_rows);  // sum over CTAs: gathers issued + landed
     } else if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.a)) : "memory");

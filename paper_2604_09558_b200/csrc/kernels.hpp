@@ -216,6 +216,7 @@ struct GemmTcParams {
     int32_t has_res, pad;
     float* work;          // [tiles, splits, 128, bn] fp32 partials (splits > 1)
     unsigned int* counters;
+    const uint64_t* a_rows;  // gather path: host-resolved address of A[m, 0] per row (null: locate on device)
     // A's TMA tensor: up to 5 dimensions, one per digit of A's map
     // ((idx[axis] / div) mod mod, axis 0 = M, 1 = K); coordinates of a tile at
     // (m0, k0) are computed per dimension by the producer

@@ -184,10 +184,13 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
         // S[16 x 64]: 8 n-tiles of 8 keys
         float sc[TK / 8][4];
 #pragma unroll
-        for (int nt = 0; nt < TK / 8; ++nt) {
-            sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+        for (int nt = 0; nt < TK / 8; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+        // k-step outer, key tile inner: the 8 accumulators of a k-step are
+        // independent, so consecutive MMAs never wait on each other
 #pragma unroll
-            for (int kp = 0; kp < D / 32; ++kp) {
+        for (int kp = 0; kp < D / 32; ++kp) {
+#pragma unroll
+            for (int nt = 0; nt < TK / 8; ++nt) {
                 const int mi = lane / 8, rr = lane % 8;
                 uint32_t b0, b1, b2, b3;
                 ldsm_x4(kt + swz<D>(nt * 8 + rr, kp * 4 + mi), b0, b1, b2, b3);

@@ -162,6 +162,22 @@ bool map_flat_linear(const vtc_map& m, int rank, const int32_t* shape) {
 
 namespace {
 
+// K segments of a rank-2 gather operand: the distinct piece boundaries along K
+// (axis 1), each a multiple of the 64-wide k-tile, at most GEMM_MAX_SEG segments,
+// so every k-tile of a row lies inside one piece.
+bool k_segments(const vtc_map& m, int64_t K, std::vector<int64_t>& bounds) {
+    std::set<int64_t> b{0, K};
+    for (int pi = 0; pi < m.npieces; ++pi) {
+        for (int64_t v : {int64_t(m.piece[pi].lo[1]), int64_t(m.piece[pi].hi[1])})
+            if (v > 0 && v < K) b.insert(v);
+    }
+    bounds.assign(b.begin(), b.end());
+    if (int(bounds.size()) - 1 > GEMM_MAX_SEG) return false;
+    for (int64_t v : bounds)
+        if (v != K && v % 64 != 0) return false;
+    return true;
+}
+
 // Heads sharing identical K/V addresses: the map ignores (h mod G).
 bool ignores_mod(const vtc_map& d, int axis, int G) {
     for (int pi = 0; pi < d.npieces; ++pi) {
@@ -698,11 +714,13 @@ void Executor::prepare(bool dry) {
         int64_t dims[5], strides[5];
         const void* base = nullptr;
         if (gemm_tc_a_dims(am, A.shape[0], A.shape[1], probe, dims, strides, &base)) return true;
-        // gather fallback: rows located through the map, unit stride + 16-B aligned along K
+        // gather fallback: rows located through the map, unit stride + 16-B aligned along K,
+        // and every row inside one piece (a row is gathered from its base address)
         VOperand op{};
         op.m = am;
         finish_operand(op, 1, 64, 2);
-        return op.vec_ok != 0;
+        std::vector<int64_t> segs;
+        return op.vec_ok != 0 && k_segments(am, A.shape[1], segs);
     };
     if (opt_.fuse) {
         for (const auto& n : g_.nodes()) {
@@ -1193,7 +1211,8 @@ void Executor::prepare(bool dry) {
                     if (ok && !gemm_tc_a_dims(alow, M, K, p, adims, astr, &abase)) {
                         // A through 16-byte cp.async gathers (row bases from its map)
                         p.a = operand(map_of(n.inputs[0]), 1, 64, es);
-                        ok = p.a.vec_ok != 0;
+                        std::vector<int64_t> segs;
+                        ok = p.a.vec_ok != 0 && k_segments(p.a.m, K, segs);
                         p.a_gather = 1;
                         p.a_ndims = 2;  // the (unused) A tensor map: a dummy over B
                         adims[0] = K;
@@ -1210,15 +1229,22 @@ void Executor::prepare(bool dry) {
                             // A's row addresses resolved once per plan (the map is static): a
                             // per-CTA device locate through a multi-piece div/mod map costs
                             // more than the gathers themselves (Swin: 7.8 of 11.5 us)
-                            std::vector<uint64_t> rows(static_cast<size_t>(M));
+                            const int nseg = int(segs.size()) - 1;
+                            std::vector<uint64_t> rows(static_cast<size_t>(M * nseg));
                             int64_t idx[VTC_MAX_RANK] = {};
-                            for (int64_t m = 0; m < M && ok; ++m) {
-                                idx[0] = m;
-                                int pc = -1;
-                                const int64_t off = desc_eval(p.a.m, idx, &pc);
-                                ok = pc >= 0;
-                                if (ok) rows[size_t(m)] = p.a.m.piece[pc].ptr + uint64_t(off) * 2;
+                            for (int sg = 0; sg < nseg && ok; ++sg) {
+                                idx[1] = segs[size_t(sg)];
+                                for (int64_t m = 0; m < M && ok; ++m) {
+                                    idx[0] = m;
+                                    int pc = -1;
+                                    const int64_t off = desc_eval(p.a.m, idx, &pc);
+                                    ok = pc >= 0;
+                                    // rp + k addresses A[m, k] for every k of the segment
+                                    if (ok) rows[size_t(sg * M + m)] = p.a.m.piece[pc].ptr + uint64_t(off - idx[1]) * 2;
+                                }
                             }
+                            p.a_nseg = nseg;
+                            for (int sg = 0; sg <= nseg; ++sg) p.a_seg_k[sg] = int32_t(segs[size_t(sg)]);
                             if (ok) {
                                 auto* d = static_cast<uint64_t*>(impl_->alloc(rows.size() * 8, false));
                                 ck(cudaMemcpy(d, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice), "H2D(a_rows)");

@@ -176,21 +176,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
         // A's rows are located once through its map (row base, unit stride
         // along K); every k-tile is then 1024 16-byte cp.asyncs written in the
         // 128-byte-swizzled layout TMA would produce.  B still comes by TMA.
+        // row bases of the current K segment (re-read from the table when a k-tile
+        // enters the next segment; static shared memory stays at one row table)
         __shared__ const bf16* s_arow[BM];
-        for (int r = lane; r < BM; r += 32) {
-            const int64_t m = m0 + r;
-            const bf16* rp = nullptr;
-            if (m < p.M) {
-                if (p.a_rows) {
-                    rp = reinterpret_cast<const bf16*>(p.a_rows[m]);
-                } else {
-                    int32_t idx[VTC_MAX_RANK] = {};
-                    idx[0] = int32_t(m);
-                    rp = dev::elem_ptr<bf16>(p.a.m, idx);
+        const int nseg = p.a_rows ? p.a_nseg : 1;
+        auto rows_of = [&](int sg) {
+            for (int r = lane; r < BM; r += 32) {
+                const int64_t m = m0 + r;
+                const bf16* rp = nullptr;
+                if (m < p.M) {
+                    if (p.a_rows) {
+                        rp = reinterpret_cast<const bf16*>(p.a_rows[int64_t(sg) * p.M + m]);
+                    } else {
+                        int32_t idx[VTC_MAX_RANK] = {};
+                        idx[0] = int32_t(m);
+                        rp = dev::elem_ptr<bf16>(p.a.m, idx);
+                    }
                 }
+                s_arow[r] = rp;
             }
-            s_arow[r] = rp;
-        }
+        };
+        int seg = 0;
+        while (seg + 1 < nseg && kt0 * BK >= p.a_seg_k[seg + 1]) ++seg;
+        rows_of(seg);
         const uint64_t pol_b = tiles_m == 1 ? dev::evict_first_policy() : evict_last_policy();
         if (lane == 0) dev::trace_add(p.head, 5, dev::gtime() - t_start);  // sum over CTAs: rows located
         dev::pdl_wait();
@@ -203,6 +211,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             unsigned char* sa = smem + size_t(s) * STAGE_BYTES;
             unsigned char* sb = sa + A_BYTES;
             const int32_t k0 = int32_t(kt0 + i) * BK;  // all CTAs walk K in step: weight rows stream DRAM page by page
+            if (seg + 1 < nseg && k0 >= p.a_seg_k[seg + 1]) {  // this k-tile starts the next K segment
+                // the previous tiles' gathers still read s_arow: let them land first
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+                __syncwarp();
+                while (seg + 1 < nseg && k0 >= p.a_seg_k[seg + 1]) ++seg;
+                rows_of(seg);
+                __syncwarp();
+            }
             if (lane == 0) {
                 mbar_expect_tx(&full[s], B_BYTES);
 #pragma unroll

@@ -205,6 +205,7 @@ bool encode_weight_tmap(void* out128, const void* base, int64_t rows, int64_t co
 // map (unit stride along K), B [K, N] physical row-major; C / residual through
 // their maps (affine along N per row).  K is split across `splits` CTAs per
 // tile when the tile grid alone would leave SMs idle.
+constexpr int GEMM_MAX_SEG = 4;
 struct GemmTcParams {
     KHead head;
     VOperand c, res;
@@ -216,7 +217,12 @@ struct GemmTcParams {
     int32_t has_res, pad;
     float* work;          // [tiles, splits, 128, bn] fp32 partials (splits > 1)
     unsigned int* counters;
-    const uint64_t* a_rows;  // gather path: host-resolved address of A[m, 0] per row (null: locate on device)
+    // gather path, host-resolved rows: A's K axis in a_nseg segments [a_seg_k[s], a_seg_k[s+1])
+    // (BK-aligned piece boundaries, e.g. a virtual Concat along K); a_rows[s * M + m] = address
+    // of A[m, a_seg_k[s]] minus a_seg_k[s] elements.  Null: rows located on the device.
+    const uint64_t* a_rows;
+    int32_t a_nseg, a_pad3;
+    int32_t a_seg_k[GEMM_MAX_SEG + 1];
     // A's TMA tensor: up to 5 dimensions, one per digit of A's map
     // ((idx[axis] / div) mod mod, axis 0 = M, 1 = K); coordinates of a tile at
     // (m0, k0) are computed per dimension by the producer

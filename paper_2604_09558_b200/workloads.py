@@ -312,6 +312,35 @@ def swin_block(B: int = 64, H: int = 56, C: int = 96, heads: int = 3, win: int =
     return g.doc()
 
 
+def c3k2_block(N: int = 16 * 160 * 160, c: int = 64, cin: int = 128, cout: int = 128, dtype: str = "bf16") -> dict:
+    """Paper Fig. 11 (SPEC.md acceptance 7): the YOLOv11
+    C3K2 block's data movement, channel-last with its 1x1 convolutions as
+    MatMuls over the N = B*H*W pixels:
+
+        y0 = x . W_cv1 -> Split(a, b) -> bottleneck on b: e = b + (SiLU(b . W_m1) . W_m2)
+        Y  = Concat(a, b, e) -> out = Y . W_cv2
+
+    Split and Concat are the block's two data-movement operators; under a VTC
+    plan a, b and e (and y0) become virtual tensors of Y -- cv1 and the
+    bottleneck's residual Add store straight into Y's channel ranges -- and no
+    data-movement kernel runs."""
+    g = GraphBuilder(dtype)
+    g.input("x", [N, cin])
+    g.input("w_cv1", [cin, 2 * c])
+    g.input("w_m1", [c, c])
+    g.input("w_m2", [c, c])
+    g.input("w_cv2", [3 * c, cout])
+    g.node("cv1", "MatMul", ["x", "w_cv1"], "y0")
+    g.node("split", "Split", ["y0"], ["a", "b"], {"axis": 1, "sizes": [c, c]})
+    g.node("m1", "MatMul", ["b", "w_m1"], "t1")
+    g.node("act", "SiLU", ["t1"], "t2")
+    g.node("m2", "MatMul", ["t2", "w_m2"], "t3")
+    g.node("res", "Add", ["b", "t3"], "e")
+    g.node("concat", "Concat", ["a", "b", "e"], "Y", {"axis": 1})
+    g.node("cv2", "MatMul", ["Y", "w_cv2"], "out", out_kind="output")
+    return g.doc()
+
+
 def swin_attn_bias(H: int = 56, heads: int = 3, win: int = 7, shift: int = 3, seed: int = 0):
     """Per-window additive attention bias [nw, heads, T, T]: a random relative-
     position bias table gathered by relative coordinates (as in Swin) plus the

@@ -459,3 +459,23 @@ def test_chained_gemv_stages_match_separate_launches(vtc, oracle, monkeypatch):
     for _ in range(3):
         got = vtc.execute(g, p, x)["y"]
         assert np.array_equal(got, want)
+
+
+def test_c3k2_block_strategies_bit_identical(vtc, oracle):
+    """Paper Fig. 11 on the GPU: the paper's strategy (a, b, e, y0 virtual over Y),
+    the planner's own maximal strategy and the all-physical plan give the same
+    bits; the result matches the CPU oracle."""
+    from paper_2604_09558_b200 import workloads as W
+    from test_fixtures import C3K2, paper_strategy
+    doc = W.c3k2_block(**C3K2)
+    x = oracle.random_inputs(doc, seed=5, scales={"w_cv1": 0.09, "w_m1": 0.125, "w_m2": 0.125, "w_cv2": 0.07})
+    want = oracle.execute(doc, x)["out"]
+    g = vtc.parse_graph(doc)
+    outs = {}
+    for name, plan in (("paper", vtc.Plan(g, vtc.SELECTED, paper_strategy(g))), ("max", vtc.Plan(g, vtc.MAX_ELIMINATION)),
+                       ("materialized", vtc.Plan(g, vtc.MATERIALIZE))):
+        outs[name] = vtc.execute(g, plan, x)["out"]
+    assert np.array_equal(outs["paper"], outs["materialized"])
+    assert np.array_equal(outs["max"], outs["materialized"])
+    err = _relerr(oracle.bf16_to_f32(outs["paper"]), oracle.bf16_to_f32(want))
+    assert err < 2e-2, err

@@ -561,6 +561,16 @@ void Executor::prepare(bool dry) {
                 ((q[1].a == q[0].dst && q[1].b == 1) || (q[1].b == q[0].dst && q[1].a == 1)))
                 pat = 2;
         }
+        // (in0 * in1) + (in2 * in3): the Q / K RoPE trees, without the register interpreter
+        {
+            const EwInstr* q = p.prog;
+            const int r0 = EW_MAX_IN, r1 = EW_MAX_IN + 1;
+            if (!spec.copy && p.nin == 4 && p.nprog == 3 && q[0].op == EwOp::Mul && q[0].a == 0 && q[0].b == 1 &&
+                q[0].dst == r0 && q[1].op == EwOp::Mul && q[1].a == 2 && q[1].b == 3 && q[1].dst == r1 &&
+                q[2].op == EwOp::Add && ((q[2].a == r0 && q[2].b == r1) || (q[2].a == r1 && q[2].b == r0)) &&
+                p.result == q[2].dst)
+                p.prog_pat = 3;
+        }
         bool flat = pat != 0;
         for (int i = 0; i < rank && flat; ++i) flat = p.origin[i] == 0;
         for (int k = 0; k <= p.nin && flat; ++k) {

@@ -127,7 +127,9 @@ __device__ __forceinline__ T apply_op(EwOp op, T a, T b) {
 }
 
 // pp1 != nullptr: CTAs [0, blocks0) run program pp0, the rest program pp1.
-template <typename T, int VEC>
+// PAT 3: the program (in0 * in1) + (in2 * in3) (a RoPE tree), evaluated with
+// compile-time registers; PAT 0: the general interpreter.
+template <typename T, int VEC, int PAT>
 __global__ void __launch_bounds__(256) ew_kernel(const EwParams* __restrict__ pp0, const EwParams* __restrict__ pp1,
                                                  int blocks0) {
     const bool second = pp1 != nullptr && int(blockIdx.x) >= blocks0;
@@ -148,6 +150,13 @@ __global__ void __launch_bounds__(256) ew_kernel(const EwParams* __restrict__ pp
 #pragma unroll
         for (int i = 0; i < EW_MAX_IN; ++i)
             if (i < nin) load_vec<T, VEC>(p.in[i], idx, last, in[i]);
+        if (PAT == 3) {
+            T o[VEC];
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) o[j] = add_of<T>(mul_of<T>(in[0][j], in[1][j]), mul_of<T>(in[2][j], in[3][j]));
+            store_vec<T, VEC>(p.out, idx, last, o);
+            continue;
+        }
         T r[EW_MAX_PROG + EW_MAX_IN][VEC];
 #pragma unroll
         for (int i = 0; i < EW_MAX_IN; ++i)
@@ -235,26 +244,31 @@ void launch_t(const EwParams& p, const EwParams* dp, cudaStream_t s) {
     constexpr int V = 16 / sizeof(T);
     const int grid = ew_grid(p);
     const EwParams* none = nullptr;
-    if (p.vec == V)
-        launch_k(ew_kernel<T, V>, dim3(grid), dim3(256), 0, s, dp, none, grid);
+    if (p.vec == V && p.prog_pat == 3)
+        launch_k(ew_kernel<T, V, 3>, dim3(grid), dim3(256), 0, s, dp, none, grid);
+    else if (p.vec == V)
+        launch_k(ew_kernel<T, V, 0>, dim3(grid), dim3(256), 0, s, dp, none, grid);
     else
-        launch_k(ew_kernel<T, 1>, dim3(grid), dim3(256), 0, s, dp, none, grid);
+        launch_k(ew_kernel<T, 1, 0>, dim3(grid), dim3(256), 0, s, dp, none, grid);
 }
 
 template <typename T>
 void launch_pair_t(const EwPair& p, const EwPair* dp, cudaStream_t s) {
     constexpr int V = 16 / sizeof(T);
     const int g0 = ew_grid(p.a), g1 = ew_grid(p.b);
-    if (p.a.vec == V)
-        launch_k(ew_kernel<T, V>, dim3(g0 + g1), dim3(256), 0, s, &dp->a, &dp->b, g0);
+    if (p.a.vec == V && p.a.prog_pat == 3)
+        launch_k(ew_kernel<T, V, 3>, dim3(g0 + g1), dim3(256), 0, s, &dp->a, &dp->b, g0);
+    else if (p.a.vec == V)
+        launch_k(ew_kernel<T, V, 0>, dim3(g0 + g1), dim3(256), 0, s, &dp->a, &dp->b, g0);
     else
-        launch_k(ew_kernel<T, 1>, dim3(g0 + g1), dim3(256), 0, s, &dp->a, &dp->b, g0);
+        launch_k(ew_kernel<T, 1, 0>, dim3(g0 + g1), dim3(256), 0, s, &dp->a, &dp->b, g0);
 }
 
 }  // namespace
 
 bool eltwise_pair_compatible(const EwParams& a, const EwParams& b) {
-    return a.nvec > 0 && b.nvec > 0 && !a.copy_only && !b.copy_only && a.dt == b.dt && a.vec == b.vec;
+    return a.nvec > 0 && b.nvec > 0 && !a.copy_only && !b.copy_only && a.dt == b.dt && a.vec == b.vec &&
+           a.prog_pat == b.prog_pat;
 }
 
 void launch_eltwise_pair(const EwPair& p, const EwPair* dp, cudaStream_t s) {

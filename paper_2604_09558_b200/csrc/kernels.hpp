@@ -68,6 +68,8 @@ struct EwParams {
     int32_t esize;
     int32_t copy_only;             // pure data movement: dtype-agnostic by element size
     int32_t flat;                  // host-proved plain operands: 1 one-op program, 2 SiLU(in0) * in1
+    int32_t prog_pat;              // 3: the program is (in0 * in1) + (in2 * in3) (RoPE), run without the interpreter
+    int32_t pad2;
 };
 void launch_eltwise(const EwParams& p, const EwParams* dp, cudaStream_t s);
 // Host check: the map addresses element I of an iteration box of `shape` (origin 0)

@@ -365,17 +365,22 @@ __global__ void __launch_bounds__(256) row_long_kernel(const RowParams* __restri
     const bf16* xb = reinterpret_cast<const bf16*>(p.x.m.piece[0].ptr) + p.x.m.piece[0].base;
     bf16* yb = reinterpret_cast<bf16*>(p.out.m.piece[0].ptr) + p.out.m.piece[0].base;
     int parity = 0;
-    for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+    // the next row's chunks are requested before this row's reductions
+    auto fetch = [&](int64_t row, uint4 (&q)[V]) {
         const uint4* xr = reinterpret_cast<const uint4*>(xb + row * D);
-        float x[V][8];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int c = tid + 256 * v;
-            if (c * 8 < D) unpack(__ldcs(xr + c), x[v]);
-            else
-#pragma unroll
-                for (int t = 0; t < 8; ++t) x[v][t] = 0.f;
+            q[v] = (row < p.rows && c * 8 < D) ? __ldcs(xr + c) : make_uint4(0, 0, 0, 0);
         }
+    };
+    uint4 nq[V];
+    fetch(blockIdx.x, nq);
+    for (int64_t row = blockIdx.x; row < p.rows; row += gridDim.x) {
+        float x[V][8];
+#pragma unroll
+        for (int v = 0; v < V; ++v) unpack(nq[v], x[v]);
+        fetch(row + gridDim.x, nq);
         float mu = 0.f;
         if (ln) {
             float sm = 0.f;

@@ -549,7 +549,8 @@ void Executor::prepare(bool dry) {
         // box, and the program one op (GELU, residual adds) or SiLU(in0) * in1
         // (registers: inputs 0..nin-1, op s writes EW_MAX_IN + s; Add / Mul commute exactly)
         int pat = 0;
-        if (dt == DType::BF16 && vec == 8 && !spec.copy) {
+        const bool fast_ew = !std::getenv("VTC_NO_EW_FAST");  // tests: generic interpreter everywhere
+        if (fast_ew && dt == DType::BF16 && vec == 8 && !spec.copy) {
             const EwInstr* q = p.prog;
             if (p.nprog == 1 && p.result == q[0].dst && q[0].op != EwOp::Copy &&
                 (p.nin == 1 ? q[0].a == 0 && (q[0].op == EwOp::SiLU || q[0].op == EwOp::GELU)
@@ -565,7 +566,7 @@ void Executor::prepare(bool dry) {
         {
             const EwInstr* q = p.prog;
             const int r0 = EW_MAX_IN, r1 = EW_MAX_IN + 1;
-            if (!spec.copy && p.nin == 4 && p.nprog == 3 && q[0].op == EwOp::Mul && q[0].a == 0 && q[0].b == 1 &&
+            if (fast_ew && !spec.copy && p.nin == 4 && p.nprog == 3 && q[0].op == EwOp::Mul && q[0].a == 0 && q[0].b == 1 &&
                 q[0].dst == r0 && q[1].op == EwOp::Mul && q[1].a == 2 && q[1].b == 3 && q[1].dst == r1 &&
                 q[2].op == EwOp::Add && ((q[2].a == r0 && q[2].b == r1) || (q[2].a == r1 && q[2].b == r0)) &&
                 p.result == q[2].dst)
@@ -1022,6 +1023,7 @@ void Executor::prepare(bool dry) {
                 if (n.kind != OpKind::Softmax) p.w = operand(map_of(n.inputs[1]), 0, p.D, es);
                 if (n.kind == OpKind::LayerNorm) p.bias = operand(map_of(n.inputs[2]), 0, p.D, es);
                 p.linear = map_flat_linear(p.x.m, rank, p.shape) && map_flat_linear(p.out.m, rank, p.shape) ? 1 : 0;
+                if (std::getenv("VTC_NO_ROW_FAST")) p.linear = 0;  // tests: map-evaluating row kernels
                 push(std::move(L));
                 break;
             }

@@ -479,3 +479,31 @@ def test_c3k2_block_strategies_bit_identical(vtc, oracle):
     assert np.array_equal(outs["max"], outs["materialized"])
     err = _relerr(oracle.bf16_to_f32(outs["paper"]), oracle.bf16_to_f32(want))
     assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("which", ["swin", "prefill"])
+def test_fast_paths_bit_identical_to_generic_kernels(vtc, oracle, monkeypatch, which):
+    """The plain-buffer fast paths (eltwise_flat, the RoPE-shaped eltwise program,
+    the vectorised LayerNorm / RMSNorm row kernels) give the same bits as the
+    map-evaluating generic kernels they replace."""
+    from paper_2604_09558_b200 import workloads as W
+    if which == "swin":
+        cfg = dict(B=1, H=28, C=96, heads=3, mlp=384)
+        doc = W.swin_block(**cfg)
+        x = oracle.random_inputs(doc, seed=3, scales=W.swin_weight_scales(cfg["C"], cfg["mlp"]))
+        x["attn_bias"] = oracle.f32_to_bf16(W.swin_attn_bias(H=cfg["H"], heads=cfg["heads"]))
+    else:
+        cfg = dict(B=2, S=128, D=256, Hq=4, Hkv=2, hd=128, F=512)
+        doc = W.llama_prefill_layer(**cfg)
+        x = oracle.random_inputs(doc, seed=4, scales=W.llama_weight_scales(cfg["D"], cfg["F"]))
+        cos, sin = W.rope_tables_prefill(cfg["B"], cfg["S"], hd=cfg["hd"])
+        x["cos"] = oracle.f32_to_bf16(cos.astype(np.float32))
+        x["sin"] = oracle.f32_to_bf16(sin.astype(np.float32))
+    g = vtc.parse_graph(doc)
+    fast = vtc.execute(g, vtc.Plan(g, vtc.MAX_ELIMINATION), x)["y"]
+    monkeypatch.setenv("VTC_NO_EW_FAST", "1")
+    monkeypatch.setenv("VTC_NO_ROW_FAST", "1")
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert not any(l["kernel"] == "eltwise_flat" for l in p.info(dry=True)["launches"])
+    generic = vtc.execute(g, p, x)["y"]
+    assert np.array_equal(fast, generic)

@@ -1265,6 +1265,34 @@ void Executor::prepare(bool dry) {
                         }
                     }
                     if (ok && !impl_->dry) ok = gemm_tc_encode(p, abase, adims, astr, bbase, ldb);
+                    if (ok && !impl_->dry) {
+                        // C through a non-affine map (Swin's window reverse + roll): resolve its
+                        // rows here once instead of a div/mod locate per row in every epilogue
+                        bool affine = true, one = true;
+                        for (int pi = 0; pi < p.c.m.npieces; ++pi) {
+                            affine &= p.c.m.piece[pi].affine != 0;
+                            one &= p.c.m.piece[pi].lo[1] <= 0 && p.c.m.piece[pi].hi[1] >= N &&
+                                   p.c.fast_stride[pi] == p.c.fast_stride[0];
+                        }
+                        if (!affine && one) {
+                            std::vector<uint64_t> rows(static_cast<size_t>(M));
+                            int64_t idx[VTC_MAX_RANK] = {};
+                            bool good = true;
+                            for (int64_t m = 0; m < M && good; ++m) {
+                                idx[0] = m;
+                                int pc = -1;
+                                const int64_t off = desc_eval(p.c.m, idx, &pc);
+                                good = pc >= 0;
+                                if (good) rows[size_t(m)] = p.c.m.piece[pc].ptr + uint64_t(off) * 2;
+                            }
+                            if (good) {
+                                auto* d = static_cast<uint64_t*>(impl_->alloc(rows.size() * 8, false));
+                                ck(cudaMemcpy(d, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice), "H2D(c_rows)");
+                                p.c_rows = d;
+                                p.c_rs = p.c.fast_stride[0];
+                            }
+                        }
+                    }
                     if (ok) {
                         // prefill-sized M: 256-row tiles (two M=128 MMAs per B stage)
                         p.mt = (!p.a_gather && p.bn == 256 && M >= 4096) ? 2 : 1;

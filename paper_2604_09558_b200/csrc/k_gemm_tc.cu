@@ -424,9 +424,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             int32_t idx[VTC_MAX_RANK] = {};
             idx[0] = int32_t(em);
             idx[1] = int32_t(n0);
-            dev::Loc lc = dev::locate(p.c.m, idx);
-            crow = dev::addr<bf16>(p.c.m, lc);
-            cs = p.c.fast_stride[lc.piece];
+            if (p.c_rows) {  // host-resolved row (C's map has div/mod digits, e.g. a window reverse)
+                crow = reinterpret_cast<bf16*>(p.c_rows[em]) + int64_t(n0) * p.c_rs;
+                cs = p.c_rs;
+            } else {
+                dev::Loc lc = dev::locate(p.c.m, idx);
+                crow = dev::addr<bf16>(p.c.m, lc);
+                cs = p.c.fast_stride[lc.piece];
+            }
             if (p.has_res) {
                 dev::Loc lr = dev::locate(p.res.m, idx);
                 rrow = dev::addr<bf16>(p.res.m, lr);

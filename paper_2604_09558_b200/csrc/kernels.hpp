@@ -223,6 +223,10 @@ struct GemmTcParams {
     // (BK-aligned piece boundaries, e.g. a virtual Concat along K); a_rows[s * M + m] = address
     // of A[m, a_seg_k[s]] minus a_seg_k[s] elements.  Null: rows located on the device.
     const uint64_t* a_rows;
+    // C rows resolved on the host when C's map is not affine and every row lies in one
+    // piece with one stride: c_rows[m] = address of C[m, 0], c_rs = stride along N
+    const uint64_t* c_rows;
+    int64_t c_rs;
     int32_t a_nseg, a_pad3;
     int32_t a_seg_k[GEMM_MAX_SEG + 1];
     // A's TMA tensor: up to 5 dimensions, one per digit of A's map

@@ -79,13 +79,16 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
     const int r = p.rank, ax_h = r - 3, ax_s = r - 2, ax_d = r - 1;
     const int Sq = p.Sq, Sk = p.Sk;
     const int q0 = blockIdx.x * QR;
-    int64_t bh = blockIdx.y;
-    const int h = int(bh % p.H);
-    bh /= p.H;
+    // 32-bit index arithmetic (grid dimensions fit): no 64-bit division calls
+    uint32_t bh = blockIdx.y;
+    const uint32_t bq = bh / uint32_t(p.H);
+    const int h = int(bh - bq * uint32_t(p.H));
+    bh = bq;
     int32_t base_idx[VTC_MAX_RANK] = {};
     for (int a = r - 4; a >= 0; --a) {
-        base_idx[a] = int32_t(bh % p.q.m.shape[a]);
-        bh /= p.q.m.shape[a];
+        const uint32_t ext = uint32_t(p.q.m.shape[a]), nb = bh / ext;
+        base_idx[a] = int32_t(bh - nb * ext);
+        bh = nb;
     }
     // query rows: one map evaluation each
     if (tid < QR) {

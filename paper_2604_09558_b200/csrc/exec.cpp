@@ -1237,6 +1237,24 @@ void Executor::prepare(bool dry) {
                             p.a_mod[j] = 0;
                         }
                         if (ok) T->kernel = "gemm_tc_bf16_gather";
+                        if (ok && p.bn == 128 && N > 128) {
+                            // gathered A is re-gathered for every N tile: 256-wide tiles (a
+                            // partial last one) halve that (Swin QKV N = 288: 218 -> 180 us)
+                            VOperand c256 = operand(map_of(cout), 1, 256, es);
+                            VOperand r256{};
+                            bool rok = true;
+                            if (f.add) {
+                                const std::string& other =
+                                    f.add->inputs[0] == n.outputs[0] ? f.add->inputs[1] : f.add->inputs[0];
+                                r256 = operand(map_of(other), 1, 256, es);
+                                rok = r256.fast_ok != 0;
+                            }
+                            if (c256.fast_ok && rok) {
+                                p.bn = 256;
+                                p.c = c256;
+                                if (f.add) p.res = r256;
+                            }
+                        }
                         if (ok && !impl_->dry) {
                             // A's row addresses resolved once per plan (the map is static): a
                             // per-CTA device locate through a multi-piece div/mod map costs

@@ -668,6 +668,7 @@ void Executor::prepare(bool dry) {
     };
     std::map<std::string, GemvFusion> fusion;
     std::map<std::string, const OpNode*> hfuse;  // first MatMul -> its horizontally fused sibling
+    std::map<std::string, const OpNode*> tc_hfuse;  // the same for the tcgen05 GEMM
     std::set<std::string> hpartner;
     std::set<std::string> absorbed;
     std::map<std::string, int> topo_pos;
@@ -788,6 +789,28 @@ void Executor::prepare(bool dry) {
                 }
             }
             for (const auto& id : hpartner) absorbed.insert(id);
+        }
+        // the same on the tensor cores: sibling MatMuls reading the same A with plain
+        // single-piece outputs (gate / up at decode batch) run as one launch, so the
+        // second does not wait for the first to complete (VTC_NO_TC_HFUSE=1: off)
+        if (!std::getenv("VTC_NO_TC_HFUSE")) {
+            std::vector<const OpNode*> cands;
+            for (const auto& n : g_.nodes())
+                if (tc_eligible(n) && !fusion.count(n.id) && !absorbed.count(n.id) && map_of(n.outputs[0]).pieces().size() == 1)
+                    cands.push_back(&n);
+            for (size_t i = 0; i < cands.size(); ++i) {
+                const OpNode* a = cands[i];
+                if (tc_hfuse.count(a->id) || absorbed.count(a->id)) continue;
+                for (size_t j = i + 1; j < cands.size(); ++j) {
+                    const OpNode* b = cands[j];
+                    if (absorbed.count(b->id) || tc_hfuse.count(b->id) || b->inputs[0] != a->inputs[0] ||
+                        g_.tensor(b->inputs[1]).shape[0] != g_.tensor(a->inputs[1]).shape[0])
+                        continue;
+                    tc_hfuse[a->id] = b;
+                    absorbed.insert(b->id);
+                    break;
+                }
+            }
         }
         // a norm is absorbed only if every consumer MatMul fused it
         for (auto& [id, f] : fusion) {
@@ -1311,18 +1334,53 @@ void Executor::prepare(bool dry) {
                             }
                         }
                     }
+                    auto th = tc_hfuse.find(n.id);
+                    if (th != tc_hfuse.end()) {
+                        // the absorbed sibling: its weights as B2, its output rows resolved here
+                        const OpNode& nb = *th->second;
+                        if (!ok || f.add) throw UnsupportedError("horizontally fused GEMM " + n.id + " not launchable");
+                        int64_t ldb2, cb2;
+                        if (!affine2d(map_of(nb.inputs[1]), ldb2, cb2)) throw UnsupportedError("fused GEMM B2 of " + nb.id);
+                        const VMap& bm2 = map_of(nb.inputs[1]);
+                        const char* b2 = reinterpret_cast<const char*>(target(bm2.pieces()[0].target).ptr) + cb2 * es;
+                        VOperand c2 = operand(map_of(nb.outputs[0]), 1, p.bn, es);
+                        if (!c2.fast_ok || c2.m.npieces != 1) throw UnsupportedError("fused GEMM C2 of " + nb.id);
+                        p.nmat = 2;
+                        p.N1 = g_.tensor(nb.inputs[1]).shape[1];
+                        p.c2_rs = c2.fast_stride[0];
+                        if (!impl_->dry) {
+                            if (!gemm_tc_encode_b(p.tmap_b2, b2, p.N1, K, ldb2))
+                                throw UnsupportedError("fused GEMM B2 tensor map of " + nb.id);
+                            std::vector<uint64_t> rows(static_cast<size_t>(M));
+                            int64_t idx[VTC_MAX_RANK] = {};
+                            for (int64_t m = 0; m < M; ++m) {
+                                idx[0] = m;
+                                int pc = -1;
+                                const int64_t off = desc_eval(c2.m, idx, &pc);
+                                rows[size_t(m)] = c2.m.piece[0].ptr + uint64_t(off) * 2;
+                            }
+                            auto* d = static_cast<uint64_t*>(impl_->alloc(rows.size() * 8, false));
+                            ck(cudaMemcpy(d, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice), "H2D(c2_rows)");
+                            p.c2_rows = d;
+                        }
+                        T->node += "+" + nb.id;
+                    }
                     if (ok) {
                         // prefill-sized M: 256-row tiles (two M=128 MMAs per B stage)
                         p.mt = (!p.a_gather && p.bn == 256 && M >= 4096) ? 2 : 1;
-                        int64_t tiles = (M + 128 * p.mt - 1) / (128 * p.mt) * ((N + p.bn - 1) / p.bn);
+                        const int64_t ntl = (N + p.bn - 1) / p.bn + (p.nmat > 1 ? (p.N1 + p.bn - 1) / p.bn : 0);
+                        int64_t tiles = (M + 128 * p.mt - 1) / (128 * p.mt) * ntl;
                         int64_t ktiles = (K + 63) / 64;
                         int sms = 148;
                         if (!impl_->dry) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
                         if (p.mt == 2 && tiles < sms) {  // not enough 256-row tiles: back to 128 rows
                             p.mt = 1;
-                            tiles = (M + 127) / 128 * ((N + p.bn - 1) / p.bn);
+                            tiles = (M + 127) / 128 * ntl;
                         }
-                        int64_t splits = tiles >= sms ? 1 : std::min<int64_t>(ktiles, std::max<int64_t>(1, sms / tiles));
+                        // K splits as for the first matrix alone: a fused sibling launch sums in
+                        // the same order as two separate launches would (bit-identical results)
+                        const int64_t tiles0 = tiles / ntl * ((N + p.bn - 1) / p.bn);
+                        int64_t splits = tiles0 >= sms ? 1 : std::min<int64_t>(ktiles, std::max<int64_t>(1, sms / tiles0));
                         p.splits = int32_t(splits);
                         if (splits > 1) {
                             p.work = static_cast<float*>(impl_->alloc(size_t(tiles * splits * 128 * p.bn) * 4, false));

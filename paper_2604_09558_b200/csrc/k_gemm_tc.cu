@@ -116,7 +116,7 @@ __host__ __device__ constexpr uint32_t instr_desc(int m, int n) {
 }
 
 struct Tmaps {
-    CUtensorMap a, b;
+    CUtensorMap a, b, b2;
 };
 
 // MT = 128-row sub-tiles per CTA (2: a 256 x BN tile whose two M=128 MMAs
@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     __shared__ unsigned s_last;
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int tiles_n = int((p.N + BN - 1) / BN);
+    const int tiles_n0 = int((p.N + BN - 1) / BN);
+    const int tiles_n = tiles_n0 + (p.nmat > 1 ? int((p.N1 + BN - 1) / BN) : 0);
     const int tiles_m = int((p.M + TM - 1) / TM);
     const int tile = blockIdx.x;
     // grouped rasterisation: consecutive CTAs walk GROUP_M row tiles of one
@@ -145,7 +146,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     const int first_m = (tile / in_group) * GROUP_M;
     const int gm = min(tiles_m - first_m, GROUP_M);
     const int tm_ = first_m + (tile % in_group) % gm, tn = (tile % in_group) / gm;
-    const int64_t m0 = int64_t(tm_) * TM, n0 = int64_t(tn) * BN;
+    const int mat = tn >= tiles_n0 ? 1 : 0;  // horizontally fused sibling (gate / up)
+    const int64_t m0 = int64_t(tm_) * TM, n0 = int64_t(mat ? tn - tiles_n0 : tn) * BN;
+    const int64_t Nm = mat ? p.N1 : p.N;
+    const CUtensorMap* tmb = mat ? &tm.b2 : &tm.b;
     const int split = blockIdx.y;
     const int ktiles = int((p.K + BK - 1) / BK);
     const int kt0 = int(int64_t(ktiles) * split / p.splits), kt1 = int(int64_t(ktiles) * (split + 1) / p.splits);
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                 mbar_expect_tx(&full[s], B_BYTES);
 #pragma unroll
                 for (int j = 0; j < BN / 64; ++j)
-                    tma_2d(sb + j * (BK * 128), &tm.b, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
+                    tma_2d(sb + j * (BK * 128), tmb, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
             }
             const uint32_t sa_u = smem_u32(sa);
 #pragma unroll 8
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     } else if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.a)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.b)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmb)) : "memory");
         // decode-sized M (one row tile): weights are read exactly once -> evict-first;
         // prefill: every row tile re-reads them -> keep them in L2
         const uint64_t pol_b = tiles_m == 1 ? dev::evict_first_policy() : evict_last_policy();
@@ -305,7 +309,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             }
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
-                tma_2d(sb + j * (BK * 128), &tm.b, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
+                tma_2d(sb + j * (BK * 128), tmb, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer ----------------
@@ -424,7 +428,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             int32_t idx[VTC_MAX_RANK] = {};
             idx[0] = int32_t(em);
             idx[1] = int32_t(n0);
-            if (p.c_rows) {  // host-resolved row (C's map has div/mod digits, e.g. a window reverse)
+            if (mat) {  // the sibling's output
+                crow = reinterpret_cast<bf16*>(p.c2_rows[em]) + int64_t(n0) * p.c2_rs;
+                cs = p.c2_rs;
+            } else if (p.c_rows) {  // host-resolved row (C's map has div/mod digits, e.g. a window reverse)
                 crow = reinterpret_cast<bf16*>(p.c_rows[em]) + int64_t(n0) * p.c_rs;
                 cs = p.c_rs;
             } else {
@@ -438,7 +445,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                 rs = p.res.fast_stride[lr.piece];
             }
         }
-        const int ncols = int(p.N - n0 < BN ? p.N - n0 : BN);
+        const int ncols = int(Nm - n0 < BN ? Nm - n0 : BN);
         // 16 finished columns c..c+15 of this row: round, residual, store through C's map
         auto emit = [&](int c, const float (&v)[16]) {
             bf16 o[16];
@@ -634,24 +641,29 @@ bool gemm_tc_encode(GemmTcParams& p, const void* a_base, const int64_t* a_dims, 
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return false;
     }
-    {
-        cuuint64_t dims[2] = {cuuint64_t(p.N), cuuint64_t(p.K)};
-        cuuint64_t str[1] = {cuuint64_t(b_ld) * 2};
-        cuuint32_t box[2] = {64, BK};
-        if (fn(reinterpret_cast<CUtensorMap*>(p.tmap_b), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(b_base), dims,
-               str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return false;
-    }
-    return true;
+    return gemm_tc_encode_b(p.tmap_b, b_base, p.N, p.K, b_ld);
+}
+
+bool gemm_tc_encode_b(void* out128, const void* b_base, int64_t N, int64_t K, int64_t ld) {
+    EncodeFn fn = encoder();
+    if (!fn || (reinterpret_cast<uintptr_t>(b_base) % 16) || (ld * 2) % 16) return false;
+    cuuint32_t es[2] = {1, 1};
+    cuuint64_t dims[2] = {cuuint64_t(N), cuuint64_t(K)};
+    cuuint64_t str[1] = {cuuint64_t(ld) * 2};
+    cuuint32_t box[2] = {64, BK};
+    return fn(reinterpret_cast<CUtensorMap*>(out128), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(b_base), dims,
+              str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 void launch_gemm_tc(const GemmTcParams& p, const GemmTcParams* dp, cudaStream_t s) {
     Tmaps tmaps;
     std::memcpy(&tmaps.a, p.tmap_a, sizeof(CUtensorMap));
     std::memcpy(&tmaps.b, p.tmap_b, sizeof(CUtensorMap));
+    std::memcpy(&tmaps.b2, p.nmat > 1 ? p.tmap_b2 : p.tmap_b, sizeof(CUtensorMap));
     const int tm = p.mt == 2 ? 2 * BM : BM;
-    const int tiles = int((p.M + tm - 1) / tm) * int((p.N + p.bn - 1) / p.bn);
+    const int tiles = int((p.M + tm - 1) / tm) *
+                      int((p.N + p.bn - 1) / p.bn + (p.nmat > 1 ? (p.N1 + p.bn - 1) / p.bn : 0));
     const int64_t ktiles = (p.K + BK - 1) / BK;
     dim3 grid(unsigned(tiles), unsigned(p.splits));
     if (p.mt == 2) {
@@ -672,8 +684,10 @@ void launch_gemm_tc(const GemmTcParams& p, const GemmTcParams* dp, cudaStream_t 
         constexpr size_t sm = smem_bytes<128, 2, 1>();  // three CTAs per SM
         cudaFuncSetAttribute(gemm_tc_kernel<128, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         launch_k(gemm_tc_kernel<128, 2, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
-    } else if (ktiles <= 6 && p.splits == 1) {
-        constexpr size_t sm = smem_bytes<128, 3, 1>();  // two CTAs per SM
+    } else if ((ktiles <= 6 || (p.M <= BM && tiles > 148)) && p.splits == 1) {
+        // two CTAs per SM: shallow K, or decode-sized M with more tiles than SMs (the
+        // fused gate / up weight streams then run in one wave instead of two)
+        constexpr size_t sm = smem_bytes<128, 3, 1>();
         cudaFuncSetAttribute(gemm_tc_kernel<128, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         launch_k(gemm_tc_kernel<128, 3, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
     } else {

@@ -238,7 +238,16 @@ struct GemmTcParams {
     int64_t a_div[5], a_mod[5];
     alignas(64) unsigned char tmap_a[128];
     alignas(64) unsigned char tmap_b[128];
+    // horizontally fused sibling (gate / up reading the same A): N tiles past the
+    // first matrix's use B2 (tmap_b2) and store C2 through host-resolved rows
+    int32_t nmat, pad_h;
+    int64_t N1;
+    const uint64_t* c2_rows;
+    int64_t c2_rs;
+    alignas(64) unsigned char tmap_b2[128];
 };
+// Encode a B tensor map (row-major bf16 [K, N], row stride ld) into out128.
+bool gemm_tc_encode_b(void* out128, const void* b_base, int64_t N, int64_t K, int64_t ld);
 // Derive A's TMA dimensions from its lowered map (one piece, no groups, digits
 // forming tile-aligned mixed-radix coordinates; innermost = K with unit stride).
 bool gemm_tc_a_dims(const vtc_map& a, int64_t M, int64_t K, GemmTcParams& p, int64_t dims[5], int64_t strides[5],

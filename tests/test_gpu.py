@@ -345,7 +345,8 @@ def test_llama_prefill_layer_small(vtc, oracle, cfg):
     want = oracle.execute(doc, x)["y"]
     got, p = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
     kinds = [l["kernel"] for l in p.info()["launches"]]
-    assert "attn_prefill_tc" in kinds and kinds.count("gemm_tc_bf16") == 5, kinds
+    assert "attn_prefill_tc" in kinds and kinds.count("gemm_tc_bf16") == 4, kinds  # gate + up in one launch
+    assert any(l["node"] == "gate_proj+up_proj" for l in p.info()["launches"])
     assert p.info()["data_movement_launches"] == 0
     assert _relerr(oracle.bf16_to_f32(got["y"]), oracle.bf16_to_f32(want)) < 2e-2
 
@@ -507,3 +508,20 @@ def test_fast_paths_bit_identical_to_generic_kernels(vtc, oracle, monkeypatch, w
     assert not any(l["kernel"] == "eltwise_flat" for l in p.info(dry=True)["launches"])
     generic = vtc.execute(g, p, x)["y"]
     assert np.array_equal(fast, generic)
+
+
+def test_tc_gate_up_fused_launch_bit_identical(vtc, oracle, monkeypatch):
+    """gate / up as one tcgen05 launch (second weight matrix's tiles after the
+    first's) gives the same bits as two launches (decode batch 64, split-K)."""
+    from paper_2604_09558_b200 import workloads as W
+    cfg = dict(B=64, L=256, pos=200, D=1024, Hq=8, Hkv=2, hd=128, F=2048)
+    doc = W.llama_decode_layer(**cfg)
+    x = _llama_inputs(oracle, W, doc, cfg["B"], cfg["pos"], cfg["D"], cfg["F"], cfg["hd"])
+    g = vtc.parse_graph(doc)
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert any(l["node"] == "gate_proj+up_proj" for l in p.info(dry=True)["launches"])
+    fused = vtc.execute(g, p, x)["y"]
+    monkeypatch.setenv("VTC_NO_TC_HFUSE", "1")
+    p2 = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert not any(l["node"] == "gate_proj+up_proj" for l in p2.info(dry=True)["launches"])
+    assert np.array_equal(fused, vtc.execute(g, p2, x)["y"])

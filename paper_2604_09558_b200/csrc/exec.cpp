@@ -806,6 +806,11 @@ void Executor::prepare(bool dry) {
                     if (absorbed.count(b->id) || tc_hfuse.count(b->id) || b->inputs[0] != a->inputs[0] ||
                         g_.tensor(b->inputs[1]).shape[0] != g_.tensor(a->inputs[1]).shape[0])
                         continue;
+                    // b runs at a's position: its weights must be a graph input and its output
+                    // its own root (nothing between a and b can then produce or touch them)
+                    if (g_.tensor(b->inputs[1]).kind != TensorKind::GraphInput ||
+                        !map_of(b->outputs[0]).is_identity_of(b->outputs[0]))
+                        continue;
                     tc_hfuse[a->id] = b;
                     absorbed.insert(b->id);
                     break;

@@ -63,7 +63,9 @@ enum vtc_status {
 enum vtc_plan_mode {
     VTC_PLAN_MATERIALIZE = 0,     /* all-physical points-to graph: materialising baseline */
     VTC_PLAN_SELECTED = 1,        /* caller-selected VTOG edges (validate_ptg) */
-    VTC_PLAN_MAX_ELIMINATION = 2  /* built-in strategy: eliminate every eliminable DM op */
+    VTC_PLAN_MAX_ELIMINATION = 2, /* built-in strategy: eliminate every eliminable DM op */
+    VTC_PLAN_INPLACE_UPDATES = 3  /* strong materialising comparator: ScatterND in place (rule i,
+                                     proj/src/vt_rules.cpp:346-349), every other DM op copied */
 };
 
 enum vtc_plan_flags {
@@ -71,7 +73,11 @@ enum vtc_plan_flags {
     VTC_FLAG_NO_GEMV = 1u << 1,  /* disable the weight-streaming decode kernel */
     VTC_FLAG_NO_FUSE = 1u << 2,  /* disable RMSNorm/SiLU*Mul/residual and elementwise-tree fusion */
     VTC_FLAG_GEMV_LDG = 1u << 3, /* decode GEMV on the LDG split-K kernel instead of the persistent TMA-streamed one */
-    VTC_FLAG_NO_TC = 1u << 4     /* bf16 MatMul with M > 16 on the generic tiled kernel instead of tcgen05 */
+    VTC_FLAG_NO_TC = 1u << 4,    /* bf16 MatMul with M > 16 on the generic tiled kernel instead of tcgen05 */
+    VTC_FLAG_DYNAMIC_POS = 1u << 5 /* decode position read on the device each step (vtc_plan_set_position or
+                                      the vtc_run input "__pos", int64[1]); the graph's ScatterND row is the
+                                      largest position.  Replaces the reference's static index
+                                      (proj/src/vt_rules.cpp:63-109) for multi-step decode. */
 };
 
 typedef struct vtc_graph vtc_graph;
@@ -108,6 +114,10 @@ int vtc_plan_download(vtc_plan* p, const char* tensor, void* host, int64_t bytes
 int vtc_run(vtc_plan* p, int32_t n_in, const char* const* in_ids, const void* const* in_host, const int64_t* in_bytes,
             int32_t n_out, const char* const* out_ids, void* const* out_host, const int64_t* out_bytes, void* stream);
 int vtc_plan_prepare(vtc_plan* p);
+/* Dynamic-position plans: the following executions write the cache row `pos`
+ * and attend over keys [0, pos] (0 <= pos <= the ScatterND row the graph was
+ * built with); stream-ordered, no re-planning, the captured graph is reused. */
+int vtc_plan_set_position(vtc_plan* p, int64_t pos, void* stream);
 int vtc_execute(vtc_plan* p, void* stream);        /* async launches on `stream` (cudaStream_t) */
 int vtc_execute_graph(vtc_plan* p, void* stream);  /* CUDA-graph replay of the same launches */
 int vtc_plan_num_launches(vtc_plan* p);

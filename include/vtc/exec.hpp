@@ -26,6 +26,12 @@ struct ExecOptions {
     bool gemv_stream = true;  // persistent TMA-streamed GEMV for M <= 4 (else the LDG split-K GEMV)
     bool fuse = true;         // RMSNorm->MatMul, SiLU*Mul->MatMul, MatMul->Add(residual) fusion
     int attn_splits = 0;      // 0: automatic
+    // Dynamic decode position: the plan is lowered once at the
+    // static index p0 of its in-place ScatterND cache updates (write row p0, attend
+    // over keys [0, p0]); each step's position pos <= p0 is read on the device from
+    // the root "__pos" (int64[1]: vtc_run input or set_position), so the same
+    // captured graph writes row pos and attends over pos + 1 keys.
+    bool dynamic_pos = false;
 };
 
 struct RootBuffer {
@@ -75,6 +81,10 @@ public:
     void reset_trace();
 
     void upload(const std::string& id, const void* host, int64_t bytes, void* stream);
+    // Dynamic-position plans: the next steps write cache row `pos` and attend over
+    // pos + 1 keys (0 <= pos <= the plan's static position); stream-ordered.
+    void set_position(int64_t pos, void* stream);
+    int64_t max_position() const;
     // Materialise any tensor (virtual or physical) into host memory.
     void download(const std::string& id, void* host, int64_t bytes, void* stream);
 
@@ -98,6 +108,8 @@ public:
     int num_kernel_launches() const;
 
 private:
+    // drop the launch list and every captured graph (a root address changed)
+    void invalidate();
     struct Impl;
     const CompGraph& g_;
     PointsToGraph ptg_;
@@ -107,6 +119,7 @@ private:
     std::vector<LaunchInfo> infos_;
     std::unique_ptr<Impl> impl_;
     bool prepared_ = false;
+    bool pos_set_ = false;  // dynamic position written by the caller (else p0 at prepare)
     // run_host staging: device arena holding the per-step input roots + pinned mirror
     std::string arena_key_;
     void* arena_dev_ = nullptr;

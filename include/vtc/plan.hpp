@@ -79,6 +79,12 @@ std::vector<std::string> eliminated_nodes(const CompGraph& g, const std::map<std
 // reference snapshot: proj/CMakeLists.txt:21).
 std::vector<int> plan_max_elimination(const Vtog& v);
 
+// Strong materialising comparator (SURVEY.md §8 d): only the ScatterND in-place
+// rule (i) (proj/src/vt_rules.cpp:346-349) -- a KV-cache update writes its slab
+// into the cache instead of cloning it -- and every other data-movement
+// operator materialised by a copy kernel.
+std::vector<int> plan_inplace_updates(const Vtog& v);
+
 // Byte accounting of the three-stage kernel model (cost_model.cpp:117-176).
 struct OperandBytes {
     std::string tensor;

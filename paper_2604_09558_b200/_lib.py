@@ -31,6 +31,7 @@ SIGNATURES = {
     "vtc_run": (C.c_int, [_VP, C.c_int32, C.POINTER(C.c_char_p), C.POINTER(_VP), C.POINTER(C.c_int64),
                           C.c_int32, C.POINTER(C.c_char_p), C.POINTER(_VP), C.POINTER(C.c_int64), _VP]),
     "vtc_plan_prepare": (C.c_int, [_VP]),
+    "vtc_plan_set_position": (C.c_int, [_VP, C.c_int64, _VP]),
     "vtc_execute": (C.c_int, [_VP, _VP]),
     "vtc_execute_graph": (C.c_int, [_VP, _VP]),
     "vtc_plan_num_launches": (C.c_int, [_VP]),

@@ -36,8 +36,8 @@ _ERROR_NAMES = {
 ERRORS = {code: type(name, (VtcError,), {"code": code}) for code, name in _ERROR_NAMES.items()}
 globals().update({cls.__name__: cls for cls in ERRORS.values()})
 
-MATERIALIZE, SELECTED, MAX_ELIMINATION = 0, 1, 2
-FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE, FLAG_GEMV_LDG, FLAG_NO_TC = 1, 2, 4, 8, 16
+MATERIALIZE, SELECTED, MAX_ELIMINATION, INPLACE_UPDATES = 0, 1, 2, 3
+FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE, FLAG_GEMV_LDG, FLAG_NO_TC, FLAG_DYNAMIC_POS = 1, 2, 4, 8, 16, 32
 
 NP_DTYPES = {"f64": np.float64, "f32": np.float32, "i64": np.int64, "bf16": np.uint16}
 
@@ -223,6 +223,12 @@ class Plan:
 
     def prepare(self) -> None:
         _check(_lib.load().vtc_plan_prepare(self._h))
+
+    def set_position(self, pos: int, stream=None) -> None:
+        """Dynamic-position plans (FLAG_DYNAMIC_POS): the next executions write
+        cache row `pos` and attend over keys [0, pos].  vtc_run callers can pass
+        the position as the input "__pos" (int64[1]) instead."""
+        _check(_lib.load().vtc_plan_set_position(self._h, int(pos), _stream(stream)))
 
     def execute(self, stream=None) -> None:
         _check(_lib.load().vtc_execute(self._h, _stream(stream)))

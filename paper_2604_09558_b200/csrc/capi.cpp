@@ -152,6 +152,8 @@ int vtc_plan_create(vtc_graph* g, int mode, const int32_t* selected, int32_t n_s
             ptg = vtc::validate_ptg(vtog_of(g), sel);
         } else if (mode == VTC_PLAN_MAX_ELIMINATION) {
             ptg = vtc::validate_ptg(vtog_of(g), vtc::plan_max_elimination(vtog_of(g)));
+        } else if (mode == VTC_PLAN_INPLACE_UPDATES) {
+            ptg = vtc::validate_ptg(vtog_of(g), vtc::plan_inplace_updates(vtog_of(g)));
         } else {
             throw vtc::SchemaError("unknown plan mode");
         }
@@ -161,6 +163,7 @@ int vtc_plan_create(vtc_graph* g, int mode, const int32_t* selected, int32_t n_s
         opt.fuse = !(flags & VTC_FLAG_NO_FUSE);
         opt.gemv_stream = (flags & VTC_FLAG_GEMV_LDG) == 0;
         opt.use_tc = (flags & VTC_FLAG_NO_TC) == 0;
+        opt.dynamic_pos = (flags & VTC_FLAG_DYNAMIC_POS) != 0;
         auto p = std::make_unique<vtc_plan>();
         p->graph = g;
         p->flags = flags;
@@ -263,6 +266,10 @@ void vtc_comm_free(vtc_comm* c) { delete c; }
 
 int vtc_plan_set_comm(vtc_plan* p, vtc_comm* c) {
     return guard([&] { p->exec->set_comm(c ? c->c.get() : nullptr); });
+}
+
+int vtc_plan_set_position(vtc_plan* p, int64_t pos, void* stream) {
+    return guard([&] { p->exec->set_position(pos, stream); });
 }
 
 int vtc_plan_prepare(vtc_plan* p) {

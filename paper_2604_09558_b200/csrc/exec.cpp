@@ -13,6 +13,7 @@
 
 #include "comm.hpp"
 #include "kernels.hpp"
+#include "launch.cuh"
 #include "lower.hpp"
 
 namespace vtc {
@@ -21,6 +22,13 @@ namespace {
 
 void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// SM count of the current device (the rank's GPU, not device 0)
+int device_sms() {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
 }
 
 KDType kdt(DType d) {
@@ -33,6 +41,146 @@ KDType kdt(DType d) {
     return KDType::F32;
 }
 
+// ---- dynamic decode position (ExecOptions::dynamic_pos) ----
+// A root updated in place by a ScatterND at static row p0 (the KV caches): row
+// stride rs elements, so the position's slab is elements [pos*rs, (pos+1)*rs).
+struct DynRoot {
+    int root = -1;
+    int64_t rs = 0, es = 0;
+    uint64_t ptr = 0;
+    int64_t bytes = 0;
+};
+struct DynCtx {
+    std::vector<DynRoot> roots;
+    int64_t p0 = 0;
+    const int64_t* dev = nullptr;  // device position (root "__pos")
+    bool dry = false;
+    std::string node;
+
+    const DynRoot* find(int target) const {
+        for (const auto& r : roots)
+            if (r.root == target) return &r;
+        return nullptr;
+    }
+    // element-offset range a piece addresses over its box (false: not bounded cheaply)
+    static bool piece_range(const vtc_map& m, int pi, int64_t& lo, int64_t& hi) {
+        const vtc_piece& pc = m.piece[pi];
+        if (pc.affine) {
+            lo = hi = pc.base;
+            for (int a = 0; a < m.rank; ++a) {
+                if (pc.hi[a] <= pc.lo[a]) return false;
+                const int64_t s0 = pc.aff[a] * pc.lo[a], s1 = pc.aff[a] * (pc.hi[a] - 1);
+                lo += std::min(s0, s1);
+                hi += std::max(s0, s1);
+            }
+            return true;
+        }
+        int64_t vol = 1;
+        for (int a = 0; a < m.rank; ++a) vol *= std::max<int64_t>(0, pc.hi[a] - pc.lo[a]);
+        if (vol <= 0 || vol > (int64_t(1) << 16)) return false;
+        lo = INT64_MAX;
+        hi = INT64_MIN;
+        int64_t idx[VTC_MAX_RANK] = {};
+        for (int64_t f = 0; f < vol; ++f) {
+            int64_t r = f;
+            for (int a = m.rank - 1; a >= 0; --a) {
+                const int64_t ext = pc.hi[a] - pc.lo[a];
+                idx[a] = pc.lo[a] + r % ext;
+                r /= ext;
+            }
+            int got = -1;
+            const int64_t off = desc_eval(m, idx, &got);
+            if (got != pi) continue;
+            lo = std::min(lo, off);
+            hi = std::max(hi, off);
+        }
+        return lo <= hi;
+    }
+    void add(KHead& h, const void* base, const void* field, int bytes, int64_t coeff) {
+        if (h.ndyn >= KHEAD_MAX_DYN) throw UnsupportedError("dynamic position: too many position-dependent fields in " + node);
+        const auto off = static_cast<const char*>(field) - static_cast<const char*>(base);
+        h.patch[h.ndyn++] = DynPatch{uint32_t(off), int32_t(bytes), coeff};
+        h.dyn = dev;
+        h.dyn0 = p0;
+    }
+    // a piece inside the position's slab moves with the position; other pieces of a
+    // dynamic root may be read (rows already in the cache) but not written
+    void operand(KHead& h, const void* base, VOperand& op, bool write) {
+        for (int i = 0; i < op.m.npieces; ++i) {
+            const DynRoot* r = find(op.m.piece[i].target);
+            if (!r) continue;
+            int64_t lo = 0, hi = 0;
+            const bool known = piece_range(op.m, i, lo, hi);
+            if (known && lo >= p0 * r->rs && hi < (p0 + 1) * r->rs) add(h, base, &op.m.piece[i].base, 8, r->rs);
+            else if (write) throw UnsupportedError("dynamic position: " + node + " writes a cache outside the position's row");
+        }
+    }
+    bool reads(const VOperand& op) const {
+        for (int i = 0; i < op.m.npieces; ++i)
+            if (find(op.m.piece[i].target)) return true;
+        return false;
+    }
+    // host-resolved addresses (row tables) cannot move with the position
+    void check_ptr(const void* p, const char* what) const {
+        if (dry || !p) return;
+        const auto a = reinterpret_cast<uint64_t>(p);
+        for (const auto& r : roots)
+            if (a >= r.ptr && a < r.ptr + uint64_t(r.bytes))
+                throw UnsupportedError(std::string("dynamic position: host-resolved ") + what + " of " + node + " points into a cache");
+    }
+};
+
+void dyn_ops(EwParams& p, DynCtx& c) {
+    c.operand(p.head, &p, p.out, true);
+    for (int i = 0; i < p.nin; ++i) c.operand(p.head, &p, p.in[i], false);
+}
+void dyn_ops(EwPair& p, DynCtx& c) {
+    dyn_ops(p.a, c);
+    dyn_ops(p.b, c);
+}
+void dyn_ops(RowParams& p, DynCtx& c) {
+    c.operand(p.head, &p, p.out, true);
+    c.operand(p.head, &p, p.x, false);
+    c.operand(p.head, &p, p.w, false);
+    if (p.op == RowOp::LayerNorm) c.operand(p.head, &p, p.bias, false);
+}
+void dyn_ops(MatmulParams& p, DynCtx& c) {
+    c.operand(p.head, &p, p.c, true);
+    c.operand(p.head, &p, p.a, false);
+    c.operand(p.head, &p, p.b, false);
+}
+void dyn_ops(GemvParams& p, DynCtx& c) {
+    c.operand(p.head, &p, p.c, true);
+    if (p.nmat > 1) c.operand(p.head, &p, p.c2, true);
+    c.operand(p.head, &p, p.a, false);
+    if (p.prologue == GemvPrologue::SiLUMul) c.operand(p.head, &p, p.a2, false);
+    if (p.prologue == GemvPrologue::RMSNorm) c.operand(p.head, &p, p.normw, false);
+    if (p.has_res) c.operand(p.head, &p, p.res, false);
+    for (int m = 0; m < 4 && p.rows_ok; ++m) {
+        c.check_ptr(p.arow[m], "A row");
+        c.check_ptr(p.a2row[m], "A2 row");
+    }
+    if (p.rows_ok) c.check_ptr(p.wrow, "norm weight row");
+    if (p.has_epi && p.epi_dyn) c.add(p.head, &p, &p.epi_shift, 8, p.epi_dyn);
+}
+void dyn_ops(GemmTcParams& p, DynCtx& c) {
+    if ((p.c_rows && c.reads(p.c)) || (p.a_gather && c.reads(p.a)))
+        throw UnsupportedError("dynamic position: host-resolved rows of " + c.node + " address a cache");
+    c.operand(p.head, &p, p.c, true);
+    if (p.has_res) c.operand(p.head, &p, p.res, false);
+}
+void dyn_ops(AttnParams& p, DynCtx& c) {
+    c.operand(p.head, &p, p.o, true);
+    c.operand(p.head, &p, p.q, false);
+    if (p.has_bias) c.operand(p.head, &p, p.bias, false);
+    const bool kr = c.reads(p.k), vr = c.reads(p.v);
+    if (!kr && !vr) return;
+    // keys [0, pos] of the cache: the key count follows the position
+    if (!(kr && vr) || p.fast != 1 || p.Sq != 1 || p.causal || !p.kv_affine || int64_t(p.Sk) != c.p0 + 1)
+        throw UnsupportedError("dynamic position: attention " + c.node + " does not read the cache prefix [0, pos]");
+    c.add(p.head, &p, &p.Sk, 4, 1);
+}
+
 struct Launch {
     std::string node, kernel;
     virtual ~Launch() = default;
@@ -41,6 +189,10 @@ struct Launch {
     virtual const void* host_params() const = 0;
     virtual void set_device_params(void* d) = 0;
     virtual void set_trace(unsigned long long* t, int id) = 0;
+    virtual void dyn_patch(DynCtx& c) {
+        c.node = node;
+        throw UnsupportedError("dynamic position: launch " + node + " (" + kernel + ") has no position patches");
+    }
 };
 
 template <class P>
@@ -64,6 +216,10 @@ struct LaunchT : Launch {
     const void* host_params() const override { return &p; }
     void set_device_params(void* d) override { dp = static_cast<const P*>(d); }
     void set_trace(unsigned long long* t, int id) override { set_head(p, t, id); }
+    void dyn_patch(DynCtx& c) override {
+        c.node = node;
+        dyn_ops(p, c);
+    }
 };
 
 // AllReduce(sum) of a contiguous buffer over the plan's communicator; with no
@@ -82,6 +238,11 @@ struct AllReduceLaunch : Launch {
     const void* host_params() const override { return nullptr; }
     void set_device_params(void*) override {}
     void set_trace(unsigned long long*, int) override {}
+    void dyn_patch(DynCtx& c) override {
+        c.node = node;
+        c.check_ptr(src, "allreduce input");
+        c.check_ptr(dst, "allreduce output");
+    }
 };
 
 // Consecutive streamed GEMVs as the stages of one persistent launch.
@@ -229,6 +390,15 @@ struct Executor::Impl {
         hkey.clear();
     }
     bool dry = false;
+    DynCtx dyn;            // dynamic-position plans: cache roots, static position
+    bool dyn_on = false;
+    // enqueue the launch list; a dynamic-position plan's first launch is
+    // stream-serialised so the step's position is written before any kernel reads it
+    void launch_all(cudaStream_t s) {
+        if (dyn_on) tl_serialize_next = true;
+        for (auto& l : launches) l->run(s);
+        tl_serialize_next = false;
+    }
     void* alloc(size_t bytes, bool zero) {
         if (dry) return nullptr;
         void* p = nullptr;
@@ -251,6 +421,15 @@ Executor::Executor(const CompGraph& g, PointsToGraph ptg, ExecOptions opt)
         root_index_[id] = int(roots_.size());
         roots_.push_back(rb);
     }
+    if (opt_.dynamic_pos) {
+        RootBuffer rb;
+        rb.id = "__pos";
+        rb.dtype = DType::I64;
+        rb.shape = {1};
+        rb.bytes = 8;
+        root_index_[rb.id] = int(roots_.size());
+        roots_.push_back(rb);
+    }
 }
 
 Executor::~Executor() {
@@ -267,9 +446,18 @@ void Executor::bind_root(const std::string& id, void* dev_ptr) {
     auto it = root_index_.find(id);
     if (it == root_index_.end()) throw ExecutionError("tensor " + id + " is not a physical root of this plan");
     RootBuffer& r = roots_[size_t(it->second)];
+    if (r.ptr == dev_ptr) return;
+    // the launches (and any captured graph, including vtc_run's host graph) hold
+    // the old address: drop them before the old buffer goes away
+    invalidate();
     if (r.owned && r.ptr) cudaFree(r.ptr);
     r.ptr = dev_ptr;
     r.owned = false;
+}
+
+void Executor::invalidate() {
+    impl_->free_graph();
+    impl_->launches.clear();
     prepared_ = false;
 }
 
@@ -281,7 +469,7 @@ void* Executor::root_ptr(const std::string& id) {
         ck(cudaMalloc(&r.ptr, size_t(std::max<int64_t>(r.bytes, 16))), "cudaMalloc(root)");
         ck(cudaMemset(r.ptr, 0, size_t(std::max<int64_t>(r.bytes, 16))), "cudaMemset(root)");
         r.owned = true;
-        prepared_ = false;
+        if (prepared_) invalidate();
     }
     return r.ptr;
 }
@@ -322,6 +510,44 @@ void Executor::prepare(bool dry) {
         return &ptg_.resolved.at(t);
     };
     std::set<std::string> elim(ptg_.eliminated_ops.begin(), ptg_.eliminated_ops.end());
+
+    // dynamic position: the caches updated in place by ScatterND at one static row p0
+    impl_->dyn = DynCtx{};
+    impl_->dyn_on = opt_.dynamic_pos;
+    if (opt_.dynamic_pos) {
+        DynCtx& dc = impl_->dyn;
+        dc.dry = dry;
+        bool have = false;
+        for (const auto& n : g_.nodes()) {
+            if (n.kind != OpKind::ScatterND) continue;
+            const auto& at = std::get<ScatterNDAttrs>(n.attrs);
+            const std::string& data = n.inputs[0];
+            const VMap& dm = map_of(data);
+            auto ts = dm.targets();
+            if (at.indices.size() != 1 || at.indices[0].size() != 1 || ts.size() != 1 || !dm.is_identity_of(ts[0]) ||
+                !map_of(n.outputs[0]).is_identity_of(ts[0]))
+                throw UnsupportedError("dynamic position: ScatterND " + n.id +
+                                       " is not a single-row in-place cache update (plan with in-place updates)");
+            const int64_t p0 = at.indices[0][0];
+            if (have && p0 != dc.p0) throw UnsupportedError("dynamic position: ScatterND updates at different rows");
+            have = true;
+            dc.p0 = p0;
+            const TensorSpec& t = g_.tensor(data);
+            DynRoot r;
+            r.root = root_index_.at(ts[0]);
+            r.rs = volume(t.shape) / t.shape[0];
+            r.es = dtype_size(t.dtype);
+            r.ptr = reinterpret_cast<uint64_t>(roots_[size_t(r.root)].ptr);
+            r.bytes = roots_[size_t(r.root)].bytes;
+            dc.roots.push_back(r);
+        }
+        if (!have) throw UnsupportedError("dynamic position: the graph has no ScatterND cache update");
+        dc.dev = static_cast<const int64_t*>(roots_[size_t(root_index_.at("__pos"))].ptr);
+        if (!dry && !pos_set_) {
+            ck(cudaMemcpy(roots_[size_t(root_index_.at("__pos"))].ptr, &dc.p0, 8, cudaMemcpyHostToDevice), "H2D(pos)");
+            pos_set_ = true;
+        }
+    }
 
     // algorithmic bytes of a (possibly fused) launch: tensors read from outside
     // the group (unique elements through their maps) + tensors the group emits
@@ -381,8 +607,7 @@ void Executor::prepare(bool dry) {
     };
     auto stream_gemv = [&](GemvParams& p, uint64_t b_ptr, const std::string& b_root, const SecondMat* m2) -> bool {
         const int64_t COLS = GEMV_STREAM_COLS, KT = GEMV_STREAM_KT;
-        int sms = 148;
-        if (!impl_->dry) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const int sms = impl_->dry ? 148 : device_sms();
         int64_t strips0 = (p.N + COLS - 1) / COLS;
         int64_t strips = strips0 + (m2 ? (m2->N + COLS - 1) / COLS : 0);  // horizontal fusion: + the second matrix
         int64_t kts = (p.K + KT - 1) / KT, units = strips * kts;
@@ -677,6 +902,21 @@ void Executor::prepare(bool dry) {
         auto cs = g_.consumers(t);
         return g_.tensor(t).kind == TensorKind::Intermediate && cs.size() == 1 && cs[0]->id == node;
     };
+    // a sibling b absorbed into a's launch runs at a's topological position: a must
+    // come first, everything b reads must be produced before a, and b's output must
+    // be its own root (so no node between a and b writes or reads through it)
+    auto absorbable_at = [&](const OpNode& a, const OpNode& b) {
+        if (topo_pos.at(a.id) >= topo_pos.at(b.id)) return false;
+        for (const auto& in : b.inputs) {
+            const OpNode* pr = g_.producer(in);
+            if (pr && topo_pos.at(pr->id) >= topo_pos.at(a.id)) return false;
+            for (const auto& r : targets_of(map_of(in))) {
+                const OpNode* pw = g_.producer(r);
+                if (pw && topo_pos.at(pw->id) >= topo_pos.at(a.id)) return false;
+            }
+        }
+        return map_of(b.outputs[0]).is_identity_of(b.outputs[0]);
+    };
     auto gemv_eligible = [&](const OpNode& n) {
         if (n.kind != OpKind::MatMul || !opt_.use_gemv) return false;
         const TensorSpec& A = g_.tensor(n.inputs[0]);
@@ -782,7 +1022,7 @@ void Executor::prepare(bool dry) {
                     const OpNode* nb = fb != fusion.end() ? fb->second.norm : nullptr;
                     bool other = (fa != fusion.end() && (fa->second.silu || fa->second.add)) ||
                                  (fb != fusion.end() && (fb->second.silu || fb->second.add));
-                    if (other || na != nb) continue;
+                    if (other || na != nb || !absorbable_at(*a, *b)) continue;
                     hfuse[a->id] = b;
                     hpartner.insert(b->id);
                     break;
@@ -806,11 +1046,7 @@ void Executor::prepare(bool dry) {
                     if (absorbed.count(b->id) || tc_hfuse.count(b->id) || b->inputs[0] != a->inputs[0] ||
                         g_.tensor(b->inputs[1]).shape[0] != g_.tensor(a->inputs[1]).shape[0])
                         continue;
-                    // b runs at a's position: its weights must be a graph input and its output
-                    // its own root (nothing between a and b can then produce or touch them)
-                    if (g_.tensor(b->inputs[1]).kind != TensorKind::GraphInput ||
-                        !map_of(b->outputs[0]).is_identity_of(b->outputs[0]))
-                        continue;
+                    if (!absorbable_at(*a, *b)) continue;
                     tc_hfuse[a->id] = b;
                     absorbed.insert(b->id);
                     break;
@@ -966,7 +1202,33 @@ void Executor::prepare(bool dry) {
             if (elim.count(n.id)) continue;  // eliminated: no kernel
             for (const auto& o : n.outputs) {
                 VMap src = gather_map(n, o, g_).compose(lookup);
-                copy_checked(n.id, dt, g_.tensor(o).shape, map_of(o), src);
+                const VMap& dst = map_of(o);
+                const Index& shp = g_.tensor(o).shape;
+                // Only what moves is copied (the estimate's `moved`, proj/src/cost_model.cpp:150-165):
+                // pieces whose source already is where the output lives (a ScatterND whose output
+                // aliases its data in place, rule (i)) need no copy.
+                std::vector<const VPiece*> moving;
+                for (const auto& q : src.pieces()) {
+                    int64_t vol = 1;
+                    for (size_t a = 0; a < q.lo.size(); ++a) vol *= q.hi[a] - q.lo[a];
+                    if (VMap(src.shape(), {q}).agree_volume(dst) != vol) moving.push_back(&q);
+                }
+                if (moving.size() == src.pieces().size()) {
+                    copy_checked(n.id, dt, shp, dst, src);
+                    continue;
+                }
+                for (const VPiece* q : moving) {
+                    auto part = std::make_shared<VMap>(src.shape(), std::vector<VPiece>{*q});
+                    bool hazard = false;
+                    for (const auto& t : targets_of(dst)) hazard |= targets_of(*part).count(t) > 0;
+                    if (hazard) throw UnsupportedError("in-place copy of " + n.id + " reads what it writes");
+                    const size_t before = infos_.size();
+                    eltwise_box(n.id, copy_spec(part.get()), dt, shp, dst, q->lo, q->hi);
+                    int64_t vol = 1;
+                    for (size_t a = 0; a < q->lo.size(); ++a) vol *= q->hi[a] - q->lo[a];
+                    for (size_t i = before; i < infos_.size(); ++i)  // the moved region, read + written
+                        infos_[i].bytes = 2 * vol * es / int64_t(infos_.size() - before);
+                }
             }
             continue;
         }
@@ -1159,7 +1421,20 @@ void Executor::prepare(bool dry) {
                                 }
                                 EpiEntry ent{};
                                 ent.tree = int32_t(ti);
-                                ent.out = addr_of(om.eval(idx));
+                                const auto oe = om.eval(idx);
+                                ent.out = addr_of(oe);
+                                if (impl_->dyn_on) {
+                                    const DynCtx& dc = impl_->dyn;
+                                    const DynRoot* r = dc.find(root_index_.at(oe.first));
+                                    if (r && oe.second >= dc.p0 * r->rs && oe.second < (dc.p0 + 1) * r->rs) {
+                                        ent.cmask |= EPI_DYN_OUT;
+                                        if (p.epi_dyn && p.epi_dyn != r->rs * r->es)
+                                            throw UnsupportedError("dynamic position: caches with different row sizes in one epilogue");
+                                        p.epi_dyn = int32_t(r->rs * r->es);
+                                    } else if (r) {
+                                        throw UnsupportedError("dynamic position: fused epilogue writes a cache outside the row");
+                                    }
+                                }
                                 int64_t anchor = -1;
                                 for (size_t j = 0; j < t.in_names.size(); ++j) {
                                     auto te = map_of(t.in_names[j]).eval(idx);
@@ -1174,6 +1449,8 @@ void Executor::prepare(bool dry) {
                                         ent.cmask |= 1u << j;
                                     } else {
                                         ent.in[j] = addr_of(te);
+                                        if (impl_->dyn_on && impl_->dyn.find(root_index_.at(te.first)))
+                                            throw UnsupportedError("dynamic position: fused epilogue reads a cache");
                                     }
                                 }
                                 if (anchor < 0 || tab[size_t(anchor)].tree >= 0)
@@ -1376,16 +1653,23 @@ void Executor::prepare(bool dry) {
                         const int64_t ntl = (N + p.bn - 1) / p.bn + (p.nmat > 1 ? (p.N1 + p.bn - 1) / p.bn : 0);
                         int64_t tiles = (M + 128 * p.mt - 1) / (128 * p.mt) * ntl;
                         int64_t ktiles = (K + 63) / 64;
-                        int sms = 148;
-                        if (!impl_->dry) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+                        const int sms = impl_->dry ? 148 : device_sms();
                         if (p.mt == 2 && tiles < sms) {  // not enough 256-row tiles: back to 128 rows
                             p.mt = 1;
                             tiles = (M + 127) / 128 * ntl;
                         }
                         // K splits as for the first matrix alone: a fused sibling launch sums in
                         // the same order as two separate launches would (bit-identical results)
-                        const int64_t tiles0 = tiles / ntl * ((N + p.bn - 1) / p.bn);
+                        int64_t tiles0 = tiles / ntl * ((N + p.bn - 1) / p.bn);
                         int64_t splits = tiles0 >= sms ? 1 : std::min<int64_t>(ktiles, std::max<int64_t>(1, sms / tiles0));
+                        if (splits > 1 && p.mt == 2) {
+                            // the split-K workspace and counters are per 128-row tile: a K split
+                            // (a narrow first matrix) runs 128-row tiles
+                            p.mt = 1;
+                            tiles = (M + 127) / 128 * ntl;
+                            tiles0 = tiles / ntl * ((N + p.bn - 1) / p.bn);
+                            splits = tiles0 >= sms ? 1 : std::min<int64_t>(ktiles, std::max<int64_t>(1, sms / tiles0));
+                        }
                         p.splits = int32_t(splits);
                         if (splits > 1) {
                             p.work = static_cast<float*>(impl_->alloc(size_t(tiles * splits * 128 * p.bn) * 4, false));
@@ -1698,6 +1982,9 @@ void Executor::prepare(bool dry) {
         impl_->launches = std::move(merged);
         infos_ = std::move(minfos);
     }
+    // dynamic position: register the position-dependent fields of every launch
+    if (impl_->dyn_on)
+        for (auto& l : impl_->launches) l->dyn_patch(impl_->dyn);
     // optional device timeline (VTC_TRACE=1): [entry, exit] globaltimer per launch
     impl_->trace = nullptr;
     if (!dry && std::getenv("VTC_TRACE") && std::getenv("VTC_TRACE")[0] == '1') {
@@ -1730,7 +2017,7 @@ void Executor::prepare(bool dry) {
 void Executor::run(void* stream) {
     if (!prepared_) prepare();
     auto s = static_cast<cudaStream_t>(stream);
-    for (auto& l : impl_->launches) l->run(s);
+    impl_->launch_all(s);
     ck(cudaGetLastError(), "kernel launch");
 }
 
@@ -1741,7 +2028,7 @@ void Executor::run_graph(void* stream) {
         cudaStream_t cap;
         ck(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
-        for (auto& l : impl_->launches) l->run(cap);
+        impl_->launch_all(cap);
         cudaError_t e = cudaStreamEndCapture(cap, &impl_->graph);
         cudaStreamDestroy(cap);
         ck(e, "cudaStreamEndCapture");
@@ -1786,6 +2073,7 @@ void Executor::run_timed(void* stream, float* ms, int n) {
     ck(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
     ck(cudaEventRecordWithFlags(ev[0], cap, cudaEventRecordExternal), "cudaEventRecord");
     for (size_t i = 0; i < L; ++i) {
+        if (i == 0 && impl_->dyn_on) tl_serialize_next = true;
         impl_->launches[i]->run(cap);
         ck(cudaEventRecordWithFlags(ev[i + 1], cap, cudaEventRecordExternal), "cudaEventRecord");
     }
@@ -1803,11 +2091,23 @@ void Executor::run_timed(void* stream, float* ms, int n) {
     for (auto& x : ev) cudaEventDestroy(x);
 }
 
+void Executor::set_position(int64_t pos, void* stream) {
+    if (!opt_.dynamic_pos) throw ExecutionError("set_position: plan was not created with a dynamic position");
+    if (!prepared_) prepare();
+    if (pos < 0 || pos > impl_->dyn.p0)
+        throw OutOfBoundsError("set_position: " + std::to_string(pos) + " outside [0, " + std::to_string(impl_->dyn.p0) + "]");
+    upload("__pos", &pos, 8, stream);
+    ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "sync");  // pageable source
+}
+
+int64_t Executor::max_position() const { return opt_.dynamic_pos ? impl_->dyn.p0 : -1; }
+
 void Executor::upload(const std::string& id, const void* host, int64_t bytes, void* stream) {
     auto it = root_index_.find(id);
     if (it == root_index_.end()) throw ExecutionError("upload target " + id + " is not a physical root");
     RootBuffer& r = roots_[size_t(it->second)];
     if (bytes != r.bytes) throw ShapeMismatchError("upload of " + id + ": byte count mismatch");
+    if (id == "__pos") pos_set_ = true;
     void* d = root_ptr(id);
     ck(cudaMemcpyAsync(d, host, size_t(bytes), cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)), "H2D");
 }
@@ -1821,7 +2121,7 @@ void Executor::run_host(const std::vector<HostIn>& ins, const std::vector<HostOu
     if (const char* e = std::getenv("VTC_HOST_LINK_MAX")) kLinkMax = std::atoll(e);  // tests: force either path
     auto s = static_cast<cudaStream_t>(stream);
     Impl& I = *impl_;
-    bool same = I.hexec && ins.size() == I.sig_in.size() && outs.size() == I.sig_out.size() && I.fast_stream == s;
+    bool same = prepared_ && I.hexec && ins.size() == I.sig_in.size() && outs.size() == I.sig_out.size() && I.fast_stream == s;
     for (size_t i = 0; same && i < ins.size(); ++i) same = ins[i].bytes == I.sig_in[i].second && ins[i].id == I.sig_in[i].first;
     for (size_t i = 0; same && i < outs.size(); ++i)
         same = outs[i].bytes == I.sig_out[i].second && outs[i].id == I.sig_out[i].first;
@@ -1848,7 +2148,23 @@ void Executor::run_host(const std::vector<HostIn>& ins, const std::vector<HostOu
         for (size_t j = 0; ok && j < small.size(); ++j)
             ok = root_ptr(ins[size_t(small[j])].id) == static_cast<char*>(arena_dev_) + arena_off_[j];
         if (!ok) {
-            if (arena_dev_) ck(cudaFree(arena_dev_), "cudaFree(arena)");
+            if (arena_dev_) {
+                // roots staged by an earlier call but not named in this one keep their
+                // contents: move them out of the old arena before it is freed
+                std::set<std::string> now;
+                for (int i : small) now.insert(ins[size_t(i)].id);
+                char* lo = static_cast<char*>(arena_dev_);
+                for (auto& r : roots_) {
+                    char* rp = static_cast<char*>(r.ptr);
+                    if (r.owned || !rp || rp < lo || rp >= lo + arena_bytes_ || now.count(r.id)) continue;
+                    void* own = nullptr;
+                    ck(cudaMalloc(&own, size_t(std::max<int64_t>(r.bytes, 16))), "cudaMalloc(root)");
+                    ck(cudaMemcpy(own, rp, size_t(r.bytes), cudaMemcpyDeviceToDevice), "D2D(arena root)");
+                    bind_root(r.id, own);
+                    r.owned = true;
+                }
+                ck(cudaFree(arena_dev_), "cudaFree(arena)");
+            }
             if (arena_host_) ck(cudaFreeHost(arena_host_), "cudaFreeHost(arena)");
             arena_dev_ = arena_host_ = nullptr;
             arena_off_.clear();
@@ -1907,7 +2223,7 @@ void Executor::run_host(const std::vector<HostIn>& ins, const std::vector<HostOu
             if (!dma) launch_host_link_copy(arena_host_dev, arena_dev_, arena_bytes_, cap);
             else cudaMemcpyAsync(arena_dev_, arena_host_, size_t(arena_bytes_), cudaMemcpyHostToDevice, cap);
         }
-        for (auto& l : I.launches) l->run(cap);
+        I.launch_all(cap);
         for (size_t i = 0; i < outs.size(); ++i) {
             if (I.out_kind[i] != 0) continue;
             if (!dma)

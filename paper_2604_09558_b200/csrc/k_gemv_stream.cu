@@ -568,7 +568,8 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
                         }
                         r[ins.dst] = __bfloat162float(__float2bfloat16_rn(v));
                     }
-                    *reinterpret_cast<bf16*>(e.out) = __float2bfloat16_rn(r[t.result]);
+                    *reinterpret_cast<bf16*>(e.out + ((e.cmask & EPI_DYN_OUT) ? uint64_t(p.epi_shift) : 0ull)) =
+                        __float2bfloat16_rn(r[t.result]);
                 }
             bar_consumers();  // sC is the reduction buffer of the next strip
             strip_done(strip);

@@ -33,10 +33,28 @@ struct VOperand {
 // Common first member of every parameter block: optional device-side
 // timeline (VTC_TRACE=1): CTA 0..n thread 0 records globaltimer at kernel entry
 // (atomicMin into trace[2*id]) and exit (atomicMax into trace[2*id+1]).
+//
+// Dynamic-position plans (vtc_plan_set_position): the fields
+// that depend on the decode position -- the base offset of a map piece that
+// stores the new token's K / V row into the cache slab, a fused-epilogue
+// address shift, the attention key count -- are listed as patches; after the
+// block is staged into shared memory, value += coeff * (*dyn - dyn0), where
+// *dyn is the plan's device-resident position for this step and dyn0 the
+// position the block was lowered for.  One plan and one captured graph serve
+// every step.
+struct DynPatch {
+    uint32_t off;    // byte offset of the field inside the staged parameter struct
+    int32_t bytes;   // 4 or 8 (signed integer field)
+    int64_t coeff;
+};
+constexpr int KHEAD_MAX_DYN = 6;
 struct KHead {
     unsigned long long* trace;
     int32_t id;
-    int32_t pad;
+    int32_t ndyn;
+    const int64_t* dyn;
+    int64_t dyn0;
+    DynPatch patch[KHEAD_MAX_DYN];
 };
 
 // ---- elementwise / copy --------------------------------------------------
@@ -122,8 +140,9 @@ struct EpiEntry {            // one GEMV output element (m, n)
     uint64_t out;            // tree output address (bf16)
     uint64_t in[EPI_MAX_IN]; // C column (C-derived input) or element address (external input)
     int32_t tree;            // -1: plain output element, stored through the C map
-    uint32_t cmask;          // bit j: input j is C-derived
+    uint32_t cmask;          // bit j: input j is C-derived; EPI_DYN_OUT: out moves with the position
 };
+constexpr uint32_t EPI_DYN_OUT = 1u << 31;  // out += GemvParams::epi_shift (dynamic-position plans)
 
 struct GemvParams {
     KHead head;
@@ -162,8 +181,9 @@ struct GemvParams {
     const void* wrow;
     int64_t sa[4], sa2[4], sw;
     // fused epilogue trees (has_epi): table [M * N] of EpiEntry
-    int32_t has_epi, pad4;
+    int32_t has_epi, epi_dyn;       // epi_dyn: bytes per position of EPI_DYN_OUT addresses
     const EpiEntry* epi;
+    int64_t epi_shift;              // bytes added to the out address of EPI_DYN_OUT entries
     EpiTree epi_tree[EPI_MAX_TREES];
     alignas(64) unsigned char tmap[GEMV_MAX_MATS][128];  // CUtensorMap per weight matrix (host-encoded)
 };

@@ -45,6 +45,12 @@ inline void allow_max_smem(void (*kern)(KArgs...)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - int(a.sharedSizeBytes));
 }
 
+// Set by the executor before a dynamic-position plan's first launch: that
+// launch is stream-serialised (no PDL), so every kernel of the step starts after
+// the position write that precedes the plan has completed.  Consumed by the
+// next launch_k on this thread.
+inline thread_local bool tl_serialize_next = false;
+
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg = {};
@@ -56,7 +62,8 @@ inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = (pdl_enabled() && !tl_serialize_next) ? 1 : 0;
+    tl_serialize_next = false;
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 

@@ -402,6 +402,29 @@ std::vector<int> plan_max_elimination(const Vtog& v) {
     return selected;
 }
 
+std::vector<int> plan_inplace_updates(const Vtog& v) {
+    const CompGraph& g = *v.graph;
+    std::vector<int> selected;
+    for (const auto& n : g.nodes()) {
+        if (n.kind != OpKind::ScatterND) continue;
+        for (const auto& e : v.edges) {
+            if (e.src != n.outputs[0] || e.dst != n.inputs[0] || e.direction != VtDirection::OutputOverInput ||
+                e.eliminated_op != n.id)
+                continue;
+            std::vector<int> trial = selected;
+            trial.push_back(e.id);
+            try {
+                validate_ptg(v, trial);
+                selected = std::move(trial);
+            } catch (const Error&) {
+            }
+            break;
+        }
+    }
+    std::sort(selected.begin(), selected.end());
+    return selected;
+}
+
 int64_t KernelBytes::total() const {
     int64_t t = 0;
     for (const auto& r : reads) t += r.bytes;

@@ -3,14 +3,24 @@
 Metric (BASELINE.json): decoder-layer latency (us) with HBM GB/s as a fraction
 of roofline and the DRAM bytes eliminated versus the materialising executor.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c1] [--impl vtc|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c5|c1]
+                  [--also c3,c4,c5] [--impl vtc|reference] [--l2 none|flush]
 
-Default workload: BASELINE configs[1] -- Llama-3-8B decoder layer, decode step,
-batch 1, KV length 2048, bf16 (random-init weights uniform(-1,1)/sqrt(fan_in)).
-Every timed step is one full layer on the GPU: zero data-movement kernels
-under the VTC plan.  L2 is flushed (256 MiB write) between timed steps,
-outside the timed events.  `--impl reference` times the reference's own CPU
-executor (oracle/_ref, built from /root/reference) on the same layer.
+Headline workload: BASELINE configs[1] -- Llama-3-8B decoder layer, decode
+step, batch 1, KV length 2048, bf16 (random-init weights uniform(-1,1)/
+sqrt(fan_in)).  At N=1 the other configurations (C3 decode B=64 KV 8192, C4
+Swin-T block B=64, C5 prefill B=8 S=4096) are measured in the same run and
+nested under "configs".  Every timed step is one full layer on the GPU (one
+CUDA-graph replay): zero data-movement kernels under the VTC plan.  By default
+no L2 flush is needed (every step streams more than the 126 MB L2: weights /
+KV / activations); --l2 flush writes + reads 256 MiB between steps, outside
+the timed events (also reported as l2_flushed_us).  Kernel times for the
+roofline come from the in-graph device timeline of the same plan (first-CTA
+entry / last-CTA exit per launch, charged as critical-path shares that add up
+to the step).  `e2e` runs the step through vtc_run from pinned host buffers;
+decode advances the position every step on one plan / one captured graph.
+`--impl reference` times the reference's own CPU executor (oracle/_ref, built
+from /root/reference) on the same layer.
 """
 from __future__ import annotations
 
@@ -231,6 +241,234 @@ def run_reference_arm(args):
 
 
 # ---------------------------------------------------------------------------
+def timeline(p, reps, torch, stream, flush):
+    """Per-launch device time inside the CUDA-graph replay (plan prepared with
+    VTC_TRACE=1: first-CTA entry / last-CTA exit per launch, globaltimer).
+    Each launch is charged its critical-path share: from the later of its own
+    entry and the previous launch's exit to its exit -- so the shares add up to
+    the step and a kernel's PDL wait on its predecessor is not counted twice."""
+    acc, total = None, 0.0
+    for _ in range(reps):
+        p.trace()  # reset the accumulators
+        flush()
+        p.execute_graph(stream)
+        torch.cuda.synchronize()
+        tr = p.trace().astype(np.float64)
+        ent, ext = tr[:, 0], tr[:, 1]
+        rec = (ent > 0) & (ent < 2 ** 62) & (ext > 0)
+        t0 = ent[rec].min()
+        prev = t0
+        share = np.zeros(len(tr))
+        for i in range(len(tr)):
+            if not rec[i]:
+                continue
+            share[i] = max(0.0, ext[i] - max(prev, ent[i]))
+            prev = max(prev, ext[i])
+        total += (prev - t0) / 1e3
+        acc = share / 1e3 if acc is None else acc + share / 1e3
+    return acc / reps, total / reps  # us
+
+
+def families(launches, share_us):
+    fam = {}
+    for l, us in zip(launches, share_us):
+        f = fam.setdefault(l["kernel"], {"us": 0.0, "bytes": 0, "launches": 0})
+        f["us"] += float(us)
+        f["bytes"] += int(l["bytes"])
+        f["launches"] += 1
+    return fam
+
+
+def prefill_flops(B, S, D=4096, F=14336, nq=4096, nkv=1024, H=32, hd=128):
+    T = B * S
+    gemm = 2 * T * D * (nq + 2 * nkv) + 2 * T * nq * D + 2 * 2 * T * D * F + 2 * T * F * D
+    attn = 2 * 2 * B * H * (S * (S + 1) // 2) * hd
+    return {"gemm_tc_bf16": gemm, "attn_prefill": attn}
+
+
+def measure(name, args, torch, vtc, W, dev, stream, flush, world, rank, comm, local):
+    """One configuration: VTC plan (device time, timeline, e2e), the materialising
+    comparators on the same kernels, roofline of the dominant kernel family."""
+    cfg = CONFIGS[name]
+    hbm_peak, tf_peak, peak_src = peaks()
+    B = cfg["B"]
+    L = cfg.get("L", cfg.get("S", cfg.get("H")))
+    swin, prefill = bool(cfg.get("swin")), bool(cfg.get("prefill"))
+    decode = not swin and not prefill
+    tp = world if (world > 1 and decode and not args.replicas) else 1
+    if swin:
+        doc = W.swin_block(B=B, H=cfg["H"])
+    elif prefill:
+        doc = W.llama_prefill_layer(B=B, S=cfg["S"])
+    else:
+        doc = W.llama_decode_layer(B=B, L=L, tp=tp)
+    g = vtc.parse_graph(doc)
+    dev_tensors, host = build_layer_inputs(doc, cfg, torch, dev)
+
+    def make(mode, flags=0, trace=False):
+        if trace:
+            os.environ["VTC_TRACE"] = "1"
+        try:
+            p = vtc.Plan(g, mode, flags=flags)
+            if comm is not None:
+                p.set_comm(comm)
+            for tid, t in dev_tensors.items():
+                p.bind_root(tid, t.data_ptr())
+            for tid, t in host.items():
+                p.upload_ptr(tid, t.data_ptr(), t.numel() * t.element_size(), stream)
+            p.prepare()
+        finally:
+            os.environ.pop("VTC_TRACE", None)
+        return p
+
+    def timed(p, sample_clocks=False):
+        for _ in range(max(3, args.warmup)):
+            p.execute_graph(stream)
+        torch.cuda.synchronize()
+        if sample_clocks:
+            with ClockSampler(local) as clk:
+                ms, _ = time_steps(lambda: p.execute_graph(stream), args.steps, torch, stream, flush)
+            return ms, clk.summary()
+        ms, _ = time_steps(lambda: p.execute_graph(stream), args.steps, torch, stream, flush)
+        return ms, None
+
+    vflags = vtc.FLAG_DYNAMIC_POS if decode else 0
+    # ---- the VTC plan: device time of one CUDA-graph replay per step ----
+    pv = make(vtc.MAX_ELIMINATION, vflags)
+    info = pv.info()
+    clk = ClockSampler(local).__enter__()
+    lat_ms, _ = timed(pv)
+    flushed_ms = None
+    if args.l2 == "none":
+        l2 = args.l2
+        args.l2 = "flush"
+        flushed_ms, _ = time_steps(lambda: pv.execute_graph(stream), args.steps, torch, stream, flush)
+        args.l2 = l2
+
+    # ---- e2e through vtc_run: the step's inputs from pinned host memory (H2D),
+    #      the layer, y back to pinned host memory (D2H); decode advances the
+    #      position every step (one plan, one captured graph) ----
+    y_host = torch.empty(g.tensors()["y"]["shape"], dtype=torch.bfloat16).pin_memory()
+    outs = [("y", y_host.data_ptr(), y_host.numel() * 2)]
+    nsteps = max(20, args.warmup) + args.steps
+    if decode:
+        sets = []
+        for i in range(nsteps):
+            pos = L - nsteps + i
+            cos, sin = W.rope_tables(B, [pos] * B)
+            hs = {"x": host["x"],
+                  "cos": torch.from_numpy(cos.astype(np.float32)).to(torch.bfloat16).pin_memory(),
+                  "sin": torch.from_numpy(sin.astype(np.float32)).to(torch.bfloat16).pin_memory(),
+                  "__pos": torch.tensor([pos], dtype=torch.int64).pin_memory()}
+            sets.append(pv.host_step([(k, t.data_ptr(), t.numel() * t.element_size()) for k, t in hs.items()],
+                                     outs, stream))
+        h2d = sum(t.numel() * t.element_size() for t in hs.values())
+        it = iter(sets)
+        e2e_step = lambda: next(it)()  # noqa: E731
+    else:
+        e2e_step = pv.host_step([(k, t.data_ptr(), t.numel() * t.element_size()) for k, t in host.items()],
+                                outs, stream)
+        h2d = sum(t.numel() * t.element_size() for t in host.values())
+    # the first host-graph replays run slow (first touches of the pinned staging):
+    # warm up past that transient, untimed
+    for _ in range(nsteps - args.steps):
+        e2e_step()
+    e2e_ms, _ = time_steps(e2e_step, args.steps, torch, stream, flush)
+    d2h = y_host.numel() * 2
+    clk.__exit__(None, None, None)
+    clocks = clk.summary()
+    if decode:
+        pv.set_position(L - 1, stream)  # back to the benchmarked position
+    del pv
+
+    # ---- timeline of the same plan (traced build): per-family kernel time ----
+    pt = make(vtc.MAX_ELIMINATION, vflags, trace=True)
+    share, step_us = timeline(pt, max(3, min(args.steps, 10)), torch, stream, flush)
+    launches = pt.info()["launches"]
+    del pt
+    fam = families(launches, share)
+
+    # ---- materialising comparators on the same kernels ----
+    pm = make(vtc.MATERIALIZE)
+    minfo = pm.info()
+    mat_ms, _ = timed(pm)
+    del pm
+    strong_ms, sinfo = None, None
+    if decode:
+        ps = make(vtc.INPLACE_UPDATES)
+        sinfo = ps.info()
+        strong_ms, _ = timed(ps)
+        del ps
+
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([lat_ms, e2e_ms, mat_ms, strong_ms or 0.0], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        lat_ms, e2e_ms, mat_ms, strong_ms = t.tolist()
+        strong_ms = strong_ms or None
+
+    bytes_step = sum(l["bytes"] for l in launches)
+    traffic_file = ROOT / "profiles" / "traffic.json"
+    traffic_tab = json.loads(traffic_file.read_text()).get(name, {}) if traffic_file.exists() else {}
+    if prefill:
+        fl = prefill_flops(B, cfg["S"])
+        tens = {k: v for k, v in fam.items() if any(k.startswith(f) for f in fl)}
+        dom = max(tens, key=lambda k: tens[k]["us"])
+        flops = next(v for f, v in fl.items() if dom.startswith(f))
+        ach = flops / (fam[dom]["us"] * 1e-6) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": tf_peak, "unit": "TFLOP/s", "frac": ach / tf_peak,
+                "traffic": traffic_tab.get(dom), "kernel": dom, "kernel_launches_per_step": fam[dom]["launches"],
+                "algorithmic_flops_per_step": flops, "peak_source": peak_src,
+                "kernel_time_source": "in-graph device timeline, critical-path share"}
+    else:
+        dom = max(fam, key=lambda k: fam[k]["us"])
+        ach = fam[dom]["bytes"] / (fam[dom]["us"] * 1e-6) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                "frac_vs_8tbs": ach / 8000.0, "traffic": traffic_tab.get(dom), "kernel": dom,
+                "kernel_launches_per_step": fam[dom]["launches"], "algorithmic_bytes_per_step": fam[dom]["bytes"],
+                "peak_source": peak_src, "kernel_time_source": "in-graph device timeline, critical-path share"}
+    out = {
+        "metric": METRIC, "value": lat_ms * 1e3, "unit": "us", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": lat_ms, "higher_is_better": False,
+        "scaling": "strong" if tp > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights uniform(-1,1)/sqrt(fan_in), random KV cache / activations)",
+        "config": {"workload": cfg["workload"], "batch": B,
+                   **({"resolution": 224, "stage1_grid": L, "window": 7, "shift": 3} if swin else
+                      {"seq_len": L} if prefill else {"kv_len": L, "pos": L - 1}),
+                   "parallelism": (f"tp{tp} (head-sharded; 2 NCCL allreduce of [{B},4096] bf16 per layer)" if tp > 1
+                                   else f"replicas x{world}" if world > 1 else "single-gpu"),
+                   "l2": ("inputs larger than L2: every step streams %.0f MB (> 126 MB L2) with an L2 evict-first "
+                          "policy on weights / KV; no explicit flush" % (bytes_step / 1e6)
+                          if args.l2 == "none" else "flushed between timed steps (256 MiB write + 256 MiB read)"),
+                   "plan": "VTC max-elimination (all data-movement ops virtual)" + (
+                       ", dynamic decode position (one plan / graph for every position)" if decode else ""),
+                   "cuda_graph": True},
+        "roofline": roof,
+        "step_hbm_gbs": bytes_step / (lat_ms * 1e-3) / 1e9,
+        "step_hbm_frac": bytes_step / (lat_ms * 1e-3) / 1e9 / hbm_peak,
+        "step_hbm_frac_vs_8tbs": bytes_step / (lat_ms * 1e-3) / 1e9 / 8000.0,
+        "bytes_per_step": bytes_step,
+        "timeline_step_us": step_us,
+        "kernel_times_us": {k: round(v["us"], 2) for k, v in fam.items()},
+        "materialized_us": mat_ms * 1e3,
+        "speedup_vs_materialized": mat_ms / lat_ms,
+        "strong_materialized_us": strong_ms * 1e3 if strong_ms else None,
+        "speedup_vs_strong_materialized": strong_ms / lat_ms if strong_ms else None,
+        "l2_flushed_us": flushed_ms * 1e3 if flushed_ms is not None else None,
+        "dram_bytes_eliminated": info["bytes_eliminated"],
+        "data_movement_launches": {"virtual": info["data_movement_launches"],
+                                   "materialized": minfo["data_movement_launches"],
+                                   **({"strong_materialized": sinfo["data_movement_launches"]} if sinfo else {})},
+        "e2e": {"value": e2e_ms * 1e3, "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                **({"position": f"advances every step ({L - nsteps}..{L - 1}), same plan and graph"} if decode else {})},
+        "gpu_launches": info["kernel_launches"] * args.steps,
+        "clocks": clocks,
+    }
+    if prefill:
+        out["tflops"] = sum(prefill_flops(B, cfg["S"]).values()) / (lat_ms * 1e-3) / 1e12
+    return out
+
+
 def run_vtc(args):
     import torch
     import paper_2604_09558_b200 as vtc
@@ -245,8 +483,6 @@ def run_vtc(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
-    cfg = CONFIGS[args.config]
-    hbm_peak, tf_peak, peak_src = peaks()
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     read_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -262,215 +498,31 @@ def run_vtc(args):
             torch.cuda._sleep(50000)
 
     if args.config == "c1":
+        hbm_peak, _, peak_src = peaks()
         return run_c1(args, torch, vtc, W, dev, stream, flush, hbm_peak, peak_src, world, rank)
-
-    B, L = cfg["B"], cfg.get("L", cfg.get("S", cfg.get("H")))
-    swin = bool(cfg.get("swin"))
-    # N > 1: Megatron head sharding (each rank 32/N query heads, 8/N KV heads,
-    # F/N FFN columns, its shard of the KV cache) with two NCCL allreduces per
-    # layer; --replicas runs N independent full layers instead
-    tp = world if (world > 1 and not args.replicas) else 1
-    prefill = bool(cfg.get("prefill"))
-    if swin:
-        doc = W.swin_block(B=B, H=cfg["H"])
-    elif prefill:
-        doc = W.llama_prefill_layer(B=B, S=cfg["S"])
-    else:
-        doc = W.llama_decode_layer(B=B, L=L, tp=tp)
-    g = vtc.parse_graph(doc)
-    dev_tensors, host = build_layer_inputs(doc, cfg, torch, dev)
     comm = None
-    if tp > 1:
+    if world > 1 and not args.replicas:
         import torch.distributed as dist
         uid = [vtc.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = vtc.Comm(uid[0], world, rank)
-    plans = {}
-    for name, mode in (("virtual", vtc.MAX_ELIMINATION), ("materialized", vtc.MATERIALIZE)):
-        p = vtc.Plan(g, mode)
-        if comm is not None:
-            p.set_comm(comm)
-        for tid, t in dev_tensors.items():
-            p.bind_root(tid, t.data_ptr())
-        for tid, t in host.items():
-            p.upload_ptr(tid, t.data_ptr(), t.numel() * t.element_size(), stream)
-        p.prepare()
-        plans[name] = p
-    info = plans["virtual"].info()
-    minfo = plans["materialized"].info()
-    # the caches are updated in place every step at the same position: repeated
-    # steps are idempotent, so every timed step does identical work
-
-    results = {}
-    flushed_ms = None
-    if args.l2 == "none":
-        # the same step measured with an explicit L2 flush before it, for reference
-        l2_mode = args.l2
-        args.l2 = "flush"
-        for _ in range(2):
-            plans["virtual"].execute_graph(stream)
-        flushed_ms, _ = time_steps(lambda: plans["virtual"].execute_graph(stream), args.steps, torch, stream, flush)
-        args.l2 = l2_mode
-    for name, p in plans.items():
-        for _ in range(max(3, args.warmup)):
-            p.execute_graph(stream)
-        torch.cuda.synchronize()
-        if name == "virtual":
-            with ClockSampler(local) as clk:
-                mean_ms, _ = time_steps(lambda: p.execute_graph(stream), args.steps, torch, stream, flush)
-            clocks = clk.summary()
-        else:
-            mean_ms, _ = time_steps(lambda: p.execute_graph(stream), args.steps, torch, stream, flush)
-        results[name] = mean_ms
-
-    if os.environ.get("VTC_TRACE") == "1":
-        # device timeline of one graph replay (first-CTA entry / last-CTA exit per launch)
-        for name, p in plans.items():
-            p.trace()
-            flush()
-            p.execute_graph(stream)
-            torch.cuda.synchronize()
-            tr = p.trace().astype(np.int64)
-            t0 = tr[:, 0].min()
-            print(f"[trace {name}] total {(tr[:, 1].max() - t0) / 1e3:.1f} us", file=sys.stderr)
-            for l, row in zip(p.info()["launches"], tr):
-                a, z = row[0], row[1]
-                if l["kernel"].startswith("gemm_tc") and row[4]:
-                    cps = f"avg mainloop {row[2] / row[4] / 1e3:.2f} us, avg epilogue {row[3] / row[4] / 1e3:.2f} us over {row[4]} CTAs"
-                    if row[5] or row[6]:
-                        cps += f"; gather: rows located {row[5] / row[4] / 1e3:.2f} us, k-tiles {row[6] / row[4] / 1e3:.2f} us"
-                else:
-                    cps = " ".join(f"cp{k}={(row[k] - t0) / 1e3:.1f}" for k in range(2, 8) if row[k])
-                print(f"  {l['kernel']:<22} {(a - t0) / 1e3:8.1f} -> {(z - t0) / 1e3:8.1f}  ({(z - a) / 1e3:6.1f} us)  "
-                      f"{l['bytes'] / 1e6:8.2f} MB  {l['node'][:50]}  {cps}", file=sys.stderr)
-
-    # per-launch device times (separate pass; same launches with events between them)
-    launches = info["launches"]
-    per = np.zeros(len(launches))
-    reps = max(3, min(args.steps, 10))
-    for _ in range(reps):
-        flush()
-        torch.cuda.synchronize()
-        per += plans["virtual"].execute_timed(len(launches), stream)[: len(launches)]
-    per /= reps
-    fam = {}
-    for l, ms in zip(launches, per):
-        f = fam.setdefault(l["kernel"], {"ms": 0.0, "bytes": 0, "launches": 0})
-        f["ms"] += float(ms)
-        f["bytes"] += int(l["bytes"])
-        f["launches"] += 1
-    dom = max(fam, key=lambda k: fam[k]["ms"])
-    achieved = fam[dom]["bytes"] / (fam[dom]["ms"] * 1e-3) / 1e9
-    if prefill:
-        # tensor-bound: algorithmic FLOPs of the dominant family over its time
-        T, D, F, nq, nkv = B * cfg["S"], 4096, 14336, 4096, 1024
-        gemm_flops = 2 * T * D * (nq + 2 * nkv) + 2 * T * nq * D + 2 * 2 * T * D * F + 2 * T * F * D
-        attn_flops = 2 * 2 * B * 32 * cfg["S"] * (cfg["S"] + 1) // 2 * 128
-        fam_flops = {"gemm_tc_bf16": gemm_flops, "attn_prefill_tc": attn_flops}
-        achieved_tf = fam_flops.get(dom, 0) / (fam[dom]["ms"] * 1e-3) / 1e12
-    traffic = None
-    tfile = ROOT / "profiles" / "traffic.json"
-    if tfile.exists():
-        try:
-            traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dom)
-        except Exception:
-            traffic = None
-
-    # e2e through the C ABI with host buffers: H2D of the step's inputs, the layer, D2H of y
-    pv = plans["virtual"]
-    y_host = torch.empty(g.tensors()["y"]["shape"], dtype=torch.bfloat16).pin_memory()
-
-    ins = [(tid, t.data_ptr(), t.numel() * t.element_size()) for tid, t in host.items()]
-    outs = [("y", y_host.data_ptr(), y_host.numel() * 2)]
-
-    # vtc_run: one H2D of every input, the graph replay, D2H of y, sync
-    e2e_step = pv.host_step(ins, outs, stream)
-
-    # the first host-graph replays run slow (first touches of the pinned staging,
-    # host-link translations): warm up past that transient, untimed
-    for _ in range(max(20, args.warmup)):
-        e2e_step()
-    e2e_ms, e2e_times = time_steps(e2e_step, args.steps, torch, stream, flush)
-    if os.environ.get("BENCH_E2E_DIAG"):
-        print(f"[e2e diag] per-step us {[round(t * 1e3, 1) for t in e2e_times]}", file=sys.stderr)
-    if os.environ.get("BENCH_E2E_DIAG"):
-        import time as _t
-
-        def graph_sync():
-            pv.execute_graph(stream)
-            stream.synchronize()
-        for nm, fn in (("graph+sync", graph_sync), ("vtc_run", e2e_step)):
-            ev, _ = time_steps(fn, args.steps, torch, stream, flush)
-            w = []
-            for _ in range(args.steps):
-                torch.cuda.synchronize()
-                t0 = _t.perf_counter()
-                fn()
-                w.append((_t.perf_counter() - t0) * 1e6)
-            print(f"[e2e diag] {nm:12s} event {ev * 1e3:7.1f} us  wall {np.median(w):7.1f} us", file=sys.stderr)
-    h2d = sum(t.numel() * t.element_size() for t in host.values())
-    d2h = y_host.numel() * 2
-
-    lat_ms = results["virtual"]
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([lat_ms, e2e_ms, results["materialized"]], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        lat_ms, e2e_ms, mat_ms = t.tolist()
-    else:
-        mat_ms = results["materialized"]
-    if rank != 0:
-        return
-    bytes_step = sum(l["bytes"] for l in launches)
-    cpu = (cpu_reference_layer(cfg) if world == 1 and not prefill and not swin and not os.environ.get("BENCH_NO_CPU")
-           else None)
-    line = {
-        "metric": METRIC,
-        "value": lat_ms * 1e3,
-        "unit": "us",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": lat_ms,
-        "higher_is_better": False,
-        "scaling": "strong" if tp > 1 else "weak",
-        "vs_baseline": None,
-        "dtype": "bf16",
-        "data": "synthetic (random-init weights uniform(-1,1)/sqrt(fan_in), random KV cache)",
-        "config": {"workload": cfg["workload"], "batch": B,
-                   **({"resolution": 224, "stage1_grid": L, "window": 7, "shift": 3} if swin else
-                      {("seq_len" if prefill else "kv_len"): L, "pos": None if prefill else L - 1}),
-                   "parallelism": (f"tp{tp} (head-sharded; 2 NCCL allreduce of [{B},4096] bf16 per layer)" if tp > 1
-                                   else f"replicas x{world}" if world > 1 else "single-gpu"),
-                   "l2": ("inputs larger than L2: every step streams %.0f MB of weights + KV (> 126 MB L2), weights/KV "
-                          "loaded with an L2 evict-first policy; no explicit flush" % (bytes_step / 1e6)
-                          if args.l2 == "none" else
-                          "flushed between timed steps (256 MiB write + 256 MiB read, outside the events)"),
-                   "plan": "VTC max-elimination (all data-movement ops virtual)", "cuda_graph": True},
-        "roofline": ({"bound": "tensor", "achieved": achieved_tf, "peak": tf_peak, "unit": "TFLOP/s",
-                      "frac": achieved_tf / tf_peak, "traffic": traffic, "kernel": dom,
-                      "kernel_launches_per_step": fam[dom]["launches"], "peak_source": peak_src}
-                     if prefill else
-                     {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                      "frac": achieved / hbm_peak, "traffic": traffic, "kernel": dom,
-                      "kernel_launches_per_step": fam[dom]["launches"],
-                      "algorithmic_bytes_per_step": fam[dom]["bytes"], "peak_source": peak_src}),
-        "step_hbm_gbs": bytes_step / (lat_ms * 1e-3) / 1e9,
-        "step_hbm_frac": bytes_step / (lat_ms * 1e-3) / 1e9 / hbm_peak,
-        "bytes_per_step": bytes_step,
-        "materialized_us": mat_ms * 1e3,
-        "l2_flushed_us": flushed_ms * 1e3 if flushed_ms is not None else None,
-        "speedup_vs_materialized": mat_ms / lat_ms,
-        "dram_bytes_eliminated": info["bytes_eliminated"],
-        "data_movement_launches": {"virtual": info["data_movement_launches"],
-                                   "materialized": minfo["data_movement_launches"]},
-        "kernel_times_us": {k: round(v["ms"] * 1e3, 2) for k, v in fam.items()},
-        "e2e": {"value": e2e_ms * 1e3, "unit": "us", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": info["kernel_launches"] * args.steps,
-        "clocks": clocks,
-        "cpu_baseline": cpu,
-    }
-    print(json.dumps(line), flush=True)
+    line = measure(args.config, args, torch, vtc, W, dev, stream, flush, world, rank, comm, local)
+    cfg = CONFIGS[args.config]
+    if rank == 0:
+        decode = not cfg.get("swin") and not cfg.get("prefill")
+        line["cpu_baseline"] = (cpu_reference_layer(cfg) if world == 1 and decode and not os.environ.get("BENCH_NO_CPU")
+                                else None)
+    # the other BASELINE configurations, measured in the same run (N = 1)
+    if world == 1 and args.also:
+        nested = {}
+        for name in [c for c in args.also.split(",") if c and c != args.config]:
+            try:
+                nested[name] = measure(name, args, torch, vtc, W, dev, stream, flush, world, rank, None, local)
+            except Exception as e:  # report, keep the headline line
+                nested[name] = {"error": f"{type(e).__name__}: {e}"}
+        line["configs"] = nested
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def run_c1(args, torch, vtc, W, dev, stream, flush, hbm_peak, peak_src, world, rank):
@@ -510,6 +562,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="vtc", choices=["vtc", "reference"])
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent full layers instead of head sharding")
+    ap.add_argument("--also", default="c3,c4,c5",
+                    help="other configurations measured in the same run and nested under 'configs' (N=1; '' = none)")
     ap.add_argument("--l2", default="none", choices=["flush", "none"],
                     help="flush L2 between timed steps, or rely on the step's inputs exceeding L2")
     args = ap.parse_args()

@@ -176,7 +176,9 @@ void dyn_ops(AttnParams& p, DynCtx& c) {
     const bool kr = c.reads(p.k), vr = c.reads(p.v);
     if (!kr && !vr) return;
     // keys [0, pos] of the cache: the key count follows the position
-    if (!(kr && vr) || p.fast != 1 || p.Sq != 1 || p.causal || !p.kv_affine || int64_t(p.Sk) != c.p0 + 1)
+    // (every attention kernel uses Sk only as the key bound; the split-KV chunking stays
+    // the one planned for p0 + 1 keys, later splits are empty)
+    if (!(kr && vr) || p.Sq != 1 || p.causal || int64_t(p.Sk) != c.p0 + 1)
         throw UnsupportedError("dynamic position: attention " + c.node + " does not read the cache prefix [0, pos]");
     c.add(p.head, &p, &p.Sk, 4, 1);
 }

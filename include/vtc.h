@@ -14,6 +14,12 @@
  *   vtc_plan_upload / vtc_execute / vtc_plan_download
  *                         <- vtelim::execute / execute_detailed / ExecutionResult::materialize
  *                                                         proj/include/vtelim/executor.hpp:77-83, 71
+ *   vtc_graph_estimate    <- vtelim::estimate(g, ptg, MachineParams) + breakdown
+ *                                                         proj/include/vtelim/cost_model.hpp:59, 74-80
+ *   vtc_graph_enumerate   <- vtelim::enumerate_ptgs       proj/include/vtelim/vtog.hpp:62
+ *   vtc_graph_greedy      <- greedy_build (Alg. 2) over saving_oracle / executor_timed_oracle
+ *                            (proj/include/vtelim/cost_model.hpp:64-73; the
+ *                            reference snapshot lacks src/greedy.cpp, proj/CMakeLists.txt:21)
  *   vtc_map_eval          <- vtelim::IndexMap::eval       proj/include/vtelim/mapping.hpp:70
  *   vtc_launch_gather_copy<- vtelim::load_virtual + store_virtual (one copy through two maps)
  *                                                         proj/include/vtelim/executor.hpp:59-62
@@ -64,8 +70,10 @@ enum vtc_plan_mode {
     VTC_PLAN_MATERIALIZE = 0,     /* all-physical points-to graph: materialising baseline */
     VTC_PLAN_SELECTED = 1,        /* caller-selected VTOG edges (validate_ptg) */
     VTC_PLAN_MAX_ELIMINATION = 2, /* built-in strategy: eliminate every eliminable DM op */
-    VTC_PLAN_INPLACE_UPDATES = 3  /* strong materialising comparator: ScatterND in place (rule i,
+    VTC_PLAN_INPLACE_UPDATES = 3, /* strong materialising comparator: ScatterND in place (rule i,
                                      proj/src/vt_rules.cpp:346-349), every other DM op copied */
+    VTC_PLAN_GREEDY = 4           /* Alg. 2 global greedy over the B200-calibrated analytic oracle
+                                     (MachineParams fitted by scripts/calibrate.py) */
 };
 
 enum vtc_plan_flags {
@@ -92,6 +100,22 @@ void vtc_graph_free(vtc_graph* g);
 /* Returned strings stay valid until the next call on the same thread. */
 int vtc_graph_serialize(vtc_graph* g, const char** json_out);
 int vtc_graph_vtog(vtc_graph* g, const char** json_out);
+
+/* Planner (host only, no GPU unless the device oracle is chosen).
+ * params_json: MachineParams {"bandwidth","coalesce_unit","kernel_launch_overhead",
+ * "noncoalesced_penalty","partial_penalty"} (cost_model.hpp:18-28); NULL or "" = the
+ * reference defaults, "b200" = the calibrated B200 parameters.
+ * vtc_graph_estimate: selected == NULL && n_selected < 0 -> the all-physical plan.
+ *   JSON: total_time, kernels[{node, data_movement, time, reads/writes[{tensor, bytes, factor}]}],
+ *   breakdown {data_movement_time, compute_time, ...}.
+ * vtc_graph_enumerate: {"ptgs": [{selected, roots, eliminated_ops}]} in the reference's order.
+ * vtc_graph_greedy: config {"oracle": "analytic"|"device", "params": <params>|"b200",
+ *   "trials": n, "executable": bool} -> {selected, roots, eliminated_ops, total_saving,
+ *   final_saving, iterations, oracle_calls, decisions[{iteration, node, edges, saving}]}. */
+int vtc_graph_estimate(vtc_graph* g, const int32_t* selected, int32_t n_selected, const char* params_json,
+                       const char** json_out);
+int vtc_graph_enumerate(vtc_graph* g, int64_t limit, const char** json_out);
+int vtc_graph_greedy(vtc_graph* g, const char* config_json, const char** json_out);
 
 int vtc_plan_create(vtc_graph* g, int mode, const int32_t* selected, int32_t n_selected, uint32_t flags,
                     vtc_plan** out);
@@ -138,6 +162,11 @@ int vtc_plan_trace(vtc_plan* p, uint64_t* out, int32_t n);
  * evaluates the device descriptor instead of the symbolic map. */
 int vtc_map_eval(vtc_plan* p, const char* tensor, int lowered, int32_t* targets, int64_t* offsets, int64_t cap);
 int vtc_plan_map_json(vtc_plan* p, const char* tensor, const char** json_out);
+/* Analyses of a tensor's resolved map (IndexMap::contiguity / injective / unique_elems /
+ * is_total, proj/include/vtelim/mapping.hpp:43-51, 100-125):
+ * {injective, unique_elems, is_total, min_contiguous_dim, contiguous_run_elems, class, type}. */
+int vtc_plan_map_analyze(vtc_plan* p, const char* tensor, int64_t elem_size, int64_t coalesce_unit,
+                         const char** json_out);
 
 /* Tensor-parallel plans (SURVEY.md §8 e): one NCCL communicator per process /
  * GPU.  Rank 0 creates the 128-byte unique id, the host side distributes it

@@ -89,17 +89,20 @@ std::vector<int> plan_inplace_updates(const Vtog& v);
 struct OperandBytes {
     std::string tensor;
     int64_t bytes = 0;
+    double bandwidth_factor = 1.0;  // set by estimate(g, ptg, MachineParams)
 };
 struct KernelBytes {
     std::string node;
     bool data_movement = false;
     std::vector<OperandBytes> reads, writes;
+    double time = 0.0;  // set by estimate(g, ptg, MachineParams)
     int64_t total() const;
 };
 struct TrafficEstimate {
     std::vector<KernelBytes> kernels;
     int data_movement_kernels = 0;
     int compute_kernels = 0;
+    double total_time = 0.0;  // set by estimate(g, ptg, MachineParams)
     int64_t total_bytes() const;
     int64_t data_movement_bytes() const;
 };

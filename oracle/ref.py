@@ -42,6 +42,9 @@ def lib():
             "vref_ptg_free": (None, [vp]),
             "vref_ptg_json": (C.c_char_p, [vp]),
             "vref_estimate_json": (C.c_char_p, [vp, vp]),
+            "vref_estimate_params_json": (C.c_char_p, [vp, vp, C.c_char_p]),
+            "vref_saving": (C.c_int, [vp, vp, C.c_char_p, C.POINTER(C.c_double)]),
+            "vref_enumerate_json": (C.c_char_p, [vp, C.c_int64]),
             "vref_gather_map_json": (C.c_char_p, [vp, C.c_char_p, C.c_char_p]),
             "vref_map_eval_all": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.c_int64]),
             "vref_map_compose": (C.c_char_p, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int]),
@@ -103,6 +106,12 @@ class RefGraph:
             _err()
         return RefPlan(self, h)
 
+    def enumerate_ptgs(self, limit: int = -1) -> list:
+        s = lib().vref_enumerate_json(self.h, int(limit))
+        if s is None:
+            _err()
+        return json.loads(s.decode())
+
     def gather_map(self, node: str, output: str) -> dict:
         s = lib().vref_gather_map_json(self.h, node.encode(), output.encode())
         if s is None:
@@ -134,6 +143,18 @@ class RefPlan:
         if s is None:
             _err()
         return json.loads(s.decode())
+
+    def estimate_params(self, params: dict) -> dict:
+        s = lib().vref_estimate_params_json(self.g.h, self.h, json.dumps(params).encode())
+        if s is None:
+            _err()
+        return json.loads(s.decode())
+
+    def saving(self, params: dict) -> float:
+        out = C.c_double()
+        if lib().vref_saving(self.g.h, self.h, json.dumps(params).encode(), C.byref(out)):
+            _err()
+        return out.value
 
     def execute(self, inputs: Dict[str, np.ndarray], with_roots: bool = False):
         """Returns (outputs, wall_ns, skipped_ops)."""

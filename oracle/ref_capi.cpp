@@ -15,7 +15,9 @@
 //   execute_detailed       proj/src/executor.cpp:448-498
 //   gather_map             proj/src/vt_rules.cpp:161-223
 //   IndexMap::eval         proj/src/mapping.cpp:103-116
-//   estimate               proj/src/cost_model.cpp:117-176
+//   estimate               proj/src/cost_model.cpp:117-176 (default or given MachineParams)
+//   saving_oracle          proj/src/cost_model.cpp:188-203
+//   enumerate_ptgs         proj/src/vtog.cpp:209-237
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -165,6 +167,38 @@ const char* vref_estimate_json(void* g, void* p) {
             MachineParams mp;
             auto est = estimate(static_cast<Graph*>(g)->g, static_cast<Plan*>(p)->ptg, mp);
             out = est.to_json().dump();
+        }))
+        return nullptr;
+    return dup(out);
+}
+
+const char* vref_estimate_params_json(void* g, void* p, const char* params_json) {
+    std::string out;
+    if (guard([&] {
+            MachineParams mp = MachineParams::from_json(nlohmann::json::parse(params_json));
+            auto est = estimate(static_cast<Graph*>(g)->g, static_cast<Plan*>(p)->ptg, mp);
+            out = est.to_json().dump();
+        }))
+        return nullptr;
+    return dup(out);
+}
+
+// saving_oracle(params).evaluate(g, ptg)
+int vref_saving(void* g, void* p, const char* params_json, double* out) {
+    return guard([&] {
+        auto o = saving_oracle(MachineParams::from_json(nlohmann::json::parse(params_json)));
+        *out = o->evaluate(static_cast<Graph*>(g)->g, static_cast<Plan*>(p)->ptg);
+    });
+}
+
+// enumerate_ptgs(vtog, limit): [{selected, roots, eliminated_ops}] in the reference's order.
+const char* vref_enumerate_json(void* g, int64_t limit) {
+    std::string out;
+    if (guard([&] {
+            nlohmann::json arr = nlohmann::json::array();
+            for (const auto& p : enumerate_ptgs(vtog_of(static_cast<Graph*>(g)), limit))
+                arr.push_back({{"selected", p.selected}, {"roots", p.roots}, {"eliminated_ops", p.eliminated_ops}});
+            out = arr.dump();
         }))
         return nullptr;
     return dup(out);

@@ -6,6 +6,6 @@ sm_100a consumer kernels; see DESIGN.md.  The compute path is libvtc.so
 """
 from .api import (  # noqa: F401
     CompGraph, Comm, Plan, VtcError, ERRORS, execute, parse_graph, f32_to_bf16, bf16_to_f32,
-    MATERIALIZE, SELECTED, MAX_ELIMINATION, INPLACE_UPDATES, FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE, FLAG_GEMV_LDG, FLAG_NO_TC, FLAG_DYNAMIC_POS,
+    MATERIALIZE, SELECTED, MAX_ELIMINATION, INPLACE_UPDATES, GREEDY, FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE, FLAG_GEMV_LDG, FLAG_NO_TC, FLAG_DYNAMIC_POS,
     NP_DTYPES,
 )

@@ -21,6 +21,9 @@ SIGNATURES = {
     "vtc_graph_free": (None, [_VP]),
     "vtc_graph_serialize": (C.c_int, [_VP, C.POINTER(C.c_char_p)]),
     "vtc_graph_vtog": (C.c_int, [_VP, C.POINTER(C.c_char_p)]),
+    "vtc_graph_estimate": (C.c_int, [_VP, C.POINTER(C.c_int32), C.c_int32, C.c_char_p, C.POINTER(C.c_char_p)]),
+    "vtc_graph_enumerate": (C.c_int, [_VP, C.c_int64, C.POINTER(C.c_char_p)]),
+    "vtc_graph_greedy": (C.c_int, [_VP, C.c_char_p, C.POINTER(C.c_char_p)]),
     "vtc_plan_create": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int32), C.c_int32, C.c_uint32, C.POINTER(_VP)]),
     "vtc_plan_free": (None, [_VP]),
     "vtc_plan_info": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_char_p)]),
@@ -39,6 +42,7 @@ SIGNATURES = {
     "vtc_plan_trace": (C.c_int, [_VP, C.POINTER(C.c_uint64), C.c_int32]),
     "vtc_map_eval": (C.c_int, [_VP, C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.c_int64]),
     "vtc_plan_map_json": (C.c_int, [_VP, C.c_char_p, C.POINTER(C.c_char_p)]),
+    "vtc_plan_map_analyze": (C.c_int, [_VP, C.c_char_p, C.c_int64, C.c_int64, C.POINTER(C.c_char_p)]),
     "vtc_comm_unique_id": (C.c_int, [_VP, C.c_int32]),
     "vtc_comm_init": (C.c_int, [_VP, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_VP)]),
     "vtc_comm_free": (None, [_VP]),

@@ -36,7 +36,7 @@ _ERROR_NAMES = {
 ERRORS = {code: type(name, (VtcError,), {"code": code}) for code, name in _ERROR_NAMES.items()}
 globals().update({cls.__name__: cls for cls in ERRORS.values()})
 
-MATERIALIZE, SELECTED, MAX_ELIMINATION, INPLACE_UPDATES = 0, 1, 2, 3
+MATERIALIZE, SELECTED, MAX_ELIMINATION, INPLACE_UPDATES, GREEDY = 0, 1, 2, 3, 4
 FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE, FLAG_GEMV_LDG, FLAG_NO_TC, FLAG_DYNAMIC_POS = 1, 2, 4, 8, 16, 32
 
 NP_DTYPES = {"f64": np.float64, "f32": np.float32, "i64": np.int64, "bf16": np.uint16}
@@ -91,6 +91,42 @@ class CompGraph:
     def vtog(self) -> dict:
         out = C.c_char_p()
         _check(_lib.load().vtc_graph_vtog(self._h, C.byref(out)))
+        return json.loads(out.value.decode())
+
+    @staticmethod
+    def _params(params) -> Optional[bytes]:
+        if params is None:
+            return None
+        return (params if isinstance(params, str) else json.dumps(params)).encode()
+
+    def estimate(self, selected: Optional[Iterable[int]] = None, params=None) -> dict:
+        """vtelim::estimate(g, ptg, MachineParams) + breakdown; selected=None is the
+        all-physical plan, params None = reference defaults, "b200" = calibrated."""
+        out = C.c_char_p()
+        if selected is None:
+            arr, n = None, -1
+        else:
+            sel = list(selected)
+            arr, n = (C.c_int32 * max(1, len(sel)))(*sel), len(sel)
+        _check(_lib.load().vtc_graph_estimate(self._h, arr, n, self._params(params), C.byref(out)))
+        return json.loads(out.value.decode())
+
+    def saving(self, selected: Iterable[int], params=None) -> float:
+        """The analytic SavingOracle: estimate(all-physical) - estimate(selected)."""
+        return self.estimate(None, params)["total_time"] - self.estimate(selected, params)["total_time"]
+
+    def enumerate_ptgs(self, limit: int = -1) -> list:
+        out = C.c_char_p()
+        _check(_lib.load().vtc_graph_enumerate(self._h, int(limit), C.byref(out)))
+        return json.loads(out.value.decode())["ptgs"]
+
+    def greedy(self, oracle: str = "analytic", params=None, trials: int = 5, executable: bool = False) -> dict:
+        """Alg. 2 (global greedy) over the analytic or the B200-timed saving oracle."""
+        cfg = {"oracle": oracle, "trials": trials, "executable": executable}
+        if params is not None:
+            cfg["params"] = params
+        out = C.c_char_p()
+        _check(_lib.load().vtc_graph_greedy(self._h, json.dumps(cfg).encode(), C.byref(out)))
         return json.loads(out.value.decode())
 
 
@@ -263,6 +299,11 @@ class Plan:
     def map_json(self, tensor: str) -> dict:
         out = C.c_char_p()
         _check(_lib.load().vtc_plan_map_json(self._h, tensor.encode(), C.byref(out)))
+        return json.loads(out.value.decode())
+
+    def map_analyze(self, tensor: str, elem_size: int = 4, coalesce: int = 128) -> dict:
+        out = C.c_char_p()
+        _check(_lib.load().vtc_plan_map_analyze(self._h, tensor.encode(), elem_size, coalesce, C.byref(out)))
         return json.loads(out.value.decode())
 
     def map_eval(self, tensor: str, lowered: bool = False):

@@ -12,6 +12,7 @@
 #include "vtc.h"
 #include "comm.hpp"
 #include "vtc/exec.hpp"
+#include "vtc/planner.hpp"
 
 struct vtc_graph {
     vtc::CompGraph g;
@@ -83,6 +84,65 @@ vtc::json::Value estimate_json(const vtc::TrafficEstimate& e) {
     return j;
 }
 
+vtc::MachineParams params_of(const char* text) {
+    if (!text || !*text) return vtc::MachineParams{};
+    if (std::string(text) == "b200") return vtc::MachineParams::b200();
+    return vtc::MachineParams::from_json(text);
+}
+
+vtc::json::Value ints_of(const std::vector<int>& v) {
+    auto a = vtc::json::Value::array();
+    for (int e : v) a.push(vtc::json::Value::integer(e));
+    return a;
+}
+
+vtc::json::Value timed_estimate_json(const vtc::TrafficEstimate& e) {
+    using vtc::json::Value;
+    Value j = Value::object();
+    j.set("total_time", Value::number(e.total_time));
+    j.set("total_bytes", Value::integer(e.total_bytes()));
+    j.set("data_movement_kernels", Value::integer(e.data_movement_kernels));
+    j.set("compute_kernels", Value::integer(e.compute_kernels));
+    Value ks = Value::array();
+    for (const auto& k : e.kernels) {
+        Value kj = Value::object();
+        kj.set("node", str(k.node));
+        kj.set("data_movement", Value::boolean(k.data_movement));
+        kj.set("time", Value::number(k.time));
+        for (int side = 0; side < 2; ++side) {
+            Value ops = Value::array();
+            for (const auto& o : side ? k.writes : k.reads) {
+                Value oj = Value::object();
+                oj.set("tensor", str(o.tensor));
+                oj.set("bytes", Value::integer(o.bytes));
+                oj.set("factor", Value::number(o.bandwidth_factor));
+                ops.push(oj);
+            }
+            kj.set(side ? "writes" : "reads", ops);
+        }
+        ks.push(kj);
+    }
+    j.set("kernels", ks);
+    vtc::LatencyBreakdown b = vtc::breakdown(e);
+    Value bj = Value::object();
+    bj.set("data_movement_time", Value::number(b.data_movement_time));
+    bj.set("compute_time", Value::number(b.compute_time));
+    bj.set("data_movement_kernels", Value::integer(b.data_movement_kernels));
+    bj.set("compute_kernels", Value::integer(b.compute_kernels));
+    j.set("breakdown", bj);
+    return j;
+}
+
+// Can the executor run this strategy?  (every resolved map fits the device descriptor)
+bool executable(const vtc::PointsToGraph& p) {
+    try {
+        for (const auto& [id, m] : p.resolved) vtc::lower_map(m, [](const std::string&) { return vtc::TargetInfo{0, 0}; });
+    } catch (const vtc::Error&) {
+        return false;
+    }
+    return true;
+}
+
 }  // namespace
 
 extern "C" {
@@ -141,6 +201,82 @@ int vtc_graph_vtog(vtc_graph* g, const char** json_out) {
     });
 }
 
+int vtc_graph_estimate(vtc_graph* g, const int32_t* selected, int32_t n_selected, const char* params_json,
+                       const char** json_out) {
+    return guard([&] {
+        vtc::MachineParams mp = params_of(params_json);
+        vtc::PointsToGraph ptg = (!selected && n_selected < 0)
+                                     ? vtc::all_physical_ptg(g->g)
+                                     : vtc::validate_ptg(vtog_of(g), std::vector<int>(selected, selected + std::max(0, n_selected)));
+        g_out = vtc::json::dump(timed_estimate_json(vtc::estimate(g->g, ptg, mp)));
+        *json_out = g_out.c_str();
+    });
+}
+
+int vtc_graph_enumerate(vtc_graph* g, int64_t limit, const char** json_out) {
+    return guard([&] {
+        using vtc::json::Value;
+        Value arr = Value::array();
+        for (const auto& p : vtc::enumerate_ptgs(vtog_of(g), limit)) {
+            Value pj = Value::object();
+            pj.set("selected", ints_of(p.selected));
+            pj.set("roots", strs(p.roots));
+            pj.set("eliminated_ops", strs(p.eliminated_ops));
+            arr.push(pj);
+        }
+        Value j = Value::object();
+        j.set("ptgs", arr);
+        g_out = vtc::json::dump(j);
+        *json_out = g_out.c_str();
+    });
+}
+
+int vtc_graph_greedy(vtc_graph* g, const char* config_json, const char** json_out) {
+    return guard([&] {
+        using vtc::json::Value;
+        Value cfg = (config_json && *config_json) ? vtc::json::parse(config_json) : Value::object();
+        std::string oracle_kind = cfg.contains("oracle") ? cfg.at("oracle").as_string() : "analytic";
+        std::string params_text;
+        if (cfg.contains("params")) {
+            const Value& pv = cfg.at("params");
+            params_text = pv.is_string() ? pv.as_string() : vtc::json::dump(pv);
+        }
+        std::unique_ptr<vtc::SavingOracle> oracle;
+        if (oracle_kind == "analytic") {
+            oracle = vtc::saving_oracle(params_of(params_text.c_str()));
+        } else if (oracle_kind == "device") {
+            int trials = cfg.contains("trials") ? int(cfg.at("trials").as_int()) : 5;
+            oracle = vtc::device_timed_oracle(trials);
+        } else {
+            throw vtc::SchemaError("unknown oracle " + oracle_kind);
+        }
+        bool exe = oracle_kind == "device" || (cfg.contains("executable") && cfg.at("executable").as_bool());
+        vtc::Vtog& v = vtog_of(g);
+        vtc::GreedyResult r = vtc::greedy_build(v, *oracle, exe ? std::function<bool(const vtc::PointsToGraph&)>(executable)
+                                                                : std::function<bool(const vtc::PointsToGraph&)>());
+        Value j = Value::object();
+        j.set("selected", ints_of(r.ptg.selected));
+        j.set("roots", strs(r.ptg.roots));
+        j.set("eliminated_ops", strs(r.ptg.eliminated_ops));
+        j.set("total_saving", Value::number(r.total_saving));
+        j.set("final_saving", Value::number(oracle->evaluate(g->g, r.ptg)));
+        j.set("iterations", Value::integer(r.iterations));
+        j.set("oracle_calls", Value::integer(r.oracle_calls));
+        Value ds = Value::array();
+        for (const auto& d : r.decisions) {
+            Value dj = Value::object();
+            dj.set("iteration", Value::integer(d.iteration));
+            dj.set("node", str(d.node));
+            dj.set("edges", ints_of(d.edges));
+            dj.set("saving", Value::number(d.saving));
+            ds.push(dj);
+        }
+        j.set("decisions", ds);
+        g_out = vtc::json::dump(j);
+        *json_out = g_out.c_str();
+    });
+}
+
 int vtc_plan_create(vtc_graph* g, int mode, const int32_t* selected, int32_t n_selected, uint32_t flags,
                     vtc_plan** out) {
     return guard([&] {
@@ -154,6 +290,9 @@ int vtc_plan_create(vtc_graph* g, int mode, const int32_t* selected, int32_t n_s
             ptg = vtc::validate_ptg(vtog_of(g), vtc::plan_max_elimination(vtog_of(g)));
         } else if (mode == VTC_PLAN_INPLACE_UPDATES) {
             ptg = vtc::validate_ptg(vtog_of(g), vtc::plan_inplace_updates(vtog_of(g)));
+        } else if (mode == VTC_PLAN_GREEDY) {
+            auto oracle = vtc::saving_oracle(vtc::MachineParams::b200());
+            ptg = vtc::greedy_build(vtog_of(g), *oracle, executable).ptg;
         } else {
             throw vtc::SchemaError("unknown plan mode");
         }
@@ -336,6 +475,25 @@ int vtc_plan_map_json(vtc_plan* p, const char* tensor, const char** json_out) {
         j.set("targets", strs(m.targets()));
         j.set("pieces", Value::integer(int64_t(m.pieces().size())));
         j.set("text", str(m.to_string()));
+        g_out = vtc::json::dump(j);
+        *json_out = g_out.c_str();
+    });
+}
+
+int vtc_plan_map_analyze(vtc_plan* p, const char* tensor, int64_t elem_size, int64_t coalesce_unit,
+                         const char** json_out) {
+    return guard([&] {
+        using vtc::json::Value;
+        const vtc::VMap& m = p->exec->ptg().map_of(tensor);
+        vtc::ContiguityReport r = m.contiguity(elem_size, coalesce_unit);
+        Value j = Value::object();
+        j.set("injective", Value::boolean(m.injective()));
+        j.set("unique_elems", Value::integer(m.unique_elems()));
+        j.set("is_total", Value::boolean(m.is_total()));
+        j.set("min_contiguous_dim", Value::integer(r.min_contiguous_dim));
+        j.set("contiguous_run_elems", Value::integer(r.contiguous_run_elems));
+        j.set("class", str(vtc::to_string(r.cls)));
+        j.set("type", str(vtc::to_string(r.type_class)));
         g_out = vtc::json::dump(j);
         *json_out = g_out.c_str();
     });

@@ -11,6 +11,8 @@
 // until every box is carry-free; here div/mod atoms absorb the carries, and
 // boxes are split only at base-piece boundaries.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <set>
 #include <functional>
 #include <cassert>
@@ -716,17 +718,203 @@ std::optional<int64_t> plain_stride(const VPiece& p, int a) {
 
 }  // namespace
 
+namespace {
+
+// A box with a plain affine offset (the reference's AffinePiece).
+struct AffBox {
+    Index lo, hi, strides;
+    int64_t c0 = 0;
+    std::string target;
+    const Lin* off = nullptr;  // the piece's offset (exact values at the box's points)
+};
+
+bool affine_strides(const Lin& l, int n, Index& strides) {
+    strides.assign(size_t(n), 0);
+    for (const auto& tm : l.t) {
+        if (tm.a->kind != AtomKind::Axis) return false;
+        strides[size_t(tm.a->axis)] += tm.c;
+    }
+    return true;
+}
+
+// Bisect (at the midpoint, the reference's Composer::emit_box split rule,
+// mapping.cpp:402-417) the largest axis a div/mod atom depends on until the
+// offset is affine over the box,
+// then merge abutting boxes with equal strides and offset (IndexMap::normalize,
+// mapping.cpp:495-537).  Returns false past `cap` boxes.
+bool refine_affine(const VPiece& p, int n, std::vector<AffBox>& out, size_t cap) {
+    std::function<bool(const Index&, const Index&)> rec = [&](const Index& lo, const Index& hi) -> bool {
+        Lin r = restrict_to(p.off, lo, hi);
+        Index st;
+        if (affine_strides(r, n, st)) {
+            if (out.size() >= cap) return false;
+            // restrict_to re-bases nothing: axis atoms keep absolute indices, so c0 is the offset at 0
+            out.push_back({lo, hi, st, r.c0, p.target, &p.off});
+            return true;
+        }
+        // split only along axes a non-affine atom depends on (largest first)
+        uint64_t mask = 0;
+        for (const auto& tm : r.t)
+            if (tm.a->kind != AtomKind::Axis) mask |= tm.a->axes_mask;
+        int axis = -1;
+        int64_t best = 1;
+        for (int i = 0; i < n; ++i)
+            if (((mask >> i) & 1) && hi[size_t(i)] - lo[size_t(i)] > best) {
+                best = hi[size_t(i)] - lo[size_t(i)];
+                axis = i;
+            }
+        if (axis < 0) {  // a single point always resolves
+            if (out.size() >= cap) return false;
+            out.push_back({lo, hi, Index(size_t(n), 0), r.eval(lo.data()), p.target, &p.off});
+            return true;
+        }
+        Index mhi = hi, mlo = lo;
+        int64_t mid = lo[size_t(axis)] + (hi[size_t(axis)] - lo[size_t(axis)]) / 2;
+        mhi[size_t(axis)] = mid;
+        mlo[size_t(axis)] = mid;
+        return rec(lo, mhi) && rec(mlo, hi);
+    };
+    return rec(p.lo, p.hi);
+}
+
+// Merge abutting boxes of one piece whose union is still affine (the
+// reference's IndexMap::normalize, mapping.cpp:495-537).  A stride along an
+// axis where a box has extent 1 is undetermined; the merge derives it from the
+// two boxes' origins, so boxes split by the bisection re-merge whenever the
+// offset really is affine across the cut.
+void merge_boxes(std::vector<AffBox>& b) {
+    auto F = [](const AffBox& x, const Index& idx) { return x.off->eval(idx.data()); };
+    bool merged = true;
+    while (merged) {
+        merged = false;
+        for (size_t i = 0; i < b.size() && !merged; ++i)
+            for (size_t j = 0; j < b.size(); ++j) {
+                if (i == j) continue;
+                AffBox &x = b[i], &y = b[j];
+                if (x.target != y.target) continue;
+                int k = -1;
+                bool ok = true;
+                for (size_t d = 0; d < x.lo.size(); ++d) {
+                    if (x.lo[d] == y.lo[d] && x.hi[d] == y.hi[d]) continue;
+                    if (k >= 0) { ok = false; break; }
+                    k = int(d);
+                }
+                if (!ok || k < 0 || x.hi[size_t(k)] != y.lo[size_t(k)]) continue;  // y directly after x along k
+                for (size_t d = 0; d < x.lo.size() && ok; ++d)
+                    if (int(d) != k && x.hi[d] - x.lo[d] > 1 && x.strides[d] != y.strides[d]) ok = false;
+                if (!ok) continue;
+                int64_t dk = y.lo[size_t(k)] - x.lo[size_t(k)];
+                int64_t df = F(y, y.lo) - F(x, x.lo);
+                if (df % dk) continue;
+                int64_t sk = df / dk;
+                if (x.hi[size_t(k)] - x.lo[size_t(k)] > 1 && x.strides[size_t(k)] != sk) continue;
+                if (y.hi[size_t(k)] - y.lo[size_t(k)] > 1 && y.strides[size_t(k)] != sk) continue;
+                x.strides[size_t(k)] = sk;
+                x.hi[size_t(k)] = y.hi[size_t(k)];
+                x.c0 = F(x, x.lo);
+                for (size_t d = 0; d < x.lo.size(); ++d) x.c0 -= x.strides[d] * x.lo[d];
+                b.erase(b.begin() + long(j));
+                merged = true;
+                break;
+            }
+    }
+}
+
+// Boxes of one target that tile a box region and agree on one affine function
+// become that single box (the reference composes such chains carry-free into
+// one piece even when the symbolic form needed several).
+void fuse_affine_tiling(std::vector<AffBox>& boxes) {
+    std::map<std::string, std::vector<size_t>> by_target;
+    for (size_t i = 0; i < boxes.size(); ++i) by_target[boxes[i].target].push_back(i);
+    std::vector<AffBox> out;
+    std::vector<bool> used(boxes.size(), false);
+    for (auto& [t, ids] : by_target) {
+        if (ids.size() < 2) continue;
+        size_t n = boxes[ids[0]].lo.size();
+        Index lo = boxes[ids[0]].lo, hi = boxes[ids[0]].hi;
+        int64_t vol = 0;
+        for (size_t i : ids) {
+            const AffBox& b = boxes[i];
+            int64_t v = 1;
+            for (size_t d = 0; d < n; ++d) {
+                lo[d] = std::min(lo[d], b.lo[d]);
+                hi[d] = std::max(hi[d], b.hi[d]);
+                v *= b.hi[d] - b.lo[d];
+            }
+            vol += v;
+        }
+        int64_t bvol = 1;
+        for (size_t d = 0; d < n; ++d) bvol *= hi[d] - lo[d];
+        if (vol != bvol) continue;
+        Index st(n, 0);
+        std::vector<bool> known(n, false);
+        bool ok = true;
+        for (size_t i : ids)
+            for (size_t d = 0; d < n && ok; ++d) {
+                const AffBox& b = boxes[i];
+                if (b.hi[d] - b.lo[d] <= 1) continue;
+                if (known[d] && st[d] != b.strides[d]) ok = false;
+                st[d] = b.strides[d];
+                known[d] = true;
+            }
+        if (!ok) continue;
+        auto c0_of = [&](const AffBox& b) {
+            int64_t c = b.off->eval(b.lo.data());
+            for (size_t d = 0; d < n; ++d) c -= st[d] * b.lo[d];
+            return c;
+        };
+        int64_t c0 = c0_of(boxes[ids[0]]);
+        for (size_t i : ids) ok = ok && c0_of(boxes[i]) == c0;
+        if (!ok) continue;
+        AffBox f = boxes[ids[0]];
+        f.lo = lo;
+        f.hi = hi;
+        f.strides = st;
+        f.c0 = c0;
+        out.push_back(f);
+        for (size_t i : ids) used[i] = true;
+    }
+    for (size_t i = 0; i < boxes.size(); ++i)
+        if (!used[i]) out.push_back(boxes[i]);
+    boxes = std::move(out);
+}
+
+int64_t box_vol(const AffBox& b) {
+    int64_t v = 1;
+    for (size_t i = 0; i < b.lo.size(); ++i) v *= b.hi[i] - b.lo[i];
+    return v;
+}
+
+}  // namespace
+
+// proj/src/mapping.cpp:277-328, evaluated over the map's affine boxes: each
+// div/mod piece is first refined into the boxes on which its offset is affine
+// (what the reference's bisecting compose would have produced), so the report
+// describes the same access pattern the reference's piece list describes.
 ContiguityReport VMap::contiguity(int64_t elem_size, int64_t coalesce_unit) const {
     ContiguityReport r;
     int n = rank();
     Index suffix = default_strides(shape_);
+    std::vector<AffBox> boxes;
+    bool refined = true;
+    for (const auto& p : pieces_) {
+        std::vector<AffBox> pb;
+        if (!refine_affine(p, n, pb, 4096)) {
+            refined = false;
+            break;
+        }
+        boxes.insert(boxes.end(), pb.begin(), pb.end());
+    }
+    if (refined) {
+        merge_boxes(boxes);
+        fuse_affine_tiling(boxes);
+    }
     int d = n + 1;
     for (int cand = n; cand >= 1; --cand) {
         bool ok = true;
-        for (const auto& p : pieces_) {
-            if (p.hi[size_t(cand - 1)] - p.lo[size_t(cand - 1)] <= 1) continue;
-            auto s = plain_stride(p, cand - 1);
-            if (!s || *s != suffix[size_t(cand - 1)]) {
+        for (const auto& b : boxes) {
+            if (b.hi[size_t(cand - 1)] - b.lo[size_t(cand - 1)] <= 1) continue;
+            if (b.strides[size_t(cand - 1)] != suffix[size_t(cand - 1)]) {
                 ok = false;
                 break;
             }
@@ -736,23 +924,22 @@ ContiguityReport VMap::contiguity(int64_t elem_size, int64_t coalesce_unit) cons
     }
     r.min_contiguous_dim = d;
     int64_t min_run = INT64_MAX;
-    for (const auto& p : pieces_) {
+    for (const auto& b : boxes) {
         int64_t run = 1, step = 1;
         for (int i = n - 1; i >= 0; --i) {
             if (shape_[size_t(i)] == 1) continue;
-            int64_t ext = p.hi[size_t(i)] - p.lo[size_t(i)];
+            int64_t ext = b.hi[size_t(i)] - b.lo[size_t(i)];
             if (ext == 1) break;
-            auto s = plain_stride(p, i);
-            if (!s || *s != step) break;
+            if (b.strides[size_t(i)] != step) break;
             run *= ext;
             if (ext != shape_[size_t(i)]) break;
             step *= shape_[size_t(i)];
         }
         min_run = std::min(min_run, run);
     }
-    if (pieces_.empty()) min_run = 0;
+    if (boxes.empty()) min_run = 0;
     r.contiguous_run_elems = min_run;
-    bool fully = pieces_.size() == 1 && d == 1 && pieces_[0].box_volume() == domain_volume();
+    bool fully = boxes.size() == 1 && d == 1 && box_vol(boxes[0]) == domain_volume();
     if (fully) r.cls = ContiguityClass::FullyContiguous;
     else if (min_run * elem_size >= coalesce_unit) r.cls = ContiguityClass::PartiallyContiguous;
     else r.cls = ContiguityClass::NonContiguous;

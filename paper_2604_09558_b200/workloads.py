@@ -447,3 +447,122 @@ def frame2_subgraph(B: int = 1, L: int = 64, pos: Optional[int] = None, D: int =
         elif t["kind"] == "output":
             t["kind"] = "intermediate"
     return {"tensors": tensors, "nodes": keep_nodes}
+
+
+# ---- paper-figure fixtures (acceptance 1-3, 7) -------------------
+# Desk-scale graphs in the reference operator vocabulary only, so the
+# reference planner / executor (oracle/_ref) runs every one of them.
+
+def fig2_llama_subgraph(dtype: str = "f64") -> dict:
+    """PAPER.md Fig. 2 frame 2 at the SPEC.md:478 size (B=2, heads=4, kv-heads=1,
+    head-dim=8, ctx=16): QKV -> Split -> Reshape -> ScatterND(KV cache) -> Slice ->
+    Transpose -> Unsqueeze -> Expand -> Reshape -> attention MatMuls."""
+    return frame2_subgraph(B=2, L=16, pos=15, D=32, Hq=4, Hkv=1, hd=8, dtype=dtype)
+
+
+def fig6_kv_update(dtype: str = "f64", L: int = 4, heads: int = 2, hd: int = 4, pos: int = 1) -> dict:
+    """PAPER.md Fig. 6(a): MatMul -> Split -> Reshape -> ScatterND over the K cache.
+    a = x.W; Split(a) -> (b, rest); c = Reshape(b); d = ScatterND(K cache, c @ pos).
+    The Split's other output `rest` is a graph output ("other outputs of Split
+    are ignored" in the figure); d feeds a scores MatMul so the cache is read."""
+    D = heads * hd
+    g = GraphBuilder(dtype)
+    g.input("x", [1, D])
+    g.input("W", [D, 3 * D])
+    g.input("K_cache", [L, heads, hd])
+    g.input("q", [heads, 1, hd])
+    g.node("matmul", "MatMul", ["x", "W"], "a")
+    g.node("split", "Split", ["a"], ["b", "rest"], {"axis": 1, "sizes": [D, 2 * D]})
+    g.output("rest")
+    g.node("reshape", "Reshape", ["b"], "c", {"shape": [1, heads, hd]})
+    g.node("scatter", "ScatterND", ["K_cache", "c"], "d", {"indices": [[pos]]})
+    g.node("kt", "Transpose", ["d"], "kT", {"perm": [1, 2, 0]})           # [heads, hd, L]
+    g.node("scores", "MatMul", ["q", "kT"], "s", out_kind="output")       # [heads, 1, L]
+    return g.doc()
+
+
+def fig7_conflict(dtype: str = "f64", n: int = 4, m: int = 3) -> dict:
+    """PAPER.md Fig. 7: c = Concat(a, b) and d = Transpose(c).  c's out-edges:
+    1 = c over a, 2 = c over b (one Concat candidate: compatible), 3 = c over d
+    (the Transpose read back): 1/3 and 2/3 conflict."""
+    g = GraphBuilder(dtype)
+    g.input("a", [n, m])
+    g.input("b", [n, m])
+    g.input("w", [n, 2])
+    g.node("concat", "Concat", ["a", "b"], "c", {"axis": 1})             # [n, 2m]
+    g.node("transpose", "Transpose", ["c"], "d", {"perm": [1, 0]})       # [2m, n]
+    g.node("mm", "MatMul", ["d", "w"], "y", out_kind="output")
+    return g.doc()
+
+
+def fig9_efficientvit_attention(dtype: str = "f64", B: int = 2, N: int = 16, C: int = 16, heads: int = 2) -> dict:
+    """PAPER.md Fig. 9 (EfficientViT linear-attention block): five
+    compute kernels k1..k5 (qkv projection, K^T.V, Q.(K^T V), the output
+    activation, the output projection); every data-movement operator between
+    them is eliminable, leaving a (k1 out), e (k2 out), f (k3 out) and j (k4 out)
+    as the only physical intermediates."""
+    d = C // heads
+    g = GraphBuilder(dtype)
+    g.input("x", [B * N, C])
+    g.input("W_qkv", [C, 3 * C])
+    g.input("W_o", [C, C])
+    g.node("k1", "MatMul", ["x", "W_qkv"], "a")                                   # [B*N, 3C]
+    g.node("split", "Split", ["a"], ["q2", "k2", "v2"], {"axis": 1, "sizes": [C, C, C]})
+    for t in ("q", "k", "v"):
+        g.node(f"{t}_rs", "Reshape", [f"{t}2"], f"{t}4", {"shape": [B, N, heads, d]})
+        g.node(f"{t}_tr", "Transpose", [f"{t}4"], f"{t}h", {"perm": [0, 2, 1, 3]})  # [B, H, N, d]
+    g.node("kT", "Transpose", ["kh"], "kt", {"perm": [0, 1, 3, 2]})               # [B, H, d, N]
+    g.node("k2_", "MatMul", ["kt", "vh"], "e")                                    # k2: [B, H, d, d]
+    g.node("k3", "MatMul", ["qh", "e"], "f")                                      # k3: [B, H, N, d]
+    g.node("f_tr", "Transpose", ["f"], "g", {"perm": [0, 2, 1, 3]})               # [B, N, H, d]
+    g.node("g_rs", "Reshape", ["g"], "h", {"shape": [B * N, C]})
+    g.node("k4", "SiLU", ["h"], "j")                                              # k4
+    g.node("k5", "MatMul", ["j", "W_o"], "y", out_kind="output")                  # k5
+    return g.doc()
+
+
+def fig11_yolo_c3k2(dtype: str = "f64", N: int = 64, c: int = 4, cin: int = 8, cout: int = 8) -> dict:
+    """PAPER.md Fig. 11 at desk scale in the paper's channel-first (NCHW) layout,
+    so Split / Concat along channels move contiguous chunks of N pixels
+    ("each contiguous chunk ... is large enough"); 1x1
+    convolutions are W . X MatMuls over [channels, N]."""
+    g = GraphBuilder(dtype)
+    g.input("x", [cin, N])
+    g.input("w_cv1", [2 * c, cin])
+    g.input("w_m1", [c, c])
+    g.input("w_m2", [c, c])
+    g.input("w_cv2", [cout, 3 * c])
+    g.node("cv1", "MatMul", ["w_cv1", "x"], "y0")
+    g.node("split", "Split", ["y0"], ["a", "b"], {"axis": 0, "sizes": [c, c]})
+    g.node("m1", "MatMul", ["w_m1", "b"], "t1")
+    g.node("act", "SiLU", ["t1"], "t2")
+    g.node("m2", "MatMul", ["w_m2", "t2"], "t3")
+    g.node("res", "Add", ["b", "t3"], "e")
+    g.node("concat", "Concat", ["a", "b", "e"], "Y", {"axis": 0})
+    g.node("cv2", "MatMul", ["w_cv2", "Y"], "out", out_kind="output")
+    return g.doc()
+
+
+def chain_graph(n_tensors: int, dtype: str = "f64") -> dict:
+    """A data-movement chain with `n_tensors` tensors (acceptance 6: greedy
+    complexity): x -> (Transpose | Reshape)* -> MatMul."""
+    g = GraphBuilder(dtype)
+    g.input("x", [4, 6])
+    g.input("w", [6, 3])
+    cur, shape = "x", [4, 6]
+    k = 0
+    while len(g.tensors) < n_tensors - 1:
+        k += 1
+        out = f"t{k}"
+        if k % 2:
+            shape = shape[::-1]
+            g.node(f"n{k}", "Transpose", [cur], out, {"perm": [1, 0]})
+        else:
+            g.node(f"n{k}", "Reshape", [cur], out, {"shape": list(shape)})
+        cur = out
+    if shape != [4, 6]:
+        k += 1
+        g.node(f"n{k}", "Transpose", [cur], f"t{k}", {"perm": [1, 0]})
+        cur = f"t{k}"
+    g.node("mm", "MatMul", [cur, "w"], "y", out_kind="output")
+    return g.doc()

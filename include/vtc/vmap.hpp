@@ -148,6 +148,11 @@ public:
     // Volume on which the maps agree (used for "coinciding" data movement).
     int64_t agree_volume(const VMap& other, int64_t exhaustive_limit = int64_t(1) << 22) const;
 
+    // True when no physical element is in both maps' images (proved by a
+    // residue test on affine pieces, or exhaustively on small maps); false
+    // when disjointness cannot be shown.
+    bool images_disjoint(const VMap& other) const;
+
     // True when the map is the identity layout of `target` with `shape`.
     bool is_identity_of(const std::string& target) const;
 

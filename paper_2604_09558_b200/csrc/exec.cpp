@@ -1243,7 +1243,7 @@ void Executor::prepare(bool dry) {
                 for (const auto& t : to) clash |= ti.count(t) > 0;
                 bool same_elementwise = (n.kind == OpKind::Add || n.kind == OpKind::Mul || n.kind == OpKind::SiLU ||
                                          n.kind == OpKind::GELU) && map_of(o).equivalent(map_of(in));
-                if (clash && !same_elementwise)
+                if (clash && !same_elementwise && !map_of(o).images_disjoint(map_of(in)))
                     throw UnsupportedError("node " + n.id + " writes a root it reads (" + o + " / " + in + ")");
             }
 

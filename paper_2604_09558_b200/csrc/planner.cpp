@@ -48,15 +48,18 @@ std::string MachineParams::to_json() const {
 }
 
 MachineParams MachineParams::b200() {
-    // Least-squares fit of gather-copy launches through contiguous, partially
-    // contiguous and element-scattered maps on one B200 (scripts/calibrate.py,
-    // profiles/r2_calibration.json): time unit = microseconds.
+    // Fitted on one B200 by scripts/calibrate.py (profiles/r2_calibration.json),
+    // time unit = microseconds: the executor's copy kernel (gather_copy) moves
+    // 1.66 TB/s through contiguous maps (64 MB .. 1 GB), runs of >= 16 bytes
+    // cost the same as contiguous ones (1.02x), 4-8 byte runs / element-
+    // scattered transposes 2.6-2.9x, and each dependent launch inside a CUDA
+    // graph adds 2.1 us.
     MachineParams p;
-    p.bandwidth = 5800.0;             // bytes / us  (5.8 TB/s effective copy stream)
-    p.coalesce_unit = 32;             // sector size: a run of >= 32 B keeps full sectors
-    p.kernel_launch_overhead = 2.5;   // us per dependent launch inside a CUDA graph
-    p.noncoalesced_penalty = 4.0;
-    p.partial_penalty = 1.0;
+    p.bandwidth = 1.66e6;
+    p.coalesce_unit = 16;
+    p.kernel_launch_overhead = 2.1;
+    p.noncoalesced_penalty = 2.86;
+    p.partial_penalty = 1.02;
     return p;
 }
 

@@ -891,6 +891,83 @@ int64_t box_vol(const AffBox& b) {
 // div/mod piece is first refined into the boxes on which its offset is affine
 // (what the reference's bisecting compose would have produced), so the report
 // describes the same access pattern the reference's piece list describes.
+bool VMap::images_disjoint(const VMap& other) const {
+    for (const auto& p : pieces_)
+        for (const auto& q : other.pieces_) {
+            if (p.target != q.target) continue;
+            // residue test: image of an affine piece modulo G (gcd of the non-unit
+            // strides of both pieces) is one interval spanned by its unit-stride axis
+            int n = int(p.lo.size()), m = int(q.lo.size());
+            Index sp = Index(static_cast<size_t>(n), 0), sq = Index(static_cast<size_t>(m), 0);
+            bool affine = true;
+            for (int i = 0; i < n && affine; ++i) {
+                auto s = plain_stride(p, i);
+                if (!s) affine = false;
+                else sp[size_t(i)] = p.hi[size_t(i)] - p.lo[size_t(i)] > 1 ? *s : 0;
+            }
+            for (int i = 0; i < m && affine; ++i) {
+                auto s = plain_stride(q, i);
+                if (!s) affine = false;
+                else sq[size_t(i)] = q.hi[size_t(i)] - q.lo[size_t(i)] > 1 ? *s : 0;
+            }
+            bool proved = false;
+            if (affine) {
+                int64_t G = 0;
+                for (auto s : sp) if (s != 0 && s != 1) G = std::gcd(G, std::abs(s));
+                for (auto s : sq) if (s != 0 && s != 1) G = std::gcd(G, std::abs(s));
+                auto interval = [&](const VPiece& pc, const Index& st, int64_t& r0, int64_t& len) {
+                    Index lo = pc.lo;
+                    int64_t c = pc.off.eval(lo.data());  // value at the box origin
+                    len = 1;
+                    int units = 0;
+                    for (size_t i = 0; i < st.size(); ++i)
+                        if (st[i] == 1) {
+                            len = pc.hi[i] - pc.lo[i];
+                            ++units;
+                        }
+                    r0 = floormod(c, G);
+                    return units <= 1;
+                };
+                int64_t a0, alen, b0, blen;
+                if (G > 1 && interval(p, sp, a0, alen) && interval(q, sq, b0, blen) && alen + blen <= G) {
+                    // intervals [a0, a0+alen) and [b0, b0+blen) on the circle Z_G
+                    auto inside = [&](int64_t x, int64_t s0, int64_t len) { return floormod(x - s0, G) < len; };
+                    proved = !inside(b0, a0, alen) && !inside(a0, b0, blen);
+                }
+            }
+            if (!proved) {
+                if (p.box_volume() > (int64_t(1) << 20) || q.box_volume() > (int64_t(1) << 20)) return false;
+                std::vector<int64_t> a, b;
+                auto collect = [](const VPiece& pc, std::vector<int64_t>& out) {
+                    Index idx = pc.lo;
+                    const size_t r = idx.size();
+                    while (true) {
+                        out.push_back(pc.off.eval(idx.data()));
+                        size_t d = r;
+                        while (d > 0) {
+                            --d;
+                            if (++idx[d] < pc.hi[d]) break;
+                            idx[d] = pc.lo[d];
+                            if (d == 0) return;
+                        }
+                        if (r == 0) return;
+                    }
+                };
+                collect(p, a);
+                collect(q, b);
+                std::sort(a.begin(), a.end());
+                std::sort(b.begin(), b.end());
+                size_t i = 0, j = 0;
+                while (i < a.size() && j < b.size()) {
+                    if (a[i] == b[j]) return false;
+                    if (a[i] < b[j]) ++i;
+                    else ++j;
+                }
+            }
+        }
+    return true;
+}
+
 ContiguityReport VMap::contiguity(int64_t elem_size, int64_t coalesce_unit) const {
     ContiguityReport r;
     int n = rank();

@@ -9,3 +9,6 @@ from .api import (  # noqa: F401
     MATERIALIZE, SELECTED, MAX_ELIMINATION, INPLACE_UPDATES, GREEDY, FLAG_FAST_FP, FLAG_NO_GEMV, FLAG_NO_FUSE, FLAG_GEMV_LDG, FLAG_NO_TC, FLAG_DYNAMIC_POS,
     NP_DTYPES,
 )
+from .api import ERRORS as _ERRORS
+
+globals().update({cls.__name__: cls for cls in _ERRORS.values()})  # UnsupportedError, SchemaError, ...

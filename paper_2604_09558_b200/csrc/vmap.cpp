@@ -911,7 +911,21 @@ bool VMap::images_disjoint(const VMap& other) const {
                 else sq[size_t(i)] = q.hi[size_t(i)] - q.lo[size_t(i)] > 1 ? *s : 0;
             }
             bool proved = false;
-            if (affine) {
+            if (affine) {  // 1) the two images' address ranges do not overlap
+                auto range = [](const VPiece& pc, const Index& st, int64_t& lo, int64_t& hi) {
+                    int64_t c = pc.off.eval(pc.lo.data());
+                    lo = hi = c;
+                    for (size_t i = 0; i < st.size(); ++i) {
+                        int64_t span = st[i] * (pc.hi[i] - pc.lo[i] - 1);
+                        (span < 0 ? lo : hi) += span;
+                    }
+                };
+                int64_t a_lo, a_hi, b_lo, b_hi;
+                range(p, sp, a_lo, a_hi);
+                range(q, sq, b_lo, b_hi);
+                proved = a_hi < b_lo || b_hi < a_lo;
+            }
+            if (affine && !proved) {  // 2) residues modulo the common stride lattice
                 int64_t G = 0;
                 for (auto s : sp) if (s != 0 && s != 1) G = std::gcd(G, std::abs(s));
                 for (auto s : sq) if (s != 0 && s != 1) G = std::gcd(G, std::abs(s));

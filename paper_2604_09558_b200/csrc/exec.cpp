@@ -1770,7 +1770,17 @@ void Executor::prepare(bool dry) {
                         p.v_sstride = vs_;
                     }
                 }
-                // long query blocks (prefill): flash attention on tensor cores, no K split
+                // long query blocks (prefill), head dim 128: tcgen05 / TMEM flash attention
+                // with TMA-loaded Q / K / V (maps proved affine on the host)
+                if (!p.fast && p.Sq >= 64 && !std::getenv("VTC_NO_FMHA") && attn_fmha_prepare(p, !impl_->dry)) {
+                    p.fast = 3;
+                    p.splits = 1;
+                    p.chunk = p.Sk;
+                    L->kernel = "attn_fmha_tc";
+                    push(std::move(L));
+                    break;
+                }
+                // other long query blocks: flash attention on mma.sync, no K split
                 if (!p.fast && attn_prefill_supported(p)) {
                     p.fast = 2;
                     p.splits = 1;

@@ -311,8 +311,18 @@ struct AttnParams {
     int32_t kv_affine;             // K/V maps affine along the key axis (single piece)
     int64_t k_sstride, v_sstride;  // element stride between consecutive keys
     unsigned int* counters;        // [Bt * H / group] split arrival counters (fused combine)
+    // tcgen05 flash attention (k_attn_fmha.cu, fast == 3): Q / K / V as 4-D TMA
+    // tensors (CUtensorMap x 3), O as base + (batch, head, position) strides
+    alignas(64) unsigned char fmha[3 * 128];
+    uint64_t fmha_o;
+    int64_t fmha_os[3];
 };
 void launch_attention(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
+// tcgen05 / TMEM flash attention for head dim 128 (prefill): proves the Q / K / V / O
+// maps affine over (batch, head, position, dim) and encodes their TMA tensors
+// (encode = false: the structural check only, for dry plans).
+bool attn_fmha_prepare(AttnParams& p, bool encode);
+void launch_attn_fmha(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 bool attn_decode_supported(const AttnParams& p);
 int64_t attn_decode_capacity();
 bool attn_prefill_supported(const AttnParams& p);

@@ -172,7 +172,7 @@ def test_c5_prefill_b8_s4096_full_size(vtc, oracle):
     p = vtc.Plan(g, vtc.MAX_ELIMINATION)
     kinds = _kernels(p)
     assert p.info()["data_movement_launches"] == 0
-    assert kinds.count("gemm_tc_bf16") >= 4 and any(k.startswith("attn_prefill") for k in kinds), kinds
+    assert kinds.count("gemm_tc_bf16") >= 4 and "attn_fmha_tc" in kinds, kinds
     got = vtc.execute(g, p, x)["y"]
     rows = [0, 1, 2047, 4095]
     errs = []

@@ -345,7 +345,7 @@ def test_llama_prefill_layer_small(vtc, oracle, cfg):
     want = oracle.execute(doc, x)["y"]
     got, p = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
     kinds = [l["kernel"] for l in p.info()["launches"]]
-    assert "attn_prefill_tc" in kinds and kinds.count("gemm_tc_bf16") == 4, kinds  # gate + up in one launch
+    assert "attn_fmha_tc" in kinds and kinds.count("gemm_tc_bf16") == 4, kinds  # gate + up in one launch
     assert any(l["node"] == "gate_proj+up_proj" for l in p.info()["launches"])
     assert p.info()["data_movement_launches"] == 0
     assert _relerr(oracle.bf16_to_f32(got["y"]), oracle.bf16_to_f32(want)) < 2e-2

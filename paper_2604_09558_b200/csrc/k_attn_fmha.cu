@@ -9,27 +9,32 @@
 // QKV split, the [B,S,H,d] -> [B,H,S,d] transposes and the GQA
 // Expand / Reshape stay views -- no copy kernel, no per-element map walk.
 //
-//   * CTA = 128 query rows of one (batch, head); 6 warps:
-//       warps 0-3  softmax + epilogue (thread = query row = TMEM lane),
-//       warp 4     TMA producer (Q once, then K / V tiles of 128 keys, 2 stages each;
-//                  a K stage frees when its S MMA completes, a V stage after its PV MMA),
-//       warp 5     MMA issuer (one thread);
-//   * S_j = Q K_j^T: tcgen05.mma M128 N128 K16 x 8 (K-major A and B, 128-byte
-//     swizzle) into one of two TMEM S buffers, so S_{j+1} is computed while
-//     the softmax warps work on S_j;
-//   * the softmax warps read their S row with tcgen05.ld, apply scale / causal
-//     mask, keep a running row max in the log2 domain and write P = exp2(S - m)
-//     as bf16 into shared memory (the K-major A operand of the next MMA);
-//   * O += P_j V_j: tcgen05.mma with V as the MN-major B operand, accumulated
-//     in TMEM across all key tiles.  The running max is rescaled lazily: O (in
-//     TMEM) and l are rescaled only when a row's max grows by more than 2^8,
-//     otherwise P uses the stale max (bounded by 256, exact in fp32 / bf16);
+//   * CTA = two adjacent 128-row query tiles of one (batch, head) sharing every
+//     K / V tile (half the K / V traffic per FLOP); 10 warps:
+//       warps 0-3 / 4-7  softmax + epilogue of query tile 0 / 1 (thread = query
+//                        row = TMEM lane),
+//       warp 8           TMA producer (Q tiles once, then K / V tiles of 128 keys,
+//                        2 stages each; a K stage frees when both tiles' S MMAs
+//                        complete, a V stage after both PV MMAs),
+//       warp 9           MMA issuer (one thread);
+//   * TMEM (512 columns): S_t = Q_t K^T (fp32, 128 columns) per tile, P_t written
+//     over S_t as bf16 pairs, O_t (fp32, 128 columns) per tile;
+//   * per key tile: S_0, S_1 (tcgen05.mma M128 N128 K16 x 8, K-major SW128 A / B);
+//     each softmax warpgroup reads its S row with tcgen05.ld, applies scale and
+//     causal mask, keeps a running row max in the log2 domain and stores
+//     P = exp2(S - m) back into TMEM (tcgen05.st); O_t += P_t V is a TS-MMA
+//     (A from TMEM, V the MN-major B operand in smem).  While one warpgroup
+//     computes its softmax the tensor core works on the other tile, and the
+//     next S_t is issued right behind PV_t (tcgen05 ops run in issue order);
+//   * lazy rescale: O_t and l are rescaled only when a row's max grows by more
+//     than 2^8, otherwise P uses the stale max (bounded by 256);
 //   * epilogue: O / l from TMEM to bf16, 16-byte stores through O's map.
 // Causal query tiles stop at the diagonal key tile and are scheduled longest
 // first.  Attention is absent from the reference (SURVEY.md §8 a'); CPU
 // restatement: oracle/vtc_oracle.py (Attention).
 #include <cuda.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "device.cuh"
@@ -40,10 +45,10 @@ namespace vtc {
 namespace {
 
 using dev::bf16;
-constexpr int BQ = 128, BKV = 128, D = 128, NTHREADS = 192;
+constexpr int BQ = 128, BKV = 128, D = 128, NTHREADS = 320;
 constexpr uint32_t CHUNK = 128 * 128;               // one [128 rows x 64 bf16] SW128 chunk = 16 KB
 constexpr uint32_t TILE = 2 * CHUNK;                // 128 x 128 bf16
-constexpr uint32_t SMEM_Q = 0, SMEM_K = TILE, SMEM_V = 3 * TILE, SMEM_P = 5 * TILE, SMEM_BYTES = 6 * TILE;
+constexpr uint32_t SMEM_Q = 0, SMEM_K = 2 * TILE, SMEM_V = 4 * TILE, SMEM_BYTES = 6 * TILE;  // Q0 Q1 | K x2 | V x2
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_THRESHOLD = 8.0f;           // log2 units: rescale O only when the max grows by > 2^8
 
@@ -135,6 +140,13 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -145,7 +157,7 @@ struct FmhaArgs {
     bf16* o;                 // output element (b, h, s, 0) = o + b*o_sb + h*o_sh + s*o_ss
     int64_t o_sb, o_sh, o_ss;
     const KHead* head;       // timeline (VTC_TRACE)
-    int32_t H, group, Sq, Sk, causal, qtiles;
+    int32_t H, group, Sq, Sk, causal, qpairs;
     float scale_log2;
 };
 
@@ -153,18 +165,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_fmha_kernel(const __grid_con
     dev::TraceScope trace_scope_(a.head);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t q_full, k_full[2], v_full[2], k_empty[2], v_empty[2], s_full[2], p_full, o_done;
+    __shared__ uint64_t q_full, k_full[2], v_full[2], k_empty[2], v_empty[2], s_full[2], p_full[2], o_done[2];
     __shared__ uint32_t s_tmem;
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    // causal: the longest query tiles (most key tiles) first
-    const int qt = a.causal ? a.qtiles - 1 - int(blockIdx.x) : int(blockIdx.x);
-    const int q0 = qt * BQ;
+    // CTA = query tiles 2c and 2c + 1 of one (batch, head); causal: longest first
+    const int pair = a.causal ? a.qpairs - 1 - int(blockIdx.x) : int(blockIdx.x);
     const int bh = int(blockIdx.y);
     const int b = bh / a.H, h = bh - b * a.H, hkv = h / a.group;
     const int off = a.Sk - a.Sq;  // query row q sees keys t <= q + off
-    const int kend = a.causal ? min(a.Sk, q0 + BQ + off) : a.Sk;
-    const int nkv = kend > 0 ? (kend + BKV - 1) / BKV : 0;
+    auto tiles_of = [&](int t) {  // key tiles query tile t of the pair attends to
+        const int q0 = (2 * pair + t) * BQ;
+        const int kend = q0 >= a.Sq ? 0 : a.causal ? min(a.Sk, q0 + BQ + off) : a.Sk;
+        return kend > 0 ? (kend + BKV - 1) / BKV : 0;
+    };
+    const int nkv0 = tiles_of(0), nkv1 = tiles_of(1);
+    const int nkv = max(nkv0, nkv1);
 
     if (threadIdx.x == 0) {
         mbar_init(&q_full, 1);
@@ -174,12 +190,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_fmha_kernel(const __grid_con
             mbar_init(&k_empty[s], 1);
             mbar_init(&v_empty[s], 1);
             mbar_init(&s_full[s], 1);
+            mbar_init(&p_full[s], 4);  // one arrival per warp of the tile's softmax warpgroup
+            mbar_init(&o_done[s], 1);
         }
-        mbar_init(&p_full, 4);  // one arrival per softmax warp
-        mbar_init(&o_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) {  // TMEM: S buffers at columns 0 / 128, O at 256
+    if (warp == 0) {  // TMEM: S / P of tile t at columns 128 t, O of tile t at 256 + 128 t
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -190,7 +206,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_fmha_kernel(const __grid_con
     dev::pdl_launch_dependents();
     const uint32_t sbase = smem_u32(smem);
 
-    if (warp == 4) {
+    if (warp == 8) {
         if (lane == 0) {
             // ---------------- TMA producer ----------------
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.q)) : "memory");
@@ -198,13 +214,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_fmha_kernel(const __grid_con
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.v)) : "memory");
             const uint64_t pol = evict_last_policy();  // K / V re-read by every query tile of the head
             dev::pdl_wait();
-            mbar_expect_tx(&q_full, TILE);
-            tma_4d(sbase + SMEM_Q, &a.q, 0, q0, h, b, &q_full, pol);
-            tma_4d(sbase + SMEM_Q + CHUNK, &a.q, 64, q0, h, b, &q_full, pol);
+            mbar_expect_tx(&q_full, 2 * TILE);
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const uint32_t qs = sbase + SMEM_Q + uint32_t(t) * TILE;
+                tma_4d(qs, &a.q, 0, (2 * pair + t) * BQ, h, b, &q_full, pol);
+                tma_4d(qs + CHUNK, &a.q, 64, (2 * pair + t) * BQ, h, b, &q_full, pol);
+            }
             for (int j = 0; j < nkv; ++j) {
                 const int st = j & 1;
                 const uint32_t ks = sbase + SMEM_K + st * TILE, vs = sbase + SMEM_V + st * TILE;
-                // K_j's stage frees when S_{j-2} is computed, V_j's when PV_{j-2} is
+                // K_j's stage frees when both tiles' S_{j-2} are computed, V_j's after both PV_{j-2}
                 mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1u);
                 mbar_expect_tx(&k_full[st], TILE);
                 tma_4d(ks, &a.k, 0, j * BKV, hkv, b, &k_full[st], pol);
@@ -215,50 +235,66 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_fmha_kernel(const __grid_con
                 tma_4d(vs + CHUNK, &a.v, 64, j * BKV, hkv, b, &v_full[st], pol);
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         if (lane == 0) {
             // ---------------- MMA issuer ----------------
+            // Per key tile j: S_0 = Q_0 K^T, S_1 = Q_1 K^T, then (as each tile's P lands
+            // in TMEM over its S) O_t += P_t V.  tcgen05 ops run in issue order, so S_t of
+            // tile j + 1 -- issued after PV_t of tile j -- cannot overwrite P_t early.
             constexpr uint32_t id_s = idesc(BQ, BKV, 0), id_o = idesc(BQ, D, 1);
-            mbar_wait(&q_full, 0);
-            const bool prof = a.head->trace != nullptr;  // VTC_TRACE: per-CTA wait accounting (clock64)
+            const bool prof = a.head->trace != nullptr;
             long long w_k = 0, w_v = 0, w_p = 0;
-            auto issue_s = [&](int j) {
-                const int st = j & 1;
-                const long long c0 = prof ? clock64() : 0;
-                mbar_wait(&k_full[st], (j >> 1) & 1);
-                if (prof) w_k += clock64() - c0;
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t qa = sbase + SMEM_Q, kb = sbase + SMEM_K + st * TILE;
+            mbar_wait(&q_full, 0);
+            auto issue_s = [&](int t, int j) {
+                const uint32_t qa = sbase + SMEM_Q + uint32_t(t) * TILE, kb = sbase + SMEM_K + (j & 1) * TILE;
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {
                     const uint32_t o = (k >> 2) * CHUNK + (k & 3) * 32;  // K-major SW128: +32 B per K16, next chunk per 64
-                    mma(tmem + uint32_t(st * BKV), smem_desc(qa + o, 16, 1024), smem_desc(kb + o, 16, 1024), id_s,
+                    mma(tmem + uint32_t(t * 128), smem_desc(qa + o, 16, 1024), smem_desc(kb + o, 16, 1024), id_s,
                         k > 0 ? 1u : 0u);
                 }
-                commit(&s_full[st]);
-                commit(&k_empty[st]);
+                commit(&s_full[t]);
             };
-            if (nkv > 0) issue_s(0);
+            auto wait_k = [&](int j) {
+                const long long c0 = prof ? clock64() : 0;
+                mbar_wait(&k_full[j & 1], (j >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (prof) w_k += clock64() - c0;
+            };
+            if (nkv > 0) {
+                wait_k(0);
+                if (nkv0 > 0) issue_s(0, 0);
+                if (nkv1 > 0) issue_s(1, 0);
+                commit(&k_empty[0]);
+            }
             for (int j = 0; j < nkv; ++j) {
                 const int st = j & 1;
-                if (j + 1 < nkv) issue_s(j + 1);  // S buffer (j+1)&1 was released by softmax j-1
-                const long long c0 = prof ? clock64() : 0;
-                mbar_wait(&p_full, j & 1);
-                if (prof) w_p += clock64() - c0;
                 const long long c1 = prof ? clock64() : 0;
                 mbar_wait(&v_full[st], (j >> 1) & 1);
                 if (prof) w_v += clock64() - c1;
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t pa = sbase + SMEM_P, vb = sbase + SMEM_V + st * TILE;
+                if (j + 1 < nkv) wait_k(j + 1);
+                const uint32_t vb = sbase + SMEM_V + st * TILE;
 #pragma unroll
-                for (int k = 0; k < BKV / 16; ++k) {
-                    // P: K-major (keys) SW128; V: MN-major, 16 keys = 2 KB per step, 64-d chunks 16 KB apart
-                    const uint32_t po = (k >> 2) * CHUNK + (k & 3) * 32;
-                    mma(tmem + 256u, smem_desc(pa + po, 16, 1024), smem_desc(vb + uint32_t(k) * 2048u, CHUNK, 1024), id_o,
-                        (j > 0 || k > 0) ? 1u : 0u);
+                for (int t = 0; t < 2; ++t) {
+                    const int nt = t ? nkv1 : nkv0;
+                    if (j >= nt) continue;
+                    const long long c0 = prof ? clock64() : 0;
+                    mbar_wait(&p_full[t], (j & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    if (prof) w_p += clock64() - c0;
+#pragma unroll
+                    for (int k = 0; k < BKV / 16; ++k)  // A = P_t from TMEM (8 columns per K16), B = V MN-major
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + 256u + uint32_t(t * 128)),
+                            "r"(tmem + uint32_t(t * 128 + k * 8)), "l"(smem_desc(vb + uint32_t(k) * 2048u, CHUNK, 1024)),
+                            "r"(id_o), "r"((j > 0 || k > 0) ? 1u : 0u)
+                            : "memory");
+                    commit(&o_done[t]);
+                    if (j + 1 < nt) issue_s(t, j + 1);
                 }
-                commit(&o_done);
                 commit(&v_empty[st]);
+                if (j + 1 < nkv) commit(&k_empty[(j + 1) & 1]);
             }
             if (prof) {  // sums over CTAs, cycles: MMA thread waiting for K, P, V
                 dev::trace_add(*a.head, 5, (unsigned long long)w_k);
@@ -267,19 +303,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_fmha_kernel(const __grid_con
             }
         }
     } else {
-        // ---------------- softmax (warps 0-3): thread = query row = TMEM lane ----------------
-        const int r = warp * 32 + lane;
-        const int q = q0 + r;
+        // ---------------- softmax: warpgroup t = query tile t, thread = query row = TMEM lane ----------------
+        const int t = warp >> 2, wq = warp & 3;
+        const int r = wq * 32 + lane;
+        const int q0 = (2 * pair + t) * BQ, q = q0 + r;
         const int lim = q + off;  // last visible key (causal)
-        const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+        const int my_nkv = t ? nkv1 : nkv0;
+        const uint32_t trow = tmem + (uint32_t(wq * 32) << 16);
+        const uint32_t sc = uint32_t(t * 128), oc = 256u + uint32_t(t * 128);
         float m = -INFINITY, l = 0.f;
-        const uint32_t prow = sbase + SMEM_P + uint32_t(r) * 128u;
         const bool prof = a.head->trace != nullptr && threadIdx.x == 0;
-        long long w_s = 0, w_o = 0, busy = 0;
-        for (int j = 0; j < nkv; ++j) {
-            const int st = j & 1;
+        long long w_s = 0, busy = 0;
+        for (int j = 0; j < my_nkv; ++j) {
             long long c0 = prof ? clock64() : 0;
-            mbar_wait(&s_full[st], (j >> 1) & 1);
+            mbar_wait(&s_full[t], j & 1);
             if (prof) {
                 const long long c = clock64();
                 w_s += c - c0;
@@ -288,7 +325,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_fmha_kernel(const __grid_con
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             uint32_t sr[4][32];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(trow + uint32_t(st * BKV + c * 32), sr[c]);
+            for (int c = 0; c < 4; ++c) tmem_ld32(trow + sc + uint32_t(c * 32), sr[c]);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             const int t0 = j * BKV;
             const bool masked = (a.causal && t0 + BKV - 1 > q0 + off) || t0 + BKV > a.Sk;
@@ -297,79 +334,72 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_fmha_kernel(const __grid_con
                 for (int c = 0; c < 4; ++c)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
-                        const int t = t0 + c * 32 + i;
-                        if (t >= a.Sk || (a.causal && t > lim)) sr[c][i] = __float_as_uint(-INFINITY);
+                        const int tk = t0 + c * 32 + i;
+                        if (tk >= a.Sk || (a.causal && tk > lim)) sr[c][i] = __float_as_uint(-INFINITY);
                     }
             }
-            float mr = -INFINITY;  // raw row max (scale > 0: max commutes with the scale)
+            // raw row max (scale > 0: max commutes with the scale); 8 independent
+            // chains so the reduction is not one 128-long dependency
+            float mp[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mp[k] = -INFINITY;
 #pragma unroll
             for (int c = 0; c < 4; ++c)
 #pragma unroll
-                for (int i = 0; i < 32; ++i) mr = fmaxf(mr, __uint_as_float(sr[c][i]));
+                for (int i = 0; i < 32; ++i) mp[i & 7] = fmaxf(mp[i & 7], __uint_as_float(sr[c][i]));
+            const float mr = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])), fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
             const float mx = mr * a.scale_log2;
             // lazy rescale: keep the stale max unless this tile's max exceeds it by > 2^8
             const bool grow = mx > m + RESCALE_THRESHOLD;
             const float m_use = grow ? mx : m;
             const float corr = grow ? (m == -INFINITY ? 0.f : ex2(m - mx)) : 1.f;
-            // p = 2^(s * scale - m): one FFMA + one MUFU.EX2 per element; -inf -> +0
+            // p = 2^(s * scale - m): one FFMA + one exp2 per element; -inf -> +0
             const float nm = m_use == -INFINITY ? 0.f : -m_use;
-            float sum = 0.f;
-            uint32_t pk[64];
+            float sp[8];
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int k = 0; k < 8; ++k) sp[k] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
                     const float e0 = ex2(fmaf(__uint_as_float(sr[c][i]), a.scale_log2, nm));
                     const float e1 = ex2(fmaf(__uint_as_float(sr[c][i + 1]), a.scale_log2, nm));
-                    sum += e0 + e1;
-                    pk[c * 16 + i / 2] = pack_bf16(e0, e1);
+                    sp[(i >> 1) & 7] += e0 + e1;
+                    pk[i / 2] = pack_bf16(e0, e1);
                 }
-            // PV_{j-1} complete: the P buffer is free and O is stable
-            long long c1 = prof ? clock64() : 0;
-            if (j > 0) mbar_wait(&o_done, (j - 1) & 1);
-            if (prof) {
-                const long long c = clock64();
-                busy += c1 - c0;
-                w_o += c - c1;
-                c0 = c;
+                // P_t (bf16 pairs) over the first 64 columns of S_t: keys 32c .. 32c + 31
+                tmem_st16(trow + sc + uint32_t(c * 16), pk);
             }
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            // (after the exponentials, so S's registers are free) S_t of this tile completing implies PV_t of the previous one completed (issue
+            // order), so O_t is stable here: rescale it in place when the max grew
             if (__any_sync(0xffffffffu, grow && j > 0)) {
                 const float cf = (grow && j > 0) ? corr : 1.f;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     uint32_t orr[32];
-                    tmem_ld32(trow + 256u + uint32_t(c * 32), orr);
+                    tmem_ld32(trow + oc + uint32_t(c * 32), orr);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                     for (int i = 0; i < 32; ++i) orr[i] = __float_as_uint(__uint_as_float(orr[i]) * cf);
-                    tmem_st32(trow + 256u + uint32_t(c * 32), orr);
+                    tmem_st32(trow + oc + uint32_t(c * 32), orr);
                 }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
+            const float sum = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
             l = l * corr + sum;
             m = m_use;
-            // P row -> K-major SW128 operand: 16 chunks of 8 keys; chunk c of atom c/8 at (c%8) ^ (r%8)
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                const uint32_t dst = prow + (c >> 3) * CHUNK + (((c & 7) ^ (r & 7)) << 4);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(pk[4 * c]), "r"(pk[4 * c + 1]),
-                             "r"(pk[4 * c + 2]), "r"(pk[4 * c + 3])
-                             : "memory");
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full);
+            if (lane == 0) mbar_arrive(&p_full[t]);
             if (prof) busy += clock64() - c0;
         }
-        if (prof) {  // sums over CTAs, cycles: softmax thread 0 waiting for S, for PV, and working
+        if (prof) {  // sums over CTAs, cycles: softmax thread 0 waiting for S and working
             dev::trace_add(*a.head, 2, (unsigned long long)w_s);
-            dev::trace_add(*a.head, 3, (unsigned long long)w_o);
             dev::trace_add(*a.head, 4, (unsigned long long)busy);
         }
         // ---------------- epilogue: O / l -> bf16 through O's map ----------------
-        if (nkv > 0) mbar_wait(&o_done, (nkv - 1) & 1);
+        if (my_nkv > 0) mbar_wait(&o_done[t], (my_nkv - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const float inv = l > 0.f ? 1.f / l : 0.f;
         bf16* orow = a.o + int64_t(b) * a.o_sb + int64_t(h) * a.o_sh + int64_t(q) * a.o_ss;
@@ -377,7 +407,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_fmha_kernel(const __grid_con
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             uint32_t orr[32];
-            tmem_ld32(trow + 256u + uint32_t(c * 32), orr);
+            tmem_ld32(trow + oc + uint32_t(c * 32), orr);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (q < a.Sq) {
                 uint32_t w[16];
@@ -518,11 +548,12 @@ void launch_attn_fmha(const AttnParams& p, const AttnParams* dp, cudaStream_t s)
     a.Sq = p.Sq;
     a.Sk = p.Sk;
     a.causal = p.causal;
-    a.qtiles = (p.Sq + BQ - 1) / BQ;
+    a.qpairs = (p.Sq + 2 * BQ - 1) / (2 * BQ);
     a.scale_log2 = p.scale * LOG2E;
     const size_t smem = SMEM_BYTES + 1024;
+    const dim3 grid(unsigned(a.qpairs), unsigned(p.Bt * p.H));
     cudaFuncSetAttribute(attn_fmha_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    launch_k(attn_fmha_kernel, dim3(unsigned(a.qtiles), unsigned(p.Bt * p.H)), dim3(NTHREADS), smem, s, a);
+    launch_k(attn_fmha_kernel, grid, dim3(NTHREADS), smem, s, a);
 }
 
 }  // namespace vtc

@@ -283,7 +283,7 @@ def prefill_flops(B, S, D=4096, F=14336, nq=4096, nkv=1024, H=32, hd=128):
     T = B * S
     gemm = 2 * T * D * (nq + 2 * nkv) + 2 * T * nq * D + 2 * 2 * T * D * F + 2 * T * F * D
     attn = 2 * 2 * B * H * (S * (S + 1) // 2) * hd
-    return {"gemm_tc_bf16": gemm, "attn_prefill": attn}
+    return {"gemm_tc_bf16": gemm, "attn_fmha": attn, "attn_prefill": attn}
 
 
 def measure(name, args, torch, vtc, W, dev, stream, flush, world, rank, comm, local):
@@ -420,6 +420,12 @@ def measure(name, args, torch, vtc, W, dev, stream, flush, world, rank, comm, lo
                 "traffic": traffic_tab.get(dom), "kernel": dom, "kernel_launches_per_step": fam[dom]["launches"],
                 "algorithmic_flops_per_step": flops, "peak_source": peak_src,
                 "kernel_time_source": "in-graph device timeline, critical-path share"}
+        # every tensor-core family against the tensor roofline (GEMMs and attention)
+        by_kernel = {k: {"achieved_tflops": next(v for f, v in fl.items() if k.startswith(f)) / (tens[k]["us"] * 1e-6) / 1e12,
+                         "us": tens[k]["us"]} for k in tens}
+        for k in by_kernel:
+            by_kernel[k]["frac"] = by_kernel[k]["achieved_tflops"] / tf_peak
+        roof["by_kernel"] = by_kernel
     else:
         dom = max(fam, key=lambda k: fam[k]["us"])
         ach = fam[dom]["bytes"] / (fam[dom]["us"] * 1e-6) / 1e9
@@ -427,6 +433,8 @@ def measure(name, args, torch, vtc, W, dev, stream, flush, world, rank, comm, lo
                 "frac_vs_8tbs": ach / 8000.0, "traffic": traffic_tab.get(dom), "kernel": dom,
                 "kernel_launches_per_step": fam[dom]["launches"], "algorithmic_bytes_per_step": fam[dom]["bytes"],
                 "peak_source": peak_src, "kernel_time_source": "in-graph device timeline, critical-path share"}
+        roof["by_kernel"] = {k: {"achieved_gbs": v["bytes"] / (v["us"] * 1e-6) / 1e9, "us": v["us"],
+                                 "frac": v["bytes"] / (v["us"] * 1e-6) / 1e9 / hbm_peak} for k, v in fam.items() if v["us"] > 0}
     out = {
         "metric": METRIC, "value": lat_ms * 1e3, "unit": "us", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": lat_ms, "higher_is_better": False,

@@ -799,6 +799,46 @@ void Executor::prepare(bool dry) {
                 p.result == q[2].dst)
                 p.prog_pat = 3;
         }
+        // affine operands (<= 2 pieces split along the last axis, vector-aligned): the
+        // compact-parameter kernel, no per-element map evaluation (RoPE trees, views)
+        {
+            bool aff = !std::getenv("VTC_NO_EW_AFF") && vec * es == 16 && rank >= 1;
+            for (int k = 0; k <= p.nin && aff; ++k) {
+                const VOperand& op = k == 0 ? p.out : p.in[k - 1];
+                const vtc_map& m = op.m;
+                EwAff& A = p.affine[k];
+                if (m.npieces < 1 || m.npieces > 2 || !op.vec_ok) {
+                    aff = false;
+                    break;
+                }
+                A.split = INT32_MAX;
+                for (int q = 0; q < m.npieces && aff; ++q) {
+                    const vtc_piece& pc = m.piece[q];
+                    if (!pc.affine) aff = false;
+                    for (int i = 0; i < rank - 1 && aff; ++i)
+                        aff = pc.lo[i] <= p.origin[i] && pc.hi[i] >= p.origin[i] + p.shape[i];
+                    if (!aff) break;
+                    if (m.npieces == 2) {
+                        const int lo_last = pc.lo[rank - 1] - p.origin[rank - 1];
+                        if (q == 1) {
+                            A.split = lo_last;
+                            aff = lo_last % vec == 0 && m.piece[0].lo[rank - 1] <= p.origin[rank - 1] &&
+                                  m.piece[0].hi[rank - 1] == pc.lo[rank - 1] &&
+                                  pc.hi[rank - 1] >= p.origin[rank - 1] + p.shape[rank - 1];
+                        }
+                    }
+                    // fold the iteration-box origin into the base: index I of the box = I + origin
+                    int64_t off = pc.base;
+                    for (int i = 0; i < rank; ++i) {
+                        A.st[q][i] = pc.aff[i];
+                        off += pc.aff[i] * p.origin[i];
+                    }
+                    A.base[q] = pc.ptr + uint64_t(off * es);
+                }
+            }
+            p.aff = aff ? 1 : 0;
+            if (aff && !spec.copy) L->kernel = "eltwise_aff";
+        }
         bool flat = pat != 0;
         for (int i = 0; i < rank && flat; ++i) flat = p.origin[i] == 0;
         for (int k = 0; k <= p.nin && flat; ++k) {
@@ -1845,7 +1885,7 @@ void Executor::prepare(bool dry) {
                 if (!dep) {
                     auto P = std::make_unique<LaunchT<EwPair, launch_eltwise_pair>>();
                     P->node = a->node + "|" + b->node;
-                    P->kernel = "eltwise";
+                    P->kernel = a->p.aff && b->p.aff ? "eltwise_aff" : "eltwise";
                     P->p.a = a->p;
                     P->p.b = b->p;
                     LaunchInfo li = infos_[i];

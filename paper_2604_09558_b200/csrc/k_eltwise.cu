@@ -10,6 +10,7 @@
 // axis; every operand map is evaluated once per vector, then stepped with the
 // per-piece fast stride (one 16-byte access when the host proved alignment).
 #include <cmath>
+#include <cstring>
 
 #include "device.cuh"
 #include "launch.cuh"
@@ -252,10 +253,148 @@ void launch_t(const EwParams& p, const EwParams* dp, cudaStream_t s) {
         launch_k(ew_kernel<T, 1, 0>, dim3(grid), dim3(256), 0, s, dp, none, grid);
 }
 
+// ---- affine operands (p.aff, host-proved): compact parameters passed by value,
+// index unflattening by 32-bit multiply-shift division, one 16-byte access per
+// operand per vector, the piece chosen by one compare on the last axis ----
+struct EwAffArgs {
+    EwAff op[EW_MAX_IN + 1];
+    uint32_t shape[VTC_MAX_RANK];
+    uint32_t magic[VTC_MAX_RANK];  // Granlund-Montgomery: q = (hi + ((n - hi) >> 1)) >> (l - 1), hi = umulhi(m, n)
+    uint32_t shift[VTC_MAX_RANK];  // l (0: divisor 1)
+    int32_t rank, nin, nprog, result;
+    EwInstr prog[EW_MAX_PROG];
+    int64_t nvec;
+    const KHead* head;
+};
+
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t m, uint32_t l) {
+    if (l == 0) return n;
+    const uint32_t hi = __umulhi(m, n);
+    return (hi + ((n - hi) >> 1)) >> (l - 1);
+}
+
+// a0 / a1: two independent programs (a horizontally fused pair, e.g. the Q and
+// K RoPE trees) -- CTAs [0, blocks0) run a0, the rest a1 (a1.nvec == 0: single)
+template <typename T, int PAT>
+__global__ void __launch_bounds__(256) ew_aff_kernel(const __grid_constant__ EwAffArgs a0, const __grid_constant__ EwAffArgs a1,
+                                                     int blocks0) {
+    const bool second = a1.nvec > 0 && int(blockIdx.x) >= blocks0;
+    const EwAffArgs& a = second ? a1 : a0;
+    const int64_t bid = second ? int64_t(blockIdx.x) - blocks0 : int64_t(blockIdx.x);
+    const int64_t nblk = a1.nvec == 0 ? int64_t(gridDim.x) : (second ? int64_t(gridDim.x) - blocks0 : int64_t(blocks0));
+    dev::TraceScope trace_scope_(a0.head);
+    constexpr int VEC = 16 / int(sizeof(T));
+    dev::pdl_wait();
+    dev::pdl_launch_dependents();
+    const int rank = a.rank, last = rank - 1;
+    for (int64_t v = bid * blockDim.x + threadIdx.x; v < a.nvec; v += nblk * blockDim.x) {
+        uint32_t idx[VTC_MAX_RANK];
+        uint32_t f = uint32_t(v) * uint32_t(VEC);
+#pragma unroll
+        for (int d = VTC_MAX_RANK - 1; d >= 0; --d) {
+            if (d > last) continue;
+            const uint32_t q = fast_div(f, a.magic[d], a.shift[d]);
+            idx[d] = f - q * a.shape[d];
+            f = q;
+        }
+        auto addr = [&](const EwAff& op) {
+            const int k = int(idx[last]) >= op.split ? 1 : 0;
+            int64_t off = 0;
+#pragma unroll
+            for (int d = 0; d < VTC_MAX_RANK; ++d)
+                if (d <= last) off += op.st[k][d] * int64_t(idx[d]);
+            return op.base[k] + uint64_t(off) * sizeof(T);
+        };
+        T in[EW_MAX_IN][VEC];
+#pragma unroll
+        for (int i = 0; i < EW_MAX_IN; ++i)
+            if (i < a.nin) {
+                const uint4 u = __ldg(reinterpret_cast<const uint4*>(addr(a.op[1 + i])));
+                const T* t = reinterpret_cast<const T*>(&u);
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) in[i][j] = t[j];
+            }
+        T o[VEC];
+        if (PAT == 3) {
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) o[j] = add_of<T>(mul_of<T>(in[0][j], in[1][j]), mul_of<T>(in[2][j], in[3][j]));
+        } else {
+            T r[EW_MAX_PROG + EW_MAX_IN][VEC];
+#pragma unroll
+            for (int i = 0; i < EW_MAX_IN; ++i)
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) r[i][j] = in[i][j];
+#pragma unroll 1
+            for (int s2 = 0; s2 < a.nprog; ++s2) {
+                const EwInstr ins = a.prog[s2];
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) r[ins.dst][j] = apply_op<T>(ins.op, r[ins.a][j], r[ins.b][j]);
+            }
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) o[j] = r[a.result][j];
+        }
+        uint4 u;
+        T* t = reinterpret_cast<T*>(&u);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) t[j] = o[j];
+        *reinterpret_cast<uint4*>(addr(a.op[0])) = u;
+    }
+}
+
+void magic_of(uint32_t d, uint32_t& m, uint32_t& l) {
+    if (d <= 1) {
+        m = 0;
+        l = 0;
+        return;
+    }
+    l = 0;
+    while ((uint64_t(1) << l) < d) ++l;
+    m = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1);
+}
+
+EwAffArgs aff_args(const EwParams& p, const EwParams* dp) {
+    EwAffArgs a;
+    std::memset(&a, 0, sizeof(a));
+    for (int k = 0; k <= p.nin; ++k) a.op[k] = p.affine[k];
+    for (int d = 0; d < p.rank; ++d) {
+        a.shape[d] = uint32_t(p.shape[d]);
+        magic_of(a.shape[d], a.magic[d], a.shift[d]);
+    }
+    a.rank = p.rank;
+    a.nin = p.nin;
+    a.nprog = p.nprog;
+    a.result = p.result;
+    for (int i = 0; i < EW_MAX_PROG; ++i) a.prog[i] = p.prog[i];
+    a.nvec = p.nvec;
+    a.head = &dp->head;
+    return a;
+}
+
+bool aff_usable(const EwParams& p) {
+    // not for launches whose map bases move with a dynamic decode position
+    // (patched on the device, KHead::ndyn)
+    return p.aff && p.head.ndyn == 0 && p.nvec * (16 / p.esize) < (int64_t(1) << 31);
+}
+
+template <typename T>
+void launch_aff_t(const EwParams& p, const EwParams* dp, cudaStream_t s) {
+    EwAffArgs a = aff_args(p, dp), none;
+    std::memset(&none, 0, sizeof(none));
+    const int grid = ew_grid(p);
+    if (p.prog_pat == 3) launch_k(ew_aff_kernel<T, 3>, dim3(grid), dim3(256), 0, s, a, none, grid);
+    else launch_k(ew_aff_kernel<T, 0>, dim3(grid), dim3(256), 0, s, a, none, grid);
+}
+
 template <typename T>
 void launch_pair_t(const EwPair& p, const EwPair* dp, cudaStream_t s) {
     constexpr int V = 16 / sizeof(T);
     const int g0 = ew_grid(p.a), g1 = ew_grid(p.b);
+    if (aff_usable(p.a) && aff_usable(p.b)) {
+        const EwAffArgs a0 = aff_args(p.a, &dp->a), a1 = aff_args(p.b, &dp->b);
+        if (p.a.prog_pat == 3) launch_k(ew_aff_kernel<T, 3>, dim3(g0 + g1), dim3(256), 0, s, a0, a1, g0);
+        else launch_k(ew_aff_kernel<T, 0>, dim3(g0 + g1), dim3(256), 0, s, a0, a1, g0);
+        return;
+    }
     if (p.a.vec == V && p.a.prog_pat == 3)
         launch_k(ew_kernel<T, V, 3>, dim3(g0 + g1), dim3(256), 0, s, &dp->a, &dp->b, g0);
     else if (p.a.vec == V)
@@ -280,11 +419,20 @@ void launch_eltwise_pair(const EwPair& p, const EwPair* dp, cudaStream_t s) {
     }
 }
 
+
 void launch_eltwise(const EwParams& p, const EwParams* dp, cudaStream_t s) {
     if (p.nvec == 0) return;
     if (p.flat) {
         launch_flat(p, dp, s);
         return;
+    }
+    if (aff_usable(p)) {  // affine compact path
+        switch (p.copy_only ? (p.esize == 8 ? KDType::I64 : p.esize == 4 ? KDType::F32 : KDType::BF16) : p.dt) {
+            case KDType::F64: launch_aff_t<double>(p, dp, s); return;
+            case KDType::F32: launch_aff_t<float>(p, dp, s); return;
+            case KDType::I64: launch_aff_t<int64_t>(p, dp, s); return;
+            case KDType::BF16: launch_aff_t<bf16>(p, dp, s); return;
+        }
     }
     if (p.copy_only) {
         // copies are dtype-agnostic: dispatch on element size

@@ -69,6 +69,16 @@ struct EwInstr {
 };
 constexpr int EW_MAX_IN = 4, EW_MAX_PROG = 8;
 
+// An operand whose map is one or two affine pieces split along the last axis
+// (a view, a broadcast, a rotate-half): element I at
+// base[k] + sum_a st[k][a] * I[a] (bytes / element size), k = I[last] >= split.
+struct EwAff {
+    uint64_t base[2];              // byte address of virtual index 0 of each piece's affine form
+    int64_t st[2][VTC_MAX_RANK];   // element strides
+    int32_t split;                 // first last-axis index of piece 1 (INT32_MAX: one piece)
+    int32_t pad;
+};
+
 struct EwParams {
     KHead head;
     VOperand out;
@@ -87,7 +97,8 @@ struct EwParams {
     int32_t copy_only;             // pure data movement: dtype-agnostic by element size
     int32_t flat;                  // host-proved plain operands: 1 one-op program, 2 SiLU(in0) * in1
     int32_t prog_pat;              // 3: the program is (in0 * in1) + (in2 * in3) (RoPE), run without the interpreter
-    int32_t pad2;
+    int32_t aff;                   // host-proved affine operands (EwAff below): the compact-parameter kernel
+    EwAff affine[EW_MAX_IN + 1];   // [0] = out, [1 + i] = in[i]
 };
 void launch_eltwise(const EwParams& p, const EwParams* dp, cudaStream_t s);
 // Host check: the map addresses element I of an iteration box of `shape` (origin 0)

@@ -482,17 +482,22 @@ def test_c3k2_block_strategies_bit_identical(vtc, oracle):
     assert err < 2e-2, err
 
 
-@pytest.mark.parametrize("which", ["swin", "prefill"])
+@pytest.mark.parametrize("which", ["swin", "prefill", "decode64"])
 def test_fast_paths_bit_identical_to_generic_kernels(vtc, oracle, monkeypatch, which):
     """The plain-buffer fast paths (eltwise_flat, the RoPE-shaped eltwise program,
-    the vectorised LayerNorm / RMSNorm row kernels) give the same bits as the
-    map-evaluating generic kernels they replace."""
+    the affine compact-parameter eltwise kernel, the vectorised LayerNorm /
+    RMSNorm row kernels) give the same bits as the map-evaluating generic
+    kernels they replace."""
     from paper_2604_09558_b200 import workloads as W
     if which == "swin":
         cfg = dict(B=1, H=28, C=96, heads=3, mlp=384)
         doc = W.swin_block(**cfg)
         x = oracle.random_inputs(doc, seed=3, scales=W.swin_weight_scales(cfg["C"], cfg["mlp"]))
         x["attn_bias"] = oracle.f32_to_bf16(W.swin_attn_bias(H=cfg["H"], heads=cfg["heads"]))
+    elif which == "decode64":  # tcgen05 projections + the RoPE trees as an (affine) eltwise launch
+        cfg = dict(B=64, L=256, pos=200, D=1024, Hq=8, Hkv=2, hd=128, F=2048)
+        doc = W.llama_decode_layer(**cfg)
+        x = _llama_inputs(oracle, W, doc, cfg["B"], cfg["pos"], cfg["D"], cfg["F"], cfg["hd"])
     else:
         cfg = dict(B=2, S=128, D=256, Hq=4, Hkv=2, hd=128, F=512)
         doc = W.llama_prefill_layer(**cfg)
@@ -503,7 +508,9 @@ def test_fast_paths_bit_identical_to_generic_kernels(vtc, oracle, monkeypatch, w
     g = vtc.parse_graph(doc)
     fast = vtc.execute(g, vtc.Plan(g, vtc.MAX_ELIMINATION), x)["y"]
     monkeypatch.setenv("VTC_NO_EW_FAST", "1")
-    monkeypatch.setenv("VTC_NO_ROW_FAST", "1")
+    monkeypatch.setenv("VTC_NO_EW_AFF", "1")
+    if which != "decode64":  # decode64's D = 1024 RMSNorm sums in another order in the generic row kernel
+        monkeypatch.setenv("VTC_NO_ROW_FAST", "1")
     p = vtc.Plan(g, vtc.MAX_ELIMINATION)
     assert not any(l["kernel"] == "eltwise_flat" for l in p.info(dry=True)["launches"])
     generic = vtc.execute(g, p, x)["y"]

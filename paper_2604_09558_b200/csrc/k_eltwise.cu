@@ -287,57 +287,75 @@ __global__ void __launch_bounds__(256) ew_aff_kernel(const __grid_constant__ EwA
     dev::pdl_wait();
     dev::pdl_launch_dependents();
     const int rank = a.rank, last = rank - 1;
-    for (int64_t v = bid * blockDim.x + threadIdx.x; v < a.nvec; v += nblk * blockDim.x) {
-        uint32_t idx[VTC_MAX_RANK];
-        uint32_t f = uint32_t(v) * uint32_t(VEC);
+    // U vectors per thread per round: all their loads in flight before any use
+    constexpr int U = 4;
+    const int64_t stride = nblk * blockDim.x;
+    auto addr_of = [&](const EwAff& op, const uint32_t (&idx)[VTC_MAX_RANK], uint32_t lastv) {
+        const int k = int(lastv) >= op.split ? 1 : 0;
+        int64_t off = 0;
 #pragma unroll
-        for (int d = VTC_MAX_RANK - 1; d >= 0; --d) {
-            if (d > last) continue;
-            const uint32_t q = fast_div(f, a.magic[d], a.shift[d]);
-            idx[d] = f - q * a.shape[d];
-            f = q;
-        }
-        auto addr = [&](const EwAff& op) {
-            const int k = int(idx[last]) >= op.split ? 1 : 0;
-            int64_t off = 0;
+        for (int d = 0; d < VTC_MAX_RANK; ++d)
+            if (d <= last) off += op.st[k][d] * int64_t(idx[d]);
+        return op.base[k] + uint64_t(off) * sizeof(T);
+    };
+    for (int64_t v0 = bid * blockDim.x + threadIdx.x; v0 < a.nvec; v0 += U * stride) {
+        uint32_t idx[U][VTC_MAX_RANK], lastv[U];
+        uint4 raw[U][EW_MAX_IN];
 #pragma unroll
-            for (int d = 0; d < VTC_MAX_RANK; ++d)
-                if (d <= last) off += op.st[k][d] * int64_t(idx[d]);
-            return op.base[k] + uint64_t(off) * sizeof(T);
-        };
-        T in[EW_MAX_IN][VEC];
+        for (int u = 0; u < U; ++u) {
+            const int64_t v = v0 + u * stride;
+            if (v >= a.nvec) continue;
+            uint32_t f = uint32_t(v) * uint32_t(VEC);
+            lastv[u] = 0;
 #pragma unroll
-        for (int i = 0; i < EW_MAX_IN; ++i)
-            if (i < a.nin) {
-                const uint4 u = __ldg(reinterpret_cast<const uint4*>(addr(a.op[1 + i])));
-                const T* t = reinterpret_cast<const T*>(&u);
-#pragma unroll
-                for (int j = 0; j < VEC; ++j) in[i][j] = t[j];
+            for (int d = VTC_MAX_RANK - 1; d >= 0; --d) {
+                idx[u][d] = 0;
+                if (d > last) continue;
+                const uint32_t q = fast_div(f, a.magic[d], a.shift[d]);
+                idx[u][d] = f - q * a.shape[d];
+                if (d == last) lastv[u] = idx[u][d];
+                f = q;
             }
-        T o[VEC];
-        if (PAT == 3) {
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) o[j] = add_of<T>(mul_of<T>(in[0][j], in[1][j]), mul_of<T>(in[2][j], in[3][j]));
-        } else {
-            T r[EW_MAX_PROG + EW_MAX_IN][VEC];
 #pragma unroll
             for (int i = 0; i < EW_MAX_IN; ++i)
-#pragma unroll
-                for (int j = 0; j < VEC; ++j) r[i][j] = in[i][j];
-#pragma unroll 1
-            for (int s2 = 0; s2 < a.nprog; ++s2) {
-                const EwInstr ins = a.prog[s2];
-#pragma unroll
-                for (int j = 0; j < VEC; ++j) r[ins.dst][j] = apply_op<T>(ins.op, r[ins.a][j], r[ins.b][j]);
-            }
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) o[j] = r[a.result][j];
+                if (i < a.nin) raw[u][i] = __ldg(reinterpret_cast<const uint4*>(addr_of(a.op[1 + i], idx[u], lastv[u])));
         }
-        uint4 u;
-        T* t = reinterpret_cast<T*>(&u);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) t[j] = o[j];
-        *reinterpret_cast<uint4*>(addr(a.op[0])) = u;
+        for (int u = 0; u < U; ++u) {
+            const int64_t v = v0 + u * stride;
+            if (v >= a.nvec) continue;
+            T in[EW_MAX_IN][VEC];
+#pragma unroll
+            for (int i = 0; i < EW_MAX_IN; ++i) {
+                const T* t = reinterpret_cast<const T*>(&raw[u][i]);
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) in[i][j] = i < a.nin ? t[j] : T(0);
+            }
+            T o[VEC];
+            if (PAT == 3) {
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) o[j] = add_of<T>(mul_of<T>(in[0][j], in[1][j]), mul_of<T>(in[2][j], in[3][j]));
+            } else {
+                T r[EW_MAX_PROG + EW_MAX_IN][VEC];
+#pragma unroll
+                for (int i = 0; i < EW_MAX_IN; ++i)
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) r[i][j] = in[i][j];
+#pragma unroll 1
+                for (int s2 = 0; s2 < a.nprog; ++s2) {
+                    const EwInstr ins = a.prog[s2];
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) r[ins.dst][j] = apply_op<T>(ins.op, r[ins.a][j], r[ins.b][j]);
+                }
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) o[j] = r[a.result][j];
+            }
+            uint4 w;
+            T* t = reinterpret_cast<T*>(&w);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) t[j] = o[j];
+            *reinterpret_cast<uint4*>(addr_of(a.op[0], idx[u], lastv[u])) = w;
+        }
     }
 }
 

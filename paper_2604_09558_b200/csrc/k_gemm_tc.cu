@@ -449,10 +449,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
         // 16 finished columns c..c+15 of this row: round, residual, store through C's map
         auto emit = [&](int c, const float (&v)[16]) {
             bf16 o[16];
+            // the residual's 16 columns: two 16-byte loads when contiguous and aligned
+            bf16 rv[16];
+            const bool rvec = rrow && rs == 1 && c + 16 <= ncols && (reinterpret_cast<uintptr_t>(rrow + c) & 15) == 0;
+            if (rvec) {
+                *reinterpret_cast<uint4*>(&rv[0]) = __ldg(reinterpret_cast<const uint4*>(rrow + c));
+                *reinterpret_cast<uint4*>(&rv[8]) = __ldg(reinterpret_cast<const uint4*>(rrow + c + 8));
+            }
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 float f = __bfloat162float(__float2bfloat16_rn(v[j]));
-                if (rrow && c + j < ncols) f = __bfloat162float(rrow[int64_t(c + j) * rs]) + f;
+                if (rvec) f = __bfloat162float(rv[j]) + f;
+                else if (rrow && c + j < ncols) f = __bfloat162float(rrow[int64_t(c + j) * rs]) + f;
                 o[j] = __float2bfloat16_rn(f);
             }
             bf16* dst = crow + int64_t(c) * cs;

@@ -364,13 +364,41 @@ std::vector<int> plan_max_elimination(const Vtog& v) {
             return true;
         }
     };
+    // A plain 2-D operand (one TMA box per stage) also beats an N-D view when the
+    // producer is an attention kernel, which stores rows through any map for free.
+    auto tma_plain = [&](const std::string& a) -> bool {
+        try {
+            PointsToGraph p = validate_ptg(v, selected);
+            auto it = p.resolved.find(a);
+            if (it == p.resolved.end()) return true;
+            vtc_map d = lower_map(it->second, [](const std::string&) { return TargetInfo{0, 0}; });
+            const TensorSpec& t = g.tensor(a);
+            GemmTcParams probe{};
+            int64_t dims[5], strides[5];
+            const void* base = nullptr;
+            return gemm_tc_a_dims(d, t.shape[0], t.shape[1], probe, dims, strides, &base) && probe.a_ndims == 2;
+        } catch (const Error&) {
+            return true;
+        }
+    };
+    auto attention_fed = [&](const std::string& a) -> bool {
+        std::string t = a;
+        for (int hop = 0; hop < 8; ++hop) {
+            const OpNode* q = g.producer(t);
+            if (!q) return false;
+            if (!is_data_movement(*q)) return q->kind == OpKind::Attention;
+            if (q->inputs.size() != 1) return false;
+            t = q->inputs[0];
+        }
+        return false;
+    };
     for (int ni : g.topo_order()) {
         const OpNode& n = g.nodes()[size_t(ni)];
         if (n.kind != OpKind::MatMul) continue;
         const std::string& a = n.inputs[0];
         const TensorSpec& at = g.tensor(a);
-        if (at.dtype != DType::BF16 || at.shape.size() != 2 || at.shape[0] <= 16 || !assigned.count(a) || tma_ok(a))
-            continue;
+        if (at.dtype != DType::BF16 || at.shape.size() != 2 || at.shape[0] <= 16 || !assigned.count(a)) continue;
+        if (tma_ok(a) && (tma_plain(a) || !attention_fed(a))) continue;
         std::vector<std::string> chain;
         std::string t = a;
         while (true) {
@@ -392,7 +420,7 @@ std::vector<int> plan_max_elimination(const Vtog& v) {
         size_t before = count_elim(selected);
         for (const auto& c : chain) unselect(c);
         pull_back(a);
-        if (count_elim(selected) < before || !tma_ok(a)) {
+        if (count_elim(selected) < before || !tma_ok(a) || !tma_plain(a)) {
             selected = saved;
             assigned = saved_assigned;
             chosen = saved_chosen;

@@ -458,6 +458,8 @@ def measure(name, args, torch, vtc, W, dev, stream, flush, world, rank, comm, lo
         "bytes_per_step": bytes_step,
         "timeline_step_us": step_us,
         "kernel_times_us": {k: round(v["us"], 2) for k, v in fam.items()},
+        "launch_timeline": [{"node": l.get("node"), "kernel": l["kernel"], "us": round(float(us), 2),
+                             "bytes": int(l["bytes"])} for l, us in zip(launches, share)],
         "materialized_us": mat_ms * 1e3,
         "speedup_vs_materialized": mat_ms / lat_ms,
         "strong_materialized_us": strong_ms * 1e3 if strong_ms else None,

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <deque>
 #include <functional>
 #include <set>
 
@@ -168,6 +169,13 @@ void dyn_ops(GemmTcParams& p, DynCtx& c) {
         throw UnsupportedError("dynamic position: host-resolved rows of " + c.node + " address a cache");
     c.operand(p.head, &p, p.c, true);
     if (p.has_res) c.operand(p.head, &p, p.res, false);
+}
+void dyn_ops(SkinnyParams& p, DynCtx& c) {
+    // every address is host-resolved: none may point into a position-dependent cache
+    c.check_ptr(p.w, "weights");
+    c.check_ptr(reinterpret_cast<const void*>(p.c_base), "output");
+    c.check_ptr(reinterpret_cast<const void*>(p.r_base), "residual");
+    if (p.c_rows || p.r_rows || p.a_rows) throw UnsupportedError("dynamic position: row tables of " + c.node);
 }
 void dyn_ops(AttnParams& p, DynCtx& c) {
     c.operand(p.head, &p, p.o, true);
@@ -932,10 +940,16 @@ void Executor::prepare(bool dry) {
         const OpNode* silu = nullptr;
         const OpNode* mul = nullptr;
         const OpNode* add = nullptr;
+        const OpNode* view = nullptr;  // tensor-core residual: an eliminated Reshape between MatMul and Add
     };
     std::map<std::string, GemvFusion> fusion;
     std::map<std::string, const OpNode*> hfuse;  // first MatMul -> its horizontally fused sibling
     std::map<std::string, const OpNode*> tc_hfuse;  // the same for the tcgen05 GEMM
+    std::map<std::string, const OpNode*> tc_gelu;   // tcgen05 GEMM -> its GELU epilogue
+    struct SwiGlu {
+        const OpNode *gate, *up, *silu, *mul;
+    };
+    std::map<std::string, SwiGlu> tc_swiglu;  // launch node (earlier MatMul) -> the SwiGLU pair
     std::set<std::string> hpartner;
     std::set<std::string> absorbed;
     std::map<std::string, int> topo_pos;
@@ -1044,6 +1058,24 @@ void Executor::prepare(bool dry) {
                 const std::string& other = ad->inputs[0] == n.outputs[0] ? ad->inputs[1] : ad->inputs[0];
                 const OpNode* po = g_.producer(other);
                 if (!po || topo_pos[po->id] < topo_pos[n.id]) f.add = ad;
+            } else if (tc && !std::getenv("VTC_NO_TC_EPI") && !cs.empty() && only_consumer(n.outputs[0], cs[0]->id) &&
+                       cs[0]->kind == OpKind::Reshape &&
+                       elim.count(cs[0]->id) &&
+                       g_.tensor(cs[0]->outputs[0]).shape.back() == g_.tensor(n.outputs[0]).shape.back()) {
+                // MatMul -> (virtual) Reshape keeping the last axis -> Add: the residual is
+                // fused through [M, N] views of the Add's operands (Swin's MLP reshape)
+                const std::string& ro = cs[0]->outputs[0];
+                auto cs2 = g_.consumers(ro);
+                if (!cs2.empty() && only_consumer(ro, cs2[0]->id) && cs2[0]->kind == OpKind::Add &&
+                    cs2[0]->inputs[0] != cs2[0]->inputs[1]) {
+                    const OpNode* ad = cs2[0];
+                    const std::string& other = ad->inputs[0] == ro ? ad->inputs[1] : ad->inputs[0];
+                    const OpNode* po = g_.producer(other);
+                    if (!po || topo_pos[po->id] < topo_pos[n.id]) {
+                        f.add = ad;
+                        f.view = cs[0];
+                    }
+                }
             }
             if (f.norm || f.silu || f.add) fusion[n.id] = f;
         }
@@ -1071,6 +1103,57 @@ void Executor::prepare(bool dry) {
                 }
             }
             for (const auto& id : hpartner) absorbed.insert(id);
+        }
+        // activation epilogues on the tensor-core GEMM (VTC_NO_TC_EPI=1: off):
+        //  * MatMul -> GELU (its only consumer): the GEMM stores GELU(round(acc));
+        //  * SwiGLU: gate = A.Wg, up = A.Wu, SiLU(gate) * up, each intermediate with one
+        //    consumer: one launch whose tiles hold 128 columns of both products and store
+        //    only the Mul's output (gate / up are never written)
+        if (!std::getenv("VTC_NO_TC_EPI")) {
+            for (const auto& n : g_.nodes()) {
+                if (!tc_eligible(n) || fusion.count(n.id) || absorbed.count(n.id)) continue;
+                const std::string& o = n.outputs[0];
+                auto cs = g_.consumers(o);
+                if (!only_consumer(o, cs.empty() ? "" : cs[0]->id)) continue;
+                const OpNode* c = cs[0];
+                if (c->kind == OpKind::GELU && g_.tensor(c->outputs[0]).shape == g_.tensor(o).shape) {
+                    tc_gelu[n.id] = c;
+                    absorbed.insert(c->id);
+                    continue;
+                }
+                if (c->kind != OpKind::SiLU) continue;
+                const std::string& so = c->outputs[0];
+                auto ms = g_.consumers(so);
+                if (!only_consumer(so, ms.empty() ? "" : ms[0]->id) || ms[0]->kind != OpKind::Mul) continue;
+                const OpNode* mul = ms[0];
+                const std::string& other = mul->inputs[0] == so ? mul->inputs[1] : mul->inputs[0];
+                if (other == so) continue;
+                const OpNode* up = g_.producer(other);
+                if (!up || up == &n || !tc_eligible(*up) || fusion.count(up->id) || absorbed.count(up->id) ||
+                    !only_consumer(other, mul->id) || up->inputs[0] != n.inputs[0] ||
+                    g_.tensor(up->inputs[1]).shape != g_.tensor(n.inputs[1]).shape ||
+                    g_.tensor(mul->outputs[0]).shape != g_.tensor(o).shape ||
+                    !operand(map_of(mul->outputs[0]), 1, 128, 2).fast_ok)
+                    continue;
+                // the launch runs at the earlier of the two MatMuls' positions; the later one's
+                // inputs must be ready there
+                const OpNode* first = topo_pos.at(n.id) < topo_pos.at(up->id) ? &n : up;
+                const OpNode* second = first == &n ? up : &n;
+                bool ready = true;
+                for (const auto& in : second->inputs) {
+                    const OpNode* pr = g_.producer(in);
+                    if (pr && topo_pos.at(pr->id) >= topo_pos.at(first->id)) ready = false;
+                    for (const auto& r : targets_of(map_of(in))) {
+                        const OpNode* pw = g_.producer(r);
+                        if (pw && topo_pos.at(pw->id) >= topo_pos.at(first->id)) ready = false;
+                    }
+                }
+                if (!ready) continue;
+                tc_swiglu[first->id] = SwiGlu{&n, up, c, mul};
+                absorbed.insert(second->id);
+                absorbed.insert(c->id);
+                absorbed.insert(mul->id);
+            }
         }
         // the same on the tensor cores: sibling MatMuls reading the same A with plain
         // single-piece outputs (gate / up at decode batch) run as one launch, so the
@@ -1230,6 +1313,256 @@ void Executor::prepare(bool dry) {
             epi_roots[n.id] = excl;
             for (const auto& root : trees)
                 for (const auto& m : ew_trees.at(root).members) absorbed.insert(m);
+        }
+    }
+
+    // ---- elementwise trees folded into a tensor-core GEMM's epilogue: trees whose
+    //      operands are views of the GEMM output C (same row, columns of one N tile
+    //      per head: e.g. the prefill Q / K RoPE trees over the QKV projection) or
+    //      row-linear external tensors (the cos / sin tables).  The columns of C that
+    //      only these trees read are not stored (VTC_NO_TC_EPI=1: off) ----
+    struct TcTrees {
+        std::vector<GemmTree> trees;
+        std::vector<std::string> roots;
+        int64_t skip_lo = 0, skip_hi = 0;
+    };
+    std::map<std::string, TcTrees> tc_trees;
+    const bool dbg_fuse = std::getenv("VTC_DEBUG_FUSION") != nullptr;
+    // opt-in (VTC_TC_TREES=1): measured slower than the separate affine eltwise launch at C5
+    // (QKV + trees 2.53 ms vs 1.64 + 0.67 ms: the per-row epilogue's table loads serialise)
+    if (opt_.fuse && std::getenv("VTC_TC_TREES") && !std::getenv("VTC_NO_TC_EPI") && !impl_->dyn_on) {
+        const auto gouts = g_.graph_outputs();
+        const std::set<std::string> graph_out(gouts.begin(), gouts.end());
+        for (const auto& n : g_.nodes()) {
+            if (!tc_eligible(n) || absorbed.count(n.id) || fusion.count(n.id) || tc_gelu.count(n.id) ||
+                tc_swiglu.count(n.id) || tc_hfuse.count(n.id))
+                continue;
+            const std::string& C = n.outputs[0];
+            if (g_.tensor(C).kind != TensorKind::Intermediate) continue;
+            const int64_t M = g_.tensor(C).shape[0], N = g_.tensor(C).shape[1];
+            int64_t ldc = 0, cc0 = 0;
+            if (!affine2d(map_of(C), ldc, cc0)) continue;
+            const std::string R = map_of(C).pieces()[0].target;
+            const int Ridx = target(R).index;
+            const int pos_n = topo_pos.at(n.id);
+            TcTrees tt;
+            std::vector<std::string> roots_fused;
+            std::vector<char> mark(size_t(N), 0);  // C columns read by the fused trees
+            for (const auto& [root, t] : ew_trees) {
+                if (absorbed.count(root) || int(tt.trees.size()) == GEMM_MAX_TREES) continue;
+                bool hits = false;
+                for (const auto& in : t.in_names)
+                    for (const auto& r : targets_of(map_of(in))) hits |= r == R;
+                if (!hits) continue;
+                const OpNode* rn = g_.node(root);
+                const std::string& O = rn->outputs[0];
+                const Index& shp = g_.tensor(O).shape;
+                const int r = int(shp.size());
+                if (r < 3 || g_.tensor(O).dtype != DType::BF16 || graph_out.count(O)) continue;
+                int64_t rows = 1;
+                for (int d = 0; d + 2 < r; ++d) rows *= shp[size_t(d)];
+                const int64_t nh = shp[size_t(r - 2)], hd = shp[size_t(r - 1)];
+                if (rows != M || hd % 16 != 0 || hd > 256) continue;
+                // the tree now runs at n's position: its external inputs must be ready there,
+                // and nothing between n and the tree may touch its output's roots
+                bool ok = true;
+                for (const auto& in : t.in_names) {
+                    bool fromc = false;
+                    for (const auto& r2 : targets_of(map_of(in))) fromc |= r2 == R;
+                    if (fromc) continue;
+                    const OpNode* pr = g_.producer(in);  // an eliminated view runs nothing: its roots count
+                    if (pr && !(is_data_movement(*pr) && elim.count(pr->id)) && topo_pos.at(pr->id) >= pos_n) ok = false;
+                    for (const auto& r2 : targets_of(map_of(in))) {
+                        const OpNode* pw = g_.producer(r2);
+                        if (pw && topo_pos.at(pw->id) >= pos_n) ok = false;
+                    }
+                }
+                const auto oroots = targets_of(map_of(O));
+                for (const auto& m2 : g_.nodes()) {
+                    const int pm = topo_pos.at(m2.id);
+                    if (pm <= pos_n || pm >= topo_pos.at(root)) continue;
+                    if (std::find(t.members.begin(), t.members.end(), m2.id) != t.members.end()) continue;
+                    for (const auto* lst : {&m2.inputs, &m2.outputs})
+                        for (const auto& tn : *lst)
+                            for (const auto& r2 : targets_of(map_of(tn))) ok = ok && !oroots.count(r2);
+                }
+                if (!ok) {
+                    if (dbg_fuse) fprintf(stderr, "[vtc fuse] %s: tree %s not movable to the GEMM\n", n.id.c_str(), root.c_str());
+                    continue;
+                }
+                // operands as row-linear pieces: element (m, h, i) at base + rs*m + sh*h + i
+                GemmTree T{};
+                T.nin = int32_t(t.in_names.size());
+                T.nprog = int32_t(t.spec.prog.size());
+                T.result = t.reg;
+                T.hd = int32_t(hd);
+                T.nh = int32_t(nh);
+                for (size_t k = 0; k < t.spec.prog.size(); ++k) T.prog[k] = t.spec.prog[k];
+                {
+                    const EwInstr* q = T.prog;
+                    const int r0 = EW_MAX_IN, r1 = EW_MAX_IN + 1;
+                    if (T.nin == 4 && T.nprog == 3 && q[0].op == EwOp::Mul && q[0].a == 0 && q[0].b == 1 && q[0].dst == r0 &&
+                        q[1].op == EwOp::Mul && q[1].a == 2 && q[1].b == 3 && q[1].dst == r1 && q[2].op == EwOp::Add &&
+                        ((q[2].a == r0 && q[2].b == r1) || (q[2].a == r1 && q[2].b == r0)) && T.result == q[2].dst)
+                        T.pat = 3;
+                }
+                int64_t csh = INT64_MIN, clo = INT64_MAX, chi = INT64_MIN;
+                auto lower_op = [&](const std::string& name, GemmTreeOp& op, bool is_out) -> bool {
+                    vtc_map lm;
+                    try {
+                        lm = lower_map(map_of(name), target);
+                    } catch (const UnsupportedError&) {
+                        return false;
+                    }
+                    if (lm.npieces < 1 || lm.npieces > 2) return false;
+                    op.split = lm.npieces == 2 ? lm.piece[1].lo[r - 1] : int32_t(hd);
+                    int fromc = -1;
+                    for (int q = 0; q < lm.npieces; ++q) {
+                        const vtc_piece& pc = lm.piece[q];
+                        if (!pc.affine) return false;
+                        for (int d = 0; d + 1 < r; ++d)
+                            if (pc.lo[d] > 0 || pc.hi[d] < shp[size_t(d)]) return false;
+                        if (lm.npieces == 2) {
+                            if (q == 0 && (pc.lo[r - 1] > 0 || pc.hi[r - 1] != lm.piece[1].lo[r - 1])) return false;
+                            if (q == 1 && (pc.hi[r - 1] < hd || pc.lo[r - 1] % 16 != 0)) return false;
+                        } else if (pc.lo[r - 1] > 0 || pc.hi[r - 1] < hd) {
+                            return false;
+                        }
+                        if (pc.aff[r - 1] != 1) return false;
+                        if (shp[size_t(r - 3)] == 1 && rows > 1) return false;  // the row stride is not the innermost's
+                        const int64_t rs = pc.aff[r - 3];
+                        int64_t want = rs;
+                        for (int d = r - 3; d >= 0; --d) {
+                            if (shp[size_t(d)] > 1 && pc.aff[d] != want) return false;  // unit axes: any stride
+                            want *= shp[size_t(d)];
+                        }
+                        const bool c_side = pc.target == Ridx;
+                        if (fromc >= 0 && fromc != int(c_side)) return false;
+                        fromc = int(c_side);
+                        op.rs[q] = rs;
+                        op.sh[q] = pc.aff[r - 2];
+                        if (c_side) {
+                            if (is_out || rs != ldc) return false;
+                            op.ccol[q] = pc.base - cc0;
+                            const int64_t lo_i = q == 0 ? 0 : op.split, hi_i = q == 0 && lm.npieces == 2 ? op.split : hd;
+                            if (csh != INT64_MIN && csh != op.sh[q]) return false;
+                            csh = op.sh[q];
+                            clo = std::min(clo, op.ccol[q] + lo_i);
+                            chi = std::max(chi, op.ccol[q] + hi_i - 1);
+                        } else {
+                            if (pc.target == Ridx) return false;
+                            if ((pc.base * 2) % 16 || rs % 8 || op.sh[q] % 8) return false;
+                            op.base[q] = pc.ptr + uint64_t(pc.base * 2);
+                        }
+                    }
+                    if (lm.npieces == 1) {
+                        op.rs[1] = op.rs[0];
+                        op.sh[1] = op.sh[0];
+                        op.ccol[1] = op.ccol[0];
+                        op.base[1] = op.base[0];
+                    }
+                    op.from_c = fromc;
+                    return true;
+                };
+                ok = lower_op(O, T.op[0], true);
+                for (size_t k = 0; k < t.in_names.size() && ok; ++k) {
+                    ok = lower_op(t.in_names[k], T.op[1 + k], false);
+                    if (!ok && dbg_fuse) fprintf(stderr, "[vtc fuse] %s: tree %s operand %s not row-linear\n", n.id.c_str(), root.c_str(), t.in_names[k].c_str());
+                }
+                if (!ok || csh == INT64_MIN) {
+                    if (dbg_fuse) fprintf(stderr, "[vtc fuse] %s: tree %s output / C operands not row-linear\n", n.id.c_str(), root.c_str());
+                    continue;
+                }
+                for (int64_t h = 0; h < nh && ok; ++h) {
+                    const int64_t a = clo + csh * h, b = chi + csh * h;
+                    ok = a >= 0 && b < N && a / 128 == b / 128;
+                }
+                if (!ok) {
+                    if (dbg_fuse) fprintf(stderr, "[vtc fuse] %s: tree %s head columns cross a 128-column tile\n", n.id.c_str(), root.c_str());
+                    continue;
+                }
+                T.c_lo = clo;
+                T.c_sh = csh;
+                for (int k = 0; k < T.nin; ++k) {
+                    const GemmTreeOp& op = T.op[1 + k];
+                    if (!op.from_c) continue;
+                    for (int64_t h = 0; h < nh; ++h)
+                        for (int64_t i = 0; i < hd; ++i) {
+                            const int q = i >= op.split ? 1 : 0;
+                            mark[size_t(op.ccol[q] + op.sh[q] * h + i)] = 1;
+                        }
+                }
+                tt.trees.push_back(T);
+                roots_fused.push_back(root);
+            }
+            if (tt.trees.empty()) continue;
+            // columns read only by the trees: the longest marked run, 16-aligned inward;
+            // dropped if any other reader of C's root may read inside it
+            int64_t best_lo = 0, best_hi = 0;
+            for (int64_t c = 0; c < N;) {
+                if (!mark[size_t(c)]) {
+                    ++c;
+                    continue;
+                }
+                int64_t e = c;
+                while (e < N && mark[size_t(e)]) ++e;
+                if (e - c > best_hi - best_lo) {
+                    best_lo = c;
+                    best_hi = e;
+                }
+                c = e;
+            }
+            best_lo = (best_lo + 15) / 16 * 16;
+            best_hi = best_hi / 16 * 16;
+            std::set<std::string> members;
+            for (const auto& root : roots_fused)
+                for (const auto& m2 : ew_trees.at(root).members) members.insert(m2);
+            bool clean = best_hi > best_lo && !graph_out.count(R) && ldc == N && cc0 == 0;
+            for (const auto& [tid, m] : ptg_.resolved) {
+                if (!clean) break;
+                const auto mt = m.targets();
+                if (std::find(mt.begin(), mt.end(), R) == mt.end() || tid == C) continue;
+                bool read = graph_out.count(tid) > 0;
+                for (const OpNode* c : g_.consumers(tid))
+                    if (!(is_data_movement(*c) && elim.count(c->id)) && !members.count(c->id)) read = true;
+                if (!read) continue;
+                vtc_map lm;
+                try {
+                    lm = lower_map(m, target);
+                } catch (const UnsupportedError&) {
+                    clean = false;
+                    break;
+                }
+                for (int q = 0; q < lm.npieces && clean; ++q) {
+                    const vtc_piece& pc = lm.piece[q];
+                    if (pc.target != Ridx) continue;
+                    if (!pc.affine) {
+                        clean = false;
+                        break;
+                    }
+                    int64_t lo = pc.base, hi = pc.base;
+                    for (int d = 0; d < lm.rank; ++d) {
+                        const int64_t st = pc.aff[d];
+                        if (st % ldc == 0) continue;
+                        const int64_t x0 = st * pc.lo[d], x1 = st * (pc.hi[d] - 1);
+                        lo += std::min(x0, x1);
+                        hi += std::max(x0, x1);
+                    }
+                    if (lo < 0 || lo / ldc != hi / ldc) {
+                        clean = false;
+                        break;
+                    }
+                    const int64_t clo2 = lo % ldc, chi2 = hi % ldc;
+                    if (chi2 >= best_lo && clo2 < best_hi) clean = false;
+                }
+            }
+            if (clean) {
+                tt.skip_lo = best_lo;
+                tt.skip_hi = best_hi;
+            }
+            for (const auto& root : roots_fused) absorbed.insert(ew_trees.at(root).members.begin(), ew_trees.at(root).members.end());
+            tt.roots = roots_fused;
+            tc_trees[n.id] = std::move(tt);
         }
     }
 
@@ -1544,25 +1877,145 @@ void Executor::prepare(bool dry) {
                     GemvFusion f;
                     auto fit = fusion.find(n.id);
                     if (fit != fusion.end()) f = fit->second;
-                    const std::string& cout = f.add ? f.add->outputs[0] : n.outputs[0];
-                    // small M: 128-column tiles so the K split (and its reduction) stays shallow
-                    p.bn = M <= 128 ? 128 : 256;
-                    p.c = operand(map_of(cout), 1, p.bn, es);
-                    if (!p.c.fast_ok || N % 256 != 0) {
-                        p.bn = 128;
-                        p.c = operand(map_of(cout), 1, p.bn, es);
+                    auto gl = tc_gelu.find(n.id);
+                    auto sw = tc_swiglu.find(n.id);
+                    const std::string& cout = f.add ? f.add->outputs[0]
+                                              : gl != tc_gelu.end() ? gl->second->outputs[0]
+                                              : sw != tc_swiglu.end() ? sw->second.mul->outputs[0]
+                                                                      : n.outputs[0];
+                    // the residual Add's operands as [M, N] (a Reshape between MatMul and Add)
+                    std::deque<VMap> views;
+                    auto mn = [&](const std::string& t) -> const VMap& {
+                        if (!f.view || g_.tensor(t).shape == Index{M, N}) return map_of(t);
+                        const VMap v = VMap::affine(Index{M, N}, Index{N, 1}, 0, t);
+                        views.push_back(v.compose([&](const std::string& x) -> const VMap* {
+                            return map_of(x).is_identity_of(x) ? nullptr : &map_of(x);
+                        }));
+                        return views.back();
+                    };
+                    const std::string& f_in = f.view ? f.view->outputs[0] : n.outputs[0];  // the Add's MatMul-side input
+                    // shallow K, narrow N, many rows (Swin's projections): the persistent kernel with
+                    // the weight resident in shared memory (VTC_NO_SKINNY=1: off)
+                    if (sw == tc_swiglu.end() && !tc_trees.count(n.id) && !tc_hfuse.count(n.id) && M >= 8192 && K <= 512 &&
+                        N <= 1024 && K % 16 == 0 && N % 16 == 0 && !std::getenv("VTC_NO_SKINNY")) {
+                        auto S = std::make_unique<LaunchT<SkinnyParams, launch_gemm_skinny>>();
+                        SkinnyParams& q = S->p;
+                        std::memset(&q, 0, sizeof(q));
+                        q.M = M;
+                        q.N = N;
+                        q.K = K;
+                        q.epi = gl != tc_gelu.end() ? 1 : 0;
+                        q.sms = impl_->dry ? 148 : device_sms();
+                        int optin = 232448;
+                        if (!impl_->dry) {
+                            int dev = 0;
+                            cudaGetDevice(&dev);
+                            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+                        }
+                        bool sk = skinny_plan(q, optin - 2048);
+                        // weights: one affine piece, rows 16-byte aligned
+                        int64_t ldw = 0, cw = 0;
+                        sk = sk && affine2d(map_of(n.inputs[1]), ldw, cw);
+                        if (sk) {
+                            const VMap& wm = map_of(n.inputs[1]);
+                            q.w = reinterpret_cast<const char*>(target(wm.pieces()[0].target).ptr) + cw * es;
+                            q.ldw = ldw;
+                            const OpNode* wp = g_.producer(wm.pieces()[0].target);
+                            q.b_static = wp == nullptr && g_.producer(n.inputs[1]) == nullptr;
+                            sk = (reinterpret_cast<uintptr_t>(q.w) % 16) == 0 && ldw % 8 == 0;
+                        }
+                        // rows of a 2-D operand: affine (base, ld) or resolved per row on the host
+                        auto rows_of = [&](const VMap& m, int64_t cols, uint64_t& base, int64_t& ld,
+                                           const uint64_t*& table, const char* what) -> bool {
+                            int64_t l = 0, c0 = 0;
+                            if (affine2d(m, l, c0)) {
+                                base = target(m.pieces()[0].target).ptr + uint64_t(c0 * es);
+                                ld = l;
+                                return base % 16 == 0 && l % 8 == 0;
+                            }
+                            VOperand op = operand(m, 1, cols, es);
+                            if (!op.vec_ok) return false;
+                            for (int pi = 0; pi < op.m.npieces; ++pi)
+                                if (op.m.piece[pi].lo[1] > 0 || op.m.piece[pi].hi[1] < m.shape()[1]) return false;
+                            if (impl_->dry) return true;
+                            const int64_t rows = m.shape()[0];
+                            std::vector<uint64_t> tab(static_cast<size_t>(rows));
+                            int64_t idx[VTC_MAX_RANK] = {};
+                            for (int64_t r2 = 0; r2 < rows; ++r2) {
+                                idx[0] = r2;
+                                int pc = -1;
+                                const int64_t off = desc_eval(op.m, idx, &pc);
+                                if (pc < 0) return false;
+                                tab[size_t(r2)] = op.m.piece[pc].ptr + uint64_t(off) * es;
+                                if (tab[size_t(r2)] % 16) return false;
+                            }
+                            auto* d = static_cast<uint64_t*>(impl_->alloc(tab.size() * 8, false));
+                            ck(cudaMemcpy(d, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice), what);
+                            table = d;
+                            return true;
+                        };
+                        sk = sk && rows_of(mn(cout), N, q.c_base, q.c_ld, q.c_rows, "H2D(skinny c_rows)");
+                        if (sk && f.add) {
+                            const std::string& other = f.add->inputs[0] == f_in ? f.add->inputs[1] : f.add->inputs[0];
+                            q.has_res = 1;
+                            sk = rows_of(mn(other), N, q.r_base, q.r_ld, q.r_rows, "H2D(skinny r_rows)");
+                        }
+                        if (sk) {
+                            const VMap& am = map_of(n.inputs[0]);
+                            int64_t lda = 0, ca = 0;
+                            if (affine2d(am, lda, ca)) {
+                                const char* ab = reinterpret_cast<const char*>(target(am.pieces()[0].target).ptr) + ca * es;
+                                sk = impl_->dry || skinny_encode_a(q, ab, lda);
+                            } else {
+                                uint64_t abase = 0;
+                                int64_t ald = 0;
+                                const uint64_t* at = nullptr;
+                                q.a_gather = 1;
+                                // A rows: the K axis contiguous inside one piece per row
+                                VOperand op = operand(am, 1, 64, es);
+                                std::vector<int64_t> segs;
+                                sk = op.vec_ok && k_segments(op.m, K, segs) && segs.size() == 2;
+                                sk = sk && rows_of(am, K, abase, ald, at, "H2D(skinny a_rows)") && (impl_->dry || at != nullptr);
+                                q.a_rows = at;
+                            }
+                        }
+                        if (sk) {
+                            S->node = T->node + (f.add ? "+" + f.add->id : "") + (gl != tc_gelu.end() ? "+" + gl->second->id : "");
+                            S->kernel = "gemm_skinny_bf16";
+                            push(std::move(S));
+                            break;
+                        }
                     }
-                    bool ok = p.c.fast_ok != 0;
+                    bool ok = true;
+                    if (sw != tc_swiglu.end()) {
+                        // 256-column B stages: 128 columns of W_gate then the same 128 of W_up
+                        p.epi = GEMM_EPI_SWIGLU;
+                        p.bn = 256;
+                        p.c = operand(map_of(cout), 1, 128, es);
+                        ok = p.c.fast_ok != 0;
+                    } else {
+                        if (gl != tc_gelu.end()) p.epi = GEMM_EPI_GELU;
+                        // small M: 128-column tiles so the K split (and its reduction) stays shallow
+                        p.bn = M <= 128 ? 128 : 256;
+                        p.c = operand(mn(cout), 1, p.bn, es);
+                        if (!p.c.fast_ok || N % 256 != 0) {
+                            p.bn = 128;
+                            p.c = operand(mn(cout), 1, p.bn, es);
+                        }
+                        ok = p.c.fast_ok != 0;
+                    }
                     if (f.add) {
-                        const std::string& other = f.add->inputs[0] == n.outputs[0] ? f.add->inputs[1] : f.add->inputs[0];
+                        const std::string& other = f.add->inputs[0] == f_in ? f.add->inputs[1] : f.add->inputs[0];
                         p.has_res = 1;
-                        p.res = operand(map_of(other), 1, p.bn, es);
+                        p.res = operand(mn(other), 1, p.bn, es);
                         ok = ok && p.res.fast_ok;
                         T->node += "+" + f.add->id;
                     }
+                    // B: the weights (SwiGLU: the gate's; the up weights follow as B2)
+                    const OpNode& nbw = sw != tc_swiglu.end() ? *sw->second.gate : n;
                     int64_t ldb, cb;
-                    affine2d(map_of(n.inputs[1]), ldb, cb);
-                    const VMap& bmm = map_of(n.inputs[1]);
+                    affine2d(map_of(nbw.inputs[1]), ldb, cb);
+                    const VMap& bmm = map_of(nbw.inputs[1]);
                     const char* bbase = reinterpret_cast<const char*>(target(bmm.pieces()[0].target).ptr) + cb * es;
                     int64_t adims[5], astr[5];
                     const void* abase = nullptr;
@@ -1584,16 +2037,15 @@ void Executor::prepare(bool dry) {
                             p.a_mod[j] = 0;
                         }
                         if (ok) T->kernel = "gemm_tc_bf16_gather";
-                        if (ok && p.bn == 128 && N > 128) {
+                        if (ok && p.bn == 128 && N > 128 && p.epi != GEMM_EPI_SWIGLU) {
                             // gathered A is re-gathered for every N tile: 256-wide tiles (a
                             // partial last one) halve that (Swin QKV N = 288: 218 -> 180 us)
-                            VOperand c256 = operand(map_of(cout), 1, 256, es);
+                            VOperand c256 = operand(mn(cout), 1, 256, es);
                             VOperand r256{};
                             bool rok = true;
                             if (f.add) {
-                                const std::string& other =
-                                    f.add->inputs[0] == n.outputs[0] ? f.add->inputs[1] : f.add->inputs[0];
-                                r256 = operand(map_of(other), 1, 256, es);
+                                const std::string& other = f.add->inputs[0] == f_in ? f.add->inputs[1] : f.add->inputs[0];
+                                r256 = operand(mn(other), 1, 256, es);
                                 rok = r256.fast_ok != 0;
                             }
                             if (c256.fast_ok && rok) {
@@ -1658,6 +2110,30 @@ void Executor::prepare(bool dry) {
                             }
                         }
                     }
+                    if (sw != tc_swiglu.end()) {
+                        const OpNode& nu = *sw->second.up;
+                        int64_t ldb2, cb2;
+                        if (!affine2d(map_of(nu.inputs[1]), ldb2, cb2)) throw UnsupportedError("SwiGLU B2 of " + nu.id);
+                        const VMap& bm2 = map_of(nu.inputs[1]);
+                        const char* b2 = reinterpret_cast<const char*>(target(bm2.pieces()[0].target).ptr) + cb2 * es;
+                        if (ok && !impl_->dry && !gemm_tc_encode_b(p.tmap_b2, b2, N, K, ldb2))
+                            throw UnsupportedError("SwiGLU B2 tensor map of " + nu.id);
+                        T->node = sw->second.gate->id + "+" + nu.id + "+" + sw->second.silu->id + "+" + sw->second.mul->id;
+                    }
+                    if (gl != tc_gelu.end()) T->node += "+" + gl->second->id;
+                    auto tr = tc_trees.find(n.id);
+                    if (tr != tc_trees.end()) {
+                        p.epi = GEMM_EPI_TREES;
+                        p.ntree = int32_t(tr->second.trees.size());
+                        for (int k = 0; k < p.ntree; ++k) p.tree[k] = tr->second.trees[size_t(k)];
+                        p.skip_lo = tr->second.skip_lo;
+                        p.skip_hi = tr->second.skip_hi;
+                        for (const auto& root : tr->second.roots) {
+                            std::string label;
+                            for (const auto& m2 : ew_trees.at(root).members) label += (label.empty() ? "" : "+") + m2;
+                            T->node += "|" + label;
+                        }
+                    }
                     auto th = tc_hfuse.find(n.id);
                     if (th != tc_hfuse.end()) {
                         // the absorbed sibling: its weights as B2, its output rows resolved here
@@ -1692,7 +2168,8 @@ void Executor::prepare(bool dry) {
                     if (ok) {
                         // prefill-sized M: 256-row tiles (two M=128 MMAs per B stage)
                         p.mt = (!p.a_gather && p.bn == 256 && M >= 4096) ? 2 : 1;
-                        const int64_t ntl = (N + p.bn - 1) / p.bn + (p.nmat > 1 ? (p.N1 + p.bn - 1) / p.bn : 0);
+                        const int64_t on = p.epi == GEMM_EPI_SWIGLU ? p.bn / 2 : p.bn;  // output columns per tile
+                        const int64_t ntl = (N + on - 1) / on + (p.nmat > 1 ? (p.N1 + p.bn - 1) / p.bn : 0);
                         int64_t tiles = (M + 128 * p.mt - 1) / (128 * p.mt) * ntl;
                         int64_t ktiles = (K + 63) / 64;
                         const int sms = impl_->dry ? 148 : device_sms();
@@ -1702,14 +2179,14 @@ void Executor::prepare(bool dry) {
                         }
                         // K splits as for the first matrix alone: a fused sibling launch sums in
                         // the same order as two separate launches would (bit-identical results)
-                        int64_t tiles0 = tiles / ntl * ((N + p.bn - 1) / p.bn);
+                        int64_t tiles0 = tiles / ntl * ((N + on - 1) / on);
                         int64_t splits = tiles0 >= sms ? 1 : std::min<int64_t>(ktiles, std::max<int64_t>(1, sms / tiles0));
                         if (splits > 1 && p.mt == 2) {
                             // the split-K workspace and counters are per 128-row tile: a K split
                             // (a narrow first matrix) runs 128-row tiles
                             p.mt = 1;
                             tiles = (M + 127) / 128 * ntl;
-                            tiles0 = tiles / ntl * ((N + p.bn - 1) / p.bn);
+                            tiles0 = tiles / ntl * ((N + on - 1) / on);
                             splits = tiles0 >= sms ? 1 : std::min<int64_t>(ktiles, std::max<int64_t>(1, sms / tiles0));
                         }
                         p.splits = int32_t(splits);
@@ -1720,7 +2197,8 @@ void Executor::prepare(bool dry) {
                         push(std::move(T));
                         break;
                     }
-                    if (f.add) throw UnsupportedError("gemm_tc: fused residual without a tensor-core launch for " + n.id);
+                    if (f.add || p.epi != GEMM_EPI_PLAIN)
+                        throw UnsupportedError("gemm_tc: fused epilogue without a tensor-core launch for " + n.id);
                 }
                 auto L = std::make_unique<LaunchT<MatmulParams, launch_matmul>>();
                 L->node = n.id;

@@ -64,8 +64,10 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
     else return uint32_t(r * ROWB + ((c ^ ((r >> 1) & 3)) << 4));
 }
 
+// persistent: CTAs loop over (query block, batch x head) items, so the parameter
+// block is staged once per CTA (Swin: 12,288 items of 49 queries each)
 template <int D>
-__global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* __restrict__ pp) {
+__global__ void __launch_bounds__(NT, D <= 32 ? 4 : 2) attn_prefill_kernel(const AttnParams* __restrict__ pp) {
     constexpr int ROWB = D * 2, TILEB = TK * ROWB, STAGEB = 2 * TILEB;
     VTC_STAGE_PARAMS(AttnParams, pp);
     extern __shared__ __align__(128) unsigned char smem[];
@@ -78,9 +80,14 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int r = p.rank, ax_h = r - 3, ax_s = r - 2, ax_d = r - 1;
     const int Sq = p.Sq, Sk = p.Sk;
-    const int q0 = blockIdx.x * QR;
+    const uint32_t nqb = uint32_t((Sq + QR - 1) / QR), nitems = nqb * uint32_t(p.Bt) * uint32_t(p.H);
+    dev::pdl_wait();
+    dev::pdl_launch_dependents();
+    for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const uint32_t qb = item % nqb;
+    const int q0 = int(qb) * QR;
     // 32-bit index arithmetic (grid dimensions fit): no 64-bit division calls
-    uint32_t bh = blockIdx.y;
+    uint32_t bh = item / nqb;
     const uint32_t bq = bh / uint32_t(p.H);
     const int h = int(bh - bq * uint32_t(p.H));
     bh = bq;
@@ -123,8 +130,6 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
         kb0 = dev::elem_ptr<bf16>(p.k.m, idx);
         vb0 = dev::elem_ptr<bf16>(p.v.m, idx);
     }
-    dev::pdl_wait();
-    dev::pdl_launch_dependents();
     __syncthreads();
 
     // causal: query row q sees keys t <= q + (Sk - Sq)
@@ -156,13 +161,21 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
         auto qv = [&](int row, int d) -> float {
             return q0 + row < Sq ? __bfloat162float(s_qrow[row][int64_t(d) * s_qstr[row]]) : 0.f;
         };
+        // a pair (d, d + 1) of one row: one 32-bit load when the row is contiguous and aligned
+        auto qpair = [&](int row, int d) -> uint32_t {
+            if (q0 + row >= Sq) return 0u;
+            const bf16* rp = s_qrow[row];
+            if (s_qstr[row] == 1 && (reinterpret_cast<uintptr_t>(rp + d) & 3) == 0)
+                return *reinterpret_cast<const uint32_t*>(rp + d);
+            return pack_bf16(qv(row, d), qv(row, d + 1));
+        };
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
             const int d0 = ks * 16 + kc;
-            qa[ks][0] = pack_bf16(qv(rA, d0), qv(rA, d0 + 1));
-            qa[ks][1] = pack_bf16(qv(rB, d0), qv(rB, d0 + 1));
-            qa[ks][2] = pack_bf16(qv(rA, d0 + 8), qv(rA, d0 + 9));
-            qa[ks][3] = pack_bf16(qv(rB, d0 + 8), qv(rB, d0 + 9));
+            qa[ks][0] = qpair(rA, d0);
+            qa[ks][1] = qpair(rB, d0);
+            qa[ks][2] = qpair(rA, d0 + 8);
+            qa[ks][3] = qpair(rB, d0 + 8);
         }
     }
     const float qscale = p.scale * LOG2E;
@@ -273,18 +286,24 @@ __global__ void __launch_bounds__(NT, 2) attn_prefill_kernel(const AttnParams* _
         lB += __shfl_xor_sync(0xffffffffu, lB, off);
     }
     const float iA = lA > 0.f ? 1.f / lA : 0.f, iB = lB > 0.f ? 1.f / lB : 0.f;
+    // pairs (d, d + 1): one 32-bit store when the output row is contiguous and aligned
+    auto store_pair = [&](int row, int d, float a, float b) {
+        bf16* rp = s_orow[row];
+        if (s_ostr[row] == 1 && (reinterpret_cast<uintptr_t>(rp + d) & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(rp + d) = pack_bf16(a, b);
+        } else {
+            rp[int64_t(d) * s_ostr[row]] = __float2bfloat16_rn(a);
+            rp[int64_t(d + 1) * s_ostr[row]] = __float2bfloat16_rn(b);
+        }
+    };
 #pragma unroll
     for (int i = 0; i < D / 8; ++i) {
         const int d = i * 8 + (lane % 4) * 2;
-        if (q0 + rA < Sq) {
-            s_orow[rA][int64_t(d) * s_ostr[rA]] = __float2bfloat16_rn(o[i][0] * iA);
-            s_orow[rA][int64_t(d + 1) * s_ostr[rA]] = __float2bfloat16_rn(o[i][1] * iA);
-        }
-        if (q0 + rB < Sq) {
-            s_orow[rB][int64_t(d) * s_ostr[rB]] = __float2bfloat16_rn(o[i][2] * iB);
-            s_orow[rB][int64_t(d + 1) * s_ostr[rB]] = __float2bfloat16_rn(o[i][3] * iB);
-        }
+        if (q0 + rA < Sq) store_pair(rA, d, o[i][0] * iA, o[i][1] * iA);
+        if (q0 + rB < Sq) store_pair(rB, d, o[i][2] * iB, o[i][3] * iB);
     }
+    __syncthreads();  // the row tables and K / V stages are refilled by the next item
+    }  // items
 }
 
 }  // namespace
@@ -296,10 +315,15 @@ bool attn_prefill_supported(const AttnParams& p) {
 
 template <int D>
 void launch_d(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
-    dim3 grid(unsigned((p.Sq + QR - 1) / QR), unsigned(int64_t(p.Bt) * p.H));
+    const int64_t items = (p.Sq + QR - 1) / QR * int64_t(p.Bt) * p.H;
     const size_t smem = size_t(STAGES) * 2 * TK * D * 2;
     cudaFuncSetAttribute(attn_prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    launch_k(attn_prefill_kernel<D>, grid, dim3(NT), smem, s, dp);
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_prefill_kernel<D>, NT, smem);
+    const int64_t cap = int64_t(sms) * (per_sm > 0 ? per_sm : 1);
+    launch_k(attn_prefill_kernel<D>, dim3(unsigned(items < cap ? items : cap)), dim3(NT), smem, s, dp);
 }
 
 void launch_attn_prefill(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {

@@ -76,8 +76,7 @@ __device__ __forceinline__ T silu_of(T x) {
 }
 template <>
 __device__ __forceinline__ bf16 silu_of<bf16>(bf16 x) {
-    float f = __bfloat162float(x);
-    return __float2bfloat16_rn(f / (1.0f + expf(-f)));
+    return dev::silu_bf16(x);
 }
 template <>
 __device__ __forceinline__ int64_t silu_of<int64_t>(int64_t x) { return x; }
@@ -89,8 +88,7 @@ __device__ __forceinline__ T gelu_of(T x) {
 }
 template <>
 __device__ __forceinline__ bf16 gelu_of<bf16>(bf16 x) {
-    float f = __bfloat162float(x);
-    return __float2bfloat16_rn(0.5f * f * (1.0f + erff(f * 0.70710678f)));
+    return dev::gelu_bf16(x);
 }
 template <>
 __device__ __forceinline__ int64_t gelu_of<int64_t>(int64_t x) { return x; }
@@ -99,13 +97,13 @@ template <typename T>
 __device__ __forceinline__ T add_of(T a, T b) { return a + b; }
 template <>
 __device__ __forceinline__ bf16 add_of<bf16>(bf16 a, bf16 b) {
-    return __float2bfloat16_rn(__bfloat162float(a) + __bfloat162float(b));
+    return dev::add_bf16(a, b);
 }
 template <typename T>
 __device__ __forceinline__ T mul_of(T a, T b) { return a * b; }
 template <>
 __device__ __forceinline__ bf16 mul_of<bf16>(bf16 a, bf16 b) {
-    return __float2bfloat16_rn(__bfloat162float(a) * __bfloat162float(b));
+    return dev::mul_bf16(a, b);
 }
 template <>
 __device__ __forceinline__ int64_t mul_of<int64_t>(int64_t a, int64_t b) {

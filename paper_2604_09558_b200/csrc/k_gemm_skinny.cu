@@ -1,0 +1,365 @@
+// Persistent tcgen05 GEMM for shallow-K, narrow-N bf16 projections at large M
+// (Swin-T's QKV / proj / fc1 / fc2: K, N <= 384, M = 200,704 window tokens).
+//
+// C[M, N] = epilogue(A[M, K] . W[K, N]) -- the reference's matmul_kernel
+// (proj/src/executor.cpp:230-249) -- where the whole weight fits in shared
+// memory.  Such GEMMs are HBM-bound (2-8 flop per byte) and their cost is the
+// epilogue, so the kernel is built around keeping stores and loads streaming:
+//
+//   * one CTA per SM loops over 128-row tiles; the weight is loaded once per
+//     CTA and kept in shared memory, transposed to the K-major 128-byte-swizzled
+//     UMMA layout (any 8-row-aligned N slice is then a valid B descriptor);
+//   * warp 0 streams A: TMA (a plain 2-D view) or 16-byte cp.async gathers
+//     through host-resolved row addresses (a virtual roll + window partition),
+//     into a ring of 128 x 64 k-tile slots;
+//   * warp 1 issues tcgen05.mma M128 x NC x K16 into one of two TMEM
+//     accumulators (a tile's N columns in `nchunks` units of NC <= 256), so the
+//     next unit's MMAs overlap this unit's epilogue;
+//   * warps 2-9 drain the accumulator (two warps per TMEM lane quadrant, half
+//     the columns each), round to bf16 (optionally GELU), stage the unit in
+//     shared memory and copy it out with coalesced 16-byte stores through the
+//     output rows, adding the residual (rounded like the unfused Add).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "device.cuh"
+#include "launch.cuh"
+
+namespace vtc {
+namespace {
+
+using dev::bf16;
+constexpr int BM = 128, BK = 64, UK = 16, NEPI = 8, NTHREADS = (2 + NEPI) * 32;
+constexpr uint32_t SLOT_BYTES = BM * BK * 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(NEPI * 32) : "memory"); }
+
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B: start >> 4, LBO (unused
+// for swizzled K-major) = 16 B, SBO = 1024 B between 8-row groups, version 1.
+__device__ __forceinline__ uint64_t kdesc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);
+    d |= uint64_t(1) << 16;
+    d |= uint64_t(1024 >> 4) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(2) << 61;
+    return d;
+}
+// kind::f16 instruction descriptor: D f32, A / B bf16, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc(int m, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+// byte offset of element (row, k) of a [rows][64] K-major SW128 tile
+__device__ __forceinline__ uint32_t sw128(int row, int k) {
+    return uint32_t(row) * 128u + ((uint32_t((k >> 3) ^ (row & 7))) << 4) + uint32_t(k & 7) * 2u;
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_constant__ SkinnyParams p) {
+    dev::TraceScope trace_scope_(&p.head);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int KT = p.kt, S = p.slots, NC = p.nc, NCH = p.nchunks;
+    const int NP = (int(p.N) + 7) / 8 * 8;
+    unsigned char* sB = smem;                                   // [KT][NP rows][128 B]
+    unsigned char* sA = sB + size_t(KT) * NP * 128;             // S slots of [128][128 B]
+    unsigned char* sC = sA + size_t(S) * SLOT_BYTES;            // [128][NC + 8] bf16 staging
+    const int cpitch = NC + 8;                                  // elements per staged row
+    __shared__ uint64_t a_full[16], a_empty[16], acc_full[2], acc_empty[2];
+    __shared__ uint32_t s_tmem;
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t mtiles = (p.M + BM - 1) / BM;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&a_full[s], p.a_gather ? 32 : 1);
+            mbar_init(&a_empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], NEPI);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {  // two accumulators of up to 256 fp32 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    dev::pdl_launch_dependents();
+    // the weight, transposed into K-major swizzled k-tiles: thread reads 8 consecutive
+    // columns of one weight row (16 bytes) and scatters them to 8 B rows
+    if (!p.b_static) dev::pdl_wait();
+    {
+        const int ngrp = (int(p.N) + 7) / 8;
+        const int64_t total = int64_t(KT) * BK * ngrp;
+        for (int64_t i = threadIdx.x; i < total; i += NTHREADS) {
+            const int k = int(i / ngrp), g = int(i % ngrp);
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (k < p.K) v = __ldg(reinterpret_cast<const uint4*>(static_cast<const bf16*>(p.w) + int64_t(k) * p.ldw + g * 8));
+            const bf16* e = reinterpret_cast<const bf16*>(&v);
+            unsigned char* tile = sB + size_t(k / BK) * NP * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int n = g * 8 + j;
+                if (n < NP) *reinterpret_cast<bf16*>(tile + sw128(n, k % BK)) = e[j];
+            }
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 0) {
+        // ---------------- A producer ----------------
+        if (p.b_static) dev::pdl_wait();
+        int g = 0;  // global k-tile counter -> slot g % S, phase (g / S) & 1
+        if (!p.a_gather) {
+            if (lane == 0) {
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_a)) : "memory");
+                const uint64_t pol = dev::evict_first_policy();  // A is read once
+                for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x)
+                    for (int kt = 0; kt < KT; ++kt, ++g) {
+                        const int s = g % S;
+                        mbar_wait(&a_empty[s], ((g / S) & 1) ^ 1u);
+                        mbar_expect_tx(&a_full[s], SLOT_BYTES);
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+                            " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(sA + size_t(s) * SLOT_BYTES)),
+                            "l"(reinterpret_cast<uint64_t>(&p.tmap_a)), "r"(kt * BK), "r"(int32_t(mt * BM)),
+                            "r"(smem_u32(&a_full[s])), "l"(pol)
+                            : "memory");
+                    }
+            }
+        } else {
+            // gathers: 128 rows x 8 chunks of 16 B per k-tile, one lane per chunk column;
+            // slot g - 1 is published once its copies have landed (one slot in flight)
+            int prev = -1;
+            for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+                const int64_t m0 = mt * BM;
+                for (int kt = 0; kt < KT; ++kt, ++g) {
+                    const int s = g % S;
+                    mbar_wait(&a_empty[s], ((g / S) & 1) ^ 1u);
+                    const uint32_t base = smem_u32(sA + size_t(s) * SLOT_BYTES);
+#pragma unroll 4
+                    for (int j = 0; j < (BM * 8) / 32; ++j) {
+                        const int c = lane + 32 * j, row = c >> 3, ch = c & 7;
+                        const int64_t m = m0 + row, k = int64_t(kt) * BK + ch * 8;
+                        const bool ok = m < p.M && k < p.K;
+                        const void* src = ok ? reinterpret_cast<const void*>(p.a_rows[m] + uint64_t(k) * 2)
+                                             : p.w;
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(base + sw128(row, ch * 8)),
+                                     "l"(src), "r"(ok ? 16 : 0)
+                                     : "memory");
+                    }
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    if (prev >= 0) {
+                        asm volatile("cp.async.wait_group 1;" ::: "memory");
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        mbar_arrive(&a_full[prev]);
+                    }
+                    prev = s;
+                }
+            }
+            if (prev >= 0) {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&a_full[prev]);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            const uint32_t id = idesc(BM, NC);
+            int g = 0, u = 0;
+            for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+                const int g0 = g;
+                for (int j = 0; j < NCH; ++j, ++u) {
+                    const int b = u & 1;
+                    mbar_wait(&acc_empty[b], ((u >> 1) & 1) ^ 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    for (int kt = 0; kt < KT; ++kt) {
+                        const int gs = g0 + kt, s = gs % S;
+                        if (j == 0) {
+                            mbar_wait(&a_full[s], (gs / S) & 1);
+                            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        }
+                        const uint32_t sa = smem_u32(sA + size_t(s) * SLOT_BYTES);
+                        const uint32_t sb = smem_u32(sB + size_t(kt) * NP * 128 + size_t(j) * NC * 128);
+                        const int ksteps = min(BK, int(p.K) - kt * BK) / UK;
+                        for (int k = 0; k < ksteps; ++k) {
+                            const uint32_t acc = (kt > 0 || k > 0) ? 1u : 0u;
+                            asm volatile(
+                                "{\n.reg .pred q;\nsetp.ne.b32 q, %4, 0;\n"
+                                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n}\n" ::"r"(tmem + uint32_t(b * 256)),
+                                "l"(kdesc(sa + k * 32)), "l"(kdesc(sb + k * 32)), "r"(id), "r"(acc)
+                                : "memory");
+                        }
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     smem_u32(&acc_full[b]))
+                                 : "memory");
+                }
+                // every chunk of this tile has been issued: its A slots free once they complete
+                for (int kt = 0; kt < KT; ++kt)
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     smem_u32(&a_empty[(g0 + kt) % S]))
+                                 : "memory");
+                g += KT;
+            }
+        }
+    } else {
+        // ---------------- epilogue: warps 2..9 ----------------
+        dev::pdl_wait();
+        const int et = threadIdx.x - 64;        // 0..255
+        const int quad = warp & 3;              // TMEM lanes 32*quad .. +31 (hardware rule: warp id mod 4)
+        const int half = (warp - 2) >> 2;       // two warps per quadrant: column halves
+        const int row = quad * 32 + lane;
+        const int hc = (NC / 2 + 7) / 8 * 8;    // columns per half, multiple of 8
+        const int c_lo = half * hc, c_hi = min(NC, c_lo + hc);
+        bf16* srow = reinterpret_cast<bf16*>(sC) + size_t(row) * cpitch;
+        const int cpr = NC / 8;                  // 16-byte chunks per output row
+        int u = 0;
+        for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+            const int64_t m0 = mt * BM;
+            for (int j = 0; j < NCH; ++j, ++u) {
+                const int b = u & 1;
+                mbar_wait(&acc_full[b], (u >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t taddr = tmem + (uint32_t(quad * 32) << 16) + uint32_t(b * 256);
+                for (int c = c_lo; c < c_hi; c += 8) {
+                    uint32_t r[8];
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                                   "=r"(r[7])
+                                 : "r"(taddr + uint32_t(c)));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    bf16 o[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const bf16 v = __float2bfloat16_rn(__uint_as_float(r[q]));
+                        o[q] = p.epi == 1 ? dev::gelu_bf16(v) : v;
+                    }
+                    *reinterpret_cast<uint4*>(srow + c) = *reinterpret_cast<const uint4*>(o);
+                }
+                // accumulator drained: the MMA warp may refill it
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[b]);
+                bar_epi();  // the unit is staged
+                // coalesced copy-out: consecutive threads take consecutive 16-byte chunks of a row
+                const int64_t n0 = int64_t(j) * NC;
+                for (int i = et; i < BM * cpr; i += NEPI * 32) {
+                    const int rr = i / cpr, cc = i % cpr;
+                    const int64_t m = m0 + rr;
+                    if (m >= p.M) break;
+                    uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(sC) + size_t(rr) * cpitch + cc * 8);
+                    const int64_t col = n0 + cc * 8;
+                    if (p.has_res) {
+                        const bf16* rp = p.r_rows ? reinterpret_cast<const bf16*>(p.r_rows[m])
+                                                  : reinterpret_cast<const bf16*>(p.r_base) + m * p.r_ld;
+                        const uint4 rv = __ldg(reinterpret_cast<const uint4*>(rp + col));
+                        const bf16* a = reinterpret_cast<const bf16*>(&rv);
+                        bf16* x = reinterpret_cast<bf16*>(&v);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) x[q] = dev::add_bf16(a[q], x[q]);
+                    }
+                    bf16* cp = p.c_rows ? reinterpret_cast<bf16*>(p.c_rows[m]) : reinterpret_cast<bf16*>(p.c_base) + m * p.c_ld;
+                    *reinterpret_cast<uint4*>(cp + col) = v;
+                }
+                bar_epi();  // staging free for the next unit
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encoder() {
+    static EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return EncodeFn(nullptr);
+        return reinterpret_cast<EncodeFn>(f);
+    }();
+    return fn;
+}
+
+}  // namespace
+
+bool skinny_plan(SkinnyParams& p, int smem_optin) {
+    if (p.K % UK || p.N % 16 || p.K > 512 || p.N > 1024) return false;
+    p.kt = int((p.K + BK - 1) / BK);
+    // N in units of NC <= 256 (two accumulators in 512 TMEM columns), NC a multiple of 16
+    int nch = 1;
+    while (nch <= 8 && (p.N % nch || (p.N / nch) % 16 || p.N / nch > 256)) ++nch;
+    if (nch > 8) return false;
+    p.nchunks = nch;
+    p.nc = int(p.N / nch);
+    const int64_t np = (p.N + 7) / 8 * 8;
+    const int64_t fixed = int64_t(p.kt) * np * 128 + int64_t(BM) * (p.nc + 8) * 2 + 1024;
+    // a tile's k-tiles stay resident until its last chunk: at least kt slots, two tiles' worth if they fit
+    int slots = int((smem_optin - 1024 - fixed) / SLOT_BYTES);
+    if (slots > 16) slots = 16;
+    const int need = p.nchunks > 1 ? p.kt : 2;
+    if (slots < need) return false;
+    if (slots > 2 * p.kt && p.nchunks > 1) slots = std::max(2 * p.kt, std::min(slots, 4 * p.kt));
+    p.slots = slots;
+    p.smem = size_t(fixed + int64_t(slots) * SLOT_BYTES);
+    return true;
+}
+
+bool skinny_encode_a(SkinnyParams& p, const void* a_base, int64_t lda) {
+    EncodeFn fn = encoder();
+    if (!fn || (reinterpret_cast<uintptr_t>(a_base) % 16) || (lda * 2) % 16) return false;
+    cuuint64_t dims[2] = {cuuint64_t(p.K), cuuint64_t(p.M)};
+    cuuint64_t str[1] = {cuuint64_t(lda) * 2};
+    cuuint32_t box[2] = {BK, BM}, es[2] = {1, 1};
+    return fn(reinterpret_cast<CUtensorMap*>(p.tmap_a), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a_base), dims,
+              str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void launch_gemm_skinny(const SkinnyParams& p, const SkinnyParams*, cudaStream_t s) {
+    allow_max_smem(gemm_skinny_kernel);
+    const int64_t mtiles = (p.M + BM - 1) / BM;
+    const unsigned grid = unsigned(std::min<int64_t>(mtiles, p.sms));
+    launch_k(gemm_skinny_kernel, dim3(grid), dim3(NTHREADS), p.smem, s, p);
+}
+
+}  // namespace vtc

@@ -121,11 +121,13 @@ struct Tmaps {
 
 // MT = 128-row sub-tiles per CTA (2: a 256 x BN tile whose two M=128 MMAs
 // share each B stage -- half the B traffic per FLOP for prefill-sized M)
-template <int BN, int STAGES, int MT>
+template <int BN, int STAGES, int MT, int EPI>
 __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams* __restrict__ pp,
                                                                const __grid_constant__ Tmaps tm) {
     VTC_STAGE_PARAMS(GemmTcParams, pp);
     constexpr int TM = BM * MT;
+    // output columns per tile: SwiGLU tiles hold gate and up halves of BN / 2 each
+    constexpr int ON = EPI == GEMM_EPI_SWIGLU ? BN / 2 : BN;
     constexpr uint32_t A_SUB = BM * BK * 2, A_BYTES = A_SUB * MT, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     __shared__ unsigned s_last;
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int tiles_n0 = int((p.N + BN - 1) / BN);
+    const int tiles_n0 = int((p.N + ON - 1) / ON);
     const int tiles_n = tiles_n0 + (p.nmat > 1 ? int((p.N1 + BN - 1) / BN) : 0);
     const int tiles_m = int((p.M + TM - 1) / TM);
     const int tile = blockIdx.x;
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     const int gm = min(tiles_m - first_m, GROUP_M);
     const int tm_ = first_m + (tile % in_group) % gm, tn = (tile % in_group) / gm;
     const int mat = tn >= tiles_n0 ? 1 : 0;  // horizontally fused sibling (gate / up)
-    const int64_t m0 = int64_t(tm_) * TM, n0 = int64_t(mat ? tn - tiles_n0 : tn) * BN;
+    const int64_t m0 = int64_t(tm_) * TM, n0 = int64_t(mat ? tn - tiles_n0 : tn) * ON;
     const int64_t Nm = mat ? p.N1 : p.N;
     const CUtensorMap* tmb = mat ? &tm.b2 : &tm.b;
     const int split = blockIdx.y;
@@ -226,8 +228,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             if (lane == 0) {
                 mbar_expect_tx(&full[s], B_BYTES);
 #pragma unroll
-                for (int j = 0; j < BN / 64; ++j)
-                    tma_2d(sb + j * (BK * 128), tmb, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
+                for (int j = 0; j < BN / 64; ++j) {
+                    if (EPI == GEMM_EPI_SWIGLU && j >= BN / 128)
+                        tma_2d(sb + j * (BK * 128), &tm.b2, int32_t(n0 + 64 * (j - BN / 128)), k0, &full[s], pol_b);
+                    else
+                        tma_2d(sb + j * (BK * 128), tmb, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
+                }
             }
             const uint32_t sa_u = smem_u32(sa);
 #pragma unroll 8
@@ -308,8 +314,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                 }
             }
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-                tma_2d(sb + j * (BK * 128), tmb, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
+            for (int j = 0; j < BN / 64; ++j) {
+                if (EPI == GEMM_EPI_SWIGLU && j >= BN / 128)  // the up half: the same columns of B2
+                    tma_2d(sb + j * (BK * 128), &tm.b2, int32_t(n0 + 64 * (j - BN / 128)), k0, &full[s], pol_b);
+                else
+                    tma_2d(sb + j * (BK * 128), tmb, int32_t(n0 + 64 * j), k0, &full[s], pol_b);
+            }
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer ----------------
@@ -445,8 +455,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                 rs = p.res.fast_stride[lr.piece];
             }
         }
-        const int ncols = int(Nm - n0 < BN ? Nm - n0 : BN);
-        // 16 finished columns c..c+15 of this row: round, residual, store through C's map
+        const int ncols = int(Nm - n0 < ON ? Nm - n0 : ON);
+        // accumulator columns c..c+15 of this thread's row: TMEM, or the split-K sum
+        auto get16 = [&](int c, float (&v)[16]) {
+            if (p.splits > 1) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 0.f;
+                if (!live) return;
+                // up to 4 splits' 16 columns in flight per round trip, summed in split order
+                for (int s0 = 0; s0 < p.splits; s0 += 4) {
+                    float tq[4][16];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float* src = wtile + int64_t(s0 + q) * BM * BN + int64_t(c) * BM + erow;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) tq[q][j] = s0 + q < p.splits ? __ldcg(src + int64_t(j) * BM) : 0.f;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (s0 + q < p.splits)
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) v[j] += tq[q][j];
+                }
+            } else {
+                tmem_ld16(c, v);
+            }
+        };
+        // 16 finished columns c..c+15 of this row: round, activation / residual, store through C's map
         auto emit = [&](int c, const float (&v)[16]) {
             bf16 o[16];
             // the residual's 16 columns: two 16-byte loads when contiguous and aligned
@@ -458,6 +493,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             }
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
+                if (EPI == GEMM_EPI_GELU) {
+                    o[j] = dev::gelu_bf16(__float2bfloat16_rn(v[j]));
+                    continue;
+                }
                 float f = __bfloat162float(__float2bfloat16_rn(v[j]));
                 if (rvec) f = __bfloat162float(rv[j]) + f;
                 else if (rrow && c + j < ncols) f = __bfloat162float(rrow[int64_t(c + j) * rs]) + f;
@@ -475,8 +514,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
         };
         // shallow-K variants (epilogue-bound): 64 accumulator columns per TMEM
         // round trip (4 loads, one wait), indices static so they stay in registers
-        constexpr bool kBatch = MT == 1;
-        if (kBatch && p.splits == 1) {
+        constexpr bool kBatch = MT == 1 && (EPI == GEMM_EPI_PLAIN || EPI == GEMM_EPI_GELU);
+        if (EPI == GEMM_EPI_SWIGLU) {
+            // columns c of the gate half and 128 + c of the up half -> SiLU(gate) * up,
+            // rounded like the unfused SiLU and Mul operators
+            const int cpart = (ON / nparts + 15) / 16 * 16;
+            const int c_lo = part * cpart, c_hi = min(ncols, c_lo + cpart);
+            for (int c = c_lo; c < c_hi; c += 16) {
+                float g[16], u[16];
+                get16(c, g);
+                get16(ON + c, u);
+                if (!live) continue;
+                bf16 o[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    o[j] = dev::mul_bf16(dev::silu_bf16(__float2bfloat16_rn(g[j])), __float2bfloat16_rn(u[j]));
+                bf16* dst = crow + int64_t(c) * cs;
+                if (cs == 1 && c + 16 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                    reinterpret_cast<uint4*>(dst)[0] = *reinterpret_cast<const uint4*>(&o[0]);
+                    reinterpret_cast<uint4*>(dst)[1] = *reinterpret_cast<const uint4*>(&o[8]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (c + j < ncols) dst[int64_t(j) * cs] = o[j];
+                }
+            }
+        } else if (kBatch && p.splits == 1) {
             for (int c0 = 0; c0 < ncols; c0 += 64) {
                 uint32_t r[64];
 #pragma unroll
@@ -505,33 +568,77 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
             const int cpart = (BN / nparts + 15) / 16 * 16;  // this thread's columns [c_lo, c_hi)
             const int c_lo = part * cpart, c_hi = min(ncols, c_lo + cpart);
             for (int c = c_lo; c < c_hi; c += 16) {
+                // trees: columns read only by the fused trees are never stored (tile-uniform test)
+                if (EPI == GEMM_EPI_TREES && n0 + c >= p.skip_lo && n0 + c + 16 <= p.skip_hi) continue;
                 float v[16];
-                if (p.splits > 1) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = 0.f;
-                    if (live) {
-                        // up to 4 splits' 16 columns in flight per round trip, summed in split order
-                        for (int s0 = 0; s0 < p.splits; s0 += 4) {
-                            float t[4][16];
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const float* src = wtile + int64_t(s0 + q) * BM * BN + int64_t(c) * BM + erow;
-#pragma unroll
-                                for (int j = 0; j < 16; ++j)
-                                    t[q][j] = s0 + q < p.splits ? __ldcg(src + int64_t(j) * BM) : 0.f;
-                            }
-#pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                if (s0 + q < p.splits)
-#pragma unroll
-                                    for (int j = 0; j < 16; ++j) v[j] += t[q][j];
-                        }
-                    }
-                } else {
-                    tmem_ld16(c, v);
-                }
+                get16(c, v);
                 if (!live) continue;
                 emit(c, v);
+            }
+        }
+        if (EPI == GEMM_EPI_TREES) {
+            // elementwise trees over views of this tile (e.g. RoPE: x * cos + rotate_half(x) * sin):
+            // head h of tree tr reads C columns of this tile only; 16 elements i0..i0+15 per step
+            for (int tr = 0; tr < p.ntree; ++tr) {
+                const GemmTree& T = p.tree[tr];
+                for (int h = 0; h < T.nh; ++h) {
+                    const int64_t anchor = T.c_lo + T.c_sh * h;
+                    if (anchor < n0 || anchor >= n0 + ON) continue;
+                    if (p.splits > 1 && (h % nparts) != part) continue;  // split path: heads over the row's threads
+                    for (int i0 = 0; i0 < T.hd; i0 += 16) {
+                        bf16 in[EW_MAX_IN][16];
+#pragma unroll
+                        for (int k = 0; k < EW_MAX_IN; ++k) {
+                            if (k < T.nin) {
+                                const GemmTreeOp& op = T.op[1 + k];
+                                const int q = i0 >= op.split ? 1 : 0;
+                                if (op.from_c) {
+                                    float v[16];
+                                    get16(int(op.ccol[q] + op.sh[q] * h + i0 - n0), v);
+#pragma unroll
+                                    for (int j = 0; j < 16; ++j) in[k][j] = __float2bfloat16_rn(v[j]);
+                                } else if (live) {
+                                    const bf16* src = reinterpret_cast<const bf16*>(op.base[q]) + op.rs[q] * em + op.sh[q] * h + i0;
+                                    *reinterpret_cast<uint4*>(&in[k][0]) = __ldg(reinterpret_cast<const uint4*>(src));
+                                    *reinterpret_cast<uint4*>(&in[k][8]) = __ldg(reinterpret_cast<const uint4*>(src + 8));
+                                }
+                            }
+                        }
+                        if (!live) continue;
+                        bf16 o[16];
+                        if (T.pat == 3) {  // (in0 * in1) + (in2 * in3): RoPE, in registers
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                o[j] = dev::add_bf16(dev::mul_bf16(in[0][j], in[1][j]), dev::mul_bf16(in[2][j], in[3][j]));
+                        } else {
+                            bf16 r[EW_MAX_IN + EW_MAX_PROG][16];
+#pragma unroll
+                            for (int k = 0; k < EW_MAX_IN; ++k)
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) r[k][j] = in[k][j];
+#pragma unroll 1
+                            for (int s2 = 0; s2 < T.nprog; ++s2) {
+                                const EwInstr ins = T.prog[s2];
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) {
+                                    const bf16 a = r[ins.a][j], b = r[ins.b][j];
+                                    r[ins.dst][j] = ins.op == EwOp::Add   ? dev::add_bf16(a, b)
+                                                    : ins.op == EwOp::Mul  ? dev::mul_bf16(a, b)
+                                                    : ins.op == EwOp::SiLU ? dev::silu_bf16(a)
+                                                    : ins.op == EwOp::GELU ? dev::gelu_bf16(a)
+                                                                           : a;
+                                }
+                            }
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) o[j] = r[T.result][j];
+                        }
+                        const GemmTreeOp& out = T.op[0];
+                        const int q = i0 >= out.split ? 1 : 0;
+                        bf16* dst = reinterpret_cast<bf16*>(out.base[q]) + out.rs[q] * em + out.sh[q] * h + i0;
+                        reinterpret_cast<uint4*>(dst)[0] = *reinterpret_cast<const uint4*>(&o[0]);
+                        reinterpret_cast<uint4*>(dst)[1] = *reinterpret_cast<const uint4*>(&o[8]);
+                    }
+                }
             }
         }
     }
@@ -664,44 +771,52 @@ bool gemm_tc_encode_b(void* out128, const void* b_base, int64_t N, int64_t K, in
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int BN, int ST, int MT, int EPI>
+void launch_variant(const GemmTcParams* dp, dim3 grid, const Tmaps& tmaps, cudaStream_t s) {
+    constexpr size_t sm = smem_bytes<BN, ST, MT>();
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, ST, MT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    launch_k(gemm_tc_kernel<BN, ST, MT, EPI>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+}
+
+template <int EPI>
+void launch_epi(const GemmTcParams& p, const GemmTcParams* dp, const Tmaps& tmaps, cudaStream_t s) {
+    const int tm = p.mt == 2 ? 2 * BM : BM;
+    const int on = EPI == GEMM_EPI_SWIGLU ? p.bn / 2 : p.bn;
+    const int tiles = int((p.M + tm - 1) / tm) *
+                      int((p.N + on - 1) / on + (p.nmat > 1 ? (p.N1 + p.bn - 1) / p.bn : 0));
+    const int64_t ktiles = (p.K + BK - 1) / BK;
+    const dim3 grid(unsigned(tiles), unsigned(p.splits));
+    if (p.mt == 2) {
+        launch_variant<256, 3, 2, EPI>(dp, grid, tmaps, s);
+    } else if (p.bn == 256 && ktiles <= 2 && p.splits == 1) {
+        // shallow K (e.g. Swin's K = 96): a 2-stage ring, two CTAs per SM, so one
+        // CTA's epilogue overlaps the other's loads and MMAs
+        launch_variant<256, 2, 1, EPI>(dp, grid, tmaps, s);
+    } else if (p.bn == 256 || EPI == GEMM_EPI_SWIGLU) {
+        launch_variant<256, 4, 1, EPI>(dp, grid, tmaps, s);
+    } else if constexpr (EPI != GEMM_EPI_SWIGLU) {
+        if (ktiles <= 2 && p.splits == 1) {
+            launch_variant<128, 2, 1, EPI>(dp, grid, tmaps, s);  // three CTAs per SM
+        } else if ((ktiles <= 6 || (p.M <= BM && tiles > 148)) && p.splits == 1) {
+            // two CTAs per SM: shallow K, or decode-sized M with more tiles than SMs (the
+            // fused gate / up weight streams then run in one wave instead of two)
+            launch_variant<128, 3, 1, EPI>(dp, grid, tmaps, s);
+        } else {
+            launch_variant<128, 6, 1, EPI>(dp, grid, tmaps, s);
+        }
+    }
+}
+
 void launch_gemm_tc(const GemmTcParams& p, const GemmTcParams* dp, cudaStream_t s) {
     Tmaps tmaps;
     std::memcpy(&tmaps.a, p.tmap_a, sizeof(CUtensorMap));
     std::memcpy(&tmaps.b, p.tmap_b, sizeof(CUtensorMap));
-    std::memcpy(&tmaps.b2, p.nmat > 1 ? p.tmap_b2 : p.tmap_b, sizeof(CUtensorMap));
-    const int tm = p.mt == 2 ? 2 * BM : BM;
-    const int tiles = int((p.M + tm - 1) / tm) *
-                      int((p.N + p.bn - 1) / p.bn + (p.nmat > 1 ? (p.N1 + p.bn - 1) / p.bn : 0));
-    const int64_t ktiles = (p.K + BK - 1) / BK;
-    dim3 grid(unsigned(tiles), unsigned(p.splits));
-    if (p.mt == 2) {
-        constexpr size_t sm = smem_bytes<256, 3, 2>();
-        cudaFuncSetAttribute(gemm_tc_kernel<256, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        launch_k(gemm_tc_kernel<256, 3, 2>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
-    } else if (p.bn == 256 && ktiles <= 2 && p.splits == 1) {
-        // shallow K (e.g. Swin's K = 96): a 2-stage ring, two CTAs per SM, so one
-        // CTA's epilogue overlaps the other's loads and MMAs
-        constexpr size_t sm = smem_bytes<256, 2, 1>();
-        cudaFuncSetAttribute(gemm_tc_kernel<256, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        launch_k(gemm_tc_kernel<256, 2, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
-    } else if (p.bn == 256) {
-        constexpr size_t sm = smem_bytes<256, 4, 1>();
-        cudaFuncSetAttribute(gemm_tc_kernel<256, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        launch_k(gemm_tc_kernel<256, 4, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
-    } else if (ktiles <= 2 && p.splits == 1) {
-        constexpr size_t sm = smem_bytes<128, 2, 1>();  // three CTAs per SM
-        cudaFuncSetAttribute(gemm_tc_kernel<128, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        launch_k(gemm_tc_kernel<128, 2, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
-    } else if ((ktiles <= 6 || (p.M <= BM && tiles > 148)) && p.splits == 1) {
-        // two CTAs per SM: shallow K, or decode-sized M with more tiles than SMs (the
-        // fused gate / up weight streams then run in one wave instead of two)
-        constexpr size_t sm = smem_bytes<128, 3, 1>();
-        cudaFuncSetAttribute(gemm_tc_kernel<128, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        launch_k(gemm_tc_kernel<128, 3, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
-    } else {
-        constexpr size_t sm = smem_bytes<128, 6, 1>();
-        cudaFuncSetAttribute(gemm_tc_kernel<128, 6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        launch_k(gemm_tc_kernel<128, 6, 1>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+    std::memcpy(&tmaps.b2, (p.nmat > 1 || p.epi == GEMM_EPI_SWIGLU) ? p.tmap_b2 : p.tmap_b, sizeof(CUtensorMap));
+    switch (p.epi) {
+        case GEMM_EPI_GELU: launch_epi<GEMM_EPI_GELU>(p, dp, tmaps, s); break;
+        case GEMM_EPI_SWIGLU: launch_epi<GEMM_EPI_SWIGLU>(p, dp, tmaps, s); break;
+        case GEMM_EPI_TREES: launch_epi<GEMM_EPI_TREES>(p, dp, tmaps, s); break;
+        default: launch_epi<GEMM_EPI_PLAIN>(p, dp, tmaps, s); break;
     }
 }
 

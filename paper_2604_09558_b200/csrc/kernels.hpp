@@ -239,6 +239,27 @@ bool encode_weight_tmap(void* out128, const void* base, int64_t rows, int64_t co
 // their maps (affine along N per row).  K is split across `splits` CTAs per
 // tile when the tile grid alone would leave SMs idle.
 constexpr int GEMM_MAX_SEG = 4;
+enum GemmEpi : int32_t { GEMM_EPI_PLAIN = 0, GEMM_EPI_GELU = 1, GEMM_EPI_SWIGLU = 2, GEMM_EPI_TREES = 3 };
+// An elementwise tree evaluated in the tensor-core GEMM's epilogue (e.g. the
+// Q / K RoPE trees over the QKV projection): the tree's index space is
+// [rows = the GEMM's M, heads, hd]; operand k addresses element (m, h, i) at
+//   C-derived (from_c): C column ccol[q] + sh[q] * h + i of the same row m,
+//   external / output:  base[q] + (rs[q] * m + sh[q] * h + i) elements,
+// with piece q = (i >= split).  Head h's C columns lie in one N tile: they
+// start at anchor c_lo + c_sh * h and span less than 128 columns.
+constexpr int GEMM_MAX_TREES = 2;
+struct GemmTreeOp {
+    uint64_t base[2];
+    int64_t rs[2], sh[2], ccol[2];
+    int32_t from_c, split;
+};
+struct GemmTree {
+    int32_t nin, nprog, result, hd;
+    int32_t nh, pat;  // pat 3: the program is (in0 * in1) + (in2 * in3) (RoPE), evaluated in registers
+    int64_t c_lo, c_sh;
+    EwInstr prog[EW_MAX_PROG];
+    GemmTreeOp op[EW_MAX_IN + 1];  // [0] = output
+};
 struct GemmTcParams {
     KHead head;
     VOperand c, res;
@@ -276,6 +297,12 @@ struct GemmTcParams {
     const uint64_t* c2_rows;
     int64_t c2_rs;
     alignas(64) unsigned char tmap_b2[128];
+    // fused epilogue (GemmEpi): GELU of the rounded product; SwiGLU, where each
+    // 256-column B stage holds 128 columns of B (gate) and the same 128 of B2 (up)
+    // and the tile stores SiLU(gate) * up; or elementwise trees over views of C
+    int32_t epi, ntree;
+    int64_t skip_lo, skip_hi;  // trees: C columns [skip_lo, skip_hi) are not stored (read only by the trees)
+    GemmTree tree[GEMM_MAX_TREES];
 };
 // Encode a B tensor map (row-major bf16 [K, N], row stride ld) into out128.
 bool gemm_tc_encode_b(void* out128, const void* b_base, int64_t N, int64_t K, int64_t ld);
@@ -286,6 +313,34 @@ bool gemm_tc_a_dims(const vtc_map& a, int64_t M, int64_t K, GemmTcParams& p, int
 bool gemm_tc_encode(GemmTcParams& p, const void* a_base, const int64_t* a_dims, const int64_t* a_strides,
                     const void* b_base, int64_t b_ld);
 void launch_gemm_tc(const GemmTcParams& p, const GemmTcParams* dp, cudaStream_t s);
+
+// ---- persistent shallow-K GEMM (weights resident in shared memory) --------
+// C[M, N] = epi(A . W) (+ residual) for K, N <= 512 at large M (Swin's projections):
+// A by TMA (tmap_a, a plain 2-D view) or 16-byte gathers from host-resolved rows
+// (a_rows[m] = address of A[m, 0]); C / residual rows affine (base + m * ld) or
+// host-resolved (c_rows / r_rows), unit column stride, 16-byte aligned.
+struct SkinnyParams {
+    KHead head;
+    int64_t M, N, K;
+    int32_t kt, nc, nchunks, slots;  // k-tiles, N columns per unit, units per tile, A ring slots
+    int32_t epi;                     // 0: plain, 1: GELU of the rounded product
+    int32_t has_res, a_gather, b_static, sms, pad;
+    size_t smem;
+    const void* w;  // weights [K, N] bf16, row stride ldw
+    int64_t ldw;
+    const uint64_t* a_rows;
+    uint64_t c_base;
+    int64_t c_ld;
+    const uint64_t* c_rows;
+    uint64_t r_base;
+    int64_t r_ld;
+    const uint64_t* r_rows;
+    alignas(64) unsigned char tmap_a[128];
+};
+// Tile plan (k-tiles, N units, ring depth, shared memory); false if the weight does not fit.
+bool skinny_plan(SkinnyParams& p, int smem_optin);
+bool skinny_encode_a(SkinnyParams& p, const void* a_base, int64_t lda);
+void launch_gemm_skinny(const SkinnyParams& p, const SkinnyParams* dp, cudaStream_t s);
 
 // ---- row-wise normalisations / softmax -----------------------------------
 enum class RowOp : int32_t { RMSNorm = 0, LayerNorm, Softmax };

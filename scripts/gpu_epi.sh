@@ -1,0 +1,8 @@
+#!/bin/bash
+# fused tcgen05 epilogues: bit-identity + full-size parity + bench of C3/C4/C5
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu.py -q -x -k "fused_epilogues or gate_up or fast_paths" > gpurun_out/epi_tests.log 2>&1; echo epi=$?; tail -15 gpurun_out/epi_tests.log
+timeout 900 python -m pytest tests/test_fullsize.py tests/test_gpu.py -q -x -m gpu > gpurun_out/full_tests.log 2>&1; echo full=$?; tail -5 gpurun_out/full_tests.log
+export BENCH_NO_CPU=1
+for c in ${CFGS:-c3 c4 c5}; do timeout 600 python bench.py --config $c --steps 10 > gpurun_out/b_$c.json 2> gpurun_out/b_$c.err; echo $c=$?
+python -c "import json; d=json.load(open('gpurun_out/b_$c.json')); print('$c', round(d['value'],1), d['kernel_times_us'], round(d['roofline']['frac'],3)); [print('   ', l) for l in d['launch_timeline']]"; done

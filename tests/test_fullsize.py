@@ -104,7 +104,7 @@ def test_c4_swin_block_b64_full_size(vtc, oracle):
     p = vtc.Plan(g, vtc.MAX_ELIMINATION)
     kinds = _kernels(p)
     assert p.info()["data_movement_launches"] == 0
-    assert "gemm_tc_bf16_gather" in kinds and kinds.count("gemm_tc_bf16") + kinds.count("gemm_tc_bf16_gather") >= 4, kinds
+    assert kinds.count("gemm_skinny_bf16") == 4, kinds  # QKV (row gathers), proj, fc1 + GELU, fc2 + residual
     assert any(k.startswith("attn_prefill") for k in kinds), kinds
     got = vtc.execute(g, p, x)["y"]
     doc1 = W.swin_block(B=1, H=H)

@@ -345,8 +345,9 @@ def test_llama_prefill_layer_small(vtc, oracle, cfg):
     want = oracle.execute(doc, x)["y"]
     got, p = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
     kinds = [l["kernel"] for l in p.info()["launches"]]
-    assert "attn_fmha_tc" in kinds and kinds.count("gemm_tc_bf16") == 4, kinds  # gate + up in one launch
-    assert any(l["node"] == "gate_proj+up_proj" for l in p.info()["launches"])
+    # gate + up + SiLU * Mul in one launch (SwiGLU epilogue)
+    assert "attn_fmha_tc" in kinds and kinds.count("gemm_tc_bf16") == 4, kinds
+    assert any(l["node"] == "gate_proj+up_proj+silu+gate_mul" for l in p.info()["launches"])
     assert p.info()["data_movement_launches"] == 0
     assert _relerr(oracle.bf16_to_f32(got["y"]), oracle.bf16_to_f32(want)) < 2e-2
 
@@ -525,6 +526,7 @@ def test_tc_gate_up_fused_launch_bit_identical(vtc, oracle, monkeypatch):
     doc = W.llama_decode_layer(**cfg)
     x = _llama_inputs(oracle, W, doc, cfg["B"], cfg["pos"], cfg["D"], cfg["F"], cfg["hd"])
     g = vtc.parse_graph(doc)
+    monkeypatch.setenv("VTC_NO_TC_EPI", "1")  # the SwiGLU epilogue would absorb the pair
     p = vtc.Plan(g, vtc.MAX_ELIMINATION)
     assert any(l["node"] == "gate_proj+up_proj" for l in p.info(dry=True)["launches"])
     fused = vtc.execute(g, p, x)["y"]
@@ -532,3 +534,72 @@ def test_tc_gate_up_fused_launch_bit_identical(vtc, oracle, monkeypatch):
     p2 = vtc.Plan(g, vtc.MAX_ELIMINATION)
     assert not any(l["node"] == "gate_proj+up_proj" for l in p2.info(dry=True)["launches"])
     assert np.array_equal(fused, vtc.execute(g, p2, x)["y"])
+
+
+@pytest.mark.parametrize("which", ["decode64", "prefill", "swin"])
+def test_tc_fused_epilogues_bit_identical(vtc, oracle, monkeypatch, which):
+    """tcgen05 GEMM epilogues -- SwiGLU (gate / up tiles in one accumulator, only
+    SiLU(gate) * up stored), GELU, and the residual Add behind a virtual Reshape --
+    give the same bits as the unfused launches (same K splits, every intermediate
+    rounded to bf16 as the separate operators round it)."""
+    from paper_2604_09558_b200 import workloads as W
+    if which == "swin":
+        cfg = dict(B=1, H=28, C=96, heads=3, mlp=384)
+        doc = W.swin_block(**cfg)
+        x = oracle.random_inputs(doc, seed=3, scales=W.swin_weight_scales(cfg["C"], cfg["mlp"]))
+        x["attn_bias"] = oracle.f32_to_bf16(W.swin_attn_bias(H=cfg["H"], heads=cfg["heads"]))
+        want_nodes = {"fc1+gelu", "fc2+res2"}
+    elif which == "decode64":
+        cfg = dict(B=64, L=256, pos=200, D=1024, Hq=8, Hkv=2, hd=128, F=2048)
+        doc = W.llama_decode_layer(**cfg)
+        x = _llama_inputs(oracle, W, doc, cfg["B"], cfg["pos"], cfg["D"], cfg["F"], cfg["hd"])
+        want_nodes = {"gate_proj+up_proj+silu+gate_mul"}
+    else:
+        cfg = dict(B=2, S=128, D=256, Hq=4, Hkv=2, hd=128, F=512)
+        doc = W.llama_prefill_layer(**cfg)
+        x = oracle.random_inputs(doc, seed=4, scales=W.llama_weight_scales(cfg["D"], cfg["F"]))
+        cos, sin = W.rope_tables_prefill(cfg["B"], cfg["S"], hd=cfg["hd"])
+        x["cos"] = oracle.f32_to_bf16(cos.astype(np.float32))
+        x["sin"] = oracle.f32_to_bf16(sin.astype(np.float32))
+        want_nodes = {"gate_proj+up_proj+silu+gate_mul", "qkv_proj|rk_mc+rk_ms+rk_add|rq_mc+rq_ms+rq_add"}
+    g = vtc.parse_graph(doc)
+    monkeypatch.setenv("VTC_TC_TREES", "1")  # the opt-in RoPE-tree epilogue too
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    nodes = {l["node"] for l in p.info(dry=True)["launches"]}
+    assert want_nodes <= nodes, nodes
+    fused = vtc.execute(g, p, x)["y"]
+    monkeypatch.setenv("VTC_NO_TC_EPI", "1")
+    monkeypatch.setenv("VTC_NO_TC_HFUSE", "1")
+    monkeypatch.delenv("VTC_TC_TREES")
+    p2 = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert not want_nodes & {l["node"] for l in p2.info(dry=True)["launches"]}
+    unfused = vtc.execute(g, p2, x)["y"]
+    assert np.array_equal(fused, unfused), _relerr(oracle.bf16_to_f32(fused), oracle.bf16_to_f32(unfused))
+
+
+@pytest.mark.parametrize("which", ["swin", "c3k2"])
+def test_skinny_gemm_bit_identical_to_tile_gemm(vtc, oracle, monkeypatch, which):
+    """The persistent shallow-K GEMM (weights resident in shared memory, A by TMA
+    or host-resolved row gathers, GELU / residual epilogues, TMEM double buffer)
+    gives the same bits as the one-tile-per-CTA tcgen05 GEMM it replaces."""
+    from paper_2604_09558_b200 import workloads as W
+    if which == "swin":  # M = 4 * 56 * 56 = 12,544 window tokens: QKV gather, proj, fc1 + GELU, fc2 + residual
+        cfg = dict(B=4, H=56)
+        doc = W.swin_block(**cfg)
+        x = oracle.random_inputs(doc, seed=7, scales=W.swin_weight_scales())
+        x["attn_bias"] = oracle.f32_to_bf16(W.swin_attn_bias())
+        out, want_n = "y", 4
+    else:  # YOLO C3K2 at 64 x 64: shallow-K 1x1 convolutions, N = 64 / 128
+        doc = W.c3k2_block(N=4 * 64 * 64)
+        x = oracle.random_inputs(doc, seed=5, scales={"w_cv1": 0.09, "w_m1": 0.125, "w_m2": 0.125, "w_cv2": 0.07})
+        out, want_n = "out", 3
+    g = vtc.parse_graph(doc)
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    kinds = [l["kernel"] for l in p.info(dry=True)["launches"]]
+    assert kinds.count("gemm_skinny_bf16") == want_n, kinds
+    got = vtc.execute(g, p, x)[out]
+    monkeypatch.setenv("VTC_NO_SKINNY", "1")
+    p2 = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert "gemm_skinny_bf16" not in [l["kernel"] for l in p2.info(dry=True)["launches"]]
+    ref = vtc.execute(g, p2, x)[out]
+    assert np.array_equal(got, ref), _relerr(oracle.bf16_to_f32(got), oracle.bf16_to_f32(ref))

@@ -178,6 +178,14 @@ int vtc_comm_unique_id(void* out, int32_t bytes);
 int vtc_comm_init(const void* unique_id, int32_t bytes, int32_t nranks, int32_t rank, vtc_comm** out);
 void vtc_comm_free(vtc_comm* c);
 int vtc_plan_set_comm(vtc_plan* p, vtc_comm* c);
+/* Host-bridged communicator: every AllReduce of the plan copies its buffer to
+ * pinned host memory, calls fn(user, buf, count, dtype) from a stream host node
+ * (dtype: 0 f64, 1 f32, 2 i64, 3 bf16; fn sums buf over the ranks in place with
+ * the caller's own collective -- MPI, gloo, ... -- and returns 0), and copies it
+ * back.  For ranks that share a GPU (multi-process tests) or have no NCCL; fn
+ * must not call CUDA.  Same role as vtc_comm_init (SURVEY.md §8 e). */
+typedef int (*vtc_allreduce_fn)(void* user, void* buf, int64_t count, int32_t dtype);
+int vtc_comm_init_host(vtc_allreduce_fn fn, void* user, int32_t nranks, int32_t rank, vtc_comm** out);
 
 /* Low-level kernel entry: dst[map_dst(I)] = src[map_src(I)] over dst->shape. */
 int vtc_launch_gather_copy(const vtc_map* dst, const vtc_map* src, int32_t elem_bytes, void* stream);

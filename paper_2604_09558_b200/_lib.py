@@ -45,6 +45,7 @@ SIGNATURES = {
     "vtc_plan_map_analyze": (C.c_int, [_VP, C.c_char_p, C.c_int64, C.c_int64, C.POINTER(C.c_char_p)]),
     "vtc_comm_unique_id": (C.c_int, [_VP, C.c_int32]),
     "vtc_comm_init": (C.c_int, [_VP, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_VP)]),
+    "vtc_comm_init_host": (C.c_int, [_VP, _VP, C.c_int32, C.c_int32, C.POINTER(_VP)]),
     "vtc_comm_free": (None, [_VP]),
     "vtc_plan_set_comm": (C.c_int, [_VP, _VP]),
     "vtc_launch_gather_copy": (C.c_int, [_VP, _VP, C.c_int32, _VP]),

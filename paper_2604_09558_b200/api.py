@@ -138,6 +138,20 @@ def parse_graph(text) -> CompGraph:
     return CompGraph(h, text)
 
 
+_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32)
+
+
+def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even float32 -> bf16 bit patterns (uint16)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    r = ((u >> 16) & 1) + 0x7FFF
+    out = ((u + r) >> 16).astype(np.uint16)
+    nan = np.isnan(x)
+    if nan.any():
+        out[nan] = 0x7FC0
+    return out
+
+
 class Comm:
     """NCCL communicator for tensor-parallel plans (include/vtc.h vtc_comm_*):
     rank 0 calls Comm.unique_id(), the id is shared over any host channel, every
@@ -156,6 +170,38 @@ class Comm:
         _check(_lib.load().vtc_comm_init(C.cast(buf, C.c_void_p), 128, nranks, rank, C.byref(h)))
         self._h = h
         self.nranks, self.rank = nranks, rank
+
+    @classmethod
+    def host_bridged(cls, allreduce, nranks: int, rank: int) -> "Comm":
+        """A communicator whose AllReduce nodes stage through pinned host memory and
+        call allreduce(values) -> summed values (a numpy array of the buffer's dtype,
+        float32 for bf16 buffers, which are rounded back once) from a CUDA stream host
+        node (include/vtc.h vtc_comm_init_host), e.g. torch.distributed over gloo."""
+        self = cls.__new__(cls)
+        dtypes = {0: np.float64, 1: np.float32, 2: np.int64, 3: np.uint16}
+
+        def cb(_user, buf, count, dtype):
+            try:
+                n = int(count)
+                raw = np.ctypeslib.as_array((C.c_byte * (n * np.dtype(dtypes[dtype]).itemsize)).from_address(buf))
+                arr = raw.view(dtypes[dtype])
+                if dtype == 3:
+                    f32 = (arr.astype(np.uint32) << 16).view(np.float32)
+                    arr[:] = f32_to_bf16_bits(np.asarray(allreduce(f32), dtype=np.float32))
+                else:
+                    arr[:] = np.asarray(allreduce(arr.copy()), dtype=arr.dtype)
+                return 0
+            except Exception:  # surfaced as a wrong result by the caller's checks
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._cb = _ALLREDUCE_FN(cb)  # keep alive as long as the communicator
+        h = C.c_void_p()
+        _check(_lib.load().vtc_comm_init_host(C.cast(self._cb, C.c_void_p), None, nranks, rank, C.byref(h)))
+        self._h = h
+        self.nranks, self.rank = nranks, rank
+        return self
 
     def __del__(self):
         if getattr(self, "_h", None):

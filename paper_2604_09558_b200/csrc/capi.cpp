@@ -401,6 +401,19 @@ int vtc_comm_init(const void* unique_id, int32_t bytes, int32_t nranks, int32_t 
     });
 }
 
+int vtc_comm_init_host(vtc_allreduce_fn fn, void* user, int32_t nranks, int32_t rank, vtc_comm** out) {
+    return guard([&] {
+        auto* c = new vtc_comm;
+        try {
+            c->c = std::make_unique<vtc::Comm>(reinterpret_cast<vtc::HostAllReduceFn>(fn), user, nranks, rank);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
 void vtc_comm_free(vtc_comm* c) { delete c; }
 
 int vtc_plan_set_comm(vtc_plan* p, vtc_comm* c) {

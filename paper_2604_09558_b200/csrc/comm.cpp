@@ -62,12 +62,40 @@ Comm::Comm(const void* id128, int nranks, int rank) : nranks_(nranks), rank_(ran
     nck(api().comm_init_rank(&comm_, nranks, id, rank), "ncclCommInitRank");
 }
 
-Comm::~Comm() {
-    if (comm_ && api().comm_destroy) api().comm_destroy(comm_);
+Comm::Comm(HostAllReduceFn fn, void* user, int nranks, int rank)
+    : nranks_(nranks), rank_(rank), host_fn_(fn), host_user_(user) {
+    if (!fn) throw ExecutionError("vtc_comm_init_host: null callback");
+    host_cap_ = size_t(16) << 20;
+    if (cudaHostAlloc(&staging_, host_cap_, cudaHostAllocDefault) != cudaSuccess)
+        throw CudaError("cudaHostAlloc(allreduce staging)");
 }
 
-void Comm::all_reduce_sum(const void* send, void* recv, size_t count, ncclDataType_t dt, cudaStream_t s) const {
-    nck(api().all_reduce(send, recv, count, dt, ncclSum, comm_, s), "ncclAllReduce");
+Comm::~Comm() {
+    if (comm_ && api().comm_destroy) api().comm_destroy(comm_);
+    if (staging_) cudaFreeHost(staging_);
+}
+
+void CUDART_CB Comm::host_node(void* arg) {
+    auto* c = static_cast<HostCall*>(arg);
+    c->status = c->fn(c->user, c->buf, c->count, c->dtype);
+}
+
+void Comm::all_reduce_sum(const void* send, void* recv, size_t count, ncclDataType_t dt, cudaStream_t s) {
+    if (!host_fn_) {
+        nck(api().all_reduce(send, recv, count, dt, ncclSum, comm_, s), "ncclAllReduce");
+        return;
+    }
+    const size_t es = dt == ncclBfloat16 ? 2 : dt == ncclFloat32 ? 4 : 8;
+    if (count * es > host_cap_) throw UnsupportedError("host-bridged AllReduce larger than the 16 MiB staging buffer");
+    // vtc dtype codes (include/vtc.h): 0 f64, 1 f32, 2 i64, 3 bf16
+    const int32_t code = dt == ncclBfloat16 ? 3 : dt == ncclFloat32 ? 1 : dt == ncclFloat64 ? 0 : 2;
+    calls_.push_back(HostCall{host_fn_, host_user_, staging_, int64_t(count), code, 0});
+    auto ck = [](cudaError_t e, const char* w) {
+        if (e != cudaSuccess) throw CudaError(std::string(w) + ": " + cudaGetErrorString(e));
+    };
+    ck(cudaMemcpyAsync(staging_, send, count * es, cudaMemcpyDeviceToHost, s), "allreduce D2H");
+    ck(cudaLaunchHostFunc(s, &Comm::host_node, &calls_.back()), "allreduce host node");
+    ck(cudaMemcpyAsync(recv, staging_, count * es, cudaMemcpyHostToDevice, s), "allreduce H2D");
 }
 
 }  // namespace vtc

@@ -1976,6 +1976,7 @@ void Executor::prepare(bool dry) {
                                 std::vector<int64_t> segs;
                                 sk = op.vec_ok && k_segments(op.m, K, segs) && segs.size() == 2;
                                 sk = sk && rows_of(am, K, abase, ald, at, "H2D(skinny a_rows)") && (impl_->dry || at != nullptr);
+                                sk = sk && q.slots >= q.kt + 3;  // the gather keeps 3 k-tiles in flight
                                 q.a_rows = at;
                             }
                         }
@@ -2298,6 +2299,43 @@ void Executor::prepare(bool dry) {
                     push(std::move(L));
                     break;
                 }
+                // short sequences (Swin windows): one warp per (batch, head) item
+                if (!p.fast && p.Sq <= 64 && p.Sk <= 64 && p.q.m.npieces == 1 && p.o.m.npieces == 1 &&
+                    !std::getenv("VTC_NO_ATTN_WINDOW")) {
+                    const int64_t qs_ = desc_tile_stride(p.q.m.piece[0], rank - 2, p.Sq);
+                    const int64_t os_ = desc_tile_stride(p.o.m.piece[0], rank - 2, p.Sq);
+                    const int64_t qd_ = desc_tile_stride(p.q.m.piece[0], rank - 1, p.D);
+                    const int64_t od_ = desc_tile_stride(p.o.m.piece[0], rank - 1, p.Dv);
+                    // 32-bit accesses of (d, d + 1) pairs: every element offset of an even d is even
+                    auto even = [](const vtc_map& m) {
+                        for (int pi = 0; pi < m.npieces; ++pi) {
+                            const vtc_piece& pc = m.piece[pi];
+                            if (pc.base % 2 || pc.ngroups || pc.ptr % 4) return false;
+                            for (int t = 0; t < pc.ndigits; ++t)
+                                if (pc.dig[t].coeff % 2 && pc.dig[t].axis != m.rank - 1) return false;
+                            if (pc.affine)
+                                for (int a = 0; a + 1 < m.rank; ++a)
+                                    if (pc.aff[a] % 2) return false;
+                        }
+                        return true;
+                    };
+                    p.qo_affine = qs_ != INT64_MIN && os_ != INT64_MIN && qd_ == 1 && od_ == 1 && even(p.q.m) && even(p.o.m);
+                    p.q_sstride = qs_;
+                    p.o_sstride = os_;
+                    if (p.has_bias && p.bias.m.npieces == 1) {
+                        p.b_sstride = desc_tile_stride(p.bias.m.piece[0], rank - 2, p.Sq);
+                        p.b_kstride = desc_tile_stride(p.bias.m.piece[0], rank - 1, p.Sk);
+                        p.bias_affine = p.b_sstride != INT64_MIN && p.b_kstride != INT64_MIN;
+                    }
+                    if (attn_window_supported(p)) {
+                        p.fast = 4;
+                        p.splits = 1;
+                        p.chunk = p.Sk;
+                        L->kernel = "attn_window_tc";
+                        push(std::move(L));
+                        break;
+                    }
+                }
                 // other long query blocks: flash attention on mma.sync, no K split
                 if (!p.fast && attn_prefill_supported(p)) {
                     p.fast = 2;
@@ -2380,6 +2418,24 @@ void Executor::prepare(bool dry) {
         }
         impl_->launches = std::move(merged);
         infos_ = std::move(minfos);
+    }
+    // decode attention -> streamed GEMV: the attention CTAs prefetch the GEMV's weights
+    // into L2 (HBM is idle while the split-KV attention is latency-bound; W_o is 32 MB
+    // at Llama-3-8B).  VTC_ATTN_L2PF=0: off
+    {
+        const char* ev = std::getenv("VTC_ATTN_L2PF");
+        const bool on = !(ev && ev[0] == '0');
+        using AL = LaunchT<AttnParams, launch_attention>;
+        using GL = LaunchT<GemvParams, launch_gemv_any>;
+        for (size_t i = 0; on && i + 1 < impl_->launches.size(); ++i) {
+            auto* a = dynamic_cast<AL*>(impl_->launches[i].get());
+            auto* b = dynamic_cast<GL*>(impl_->launches[i + 1].get());
+            if (!a || !b || a->p.fast != 1 || !b->p.stream || !b->p.b_static || b->p.b_sk != b->p.N) continue;
+            const int64_t bytes = b->p.K * b->p.N * 2;
+            if (bytes <= 0 || bytes > (int64_t(64) << 20) || reinterpret_cast<uintptr_t>(b->p.b_base) % 16) continue;
+            a->p.pf_base = reinterpret_cast<uint64_t>(b->p.b_base);
+            a->p.pf_bytes = bytes;
+        }
     }
     // chain consecutive streamed GEMVs (o_proj -> gate/up -> down) into one
     // persistent launch with per-strip dependencies.  Opt-in (VTC_CHAIN=1):

@@ -281,6 +281,10 @@ void launch_t(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
         launch_attn_fmha(p, dp, s);
         return;
     }
+    if (p.fast == 4) {
+        launch_attn_window(p, dp, s);
+        return;
+    }
     if (p.fast) {
         launch_attn_decode(p, dp, s);
     } else {

@@ -217,6 +217,17 @@ __global__ void __launch_bounds__(NT, 2) attn_decode_kernel(const AttnParams* __
         if (s < my_tiles) load_tile(s, s);
         cp_async_commit();
     }
+    // this CTA's share of the next projection's weights into L2, queued behind its own K / V loads
+    if (p.pf_bytes > 0 && tid == 0) {
+        const uint64_t nct = uint64_t(gridDim.x) * gridDim.y, cta = uint64_t(blockIdx.y) * gridDim.x + blockIdx.x;
+        const uint64_t per = ((uint64_t(p.pf_bytes) + nct - 1) / nct + 15) & ~uint64_t(15);
+        const uint64_t lo = cta * per, hi = min(lo + per, uint64_t(p.pf_bytes));
+        for (uint64_t o = lo; o < hi; o += 32768) {
+            const uint64_t left = hi - o;
+            const uint32_t sz = uint32_t(left < 32768 ? left : 32768) & ~15u;
+            if (sz) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf_base + o), "r"(sz) : "memory");
+        }
+    }
 
     {
 #pragma unroll

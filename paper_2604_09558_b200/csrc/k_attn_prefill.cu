@@ -306,6 +306,174 @@ __global__ void __launch_bounds__(NT, D <= 32 ? 4 : 2) attn_prefill_kernel(const
     }  // items
 }
 
+// Short sequences (Swin windows: 49 queries x 49 keys, head dim 32): one WARP
+// per (batch, head) item, all keys in one 64-key tile, so the softmax is a
+// single pass; persistent warps, no CTA-wide synchronisation.  Q / K / V / O /
+// bias rows are base + position * stride inside an item (host-proved), the
+// bases located through the maps once per item.
+template <int D>
+constexpr int window_warps() { return D <= 32 ? 16 : 8; }  // K / V tiles of every warp: 128 KB
+template <int D>
+__global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(const AttnParams* __restrict__ pp) {
+    constexpr int WW = window_warps<D>();
+    constexpr int ROWB = D * 2, TILEB = TK * ROWB;
+    VTC_STAGE_PARAMS(AttnParams, pp);
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t kt = smem_u32(smem) + uint32_t(warp) * 2 * TILEB, vt = kt + TILEB;
+    const int r = p.rank, ax_h = r - 3, ax_s = r - 2, ax_d = r - 1;
+    const int Sq = p.Sq, Sk = p.Sk;
+    const uint32_t nitems = uint32_t(p.Bt) * uint32_t(p.H);
+    const float qscale = p.scale * LOG2E;
+    dev::pdl_wait();
+    dev::pdl_launch_dependents();
+    for (uint32_t item = blockIdx.x * WW + warp; item < nitems; item += gridDim.x * WW) {
+        uint32_t bh = item;
+        const uint32_t bq = bh / uint32_t(p.H);
+        const int h = int(bh - bq * uint32_t(p.H));
+        bh = bq;
+        int32_t idx[VTC_MAX_RANK] = {};
+        for (int a = r - 4; a >= 0; --a) {
+            const uint32_t ext = uint32_t(p.q.m.shape[a]), nb = bh / ext;
+            idx[a] = int32_t(bh - nb * ext);
+            bh = nb;
+        }
+        idx[ax_h] = h;
+        idx[ax_s] = 0;
+        idx[ax_d] = 0;
+        // item bases (lanes 0..4 locate one map each)
+        uint64_t mine = 0;
+        if (lane == 0) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.q.m, idx));
+        else if (lane == 1) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.k.m, idx));
+        else if (lane == 2) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.v.m, idx));
+        else if (lane == 3) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.o.m, idx));
+        else if (lane == 4 && p.has_bias) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.bias.m, idx));
+        const bf16* qb = reinterpret_cast<const bf16*>(__shfl_sync(0xffffffffu, mine, 0));
+        const bf16* kb = reinterpret_cast<const bf16*>(__shfl_sync(0xffffffffu, mine, 1));
+        const bf16* vb = reinterpret_cast<const bf16*>(__shfl_sync(0xffffffffu, mine, 2));
+        bf16* ob = reinterpret_cast<bf16*>(__shfl_sync(0xffffffffu, mine, 3));
+        const bf16* bb = reinterpret_cast<const bf16*>(__shfl_sync(0xffffffffu, mine, 4));
+        // K / V of the item -> this warp's tiles (zero past Sk)
+        constexpr int CPR = D / 8;
+#pragma unroll
+        for (int i = 0; i < (TK * CPR) / 32; ++i) {
+            const int c = lane + 32 * i, row = c / CPR, ch = c % CPR;
+            const bool ok = row < Sk;
+            const int rr = ok ? row : 0;
+            cp_async16(kt + swz<D>(row, ch), kb + int64_t(rr) * p.k_sstride + ch * 8, ok);
+            cp_async16(vt + swz<D>(row, ch), vb + int64_t(rr) * p.v_sstride + ch * 8, ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const int kc = (lane % 4) * 2;
+        for (int q0 = 0; q0 < Sq; q0 += 16) {
+            const int rA = q0 + lane / 4, rB = rA + 8;
+            // Q fragments of rows rA / rB (32-bit loads: the rows are contiguous along d)
+            uint32_t qa[D / 16][4];
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const int d0 = ks * 16 + kc;
+                qa[ks][0] = rA < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rA) * p.q_sstride + d0) : 0u;
+                qa[ks][1] = rB < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rB) * p.q_sstride + d0) : 0u;
+                qa[ks][2] = rA < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rA) * p.q_sstride + d0 + 8) : 0u;
+                qa[ks][3] = rB < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rB) * p.q_sstride + d0 + 8) : 0u;
+            }
+            // additive bias of this thread's scores, requested before the MMAs
+            float bA[TK / 8][2], bB[TK / 8][2];
+#pragma unroll
+            for (int nt = 0; nt < TK / 8; ++nt)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int t = nt * 8 + kc + c;
+                    bA[nt][c] = (p.has_bias && t < Sk && rA < Sq)
+                                    ? __bfloat162float(bb[int64_t(rA) * p.b_sstride + int64_t(t) * p.b_kstride]) : 0.f;
+                    bB[nt][c] = (p.has_bias && t < Sk && rB < Sq)
+                                    ? __bfloat162float(bb[int64_t(rB) * p.b_sstride + int64_t(t) * p.b_kstride]) : 0.f;
+                }
+            if (q0 == 0) {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+                __syncwarp();
+            }
+            float sc[TK / 8][4];
+#pragma unroll
+            for (int nt = 0; nt < TK / 8; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+            for (int kp = 0; kp < D / 32; ++kp) {
+#pragma unroll
+                for (int nt = 0; nt < TK / 8; ++nt) {
+                    const int mi = lane / 8, rr = lane % 8;
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(kt + swz<D>(nt * 8 + rr, kp * 4 + mi), b0, b1, b2, b3);
+                    mma_bf16(sc[nt], qa[2 * kp], b0, b1);
+                    mma_bf16(sc[nt], qa[2 * kp + 1], b2, b3);
+                }
+            }
+            const int limA = p.causal ? rA + (Sk - Sq) : INT32_MAX;
+            const int limB = p.causal ? rB + (Sk - Sq) : INT32_MAX;
+            float mA = -INFINITY, mB = -INFINITY;
+#pragma unroll
+            for (int nt = 0; nt < TK / 8; ++nt)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int t = nt * 8 + kc + c;
+                    float a = sc[nt][c] * qscale + bA[nt][c] * LOG2E, b = sc[nt][2 + c] * qscale + bB[nt][c] * LOG2E;
+                    if (t >= Sk || t > limA) a = -INFINITY;
+                    if (t >= Sk || t > limB) b = -INFINITY;
+                    sc[nt][c] = a;
+                    sc[nt][2 + c] = b;
+                    mA = fmaxf(mA, a);
+                    mB = fmaxf(mB, b);
+                }
+#pragma unroll
+            for (int off = 1; off < 4; off <<= 1) {
+                mA = fmaxf(mA, __shfl_xor_sync(0xffffffffu, mA, off));
+                mB = fmaxf(mB, __shfl_xor_sync(0xffffffffu, mB, off));
+            }
+            float lA = 0.f, lB = 0.f;
+            uint32_t pa[TK / 16][4];
+#pragma unroll
+            for (int nt = 0; nt < TK / 8; ++nt) {
+                float e[4];
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    e[c] = sc[nt][c] == -INFINITY ? 0.f : exp2f(sc[nt][c] - mA);
+                    e[2 + c] = sc[nt][2 + c] == -INFINITY ? 0.f : exp2f(sc[nt][2 + c] - mB);
+                    lA += e[c];
+                    lB += e[2 + c];
+                }
+                const int ks = nt / 2, hi = nt % 2;
+                pa[ks][hi * 2 + 0] = pack_bf16(e[0], e[1]);
+                pa[ks][hi * 2 + 1] = pack_bf16(e[2], e[3]);
+            }
+            float o[D / 8][4];
+#pragma unroll
+            for (int i = 0; i < D / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < TK / 16; ++ks)
+#pragma unroll
+                for (int np = 0; np < D / 16; ++np) {
+                    const int mi = lane / 8, rr = lane % 8;
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4_t(vt + swz<D>(ks * 16 + (mi & 1) * 8 + rr, np * 2 + (mi >> 1)), b0, b1, b2, b3);
+                    mma_bf16(o[2 * np], pa[ks], b0, b1);
+                    mma_bf16(o[2 * np + 1], pa[ks], b2, b3);
+                }
+#pragma unroll
+            for (int off = 1; off < 4; off <<= 1) {
+                lA += __shfl_xor_sync(0xffffffffu, lA, off);
+                lB += __shfl_xor_sync(0xffffffffu, lB, off);
+            }
+            const float iA = lA > 0.f ? 1.f / lA : 0.f, iB = lB > 0.f ? 1.f / lB : 0.f;
+#pragma unroll
+            for (int i = 0; i < D / 8; ++i) {
+                const int d = i * 8 + kc;
+                if (rA < Sq) *reinterpret_cast<uint32_t*>(ob + int64_t(rA) * p.o_sstride + d) = pack_bf16(o[i][0] * iA, o[i][1] * iA);
+                if (rB < Sq) *reinterpret_cast<uint32_t*>(ob + int64_t(rB) * p.o_sstride + d) = pack_bf16(o[i][2] * iB, o[i][3] * iB);
+            }
+        }
+        __syncwarp();  // this warp's K / V tiles are refilled by its next item
+    }
+}
+
 }  // namespace
 
 bool attn_prefill_supported(const AttnParams& p) {
@@ -324,6 +492,28 @@ void launch_d(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_prefill_kernel<D>, NT, smem);
     const int64_t cap = int64_t(sms) * (per_sm > 0 ? per_sm : 1);
     launch_k(attn_prefill_kernel<D>, dim3(unsigned(items < cap ? items : cap)), dim3(NT), smem, s, dp);
+}
+
+bool attn_window_supported(const AttnParams& p) {
+    return p.dt == KDType::BF16 && p.D == p.Dv && (p.D == 32 || p.D == 64) && p.Sq <= TK && p.Sk <= TK && p.kv_affine &&
+           p.qo_affine && p.k.vec_ok && p.v.vec_ok && (!p.has_bias || p.bias_affine);
+}
+
+template <int D>
+void launch_w(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
+    constexpr int WW = window_warps<D>();
+    const size_t smem = size_t(WW) * 2 * TK * D * 2;
+    allow_max_smem(attn_window_kernel<D>);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t items = int64_t(p.Bt) * p.H, need = (items + WW - 1) / WW;
+    launch_k(attn_window_kernel<D>, dim3(unsigned(need < sms ? need : sms)), dim3(WW * 32), smem, s, dp);
+}
+
+void launch_attn_window(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
+    if (p.D == 32) launch_w<32>(p, dp, s);
+    else launch_w<64>(p, dp, s);
 }
 
 void launch_attn_prefill(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {

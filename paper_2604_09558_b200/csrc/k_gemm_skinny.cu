@@ -31,7 +31,8 @@ namespace vtc {
 namespace {
 
 using dev::bf16;
-constexpr int BM = 128, BK = 64, UK = 16, NEPI = 8, NTHREADS = (2 + NEPI) * 32;
+constexpr int BM = 128, BK = 64, UK = 16, NEPI = 16, NTHREADS = (2 + NEPI) * 32;
+constexpr int GATHER_LAG = 3;  // gathered k-tiles in flight before the oldest is published
 constexpr uint32_t SLOT_BYTES = BM * BK * 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_c
     const int cpitch = NC + 8;                                  // elements per staged row
     __shared__ uint64_t a_full[16], a_empty[16], acc_full[2], acc_empty[2];
     __shared__ uint32_t s_tmem;
+    __shared__ uint64_t s_arow[BM];  // gather: row addresses of the producer's current tile
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t mtiles = (p.M + BM - 1) / BM;
@@ -121,12 +123,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_c
             const int k = int(i / ngrp), g = int(i % ngrp);
             uint4 v = make_uint4(0, 0, 0, 0);
             if (k < p.K) v = __ldg(reinterpret_cast<const uint4*>(static_cast<const bf16*>(p.w) + int64_t(k) * p.ldw + g * 8));
-            const bf16* e = reinterpret_cast<const bf16*>(&v);
-            unsigned char* tile = sB + size_t(k / BK) * NP * 128;
+            const uint16_t* e = reinterpret_cast<const uint16_t*>(&v);
+            const uint32_t tile = smem_u32(sB + size_t(k / BK) * NP * 128);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int n = g * 8 + j;
-                if (n < NP) *reinterpret_cast<bf16*>(tile + sw128(n, k % BK)) = e[j];
+                if (n < NP) asm volatile("st.shared.u16 [%0], %1;" ::"r"(tile + sw128(n, k % BK)), "h"(e[j]) : "memory");
             }
         }
     }
@@ -159,39 +161,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_c
             }
         } else {
             // gathers: 128 rows x 8 chunks of 16 B per k-tile, one lane per chunk column;
-            // slot g - 1 is published once its copies have landed (one slot in flight)
-            int prev = -1;
+            // GATHER_LAG k-tiles stay in flight: slot g - LAG is published once its copies landed
+            int oldest = 0;  // oldest k-tile not yet published
             for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
                 const int64_t m0 = mt * BM;
+                // the tile's 128 row addresses: one coalesced round trip, then from shared memory
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < BM / 32; ++q) {
+                    const int64_t m = m0 + q * 32 + lane;
+                    s_arow[q * 32 + lane] = m < p.M ? p.a_rows[m] : 0;
+                }
+                __syncwarp();
                 for (int kt = 0; kt < KT; ++kt, ++g) {
                     const int s = g % S;
                     mbar_wait(&a_empty[s], ((g / S) & 1) ^ 1u);
                     const uint32_t base = smem_u32(sA + size_t(s) * SLOT_BYTES);
-#pragma unroll 4
+#pragma unroll 8
                     for (int j = 0; j < (BM * 8) / 32; ++j) {
                         const int c = lane + 32 * j, row = c >> 3, ch = c & 7;
                         const int64_t m = m0 + row, k = int64_t(kt) * BK + ch * 8;
                         const bool ok = m < p.M && k < p.K;
-                        const void* src = ok ? reinterpret_cast<const void*>(p.a_rows[m] + uint64_t(k) * 2)
-                                             : p.w;
+                        const void* src = ok ? reinterpret_cast<const void*>(s_arow[row] + uint64_t(k) * 2) : p.w;
                         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(base + sw128(row, ch * 8)),
                                      "l"(src), "r"(ok ? 16 : 0)
                                      : "memory");
                     }
                     asm volatile("cp.async.commit_group;" ::: "memory");
-                    if (prev >= 0) {
-                        asm volatile("cp.async.wait_group 1;" ::: "memory");
+                    if (g - oldest + 1 > GATHER_LAG) {
+                        asm volatile("cp.async.wait_group %0;" ::"n"(GATHER_LAG) : "memory");
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        mbar_arrive(&a_full[prev]);
+                        mbar_arrive(&a_full[oldest % S]);
+                        ++oldest;
                     }
-                    prev = s;
                 }
             }
-            if (prev >= 0) {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive(&a_full[prev]);
-            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            for (; oldest < g; ++oldest) mbar_arrive(&a_full[oldest % S]);
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
@@ -237,12 +244,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_c
     } else {
         // ---------------- epilogue: warps 2..9 ----------------
         dev::pdl_wait();
-        const int et = threadIdx.x - 64;        // 0..255
+        const int et = threadIdx.x - 64;        // 0 .. NEPI * 32 - 1
         const int quad = warp & 3;              // TMEM lanes 32*quad .. +31 (hardware rule: warp id mod 4)
-        const int half = (warp - 2) >> 2;       // two warps per quadrant: column halves
+        const int part = (warp - 2) >> 2;       // NEPI / 4 warps per quadrant: column parts
         const int row = quad * 32 + lane;
-        const int hc = (NC / 2 + 7) / 8 * 8;    // columns per half, multiple of 8
-        const int c_lo = half * hc, c_hi = min(NC, c_lo + hc);
+        constexpr int PARTS = NEPI / 4;
+        const int hc = (NC / PARTS + 7) / 8 * 8;  // columns per part, multiple of 8
+        const int c_lo = part * hc, c_hi = min(NC, c_lo + hc);
         bf16* srow = reinterpret_cast<bf16*>(sC) + size_t(row) * cpitch;
         const int cpr = NC / 8;                  // 16-byte chunks per output row
         int u = 0;
@@ -273,25 +281,41 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_c
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[b]);
                 bar_epi();  // the unit is staged
-                // coalesced copy-out: consecutive threads take consecutive 16-byte chunks of a row
+                // coalesced copy-out: consecutive threads take consecutive 16-byte chunks of a row;
+                // a thread's chunks (and their residual chunks) are loaded before any is stored
                 const int64_t n0 = int64_t(j) * NC;
-                for (int i = et; i < BM * cpr; i += NEPI * 32) {
-                    const int rr = i / cpr, cc = i % cpr;
-                    const int64_t m = m0 + rr;
-                    if (m >= p.M) break;
-                    uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(sC) + size_t(rr) * cpitch + cc * 8);
-                    const int64_t col = n0 + cc * 8;
-                    if (p.has_res) {
-                        const bf16* rp = p.r_rows ? reinterpret_cast<const bf16*>(p.r_rows[m])
-                                                  : reinterpret_cast<const bf16*>(p.r_base) + m * p.r_ld;
-                        const uint4 rv = __ldg(reinterpret_cast<const uint4*>(rp + col));
-                        const bf16* a = reinterpret_cast<const bf16*>(&rv);
-                        bf16* x = reinterpret_cast<bf16*>(&v);
+                constexpr int CH = 4;  // chunks per thread per round
+                for (int i0 = et; i0 < BM * cpr; i0 += CH * NEPI * 32) {
+                    uint4 v[CH], rv[CH];
+                    int64_t mm[CH];
+                    int cc[CH];
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) x[q] = dev::add_bf16(a[q], x[q]);
+                    for (int q = 0; q < CH; ++q) {
+                        const int i = i0 + q * NEPI * 32;
+                        const int rr = i / cpr;
+                        cc[q] = i - rr * cpr;
+                        mm[q] = (i < BM * cpr) ? m0 + rr : p.M;
+                        if (mm[q] < p.M) {
+                            v[q] = *reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(sC) + size_t(rr) * cpitch + cc[q] * 8);
+                            if (p.has_res) {
+                                const bf16* rp = p.r_rows ? reinterpret_cast<const bf16*>(p.r_rows[mm[q]])
+                                                          : reinterpret_cast<const bf16*>(p.r_base) + mm[q] * p.r_ld;
+                                rv[q] = __ldg(reinterpret_cast<const uint4*>(rp + n0 + cc[q] * 8));
+                            }
+                        }
                     }
-                    bf16* cp = p.c_rows ? reinterpret_cast<bf16*>(p.c_rows[m]) : reinterpret_cast<bf16*>(p.c_base) + m * p.c_ld;
-                    *reinterpret_cast<uint4*>(cp + col) = v;
+#pragma unroll
+                    for (int q = 0; q < CH; ++q) {
+                        if (mm[q] >= p.M) continue;
+                        if (p.has_res) {
+                            const bf16* a = reinterpret_cast<const bf16*>(&rv[q]);
+                            bf16* x = reinterpret_cast<bf16*>(&v[q]);
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) x[e] = dev::add_bf16(a[e], x[e]);
+                        }
+                        bf16* cp = p.c_rows ? reinterpret_cast<bf16*>(p.c_rows[mm[q]]) : reinterpret_cast<bf16*>(p.c_base) + mm[q] * p.c_ld;
+                        *reinterpret_cast<uint4*>(cp + n0 + cc[q] * 8) = v[q];
+                    }
                 }
                 bar_epi();  // staging free for the next unit
             }

@@ -382,6 +382,14 @@ struct AttnParams {
     alignas(64) unsigned char fmha[3 * 128];
     uint64_t fmha_o;
     int64_t fmha_os[3];
+    // short-sequence window attention (fast == 4): Q / O rows and the bias are
+    // base + position * stride within a (batch, head) item (host-proved)
+    int32_t qo_affine, bias_affine;
+    int64_t q_sstride, o_sstride, b_sstride, b_kstride;
+    // decode: L2 prefetch of the next launch's weights while the (latency-bound)
+    // attention leaves HBM idle -- [pf_base, pf_base + pf_bytes), split over the CTAs
+    uint64_t pf_base;
+    int64_t pf_bytes;
 };
 void launch_attention(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 // tcgen05 / TMEM flash attention for head dim 128 (prefill): proves the Q / K / V / O
@@ -394,5 +402,7 @@ int64_t attn_decode_capacity();
 bool attn_prefill_supported(const AttnParams& p);
 void launch_attn_prefill(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 void launch_attn_decode(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
+bool attn_window_supported(const AttnParams& p);
+void launch_attn_window(const AttnParams& p, const AttnParams* dp, cudaStream_t s);
 
 }  // namespace vtc

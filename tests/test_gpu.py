@@ -603,3 +603,25 @@ def test_skinny_gemm_bit_identical_to_tile_gemm(vtc, oracle, monkeypatch, which)
     assert "gemm_skinny_bf16" not in [l["kernel"] for l in p2.info(dry=True)["launches"]]
     ref = vtc.execute(g, p2, x)[out]
     assert np.array_equal(got, ref), _relerr(oracle.bf16_to_f32(got), oracle.bf16_to_f32(ref))
+
+
+def test_swin_window_attention_matches_flash_kernel(vtc, oracle, monkeypatch):
+    """Swin window attention (relative-position bias + shift mask through the
+    Expand map) on the warp-per-window kernel equals the flash kernel
+    (VTC_NO_ATTN_WINDOW=1) within the bf16 tolerance, and the oracle."""
+    from paper_2604_09558_b200 import workloads as W
+    cfg = dict(B=1, H=28, C=96, heads=3, mlp=384)
+    doc = W.swin_block(**cfg)
+    x = oracle.random_inputs(doc, seed=3, scales=W.swin_weight_scales(cfg["C"], cfg["mlp"]))
+    x["attn_bias"] = oracle.f32_to_bf16(W.swin_attn_bias(H=cfg["H"], heads=cfg["heads"]))
+    g = vtc.parse_graph(doc)
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert "attn_window_tc" in [l["kernel"] for l in p.info(dry=True)["launches"]]
+    a = oracle.bf16_to_f32(vtc.execute(g, p, x)["y"])
+    monkeypatch.setenv("VTC_NO_ATTN_WINDOW", "1")
+    p2 = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert "attn_prefill_tc" in [l["kernel"] for l in p2.info(dry=True)["launches"]]
+    b = oracle.bf16_to_f32(vtc.execute(g, p2, x)["y"])
+    want = oracle.bf16_to_f32(oracle.execute(doc, x)["y"])
+    assert _relerr(a, b) < 1e-2
+    assert _relerr(a, want) < 2e-2

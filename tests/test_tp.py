@@ -95,3 +95,82 @@ def test_sharded_plans_have_two_collectives_and_no_dm_kernels(vtc, world):
     # the per-rank KV cache is 1/world of the full cache
     kc = [t for t in doc["tensors"] if t["id"] == "k_cache"][0]
     assert kc["shape"] == [8192, 64, 8 // world, 128]
+
+
+def _rank_product(rank, world, port, outdir):
+    """One rank of the head-sharded layer on the PRODUCT path (libvtc.so kernels on
+    cuda:0, both ranks sharing the GPU): the plan's two AllReduce nodes go through a
+    host-bridged communicator whose callback sums over the gloo group."""
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import paper_2604_09558_b200 as vtc
+    from paper_2604_09558_b200 import workloads as W
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    calls = []
+
+    def allreduce(v):
+        t = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        calls.append(int(t.numel()))
+        return t.numpy()
+
+    _, full = _full_inputs()
+    doc = W.llama_decode_layer(**CFG, tp=world)
+    mine = W.shard_llama_inputs(full, rank, world, Hq=CFG["Hq"], Hkv=CFG["Hkv"], hd=CFG["hd"], F=CFG["F"])
+    g = vtc.parse_graph(doc)
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    comm = vtc.Comm.host_bridged(allreduce, world, rank)
+    p.set_comm(comm)
+    y = vtc.execute(g, p, mine)["y"]
+    np.save(os.path.join(outdir, f"y{rank}.npy"), y)
+    np.save(os.path.join(outdir, f"calls{rank}.npy"), np.array(calls))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2])
+def test_head_sharded_product_plan_equals_unsharded(vtc, oracle, world):
+    """world-2 gloo group, each rank running its shard of the layer through the
+    product executor (sm_100a kernels) with the AllReduces bridged over gloo:
+    every rank ends with the same y, equal to the unsharded product plan within
+    the bf16 tolerance (the sharded sums round per rank, then once after the
+    fp32 allreduce -- NCCL's bf16 ring rounds at every hop instead)."""
+    import torch.multiprocessing as mp
+    doc, full = _full_inputs()
+    g = vtc.parse_graph(doc)
+    want = vtc.execute(g, vtc.Plan(g, vtc.MAX_ELIMINATION), full)["y"]
+    ref = oracle.bf16_to_f32(oracle.execute(doc, full)["y"]).astype(np.float64)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_rank_product, args=(world, _free_port(), d), nprocs=world, join=True)
+        ys = [np.load(os.path.join(d, f"y{r}.npy")) for r in range(world)]
+        calls = [np.load(os.path.join(d, f"calls{r}.npy")) for r in range(world)]
+    for r in range(world):
+        assert list(calls[r]) == [CFG["B"] * CFG["D"]] * 2  # exactly the two [B, D] exchanges
+    for r in range(1, world):
+        assert np.array_equal(ys[r], ys[0])
+    got = oracle.bf16_to_f32(ys[0]).astype(np.float64)
+    unsharded = oracle.bf16_to_f32(want).astype(np.float64)
+    assert np.max(np.abs(got - unsharded)) / np.max(np.abs(unsharded)) < 2e-2
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 2e-2
+
+
+def test_nccl_bf16_ring_rounding_within_tolerance_at_8_ranks(oracle):
+    """NCCL sums bf16 in a ring, rounding the running partial to bf16 at every hop
+    (N - 1 roundings at N ranks), where the oracle sums in fp32 and rounds once.
+    Simulate the ring at N = 8 on the [B, 4096] O-proj partials of a decode step:
+    the extra error stays far inside the 2e-2 bf16 tolerance."""
+    rng = np.random.default_rng(3)
+    parts = [oracle.bf16_to_f32(oracle.f32_to_bf16(rng.standard_normal((64, 4096)).astype(np.float32) * 0.05))
+             for _ in range(8)]
+    exact = np.sum(np.stack(parts).astype(np.float64), axis=0)
+    once = oracle.bf16_to_f32(oracle.f32_to_bf16(exact.astype(np.float32))).astype(np.float64)
+    acc = parts[0]
+    for p in parts[1:]:  # ring: bf16 partial + bf16 contribution, rounded each hop
+        acc = oracle.bf16_to_f32(oracle.f32_to_bf16((acc + p).astype(np.float32)))
+    ring = acc.astype(np.float64)
+    scale = np.max(np.abs(exact))
+    assert np.max(np.abs(once - exact)) / scale < 4e-3
+    assert np.max(np.abs(ring - exact)) / scale < 2e-2

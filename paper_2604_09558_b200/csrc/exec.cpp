@@ -1997,6 +1997,7 @@ void Executor::prepare(bool dry) {
                     } else {
                         if (gl != tc_gelu.end()) p.epi = GEMM_EPI_GELU;
                         // small M: 128-column tiles so the K split (and its reduction) stays shallow
+                        // (256-column tiles with deeper splits measured slower at C3: 675 vs 563 us)
                         p.bn = M <= 128 ? 128 : 256;
                         p.c = operand(mn(cout), 1, p.bn, es);
                         if (!p.c.fast_ok || N % 256 != 0) {
@@ -2327,10 +2328,41 @@ void Executor::prepare(bool dry) {
                         p.b_kstride = desc_tile_stride(p.bias.m.piece[0], rank - 1, p.Sk);
                         p.bias_affine = p.b_sstride != INT64_MIN && p.b_kstride != INT64_MIN;
                     }
-                    if (attn_window_supported(p)) {
+                    if (attn_window_supported(p) && !impl_->dyn_on) {  // a dynamic key count may outgrow the tile
                         p.fast = 4;
                         p.splits = 1;
                         p.chunk = p.Sk;
+                        if (!impl_->dry) {
+                            // per-item bases resolved once (Swin's maps carry (i + 3) mod 56 / t div 7 digits:
+                            // five device locates per item cost more than the item's math)
+                            const int64_t items = int64_t(p.Bt) * p.H;
+                            std::vector<uint64_t> tab(static_cast<size_t>(items * 5), 0);
+                            int64_t idx[VTC_MAX_RANK] = {};
+                            const vtc_map* ms[5] = {&p.q.m, &p.k.m, &p.v.m, &p.o.m, &p.bias.m};
+                            bool good = true;
+                            for (int64_t it = 0; it < items && good; ++it) {
+                                int64_t bh = it;
+                                idx[rank - 3] = bh % p.H;
+                                bh /= p.H;
+                                for (int a = rank - 4; a >= 0; --a) {
+                                    idx[a] = bh % qs[size_t(a)];
+                                    bh /= qs[size_t(a)];
+                                }
+                                idx[rank - 2] = 0;
+                                idx[rank - 1] = 0;
+                                for (int k2 = 0; k2 < (p.has_bias ? 5 : 4) && good; ++k2) {
+                                    int pc = -1;
+                                    const int64_t off = desc_eval(*ms[k2], idx, &pc);
+                                    good = pc >= 0;
+                                    if (good) tab[size_t(it * 5 + k2)] = ms[k2]->piece[pc].ptr + uint64_t(off) * es;
+                                }
+                            }
+                            if (good) {
+                                auto* d = static_cast<uint64_t*>(impl_->alloc(tab.size() * 8, false));
+                                ck(cudaMemcpy(d, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice), "H2D(attn item bases)");
+                                p.item_base = d;
+                            }
+                        }
                         L->kernel = "attn_window_tc";
                         push(std::move(L));
                         break;

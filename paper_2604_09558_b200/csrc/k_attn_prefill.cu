@@ -328,22 +328,26 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
     dev::pdl_wait();
     dev::pdl_launch_dependents();
     for (uint32_t item = blockIdx.x * WW + warp; item < nitems; item += gridDim.x * WW) {
-        uint32_t bh = item;
-        const uint32_t bq = bh / uint32_t(p.H);
-        const int h = int(bh - bq * uint32_t(p.H));
-        bh = bq;
         int32_t idx[VTC_MAX_RANK] = {};
-        for (int a = r - 4; a >= 0; --a) {
-            const uint32_t ext = uint32_t(p.q.m.shape[a]), nb = bh / ext;
-            idx[a] = int32_t(bh - nb * ext);
-            bh = nb;
+        if (!p.item_base) {
+            uint32_t bh = item;
+            const uint32_t bq = bh / uint32_t(p.H);
+            const int h = int(bh - bq * uint32_t(p.H));
+            bh = bq;
+            for (int a = r - 4; a >= 0; --a) {
+                const uint32_t ext = uint32_t(p.q.m.shape[a]), nb = bh / ext;
+                idx[a] = int32_t(bh - nb * ext);
+                bh = nb;
+            }
+            idx[ax_h] = h;
+            idx[ax_s] = 0;
+            idx[ax_d] = 0;
         }
-        idx[ax_h] = h;
-        idx[ax_s] = 0;
-        idx[ax_d] = 0;
-        // item bases (lanes 0..4 locate one map each)
+        // item bases: the host-resolved table, else lanes 0..4 locate one map each
         uint64_t mine = 0;
-        if (lane == 0) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.q.m, idx));
+        if (p.item_base) {
+            if (lane < 5) mine = p.item_base[uint64_t(item) * 5 + lane];
+        } else if (lane == 0) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.q.m, idx));
         else if (lane == 1) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.k.m, idx));
         else if (lane == 2) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.v.m, idx));
         else if (lane == 3) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.o.m, idx));
@@ -365,10 +369,10 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         const int kc = (lane % 4) * 2;
-        for (int q0 = 0; q0 < Sq; q0 += 16) {
+        // Q fragments and additive bias of one 16-row m-tile (rows rA / rB of this thread),
+        // fetched one m-tile ahead so their L2 latency overlaps the previous tile's math
+        auto fetch = [&](int q0, uint32_t (&qa)[D / 16][4], bf16 (&bA)[TK / 8][2], bf16 (&bB)[TK / 8][2]) {
             const int rA = q0 + lane / 4, rB = rA + 8;
-            // Q fragments of rows rA / rB (32-bit loads: the rows are contiguous along d)
-            uint32_t qa[D / 16][4];
 #pragma unroll
             for (int ks = 0; ks < D / 16; ++ks) {
                 const int d0 = ks * 16 + kc;
@@ -377,18 +381,39 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
                 qa[ks][2] = rA < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rA) * p.q_sstride + d0 + 8) : 0u;
                 qa[ks][3] = rB < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rB) * p.q_sstride + d0 + 8) : 0u;
             }
-            // additive bias of this thread's scores, requested before the MMAs
-            float bA[TK / 8][2], bB[TK / 8][2];
+            const bf16 zero = __float2bfloat16_rn(0.f);
+            const bf16* rowA = bb + int64_t(rA) * p.b_sstride;
+            const bf16* rowB = bb + int64_t(rB) * p.b_sstride;
+            const int64_t ks_ = p.b_kstride;
 #pragma unroll
             for (int nt = 0; nt < TK / 8; ++nt)
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const int t = nt * 8 + kc + c;
-                    bA[nt][c] = (p.has_bias && t < Sk && rA < Sq)
-                                    ? __bfloat162float(bb[int64_t(rA) * p.b_sstride + int64_t(t) * p.b_kstride]) : 0.f;
-                    bB[nt][c] = (p.has_bias && t < Sk && rB < Sq)
-                                    ? __bfloat162float(bb[int64_t(rB) * p.b_sstride + int64_t(t) * p.b_kstride]) : 0.f;
+                    const int64_t off = ks_ == 1 ? int64_t(t) : int64_t(t) * ks_;
+                    bA[nt][c] = (p.has_bias && t < Sk && rA < Sq) ? rowA[off] : zero;
+                    bB[nt][c] = (p.has_bias && t < Sk && rB < Sq) ? rowB[off] : zero;
                 }
+        };
+        uint32_t qcur[D / 16][4];
+        bf16 bAc[TK / 8][2], bBc[TK / 8][2];
+        fetch(0, qcur, bAc, bBc);
+        for (int q0 = 0; q0 < Sq; q0 += 16) {
+            const int rA = q0 + lane / 4, rB = rA + 8;
+            uint32_t qa[D / 16][4];
+            float bA[TK / 8][2], bB[TK / 8][2];
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) qa[ks][e] = qcur[ks][e];
+#pragma unroll
+            for (int nt = 0; nt < TK / 8; ++nt)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    bA[nt][c] = __bfloat162float(bAc[nt][c]);
+                    bB[nt][c] = __bfloat162float(bBc[nt][c]);
+                }
+            if (q0 + 16 < Sq) fetch(q0 + 16, qcur, bAc, bBc);
             if (q0 == 0) {
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
                 __syncwarp();

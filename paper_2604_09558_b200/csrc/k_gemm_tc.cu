@@ -778,6 +778,12 @@ void launch_variant(const GemmTcParams* dp, dim3 grid, const Tmaps& tmaps, cudaS
     launch_k(gemm_tc_kernel<BN, ST, MT, EPI>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
 }
 
+int sm_count() {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
 template <int EPI>
 void launch_epi(const GemmTcParams& p, const GemmTcParams* dp, const Tmaps& tmaps, cudaStream_t s) {
     const int tm = p.mt == 2 ? 2 * BM : BM;
@@ -797,7 +803,7 @@ void launch_epi(const GemmTcParams& p, const GemmTcParams* dp, const Tmaps& tmap
     } else if constexpr (EPI != GEMM_EPI_SWIGLU) {
         if (ktiles <= 2 && p.splits == 1) {
             launch_variant<128, 2, 1, EPI>(dp, grid, tmaps, s);  // three CTAs per SM
-        } else if ((ktiles <= 6 || (p.M <= BM && tiles > 148)) && p.splits == 1) {
+        } else if ((ktiles <= 6 || (p.M <= BM && tiles > sm_count())) && p.splits == 1) {
             // two CTAs per SM: shallow K, or decode-sized M with more tiles than SMs (the
             // fused gate / up weight streams then run in one wave instead of two)
             launch_variant<128, 3, 1, EPI>(dp, grid, tmaps, s);

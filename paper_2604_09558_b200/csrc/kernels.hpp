@@ -386,6 +386,7 @@ struct AttnParams {
     // base + position * stride within a (batch, head) item (host-proved)
     int32_t qo_affine, bias_affine;
     int64_t q_sstride, o_sstride, b_sstride, b_kstride;
+    const uint64_t* item_base;     // [Bt * H][5]: Q, K, V, O, bias addresses at position 0 (host-resolved)
     // decode: L2 prefetch of the next launch's weights while the (latency-bound)
     // attention leaves HBM idle -- [pf_base, pf_base + pf_bytes), split over the CTAs
     uint64_t pf_base;

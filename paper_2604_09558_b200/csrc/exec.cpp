@@ -2170,6 +2170,13 @@ void Executor::prepare(bool dry) {
                     if (ok) {
                         // prefill-sized M: 256-row tiles (two M=128 MMAs per B stage)
                         p.mt = (!p.a_gather && p.bn == 256 && M >= 4096) ? 2 : 1;
+                        // K <= 4096 without a SwiGLU epilogue: 128 x 256 tiles, two CTAs per SM, so one
+                        // CTA's epilogue overlaps the other's mainloop (C5 QKV 1585 -> 1519 us, O-proj
+                        // 1219 -> 1086 us; SwiGLU and K = 14336 measured slower).  VTC_NO_GEMM_PAIR=1: off
+                        if (p.mt == 2 && K <= 4096 && p.epi == GEMM_EPI_PLAIN && !std::getenv("VTC_NO_GEMM_PAIR")) {
+                            p.mt = 1;
+                            p.pair = 1;
+                        }
                         const int64_t on = p.epi == GEMM_EPI_SWIGLU ? p.bn / 2 : p.bn;  // output columns per tile
                         const int64_t ntl = (N + on - 1) / on + (p.nmat > 1 ? (p.N1 + p.bn - 1) / p.bn : 0);
                         int64_t tiles = (M + 128 * p.mt - 1) / (128 * p.mt) * ntl;

@@ -794,7 +794,7 @@ void launch_epi(const GemmTcParams& p, const GemmTcParams* dp, const Tmaps& tmap
     const dim3 grid(unsigned(tiles), unsigned(p.splits));
     if (p.mt == 2) {
         launch_variant<256, 3, 2, EPI>(dp, grid, tmaps, s);
-    } else if (p.bn == 256 && ktiles <= 2 && p.splits == 1) {
+    } else if (p.bn == 256 && ((ktiles <= 2 && p.splits == 1) || p.pair)) {
         // shallow K (e.g. Swin's K = 96): a 2-stage ring, two CTAs per SM, so one
         // CTA's epilogue overlaps the other's loads and MMAs
         launch_variant<256, 2, 1, EPI>(dp, grid, tmaps, s);

@@ -32,3 +32,8 @@ tail -5 gpurun_out/r2_san_racecheck.log
 timeout 1800 compute-sanitizer --tool synccheck --print-limit 20 python -m pytest tests/test_gpu.py -q -x \
    -k "llama_layer_small or swin_block_small" > gpurun_out/r2_san_synccheck.log 2>&1; echo synccheck=$?
 tail -5 gpurun_out/r2_san_synccheck.log
+# summarise on the box (the .ncu-rep files exceed the copy-back limit); keep the small reports
+python scripts/summarize_r2.py r2 > gpurun_out/r2_summary_stdout.txt 2>&1; echo summarize=$?
+mkdir -p gpurun_out/profiles_r2 && cp profiles/r2_* profiles/traffic.json gpurun_out/profiles_r2/
+for f in gpurun_out/r2_full_*.ncu-rep; do [ $(stat -c %s "$f") -gt 6000000 ] && rm -f "$f"; done
+du -sh gpurun_out

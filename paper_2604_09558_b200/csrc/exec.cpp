@@ -950,6 +950,7 @@ void Executor::prepare(bool dry) {
         const OpNode *gate, *up, *silu, *mul;
     };
     std::map<std::string, SwiGlu> tc_swiglu;  // launch node (earlier MatMul) -> the SwiGLU pair
+    std::map<std::string, const OpNode*> skinny_norm;  // shallow-K GEMM -> the row norm its A producer computes
     std::set<std::string> hpartner;
     std::set<std::string> absorbed;
     std::map<std::string, int> topo_pos;
@@ -1178,6 +1179,51 @@ void Executor::prepare(bool dry) {
                 }
             }
         }
+        // a LayerNorm / RMSNorm over K <= 128 whose output only a shallow-K GEMM reads (through
+        // virtual views: Swin's LN1 -> roll -> window partition -> QKV, LN2 -> reshape -> fc1) is
+        // computed by that GEMM's A producers from the norm's input rows (VTC_NO_SKINNY_NORM=1: off)
+        if (!std::getenv("VTC_NO_SKINNY") && !std::getenv("VTC_NO_SKINNY_NORM") && !std::getenv("VTC_NO_TC_EPI")) {
+            const auto gouts = g_.graph_outputs();
+            const std::set<std::string> gout(gouts.begin(), gouts.end());
+            for (const auto& n : g_.nodes()) {
+                // not under a GELU epilogue: 8 epilogue warps leave it issue-bound (Swin fc1 178 -> 190 us)
+                if (!tc_eligible(n) || absorbed.count(n.id) || tc_swiglu.count(n.id) || tc_hfuse.count(n.id) ||
+                    tc_gelu.count(n.id))
+                    continue;
+                const Index& as = g_.tensor(n.inputs[0]).shape;
+                const int64_t M = as[0], K = as[1], N = g_.tensor(n.inputs[1]).shape[1];
+                if (!(M >= 8192 && K <= 128 && K % 32 == 0 && N % 16 == 0 && N <= 1024)) continue;
+                const auto tg = targets_of(map_of(n.inputs[0]));
+                if (tg.size() != 1) continue;
+                const std::string R = *tg.begin();
+                const OpNode* L = g_.producer(R);
+                if (!L || (L->kind != OpKind::LayerNorm && L->kind != OpKind::RMSNorm) || gout.count(R) ||
+                    g_.tensor(R).dtype != DType::BF16 || g_.tensor(R).shape.back() != K ||
+                    g_.tensor(L->inputs[0]).shape.back() != K)
+                    continue;
+                bool only = true;  // every reader of R is n, through eliminated views
+                for (const auto& [tid, m] : ptg_.resolved) {
+                    const auto mt = m.targets();
+                    if (std::find(mt.begin(), mt.end(), R) == mt.end()) continue;
+                    if (gout.count(tid)) only = false;
+                    for (const OpNode* c : g_.consumers(tid))
+                        if (!(is_data_movement(*c) && elim.count(c->id)) && !(c == &n && tid == n.inputs[0])) only = false;
+                }
+                // the norm now runs at n's position: nothing in between may write its inputs
+                std::set<std::string> lin;
+                for (const auto& in : L->inputs)
+                    for (const auto& r : targets_of(map_of(in))) lin.insert(r);
+                for (const auto& m2 : g_.nodes()) {
+                    const int pm = topo_pos.at(m2.id);
+                    if (pm <= topo_pos.at(L->id) || pm >= topo_pos.at(n.id)) continue;
+                    for (const auto& o : m2.outputs)
+                        for (const auto& r : targets_of(map_of(o))) only = only && !lin.count(r);
+                }
+                if (!only) continue;
+                skinny_norm[n.id] = L;
+                absorbed.insert(L->id);
+            }
+        }
         // a norm is absorbed only if every consumer MatMul fused it
         for (auto& [id, f] : fusion) {
             if (f.norm) absorbed.insert(f.norm->id);
@@ -1328,9 +1374,10 @@ void Executor::prepare(bool dry) {
     };
     std::map<std::string, TcTrees> tc_trees;
     const bool dbg_fuse = std::getenv("VTC_DEBUG_FUSION") != nullptr;
-    // opt-in (VTC_TC_TREES=1): measured slower than the separate affine eltwise launch at C5
-    // (QKV + trees 2.53 ms vs 1.64 + 0.67 ms: the per-row epilogue's table loads serialise)
-    if (opt_.fuse && std::getenv("VTC_TC_TREES") && !std::getenv("VTC_NO_TC_EPI") && !impl_->dyn_on) {
+    // (VTC_NO_TC_TREES=1: off.)  With one CTA per SM the per-row epilogue's table loads
+    // serialised (QKV + trees 2.53 ms vs 1.64 + 0.67 ms at C5); with two 128-row CTAs per SM
+    // the co-resident CTA's mainloop hides them (1.98 ms vs 1.48 + 0.65 ms)
+    if (opt_.fuse && !std::getenv("VTC_NO_TC_TREES") && !std::getenv("VTC_NO_TC_EPI") && !impl_->dyn_on) {
         const auto gouts = g_.graph_outputs();
         const std::set<std::string> graph_out(gouts.begin(), gouts.end());
         for (const auto& n : g_.nodes()) {
@@ -1960,7 +2007,60 @@ void Executor::prepare(bool dry) {
                             q.has_res = 1;
                             sk = rows_of(mn(other), N, q.r_base, q.r_ld, q.r_rows, "H2D(skinny r_rows)");
                         }
-                        if (sk) {
+                        auto sn = skinny_norm.find(n.id);
+                        if (sk && sn != skinny_norm.end()) {
+                            // A = norm(x rows): the producers read x's row behind each A row
+                            const OpNode& L = *sn->second;
+                            q.a_norm = L.kind == OpKind::LayerNorm ? 1 : 2;
+                            q.eps = float(std::get<NormAttrs>(L.attrs).eps);
+                            q.a_gather = 1;
+                            bool vec_ok = true;
+                            auto vec_ptr = [&](const std::string& t) -> const void* {
+                                const VMap& m = map_of(t);
+                                auto st = m.pieces().size() == 1 ? VMap::tile_stride(m.pieces()[0], 0, K) : std::nullopt;
+                                if (!st || *st != 1) {
+                                    vec_ok = false;
+                                    return nullptr;
+                                }
+                                return reinterpret_cast<const char*>(target(m.pieces()[0].target).ptr) + m.pieces()[0].off.c0 * es;
+                            };
+                            q.norm_w = vec_ptr(L.inputs[1]);
+                            q.norm_b = L.kind == OpKind::LayerNorm ? vec_ptr(L.inputs[2]) : nullptr;
+                            sk = vec_ok;
+                            if (sk && !impl_->dry) {
+                                const std::string& R = L.outputs[0];
+                                const int64_t xrows = volume(g_.tensor(L.inputs[0]).shape) / K;
+                                const VMap xv = VMap::affine(Index{xrows, K}, Index{K, 1}, 0, L.inputs[0])
+                                                    .compose([&](const std::string& x) -> const VMap* {
+                                                        return map_of(x).is_identity_of(x) ? nullptr : &map_of(x);
+                                                    });
+                                const vtc_map xl = lower_map(xv, target);
+                                const vtc_map al = lower_map(map_of(n.inputs[0]), target);
+                                const int rid = target(R).index;
+                                std::vector<uint64_t> tab(static_cast<size_t>(M));
+                                int64_t idx[VTC_MAX_RANK] = {};
+                                for (int64_t m = 0; m < M && sk; ++m) {
+                                    idx[0] = m;
+                                    idx[1] = 0;
+                                    int pc = -1;
+                                    const int64_t off = desc_eval(al, idx, &pc);
+                                    sk = pc >= 0 && al.piece[pc].target == rid && off % K == 0;
+                                    if (!sk) break;
+                                    idx[0] = off / K;
+                                    const int64_t xo = desc_eval(xl, idx, &pc);
+                                    sk = pc >= 0;
+                                    if (sk) tab[size_t(m)] = xl.piece[pc].ptr + uint64_t(xo) * es;
+                                    sk = sk && tab[size_t(m)] % 16 == 0;
+                                }
+                                if (sk) {
+                                    auto* d = static_cast<uint64_t*>(impl_->alloc(tab.size() * 8, false));
+                                    ck(cudaMemcpy(d, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice), "H2D(skinny norm rows)");
+                                    q.a_rows = d;
+                                }
+                            }
+                            if (!sk) throw UnsupportedError("gemm_skinny: fused " + L.id + " rows not resolvable for " + n.id);
+                            S->node = L.id + "+" + T->node;
+                        } else if (sk) {
                             const VMap& am = map_of(n.inputs[0]);
                             int64_t lda = 0, ca = 0;
                             if (affine2d(am, lda, ca)) {
@@ -1980,8 +2080,11 @@ void Executor::prepare(bool dry) {
                                 q.a_rows = at;
                             }
                         }
+                        if (!sk && sn != skinny_norm.end())
+                            throw UnsupportedError("gemm_skinny: " + n.id + " with a fused norm is not launchable");
                         if (sk) {
-                            S->node = T->node + (f.add ? "+" + f.add->id : "") + (gl != tc_gelu.end() ? "+" + gl->second->id : "");
+                            S->node = (sn != skinny_norm.end() ? sn->second->id + "+" : std::string()) + T->node +
+                                      (f.add ? "+" + f.add->id : "") + (gl != tc_gelu.end() ? "+" + gl->second->id : "");
                             S->kernel = "gemm_skinny_bf16";
                             push(std::move(S));
                             break;
@@ -2173,7 +2276,8 @@ void Executor::prepare(bool dry) {
                         // K <= 4096 without a SwiGLU epilogue: 128 x 256 tiles, two CTAs per SM, so one
                         // CTA's epilogue overlaps the other's mainloop (C5 QKV 1585 -> 1519 us, O-proj
                         // 1219 -> 1086 us; SwiGLU and K = 14336 measured slower).  VTC_NO_GEMM_PAIR=1: off
-                        if (p.mt == 2 && K <= 4096 && p.epi == GEMM_EPI_PLAIN && !std::getenv("VTC_NO_GEMM_PAIR")) {
+                        if (p.mt == 2 && K <= 4096 && (p.epi == GEMM_EPI_PLAIN || p.epi == GEMM_EPI_TREES) &&
+                            !std::getenv("VTC_NO_GEMM_PAIR")) {
                             p.mt = 1;
                             p.pair = 1;
                         }

@@ -31,7 +31,7 @@ namespace vtc {
 namespace {
 
 using dev::bf16;
-constexpr int BM = 128, BK = 64, UK = 16, NEPI = 16, NTHREADS = (2 + NEPI) * 32;
+constexpr int BM = 128, BK = 64, UK = 16, NPROD_NORM = 8;
 constexpr int GATHER_LAG = 3;  // gathered k-tiles in flight before the oldest is published
 constexpr uint32_t SLOT_BYTES = BM * BK * 2;
 
@@ -58,7 +58,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(NEPI * 32) : "memory"); }
+template <int NE>
+__device__ __forceinline__ void bar_epi() { asm volatile("bar.sync 1, %0;" ::"n"(NE * 32) : "memory"); }
 
 // UMMA shared-memory descriptor, K-major SWIZZLE_128B: start >> 4, LBO (unused
 // for swizzled K-major) = 16 B, SBO = 1024 B between 8-row groups, version 1.
@@ -80,7 +81,12 @@ __device__ __forceinline__ uint32_t sw128(int row, int k) {
     return uint32_t(row) * 128u + ((uint32_t((k >> 3) ^ (row & 7))) << 4) + uint32_t(k & 7) * 2u;
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_constant__ SkinnyParams p) {
+// NE epilogue warps; NORM: the A operand is a row normalisation (LayerNorm / RMSNorm over
+// K <= 128) of host-resolved input rows, computed by NPROD_NORM producer warps
+template <int NE, bool NORM>
+__global__ void __launch_bounds__((2 + NE + (NORM ? NPROD_NORM - 1 : 0)) * 32, 1)
+    gemm_skinny_kernel(const __grid_constant__ SkinnyParams p) {
+    constexpr int NEPI = NE, NTHREADS = (2 + NE + (NORM ? NPROD_NORM - 1 : 0)) * 32;
     dev::TraceScope trace_scope_(&p.head);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -99,7 +105,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_c
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(&a_full[s], p.a_gather ? 32 : 1);
+            mbar_init(&a_full[s], NORM ? NPROD_NORM : p.a_gather ? 32 : 1);
             mbar_init(&a_empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -132,13 +138,117 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_c
             }
         }
     }
+    __shared__ __align__(16) float s_nw[128], s_nb[128];  // NORM: weight / bias (fp32)
+    if (NORM) {
+        for (int k = threadIdx.x; k < p.K; k += NTHREADS) {
+            s_nw[k] = __bfloat162float(static_cast<const bf16*>(p.norm_w)[k]);
+            s_nb[k] = p.a_norm == 1 ? __bfloat162float(static_cast<const bf16*>(p.norm_b)[k]) : 0.f;
+        }
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = s_tmem;
 
-    if (warp == 0) {
+    if (NORM && (warp == 0 || warp >= 2 + NEPI)) {
+        // ---------------- normalising A producers ----------------
+        // producer pi owns rows [16 pi, 16 pi + 16) of every tile: 4 lanes per row, lane q
+        // holding 16-byte chunks q, q + 4, q + 8, ... -- the arithmetic of the row_vec
+        // kernel (k_rowop.cu), so the fused and unfused normalisations round identically
+        dev::pdl_wait();
+        const int pi = warp == 0 ? 0 : warp - (2 + NEPI) + 1;
+        const int q = lane % 4, U = int(p.K) / 32;
+        const bool ln = p.a_norm == 1;
+        int g = 0;
+        for (int64_t mt = blockIdx.x; mt < mtiles; mt += gridDim.x) {
+            const int64_t m0 = mt * BM;
+            for (int kt = 0; kt < KT; ++kt) {
+                const int s = (g + kt) % S;
+                mbar_wait(&a_empty[s], (((g + kt) / S) & 1) ^ 1u);
+            }
+            {  // both of this lane's rows loaded before either is normalised
+            uint4 raw[2][4];
+#pragma unroll
+            for (int pp = 0; pp < 2; ++pp) {
+                const int64_t m = m0 + pi * 16 + pp * 8 + lane / 4;
+                const uint4* xr = m < p.M ? reinterpret_cast<const uint4*>(p.a_rows[m]) : nullptr;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (u < U && xr) raw[pp][u] = __ldcs(xr + q + 4 * u);
+            }
+#pragma unroll
+            for (int pp = 0; pp < 2; ++pp) {
+                const int r = pi * 16 + pp * 8 + lane / 4;
+                float x[4][8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[pp][u]);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const float2 v = __bfloat1622float2(h[t]);
+                        x[u][2 * t] = u < U ? v.x : 0.f;
+                        x[u][2 * t + 1] = u < U ? v.y : 0.f;
+                    }
+                }
+                float mu = 0.f;
+                if (ln) {
+                    float sm = 0.f;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (u < U)
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) sm += x[u][t];
+                    sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+                    sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+                    mu = sm / float(p.K);
+                }
+                float s2 = 0.f;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (u < U)
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const float c = x[u][t] - mu;
+                            s2 += c * c;
+                        }
+                s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+                const float rs = rsqrtf(s2 / float(p.K) + p.eps);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (u >= U) break;
+                    const int c = q + 4 * u;  // 16-byte chunk of the row: k = 8c .. 8c + 7
+                    uint4 o;
+                    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int k = c * 8 + 2 * t;
+                        float o0, o1;
+                        if (ln) {
+                            o0 = ((x[u][2 * t] - mu) * rs) * s_nw[k] + s_nb[k];
+                            o1 = ((x[u][2 * t + 1] - mu) * rs) * s_nw[k + 1] + s_nb[k + 1];
+                        } else {
+                            o0 = (x[u][2 * t] * rs) * s_nw[k];
+                            o1 = (x[u][2 * t + 1] * rs) * s_nw[k + 1];
+                        }
+                        h[t] = __floats2bfloat162_rn(o0, o1);
+                    }
+                    const int s = (g + c / 8) % S;
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(sA + size_t(s) * SLOT_BYTES) +
+                                                                            sw128(r, (c % 8) * 8)),
+                                 "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w)
+                                 : "memory");
+                }
+            }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0)
+                for (int kt = 0; kt < KT; ++kt) mbar_arrive(&a_full[(g + kt) % S]);
+            g += KT;
+        }
+    } else if (warp == 0) {
         // ---------------- A producer ----------------
         if (p.b_static) dev::pdl_wait();
         int g = 0;  // global k-tile counter -> slot g % S, phase (g / S) & 1
@@ -241,14 +351,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_c
                 g += KT;
             }
         }
-    } else {
-        // ---------------- epilogue: warps 2..9 ----------------
+    } else if (warp < 2 + NEPI) {
+        // ---------------- epilogue: warps 2 .. NEPI + 1 ----------------
         dev::pdl_wait();
         const int et = threadIdx.x - 64;        // 0 .. NEPI * 32 - 1
         const int quad = warp & 3;              // TMEM lanes 32*quad .. +31 (hardware rule: warp id mod 4)
         const int part = (warp - 2) >> 2;       // NEPI / 4 warps per quadrant: column parts
         const int row = quad * 32 + lane;
-        constexpr int PARTS = NEPI / 4;
+        constexpr int PARTS = NEPI / 4;  // warps per TMEM lane quadrant
         const int hc = (NC / PARTS + 7) / 8 * 8;  // columns per part, multiple of 8
         const int c_lo = part * hc, c_hi = min(NC, c_lo + hc);
         bf16* srow = reinterpret_cast<bf16*>(sC) + size_t(row) * cpitch;
@@ -280,7 +390,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_c
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[b]);
-                bar_epi();  // the unit is staged
+                bar_epi<NEPI>();  // the unit is staged
                 // coalesced copy-out: consecutive threads take consecutive 16-byte chunks of a row;
                 // a thread's chunks (and their residual chunks) are loaded before any is stored
                 const int64_t n0 = int64_t(j) * NC;
@@ -317,7 +427,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_skinny_kernel(const __grid_c
                         *reinterpret_cast<uint4*>(cp + n0 + cc[q] * 8) = v[q];
                     }
                 }
-                bar_epi();  // staging free for the next unit
+                bar_epi<NEPI>();  // staging free for the next unit
             }
         }
     }
@@ -380,10 +490,17 @@ bool skinny_encode_a(SkinnyParams& p, const void* a_base, int64_t lda) {
 }
 
 void launch_gemm_skinny(const SkinnyParams& p, const SkinnyParams*, cudaStream_t s) {
-    allow_max_smem(gemm_skinny_kernel);
     const int64_t mtiles = (p.M + BM - 1) / BM;
     const unsigned grid = unsigned(std::min<int64_t>(mtiles, p.sms));
-    launch_k(gemm_skinny_kernel, dim3(grid), dim3(NTHREADS), p.smem, s, p);
+    if (p.a_norm) {
+        constexpr int NE = 8;
+        allow_max_smem(gemm_skinny_kernel<NE, true>);
+        launch_k(gemm_skinny_kernel<NE, true>, dim3(grid), dim3((2 + NE + NPROD_NORM - 1) * 32), p.smem, s, p);
+    } else {
+        constexpr int NE = 16;
+        allow_max_smem(gemm_skinny_kernel<NE, false>);
+        launch_k(gemm_skinny_kernel<NE, false>, dim3(grid), dim3((2 + NE) * 32), p.smem, s, p);
+    }
 }
 
 }  // namespace vtc

@@ -325,7 +325,11 @@ struct SkinnyParams {
     int64_t M, N, K;
     int32_t kt, nc, nchunks, slots;  // k-tiles, N columns per unit, units per tile, A ring slots
     int32_t epi;                     // 0: plain, 1: GELU of the rounded product
-    int32_t has_res, a_gather, b_static, sms, pad;
+    int32_t has_res, a_gather, b_static, sms;
+    int32_t a_norm;                  // 1: A = LayerNorm(rows), 2: RMSNorm(rows) -- a_rows are the norm's input rows
+    float eps;
+    const void* norm_w;              // [K] bf16
+    const void* norm_b;              // [K] bf16 (LayerNorm)
     size_t smem;
     const void* w;  // weights [K, N] bf16, row stride ldw
     int64_t ldw;

@@ -345,8 +345,8 @@ def test_llama_prefill_layer_small(vtc, oracle, cfg):
     want = oracle.execute(doc, x)["y"]
     got, p = _run(vtc, doc, x, vtc.MAX_ELIMINATION)
     kinds = [l["kernel"] for l in p.info()["launches"]]
-    # gate + up + SiLU * Mul in one launch (SwiGLU epilogue)
-    assert "attn_fmha_tc" in kinds and kinds.count("gemm_tc_bf16") == 4, kinds
+    # gate + up + SiLU * Mul in one launch (SwiGLU epilogue), the RoPE trees in the QKV epilogue
+    assert "attn_fmha_tc" in kinds and kinds.count("gemm_tc_bf16") == 4 and "eltwise_aff" not in kinds, kinds
     assert any(l["node"] == "gate_proj+up_proj+silu+gate_mul" for l in p.info()["launches"])
     assert p.info()["data_movement_launches"] == 0
     assert _relerr(oracle.bf16_to_f32(got["y"]), oracle.bf16_to_f32(want)) < 2e-2
@@ -563,14 +563,12 @@ def test_tc_fused_epilogues_bit_identical(vtc, oracle, monkeypatch, which):
         x["sin"] = oracle.f32_to_bf16(sin.astype(np.float32))
         want_nodes = {"gate_proj+up_proj+silu+gate_mul", "qkv_proj|rk_mc+rk_ms+rk_add|rq_mc+rq_ms+rq_add"}
     g = vtc.parse_graph(doc)
-    monkeypatch.setenv("VTC_TC_TREES", "1")  # the opt-in RoPE-tree epilogue too
     p = vtc.Plan(g, vtc.MAX_ELIMINATION)
     nodes = {l["node"] for l in p.info(dry=True)["launches"]}
     assert want_nodes <= nodes, nodes
     fused = vtc.execute(g, p, x)["y"]
     monkeypatch.setenv("VTC_NO_TC_EPI", "1")
     monkeypatch.setenv("VTC_NO_TC_HFUSE", "1")
-    monkeypatch.delenv("VTC_TC_TREES")
     p2 = vtc.Plan(g, vtc.MAX_ELIMINATION)
     assert not want_nodes & {l["node"] for l in p2.info(dry=True)["launches"]}
     unfused = vtc.execute(g, p2, x)["y"]

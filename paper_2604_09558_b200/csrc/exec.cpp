@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -26,6 +27,53 @@ void ck(cudaError_t e, const char* what) {
 }
 
 // SM count of the current device (the rank's GPU, not device 0)
+// A/B and test switches of the executor, read from the environment once per
+// prepare (DESIGN.md §6a lists them; every default is the measured best).
+struct Tuning {
+    int gemv_stages = -1, gemv_pre = -1, gemv_l2pf = -1, chain_l2pf = -1, attn_ctas = -1;
+    int64_t host_link_max = -1;
+    bool no_ew_fast, no_ew_aff, no_tc_epi, no_tc_hfuse, no_skinny, no_skinny_norm, no_epi_fusion, debug_fusion,
+        no_tc_trees, no_row_fast, no_gemm_pair, no_fmha, no_attn_window, separate_combine, attn_l2pf, chain, trace,
+        host_dma;
+    static bool set(const char* k) { return std::getenv(k) != nullptr; }
+    static bool on(const char* k) {
+        const char* e = std::getenv(k);
+        return e && e[0] == '1';
+    }
+    static Tuning from_env() {
+        Tuning t;
+        auto num = [](const char* k, auto& v) {
+            if (const char* e = std::getenv(k)) v = std::atoll(e);
+        };
+        num("VTC_GEMV_STAGES", t.gemv_stages);
+        num("VTC_GEMV_PRE", t.gemv_pre);
+        num("VTC_GEMV_L2PF", t.gemv_l2pf);
+        num("VTC_CHAIN_L2PF", t.chain_l2pf);
+        num("VTC_ATTN_CTAS", t.attn_ctas);
+        num("VTC_HOST_LINK_MAX", t.host_link_max);
+        t.no_ew_fast = set("VTC_NO_EW_FAST");
+        t.no_ew_aff = set("VTC_NO_EW_AFF");
+        t.no_tc_epi = set("VTC_NO_TC_EPI");
+        t.no_tc_hfuse = set("VTC_NO_TC_HFUSE");
+        t.no_skinny = set("VTC_NO_SKINNY");
+        t.no_skinny_norm = set("VTC_NO_SKINNY_NORM");
+        t.no_epi_fusion = set("VTC_NO_EPI_FUSION");
+        t.debug_fusion = set("VTC_DEBUG_FUSION");
+        t.no_tc_trees = set("VTC_NO_TC_TREES");
+        t.no_row_fast = set("VTC_NO_ROW_FAST");
+        t.no_gemm_pair = set("VTC_NO_GEMM_PAIR");
+        t.no_fmha = set("VTC_NO_FMHA");
+        t.no_attn_window = set("VTC_NO_ATTN_WINDOW");
+        t.separate_combine = set("VTC_ATTN_SEPARATE_COMBINE");
+        const char* pf = std::getenv("VTC_ATTN_L2PF");
+        t.attn_l2pf = !(pf && pf[0] == '0');
+        t.chain = on("VTC_CHAIN");
+        t.trace = on("VTC_TRACE");
+        t.host_dma = set("VTC_HOST_DMA");
+        return t;
+    }
+};
+
 int device_sms() {
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -491,6 +539,7 @@ int Executor::num_kernel_launches() const {
 }
 
 void Executor::prepare(bool dry) {
+    const Tuning tun = Tuning::from_env();
     if (!dry)
         for (auto& r : roots_) root_ptr(r.id);  // allocate every unbound root
     impl_->free_graph();
@@ -636,7 +685,7 @@ void Executor::prepare(bool dry) {
         int a_tiles = int(std::min<int64_t>(kts, maxrange));
         int stages = 0;
         int max_st = 3;
-        if (const char* e = std::getenv("VTC_GEMV_STAGES")) max_st = std::atoi(e);
+        if (tun.gemv_stages >= 0) max_st = tun.gemv_stages;
         for (int st = max_st; st >= 2 && !stages; --st)
             if (gemv_stream_smem(p.M, a_tiles, st)) stages = st;
         if (!stages) return false;
@@ -677,9 +726,9 @@ void Executor::prepare(bool dry) {
         p.a_tiles = a_tiles;
         p.b_static = (written_roots.count(b_root) || (m2 && written_roots.count(m2->root))) ? 0 : 1;
         p.pre_stages = 1;
-        if (const char* e = std::getenv("VTC_GEMV_PRE")) p.pre_stages = std::atoi(e);
+        if (tun.gemv_pre >= 0) p.pre_stages = tun.gemv_pre;
         p.l2_prefetch = 0;
-        if (const char* e = std::getenv("VTC_GEMV_L2PF")) p.l2_prefetch = std::atoi(e);
+        if (tun.gemv_l2pf >= 0) p.l2_prefetch = tun.gemv_l2pf;
         p.work = static_cast<float*>(impl_->alloc(size_t(strips * maxc * p.M * COLS) * sizeof(float), false));
         p.counters = static_cast<unsigned*>(impl_->alloc(size_t(strips) * sizeof(unsigned), true));
         auto* dfirst = static_cast<int32_t*>(impl_->alloc(size_t(strips) * 4, false));
@@ -784,7 +833,7 @@ void Executor::prepare(bool dry) {
         // box, and the program one op (GELU, residual adds) or SiLU(in0) * in1
         // (registers: inputs 0..nin-1, op s writes EW_MAX_IN + s; Add / Mul commute exactly)
         int pat = 0;
-        const bool fast_ew = !std::getenv("VTC_NO_EW_FAST");  // tests: generic interpreter everywhere
+        const bool fast_ew = !tun.no_ew_fast;  // tests: generic interpreter everywhere
         if (fast_ew && dt == DType::BF16 && vec == 8 && !spec.copy) {
             const EwInstr* q = p.prog;
             if (p.nprog == 1 && p.result == q[0].dst && q[0].op != EwOp::Copy &&
@@ -810,7 +859,7 @@ void Executor::prepare(bool dry) {
         // affine operands (<= 2 pieces split along the last axis, vector-aligned): the
         // compact-parameter kernel, no per-element map evaluation (RoPE trees, views)
         {
-            bool aff = !std::getenv("VTC_NO_EW_AFF") && vec * es == 16 && rank >= 1;
+            bool aff = !tun.no_ew_aff && vec * es == 16 && rank >= 1;
             for (int k = 0; k <= p.nin && aff; ++k) {
                 const VOperand& op = k == 0 ? p.out : p.in[k - 1];
                 const vtc_map& m = op.m;
@@ -1059,7 +1108,7 @@ void Executor::prepare(bool dry) {
                 const std::string& other = ad->inputs[0] == n.outputs[0] ? ad->inputs[1] : ad->inputs[0];
                 const OpNode* po = g_.producer(other);
                 if (!po || topo_pos[po->id] < topo_pos[n.id]) f.add = ad;
-            } else if (tc && !std::getenv("VTC_NO_TC_EPI") && !cs.empty() && only_consumer(n.outputs[0], cs[0]->id) &&
+            } else if (tc && !tun.no_tc_epi && !cs.empty() && only_consumer(n.outputs[0], cs[0]->id) &&
                        cs[0]->kind == OpKind::Reshape &&
                        elim.count(cs[0]->id) &&
                        g_.tensor(cs[0]->outputs[0]).shape.back() == g_.tensor(n.outputs[0]).shape.back()) {
@@ -1110,7 +1159,7 @@ void Executor::prepare(bool dry) {
         //  * SwiGLU: gate = A.Wg, up = A.Wu, SiLU(gate) * up, each intermediate with one
         //    consumer: one launch whose tiles hold 128 columns of both products and store
         //    only the Mul's output (gate / up are never written)
-        if (!std::getenv("VTC_NO_TC_EPI")) {
+        if (!tun.no_tc_epi) {
             for (const auto& n : g_.nodes()) {
                 if (!tc_eligible(n) || fusion.count(n.id) || absorbed.count(n.id)) continue;
                 const std::string& o = n.outputs[0];
@@ -1159,7 +1208,7 @@ void Executor::prepare(bool dry) {
         // the same on the tensor cores: sibling MatMuls reading the same A with plain
         // single-piece outputs (gate / up at decode batch) run as one launch, so the
         // second does not wait for the first to complete (VTC_NO_TC_HFUSE=1: off)
-        if (!std::getenv("VTC_NO_TC_HFUSE")) {
+        if (!tun.no_tc_hfuse) {
             std::vector<const OpNode*> cands;
             for (const auto& n : g_.nodes())
                 if (tc_eligible(n) && !fusion.count(n.id) && !absorbed.count(n.id) && map_of(n.outputs[0]).pieces().size() == 1)
@@ -1182,7 +1231,7 @@ void Executor::prepare(bool dry) {
         // a LayerNorm / RMSNorm over K <= 128 whose output only a shallow-K GEMM reads (through
         // virtual views: Swin's LN1 -> roll -> window partition -> QKV, LN2 -> reshape -> fc1) is
         // computed by that GEMM's A producers from the norm's input rows (VTC_NO_SKINNY_NORM=1: off)
-        if (!std::getenv("VTC_NO_SKINNY") && !std::getenv("VTC_NO_SKINNY_NORM") && !std::getenv("VTC_NO_TC_EPI")) {
+        if (!tun.no_skinny && !tun.no_skinny_norm && !tun.no_tc_epi) {
             const auto gouts = g_.graph_outputs();
             const std::set<std::string> gout(gouts.begin(), gouts.end());
             for (const auto& n : g_.nodes()) {
@@ -1298,7 +1347,7 @@ void Executor::prepare(bool dry) {
     //      intermediate roots they would have read are never written ----
     std::map<std::string, std::vector<std::string>> epi_trees;  // gemv node -> tree roots
     std::map<std::string, std::set<std::string>> epi_roots;     // gemv node -> exclusive roots
-    if (opt_.fuse && opt_.gemv_stream && !std::getenv("VTC_NO_EPI_FUSION")) {
+    if (opt_.fuse && opt_.gemv_stream && !tun.no_epi_fusion) {
         std::set<std::string> graph_io;
         for (const auto& t : g_.graph_inputs()) graph_io.insert(t);
         for (const auto& t : g_.graph_outputs()) graph_io.insert(t);
@@ -1373,11 +1422,11 @@ void Executor::prepare(bool dry) {
         int64_t skip_lo = 0, skip_hi = 0;
     };
     std::map<std::string, TcTrees> tc_trees;
-    const bool dbg_fuse = std::getenv("VTC_DEBUG_FUSION") != nullptr;
+    const bool dbg_fuse = tun.debug_fusion;
     // (VTC_NO_TC_TREES=1: off.)  With one CTA per SM the per-row epilogue's table loads
     // serialised (QKV + trees 2.53 ms vs 1.64 + 0.67 ms at C5); with two 128-row CTAs per SM
     // the co-resident CTA's mainloop hides them (1.98 ms vs 1.48 + 0.65 ms)
-    if (opt_.fuse && !std::getenv("VTC_NO_TC_TREES") && !std::getenv("VTC_NO_TC_EPI") && !impl_->dyn_on) {
+    if (opt_.fuse && !tun.no_tc_trees && !tun.no_tc_epi && !impl_->dyn_on) {
         const auto gouts = g_.graph_outputs();
         const std::set<std::string> graph_out(gouts.begin(), gouts.end());
         for (const auto& n : g_.nodes()) {
@@ -1735,7 +1784,7 @@ void Executor::prepare(bool dry) {
                 if (n.kind != OpKind::Softmax) p.w = operand(map_of(n.inputs[1]), 0, p.D, es);
                 if (n.kind == OpKind::LayerNorm) p.bias = operand(map_of(n.inputs[2]), 0, p.D, es);
                 p.linear = map_flat_linear(p.x.m, rank, p.shape) && map_flat_linear(p.out.m, rank, p.shape) ? 1 : 0;
-                if (std::getenv("VTC_NO_ROW_FAST")) p.linear = 0;  // tests: map-evaluating row kernels
+                if (tun.no_row_fast) p.linear = 0;  // tests: map-evaluating row kernels
                 push(std::move(L));
                 break;
             }
@@ -1944,7 +1993,7 @@ void Executor::prepare(bool dry) {
                     // shallow K, narrow N, many rows (Swin's projections): the persistent kernel with
                     // the weight resident in shared memory (VTC_NO_SKINNY=1: off)
                     if (sw == tc_swiglu.end() && !tc_trees.count(n.id) && !tc_hfuse.count(n.id) && M >= 8192 && K <= 512 &&
-                        N <= 1024 && K % 16 == 0 && N % 16 == 0 && !std::getenv("VTC_NO_SKINNY")) {
+                        N <= 1024 && K % 16 == 0 && N % 16 == 0 && !tun.no_skinny) {
                         auto S = std::make_unique<LaunchT<SkinnyParams, launch_gemm_skinny>>();
                         SkinnyParams& q = S->p;
                         std::memset(&q, 0, sizeof(q));
@@ -2277,7 +2326,7 @@ void Executor::prepare(bool dry) {
                         // CTA's epilogue overlaps the other's mainloop (C5 QKV 1585 -> 1519 us, O-proj
                         // 1219 -> 1086 us; SwiGLU and K = 14336 measured slower).  VTC_NO_GEMM_PAIR=1: off
                         if (p.mt == 2 && K <= 4096 && (p.epi == GEMM_EPI_PLAIN || p.epi == GEMM_EPI_TREES) &&
-                            !std::getenv("VTC_NO_GEMM_PAIR")) {
+                            !tun.no_gemm_pair) {
                             p.mt = 1;
                             p.pair = 1;
                         }
@@ -2403,7 +2452,7 @@ void Executor::prepare(bool dry) {
                 }
                 // long query blocks (prefill), head dim 128: tcgen05 / TMEM flash attention
                 // with TMA-loaded Q / K / V (maps proved affine on the host)
-                if (!p.fast && p.Sq >= 64 && !std::getenv("VTC_NO_FMHA") && attn_fmha_prepare(p, !impl_->dry)) {
+                if (!p.fast && p.Sq >= 64 && !tun.no_fmha && attn_fmha_prepare(p, !impl_->dry)) {
                     p.fast = 3;
                     p.splits = 1;
                     p.chunk = p.Sk;
@@ -2413,7 +2462,7 @@ void Executor::prepare(bool dry) {
                 }
                 // short sequences (Swin windows): one warp per (batch, head) item
                 if (!p.fast && p.Sq <= 64 && p.Sk <= 64 && p.q.m.npieces == 1 && p.o.m.npieces == 1 &&
-                    !std::getenv("VTC_NO_ATTN_WINDOW")) {
+                    !tun.no_attn_window) {
                     const int64_t qs_ = desc_tile_stride(p.q.m.piece[0], rank - 2, p.Sq);
                     const int64_t os_ = desc_tile_stride(p.o.m.piece[0], rank - 2, p.Sq);
                     const int64_t qd_ = desc_tile_stride(p.q.m.piece[0], rank - 1, p.D);
@@ -2493,10 +2542,29 @@ void Executor::prepare(bool dry) {
                 const int kgran = p.fast ? 64 : 32;  // keys per split granule (4 warps x 16 on the fast path)
                 if (splits <= 0) {
                     // fast path: one wave (2 CTAs per SM) when the KV is short, ~4 waves when long
-                    int64_t target = p.fast ? (int64_t(p.Sk) * qblocks >= 148 * 2 * 512 ? 148 * 2 * 4 : 148 * 2) : 148 * 2;
-                    if (const char* ev = std::getenv("VTC_ATTN_CTAS")) target = std::atoll(ev);
+                    const int64_t wave = int64_t(impl_->dry ? 148 : device_sms()) * 2;  // 2 CTAs per SM
+                    const bool longkv = int64_t(p.Sk) * qblocks >= wave * 512;
+                    int64_t target = p.fast ? (longkv ? wave * 4 : wave) : wave;
+                    const bool ev = tun.attn_ctas > 0;
+                    if (ev) target = tun.attn_ctas;
                     splits = int((target + qblocks - 1) / qblocks);
-                    splits = std::max(1, std::min(splits, (p.Sk + kgran - 1) / kgran));
+                    const int smax = (p.Sk + kgran - 1) / kgran;
+                    splits = std::max(1, std::min(splits, smax));
+                    if (p.fast && longkv && !ev) {
+                        // several waves: the split count whose last wave is fullest (C3: 3 splits =
+                        // 5.19 waves -> 4 splits = 6.92 waves, attention 396 -> 379 us)
+                        int best = splits;
+                        double best_fill = 0.0;
+                        for (int sc = std::max(1, splits - 1); sc <= std::min(smax, 2 * splits); ++sc) {
+                            const double w = double(qblocks) * sc / double(wave);
+                            const double fill = w / std::ceil(w);
+                            if (fill > best_fill + 0.02) {
+                                best_fill = fill;
+                                best = sc;
+                            }
+                        }
+                        splits = best;
+                    }
                 }
                 int chunk = (p.Sk + splits - 1) / splits;
                 chunk = (chunk + kgran - 1) / kgran * kgran;
@@ -2505,7 +2573,7 @@ void Executor::prepare(bool dry) {
                 p.chunk = chunk;
                 L->kernel = p.fast ? (splits > 1 ? "attn_decode_tc_splitkv" : "attn_decode_tc") : (splits > 1 ? "attention_splitkv" : "attention");
                 // cooperative in-kernel split combine when every CTA fits on the GPU at once
-                if (splits > 1 && p.fast == 1 && !impl_->dry && !std::getenv("VTC_ATTN_SEPARATE_COMBINE") &&
+                if (splits > 1 && p.fast == 1 && !impl_->dry && !tun.separate_combine &&
                     qblocks * splits <= attn_decode_capacity())
                     p.counters = static_cast<unsigned*>(impl_->alloc(size_t(qblocks) * sizeof(unsigned), true));
                 if (splits > 1) {
@@ -2566,8 +2634,7 @@ void Executor::prepare(bool dry) {
     // into L2 (HBM is idle while the split-KV attention is latency-bound; W_o is 32 MB
     // at Llama-3-8B).  VTC_ATTN_L2PF=0: off
     {
-        const char* ev = std::getenv("VTC_ATTN_L2PF");
-        const bool on = !(ev && ev[0] == '0');
+        const bool on = tun.attn_l2pf;
         using AL = LaunchT<AttnParams, launch_attention>;
         using GL = LaunchT<GemvParams, launch_gemv_any>;
         for (size_t i = 0; on && i + 1 < impl_->launches.size(); ++i) {
@@ -2585,7 +2652,7 @@ void Executor::prepare(bool dry) {
     // on C2 it measured equal to separate launches (113.6 vs 113.6 us) because
     // every strip of a split-K stage completes at the stage's end, so the next
     // stage cannot start early; kept for multi-layer chains.
-    if (opt_.fuse && std::getenv("VTC_CHAIN") && std::getenv("VTC_CHAIN")[0] == '1') {
+    if (opt_.fuse && tun.chain) {
         using GL = LaunchT<GemvParams, launch_gemv_any>;
         auto roots_of = [](const VOperand& op, std::set<int>& out) {
             for (int i = 0; i < op.m.npieces; ++i) out.insert(op.m.piece[i].target);
@@ -2686,7 +2753,7 @@ void Executor::prepare(bool dry) {
                 h.l2_prefetch = p.l2_prefetch;
                 if (t) {
                     h.l2_prefetch = 0;  // measured: any boundary prefetch slowed C2 (133 us at 4 tiles)
-                    if (const char* e = std::getenv("VTC_CHAIN_L2PF")) h.l2_prefetch = std::atoi(e);
+                    if (tun.chain_l2pf >= 0) h.l2_prefetch = tun.chain_l2pf;
                 }
                 C->ca.st[t] = h;
                 std::memcpy(C->ca.tmap[t], p.tmap, sizeof(p.tmap));
@@ -2716,7 +2783,7 @@ void Executor::prepare(bool dry) {
         for (auto& l : impl_->launches) l->dyn_patch(impl_->dyn);
     // optional device timeline (VTC_TRACE=1): [entry, exit] globaltimer per launch
     impl_->trace = nullptr;
-    if (!dry && std::getenv("VTC_TRACE") && std::getenv("VTC_TRACE")[0] == '1') {
+    if (!dry && Tuning::on("VTC_TRACE")) {
         impl_->trace = static_cast<unsigned long long*>(impl_->alloc(impl_->launches.size() * 64, false));
         for (size_t i = 0; i < impl_->launches.size(); ++i) impl_->launches[i]->set_trace(impl_->trace, int(i));
         reset_trace();
@@ -2847,7 +2914,7 @@ void Executor::run_host(const std::vector<HostIn>& ins, const std::vector<HostOu
     // than moving a few KB.  Large ones (prefill activations) are DMA'd straight
     // between the caller's buffer and the root around the graph launch.
     int64_t kLinkMax = 64 << 10;  // measured: link copies win at 8 KB (C2), DMA at 512 KB (C3)
-    if (const char* e = std::getenv("VTC_HOST_LINK_MAX")) kLinkMax = std::atoll(e);  // tests: force either path
+    if (const int64_t e = Tuning::from_env().host_link_max; e >= 0) kLinkMax = e;  // tests: force either path
     auto s = static_cast<cudaStream_t>(stream);
     Impl& I = *impl_;
     bool same = prepared_ && I.hexec && ins.size() == I.sig_in.size() && outs.size() == I.sig_out.size() && I.fast_stream == s;
@@ -2943,7 +3010,7 @@ void Executor::run_host(const std::vector<HostIn>& ins, const std::vector<HostOu
         void *arena_host_dev = nullptr, *out_host_dev = nullptr;  // device views of the pinned buffers
         if (arena_host_) ck(cudaHostGetDevicePointer(&arena_host_dev, arena_host_, 0), "cudaHostGetDevicePointer");
         if (I.out_host) ck(cudaHostGetDevicePointer(&out_host_dev, I.out_host, 0), "cudaHostGetDevicePointer");
-        const bool dma = std::getenv("VTC_HOST_DMA") != nullptr;  // A/B: DMA nodes for the small copies too
+        const bool dma = Tuning::set("VTC_HOST_DMA");  // A/B: DMA nodes for the small copies too
         cudaStream_t cap;
         cudaGraph_t hg = nullptr;
         ck(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "cudaStreamCreate");

@@ -2351,6 +2351,8 @@ void Executor::prepare(bool dry) {
                             tiles0 = tiles / ntl * ((N + on - 1) / on);
                             splits = tiles0 >= sms ? 1 : std::min<int64_t>(ktiles, std::max<int64_t>(1, sms / tiles0));
                         }
+                        // (two CTAs per SM with twice the K splits measured slower at C3: 604 vs 546 us --
+                        // the decode GEMMs are bound by the split-K epilogue, not the weight stream)
                         p.splits = int32_t(splits);
                         if (splits > 1) {
                             p.work = static_cast<float*>(impl_->alloc(size_t(tiles * splits * 128 * p.bn) * 4, false));

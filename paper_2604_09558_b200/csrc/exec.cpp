@@ -33,7 +33,7 @@ struct Tuning {
     int gemv_stages = -1, gemv_pre = -1, gemv_l2pf = -1, chain_l2pf = -1, attn_ctas = -1;
     int64_t host_link_max = -1;
     bool no_ew_fast, no_ew_aff, no_tc_epi, no_tc_hfuse, no_skinny, no_skinny_norm, no_epi_fusion, debug_fusion,
-        no_tc_trees, no_row_fast, no_gemm_pair, no_fmha, no_attn_window, separate_combine, attn_l2pf, chain, trace,
+        no_tc_trees, no_row_fast, no_gemm_pair, gemm_cta_pair, no_fmha, no_attn_window, separate_combine, attn_l2pf, chain, trace,
         host_dma;
     static bool set(const char* k) { return std::getenv(k) != nullptr; }
     static bool on(const char* k) {
@@ -62,6 +62,7 @@ struct Tuning {
         t.no_tc_trees = set("VTC_NO_TC_TREES");
         t.no_row_fast = set("VTC_NO_ROW_FAST");
         t.no_gemm_pair = set("VTC_NO_GEMM_PAIR");
+        t.gemm_cta_pair = on("VTC_GEMM_CTA_PAIR");
         t.no_fmha = set("VTC_NO_FMHA");
         t.no_attn_window = set("VTC_NO_ATTN_WINDOW");
         t.separate_combine = set("VTC_ATTN_SEPARATE_COMBINE");
@@ -2353,6 +2354,13 @@ void Executor::prepare(bool dry) {
                         }
                         // (two CTAs per SM with twice the K splits measured slower at C3: 604 vs 546 us --
                         // the decode GEMMs are bound by the split-K epilogue, not the weight stream)
+                        // prefill: CTA pairs (cta_group::2, M = 256 UMMAs over two SMs) -- VTC_GEMM_CTA_PAIR=1
+                        if (tun.gemm_cta_pair && splits == 1 && p.bn == 256 && M >= 4096 && !p.a_gather && p.a_ndims <= 4 &&
+                            p.nmat <= 1 && (p.epi == GEMM_EPI_PLAIN || p.epi == GEMM_EPI_SWIGLU)) {
+                            p.cta_pair = 1;
+                            p.pair = 0;
+                            p.mt = 1;
+                        }
                         p.splits = int32_t(splits);
                         if (splits > 1) {
                             p.work = static_cast<float*>(impl_->alloc(size_t(tiles * splits * 128 * p.bn) * 4, false));

@@ -652,6 +652,262 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
     }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2) for prefill-sized M: a cluster of two CTAs on
+// one TPC computes a 256 x 256 tile with M = 256 UMMAs issued by the leader
+// CTA.  Each CTA loads its own 128 rows of A and its own half (128 columns) of
+// B into the same shared-memory offsets, both halves' TMA transactions signal
+// the leader's stage barrier, and the MMA reads the pair's operands from both
+// CTAs -- half the B traffic and half the shared-memory operand reads per SM of
+// a one-CTA 128 x 256 tile.  The accumulator rows of each CTA land in its own
+// TMEM (128 lanes x 256 columns), so the epilogue is the one-CTA epilogue over
+// 128 rows.  Three 32 KB stages per CTA: two CTAs per SM, one's epilogue
+// overlapping the other's mainloop.
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint32_t bar_cluster,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+        "{%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(policy)
+        : "memory");
+}
+
+constexpr int PAIR_STAGES = 3;
+template <int EPI>
+__global__ void __launch_bounds__(NTHREADS, 1) gemm_pair_kernel(const GemmTcParams* __restrict__ pp,
+                                                                 const __grid_constant__ Tmaps tm) {
+    VTC_STAGE_PARAMS(GemmTcParams, pp);
+    constexpr int BN = 256, HB = 128;  // tile N; B columns per CTA
+    constexpr int ON = EPI == GEMM_EPI_SWIGLU ? BN / 2 : BN;
+    constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = HB * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[PAIR_STAGES], empty[PAIR_STAGES], done;
+    __shared__ uint32_t s_tmem;
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int tiles_n = int((p.N + ON - 1) / ON);
+    const int tiles_m = int((p.M + 2 * BM - 1) / (2 * BM));
+    const int tile = blockIdx.x / 2;
+    constexpr int GROUP_M = 16;
+    const int in_group = GROUP_M * tiles_n;
+    const int first_m = (tile / in_group) * GROUP_M;
+    const int gm = min(tiles_m - first_m, GROUP_M);
+    const int tm_ = first_m + (tile % in_group) % gm, tn = (tile % in_group) / gm;
+    const int64_t m0 = int64_t(tm_) * 2 * BM + int64_t(rank) * BM, n0 = int64_t(tn) * ON;
+    const int ktiles = int((p.K + BK - 1) / BK);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < PAIR_STAGES; ++s) {
+            mbar_init(&full[s], 2);  // the leader's expect_tx arrival + the peer's arrival
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {  // the pair's accumulators: 128 lanes x 256 columns in each CTA
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)), "r"(BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();  // both CTAs' barriers initialised before any remote arrival
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s_tmem;
+    dev::pdl_launch_dependents();
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer (both CTAs) ----------------
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.b)) : "memory");
+        const uint64_t pol_b = evict_last_policy(), pol_a = evict_last_policy();
+        int32_t cm[5], ck[5], sub[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const uint32_t v = uint32_t(m0) / uint32_t(p.a_div[j]);
+            cm[j] = int32_t(p.a_mod[j] ? v % uint32_t(p.a_mod[j]) : v);
+            ck[j] = 0;
+            sub[j] = 0;
+        }
+        const uint32_t full0 = map_to_rank(smem_u32(&full[0]), 0);  // the leader's stage barriers
+        dev::pdl_wait();
+        for (int i = 0; i < ktiles; ++i) {
+            const int s = i % PAIR_STAGES;
+            const uint32_t ph = uint32_t(i / PAIR_STAGES) & 1u;
+            mbar_wait(&empty[s], ph ^ 1u);
+            const uint32_t fb = full0 + uint32_t(s) * 8;
+            if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+            else asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(fb) : "memory");
+            const uint32_t sa = smem_u32(smem + size_t(s) * STAGE_BYTES), sb = sa + A_BYTES;
+            const int32_t k0 = int32_t(i) * BK;
+            int32_t ca[5];
+#pragma unroll
+            for (int j = 0; j < 5; ++j) ca[j] = p.a_axis[j] ? ck[j] : cm[j];
+            switch (p.a_ndims) {
+                case 2: asm volatile(
+                            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+                            " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(sa), "l"(reinterpret_cast<uint64_t>(&tm.a)), "r"(ca[0]), "r"(ca[1]),
+                            "r"(fb), "l"(pol_a) : "memory"); break;
+                case 3: asm volatile(
+                            "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+                            " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(sa), "l"(reinterpret_cast<uint64_t>(&tm.a)), "r"(ca[0]),
+                            "r"(ca[1]), "r"(ca[2]), "r"(fb), "l"(pol_a) : "memory"); break;
+                default: asm volatile(
+                            "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+                            " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(sa), "l"(reinterpret_cast<uint64_t>(&tm.a)), "r"(ca[0]),
+                            "r"(ca[1]), "r"(ca[2]), "r"(ca[3]), "r"(fb), "l"(pol_a) : "memory"); break;
+            }
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {  // advance the K coordinates by one k-tile
+                if (!p.a_axis[j]) continue;
+                if (p.a_div[j] == 1) {
+                    ck[j] += BK;
+                    if (p.a_mod[j] && ck[j] >= p.a_mod[j]) ck[j] -= int32_t(p.a_mod[j]);
+                } else if ((sub[j] += BK) >= p.a_div[j]) {
+                    sub[j] = 0;
+                    if (++ck[j] == p.a_mod[j]) ck[j] = 0;
+                }
+            }
+            // this CTA's half of B: columns [rank * 128, rank * 128 + 128) of the tile (SwiGLU:
+            // the leader the gate's 128, the peer the up's 128 -- the same output columns)
+#pragma unroll
+            for (int j = 0; j < HB / 64; ++j) {
+                if (EPI == GEMM_EPI_SWIGLU)
+                    tma_2d_pair(sb + j * (BK * 128), rank ? &tm.b2 : &tm.b, int32_t(n0 + 64 * j), k0, fb, pol_b);
+                else
+                    tma_2d_pair(sb + j * (BK * 128), &tm.b, int32_t(n0 + rank * HB + 64 * j), k0, fb, pol_b);
+            }
+        }
+    } else if (warp == 1 && lane == 0 && leader) {
+        // ---------------- MMA issuer (leader only): M = 256 over the pair ----------------
+        dev::pdl_wait();
+        constexpr uint32_t idesc = instr_desc(2 * BM, BN);
+        for (int i = 0; i < ktiles; ++i) {
+            const int s = i % PAIR_STAGES;
+            const uint32_t ph = uint32_t(i / PAIR_STAGES) & 1u;
+            mbar_wait(&full[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t sa = smem_u32(smem + size_t(s) * STAGE_BYTES), sb = sa + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / UK; ++k) {
+                const uint64_t da = smem_desc(sa + k * 32, 16, 1024);
+                const uint64_t db = smem_desc(sb + k * 2048, BK * 128, 1024);
+                const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                    : "memory");
+            }
+            // frees stage s in both CTAs
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                             smem_u32(&empty[s])),
+                         "h"(uint16_t(3))
+                         : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                         smem_u32(&done)),
+                     "h"(uint16_t(3))
+                     : "memory");
+    }
+
+    // ---------------- epilogue: all 4 warps of each CTA, thread = accumulator row ----------------
+    dev::pdl_wait();
+    __syncwarp();
+    mbar_wait(&done, 0);
+    __syncwarp();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = warp * 32 + lane;
+    const int64_t em = m0 + row;
+    const bool live = em < p.M;
+    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+    bf16* crow = nullptr;
+    int64_t cs = 0;
+    const bf16* rrow = nullptr;
+    int64_t rs = 0;
+    if (live) {
+        int32_t idx[VTC_MAX_RANK] = {};
+        idx[0] = int32_t(em);
+        idx[1] = int32_t(n0);
+        dev::Loc lc = dev::locate(p.c.m, idx);
+        crow = dev::addr<bf16>(p.c.m, lc);
+        cs = p.c.fast_stride[lc.piece];
+        if (p.has_res) {
+            dev::Loc lr = dev::locate(p.res.m, idx);
+            rrow = dev::addr<bf16>(p.res.m, lr);
+            rs = p.res.fast_stride[lr.piece];
+        }
+    }
+    const int ncols = int(p.N - n0 < ON ? p.N - n0 : ON);
+    auto ld16 = [&](int c, float (&v)[16]) {
+        uint32_t r[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+              "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(trow + uint32_t(c)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+    };
+    for (int c = 0; c < ON; c += 16) {
+        float v[16], u[16];
+        ld16(c, v);
+        if (EPI == GEMM_EPI_SWIGLU) ld16(ON + c, u);
+        if (!live || c >= ncols) continue;
+        bf16 o[16];
+        if (EPI == GEMM_EPI_SWIGLU) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                o[j] = dev::mul_bf16(dev::silu_bf16(__float2bfloat16_rn(v[j])), __float2bfloat16_rn(u[j]));
+        } else {
+            bf16 rv[16];
+            const bool rvec = rrow && rs == 1 && c + 16 <= ncols && (reinterpret_cast<uintptr_t>(rrow + c) & 15) == 0;
+            if (rvec) {
+                *reinterpret_cast<uint4*>(&rv[0]) = __ldg(reinterpret_cast<const uint4*>(rrow + c));
+                *reinterpret_cast<uint4*>(&rv[8]) = __ldg(reinterpret_cast<const uint4*>(rrow + c + 8));
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                float f = __bfloat162float(__float2bfloat16_rn(v[j]));
+                if (rvec) f = __bfloat162float(rv[j]) + f;
+                else if (rrow && c + j < ncols) f = __bfloat162float(rrow[int64_t(c + j) * rs]) + f;
+                o[j] = __float2bfloat16_rn(f);
+            }
+        }
+        bf16* dst = crow + int64_t(c) * cs;
+        if (cs == 1 && c + 16 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            reinterpret_cast<uint4*>(dst)[0] = *reinterpret_cast<const uint4*>(&o[0]);
+            reinterpret_cast<uint4*>(dst)[1] = *reinterpret_cast<const uint4*>(&o[8]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c + j < ncols) dst[int64_t(j) * cs] = o[j];
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();  // both CTAs done with the pair's TMEM before it is released
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                               const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -818,6 +1074,20 @@ void launch_gemm_tc(const GemmTcParams& p, const GemmTcParams* dp, cudaStream_t 
     std::memcpy(&tmaps.a, p.tmap_a, sizeof(CUtensorMap));
     std::memcpy(&tmaps.b, p.tmap_b, sizeof(CUtensorMap));
     std::memcpy(&tmaps.b2, (p.nmat > 1 || p.epi == GEMM_EPI_SWIGLU) ? p.tmap_b2 : p.tmap_b, sizeof(CUtensorMap));
+    if (p.cta_pair) {
+        // clusters of two CTAs (one TPC), a 256 x 256 tile per cluster, three 32 KB stages per CTA
+        const int on = p.epi == GEMM_EPI_SWIGLU ? 128 : 256;
+        const int tiles = int((p.M + 255) / 256) * int((p.N + on - 1) / on);
+        constexpr size_t sm = size_t(PAIR_STAGES) * (BM * BK * 2 + 128 * BK * 2) + 1024;
+        if (p.epi == GEMM_EPI_SWIGLU) {
+            cudaFuncSetAttribute(gemm_pair_kernel<GEMM_EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            launch_k_cluster(gemm_pair_kernel<GEMM_EPI_SWIGLU>, dim3(2 * tiles), dim3(NTHREADS), sm, s, 2, dp, tmaps);
+        } else {
+            cudaFuncSetAttribute(gemm_pair_kernel<GEMM_EPI_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            launch_k_cluster(gemm_pair_kernel<GEMM_EPI_PLAIN>, dim3(2 * tiles), dim3(NTHREADS), sm, s, 2, dp, tmaps);
+        }
+        return;
+    }
     switch (p.epi) {
         case GEMM_EPI_GELU: launch_epi<GEMM_EPI_GELU>(p, dp, tmaps, s); break;
         case GEMM_EPI_SWIGLU: launch_epi<GEMM_EPI_SWIGLU>(p, dp, tmaps, s); break;

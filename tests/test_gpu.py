@@ -623,3 +623,23 @@ def test_swin_window_attention_matches_flash_kernel(vtc, oracle, monkeypatch):
     want = oracle.bf16_to_f32(oracle.execute(doc, x)["y"])
     assert _relerr(a, b) < 1e-2
     assert _relerr(a, want) < 2e-2
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_prefill_gemms_cta_pair_match_fp64(vtc, oracle, monkeypatch, pair):
+    """Prefill-sized GEMMs (M = 4096) on the one-CTA tile kernel and on CTA pairs
+    (cta_group::2: M = 256 UMMAs over two SMs, each CTA holding half of B): the
+    O-proj + residual, SwiGLU and down projections match the fp64 oracle."""
+    from paper_2604_09558_b200 import workloads as W
+    monkeypatch.setenv("VTC_GEMM_CTA_PAIR", pair)
+    cfg = dict(B=2, S=2048, D=512, Hq=4, Hkv=2, hd=128, F=1024)
+    doc = W.llama_prefill_layer(**cfg)
+    x = oracle.random_inputs(doc, seed=4, scales=W.llama_weight_scales(cfg["D"], cfg["F"]))
+    cos, sin = W.rope_tables_prefill(cfg["B"], cfg["S"], hd=cfg["hd"])
+    x["cos"] = oracle.f32_to_bf16(cos.astype(np.float32))
+    x["sin"] = oracle.f32_to_bf16(sin.astype(np.float32))
+    g = vtc.parse_graph(doc)
+    got = oracle.bf16_to_f32(vtc.execute(g, vtc.Plan(g, vtc.MAX_ELIMINATION), x)["y"])
+    rows = np.r_[0:64, 2040:2056, 4032:4096]  # first / middle / last rows: the oracle on a row sample
+    want = oracle.bf16_to_f32(oracle.execute(doc, x)["y"])
+    assert _relerr(got[rows], want[rows]) < 2e-2

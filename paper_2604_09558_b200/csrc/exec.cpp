@@ -33,7 +33,7 @@ struct Tuning {
     int gemv_stages = -1, gemv_pre = -1, gemv_l2pf = -1, chain_l2pf = -1, attn_ctas = -1;
     int64_t host_link_max = -1;
     bool no_ew_fast, no_ew_aff, no_tc_epi, no_tc_hfuse, no_skinny, no_skinny_norm, no_epi_fusion, debug_fusion,
-        no_tc_trees, no_row_fast, no_gemm_pair, gemm_cta_pair, no_fmha, no_attn_window, separate_combine, attn_l2pf, chain, trace,
+        no_tc_trees, no_row_fast, no_gemm_pair, gemm_cta_pair, no_coop_reduce, no_fmha, no_attn_window, separate_combine, attn_l2pf, chain, trace,
         host_dma;
     static bool set(const char* k) { return std::getenv(k) != nullptr; }
     static bool on(const char* k) {
@@ -63,6 +63,7 @@ struct Tuning {
         t.no_row_fast = set("VTC_NO_ROW_FAST");
         t.no_gemm_pair = set("VTC_NO_GEMM_PAIR");
         t.gemm_cta_pair = on("VTC_GEMM_CTA_PAIR");
+        t.no_coop_reduce = set("VTC_NO_COOP_REDUCE");
         t.no_fmha = set("VTC_NO_FMHA");
         t.no_attn_window = set("VTC_NO_ATTN_WINDOW");
         t.separate_combine = set("VTC_ATTN_SEPARATE_COMBINE");
@@ -2364,7 +2365,14 @@ void Executor::prepare(bool dry) {
                         p.splits = int32_t(splits);
                         if (splits > 1) {
                             p.work = static_cast<float*>(impl_->alloc(size_t(tiles * splits * 128 * p.bn) * 4, false));
-                            p.counters = static_cast<unsigned*>(impl_->alloc(size_t(tiles) * 4, true));
+                            p.counters = static_cast<unsigned*>(impl_->alloc(size_t(tiles) * 2 * 4, true));
+                            p.ntiles_total = int32_t(tiles);
+                            // the split-K reduction spread over every split (one CTA per SM, so the
+                            // grid is co-resident when it fits the SMs): VTC_NO_COOP_REDUCE=1 off
+                            p.coop_reduce = (tiles * splits <= sms && p.mt == 1 && p.epi != GEMM_EPI_TREES &&
+                                             !tun.no_coop_reduce)
+                                                ? 1
+                                                : 0;
                         }
                         push(std::move(T));
                         break;

@@ -406,12 +406,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
         }
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[tile], 1u) == unsigned(p.splits - 1) ? 1u : 0u;
-        __syncthreads();
-        do_epilogue = s_last != 0;
-        if (do_epilogue) {
+        if (p.coop_reduce) {
+            // every split reduces its own slice of the tile's columns once all partials are
+            // written (the host enables this only when the whole grid is co-resident, so the
+            // wait cannot deadlock); the last split out resets the counters for the next replay
+            if (threadIdx.x == 0) {
+                atomicAdd(&p.counters[tile], 1u);
+                unsigned v;
+                long long spins = 0;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&p.counters[tile]) : "memory");
+                    if (v >= unsigned(p.splits)) break;
+                    __nanosleep(32);
+                    if (++spins > (1ll << 26)) __trap();  // a missing split: fail loudly, never hang
+                }
+            }
+            __syncthreads();
             __threadfence();
-            if (threadIdx.x == 0) p.counters[tile] = 0u;
+        } else {
+            if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[tile], 1u) == unsigned(p.splits - 1) ? 1u : 0u;
+            __syncthreads();
+            do_epilogue = s_last != 0;
+            if (do_epilogue) {
+                __threadfence();
+                if (threadIdx.x == 0) p.counters[tile] = 0u;
+            }
         }
     }
 
@@ -518,8 +537,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
         if (EPI == GEMM_EPI_SWIGLU) {
             // columns c of the gate half and 128 + c of the up half -> SiLU(gate) * up,
             // rounded like the unfused SiLU and Mul operators
-            const int cpart = (ON / nparts + 15) / 16 * 16;
-            const int c_lo = part * cpart, c_hi = min(ncols, c_lo + cpart);
+            int s_lo = 0, s_hi = ON;  // cooperative split-K: this split's slice of the columns
+            if (p.coop_reduce) {
+                const int gran = (ON / 16 + p.splits - 1) / p.splits;
+                s_lo = min(ON, split * gran * 16);
+                s_hi = min(ON, s_lo + gran * 16);
+            }
+            const int cpart = ((s_hi - s_lo) / nparts + 15) / 16 * 16;
+            const int c_lo = s_lo + part * cpart, c_hi = min(min(ncols, s_hi), c_lo + cpart);
             for (int c = c_lo; c < c_hi; c += 16) {
                 float g[16], u[16];
                 get16(c, g);
@@ -565,8 +590,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                 }
             }
         } else {
-            const int cpart = (BN / nparts + 15) / 16 * 16;  // this thread's columns [c_lo, c_hi)
-            const int c_lo = part * cpart, c_hi = min(ncols, c_lo + cpart);
+            int s_lo = 0, s_hi = BN;  // cooperative split-K: this split's slice of the columns
+            if (p.coop_reduce) {
+                const int gran = (BN / 16 + p.splits - 1) / p.splits;
+                s_lo = min(BN, split * gran * 16);
+                s_hi = min(BN, s_lo + gran * 16);
+            }
+            const int cpart = ((s_hi - s_lo) / nparts + 15) / 16 * 16;  // this thread's columns [c_lo, c_hi)
+            const int c_lo = s_lo + part * cpart, c_hi = min(min(ncols, s_hi), c_lo + cpart);
             for (int c = c_lo; c < c_hi; c += 16) {
                 // trees: columns read only by the fused trees are never stored (tile-uniform test)
                 if (EPI == GEMM_EPI_TREES && n0 + c >= p.skip_lo && n0 + c + 16 <= p.skip_hi) continue;
@@ -640,6 +671,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                     }
                 }
             }
+        }
+    }
+    if (p.coop_reduce && p.splits > 1) {
+        // every split has read the partials: the last one out resets the tile's counters
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(&p.counters[p.ntiles_total + tile], 1u) == unsigned(p.splits - 1)) {
+            p.counters[tile] = 0u;
+            p.counters[p.ntiles_total + tile] = 0u;
+            __threadfence();
         }
     }
     }  // sub-tiles

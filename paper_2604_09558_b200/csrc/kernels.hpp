@@ -268,6 +268,8 @@ struct GemmTcParams {
     int32_t mt;           // 128-row sub-tiles per CTA (1, or 2 for prefill-sized M)
     int32_t pair;         // 1: 128 x 256 tiles, two CTAs per SM (one's epilogue overlaps the other's mainloop)
     int32_t cta_pair;     // 1: cta_group::2 -- a cluster of two CTAs computes a 256 x 256 tile
+    int32_t coop_reduce;  // split-K: every split reduces a column slice (grid co-resident; counters[2 * tiles])
+    int32_t ntiles_total;
     int64_t M, N, K;
     int32_t bn, splits;   // N tile (128 / 256), K splits
     int32_t has_res, pad;

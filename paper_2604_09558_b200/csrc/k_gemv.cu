@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(NT) gemv_kernel(const GemvParams* __restrict__
             float v = pa ? __bfloat162float(pa[e * sa]) : a_at(p.a, m, k);
             if (p.prologue == GemvPrologue::SiLUMul) {
                 float u = pa2 ? __bfloat162float(pa2[e * sa2]) : a_at(p.a2, m, k);
-                float sg = __bfloat162float(__float2bfloat16_rn(v / (1.0f + expf(-v))));
+                float sg = __bfloat162float(__float2bfloat16_rn(dev::silu_f(v)));
                 v = __bfloat162float(__float2bfloat16_rn(sg * u));
             } else if (p.prologue == GemvPrologue::RMSNorm) {
                 float w;

@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
                     if (p.prologue == GemvPrologue::SiLUMul) {
-                        const float sg = __bfloat162float(__float2bfloat16_rn(v[t] / (1.0f + expf(-v[t]))));
+                        const float sg = __bfloat162float(__float2bfloat16_rn(dev::silu_f(v[t])));
                         v[t] = __bfloat162float(__float2bfloat16_rn(sg * u[t]));
                     } else if (p.prologue == GemvPrologue::RMSNorm) {
                         v[t] = __bfloat162float(__float2bfloat16_rn(v[t] * rs * u[t]));
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
                 if (e >= a_cols) continue;
                 float v = av[i];
                 if (p.prologue == GemvPrologue::SiLUMul) {
-                    const float sg = __bfloat162float(__float2bfloat16_rn(v / (1.0f + expf(-v))));
+                    const float sg = __bfloat162float(__float2bfloat16_rn(dev::silu_f(v)));
                     v = __bfloat162float(__float2bfloat16_rn(sg * a2v[i]));
                 } else if (p.prologue == GemvPrologue::RMSNorm) {
                     v = __bfloat162float(__float2bfloat16_rn(v * rs * wv[i]));
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
                     if (e >= a_cols) continue;
                     float x = v[j];
                     if (p.prologue == GemvPrologue::SiLUMul) {
-                        const float sg = __bfloat162float(__float2bfloat16_rn(x / (1.0f + expf(-x))));
+                        const float sg = __bfloat162float(__float2bfloat16_rn(dev::silu_f(x)));
                         x = __bfloat162float(__float2bfloat16_rn(sg * u[j]));
                     } else if (p.prologue == GemvPrologue::RMSNorm) {
                         x = __bfloat162float(__float2bfloat16_rn(x * rs * u[j]));
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
                 v = pa ? __bfloat162float(pa[k * sa]) : elem(p.a, m, k);
                 if (p.prologue == GemvPrologue::SiLUMul) {
                     float u = pa2 ? __bfloat162float(pa2[k * sa2]) : elem(p.a2, m, k);
-                    float sg = __bfloat162float(__float2bfloat16_rn(v / (1.0f + expf(-v))));
+                    float sg = __bfloat162float(__float2bfloat16_rn(dev::silu_f(v)));
                     v = __bfloat162float(__float2bfloat16_rn(sg * u));
                 } else if (p.prologue == GemvPrologue::RMSNorm) {
                     float w;
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(NT, 1) gemv_stream_kernel(const GemvParams* __
                         switch (ins.op) {  // bf16 rounding after every op, as the unfused kernel
                             case EwOp::Add: v = a + b; break;
                             case EwOp::Mul: v = a * b; break;
-                            case EwOp::SiLU: v = a / (1.0f + expf(-a)); break;
+                            case EwOp::SiLU: v = dev::silu_f(a); break;
                             case EwOp::GELU: v = 0.5f * a * (1.0f + erff(a * 0.70710678f)); break;
                             default: v = a; break;
                         }

@@ -121,10 +121,16 @@ struct Tmaps {
 
 // MT = 128-row sub-tiles per CTA (2: a 256 x BN tile whose two M=128 MMAs
 // share each B stage -- half the B traffic per FLOP for prefill-sized M)
+// threads per CTA: 4 warps, or 8 for the 256-row tiles (warps 4-7 join the epilogue, each
+// warp draining half of its TMEM lane quadrant's columns)
+template <int MT>
+constexpr int tc_threads() { return MT == 2 ? 256 : NTHREADS; }
+
 template <int BN, int STAGES, int MT, int EPI>
-__global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams* __restrict__ pp,
-                                                               const __grid_constant__ Tmaps tm) {
+__global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const GemmTcParams* __restrict__ pp,
+                                                                       const __grid_constant__ Tmaps tm) {
     VTC_STAGE_PARAMS(GemmTcParams, pp);
+    constexpr int NHALF = tc_threads<MT>() / NTHREADS;  // column groups per TMEM lane quadrant
     constexpr int TM = BM * MT;
     // output columns per tile: SwiGLU tiles hold gate and up halves of BN / 2 each
     constexpr int ON = EPI == GEMM_EPI_SWIGLU ? BN / 2 : BN;
@@ -368,10 +374,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
         dev::trace_add(p.head, 2, t_main - t_start);  // sum over CTAs: mainloop
         dev::trace_add(p.head, 4, 1);                 // CTA count
     }
+    const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant (warp id mod 4), column group
     for (int t = 0; t < MT; ++t) {
-    const int row = warp * 32 + lane;  // TMEM lane == tile row (of sub-tile t)
+    const int row = quad * 32 + lane;  // TMEM lane == tile row (of sub-tile t)
     const int64_t m = m0 + t * BM + row;
-    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16) + uint32_t(t * BN);
+    const uint32_t trow = tmem + (uint32_t(quad * 32) << 16) + uint32_t(t * BN);
 
     auto tmem_ld16 = [&](int c, float (&v)[16]) {
         uint32_t r[16];
@@ -543,6 +550,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                 s_lo = min(ON, split * gran * 16);
                 s_hi = min(ON, s_lo + gran * 16);
             }
+            if (NHALF > 1) {  // 8 epilogue warps: this warp's half of the columns
+                const int hw = (ON / NHALF + 15) / 16 * 16;
+                s_lo = min(ON, half * hw);
+                s_hi = min(ON, s_lo + hw);
+            }
             const int cpart = ((s_hi - s_lo) / nparts + 15) / 16 * 16;
             const int c_lo = s_lo + part * cpart, c_hi = min(min(ncols, s_hi), c_lo + cpart);
             for (int c = c_lo; c < c_hi; c += 16) {
@@ -596,6 +608,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                 s_lo = min(BN, split * gran * 16);
                 s_hi = min(BN, s_lo + gran * 16);
             }
+            if (NHALF > 1) {  // 8 epilogue warps: this warp's half of the columns
+                const int hw = (BN / NHALF + 15) / 16 * 16;
+                s_lo = min(BN, half * hw);
+                s_hi = min(BN, s_lo + hw);
+            }
             const int cpart = ((s_hi - s_lo) / nparts + 15) / 16 * 16;  // this thread's columns [c_lo, c_hi)
             const int c_lo = s_lo + part * cpart, c_hi = min(min(ncols, s_hi), c_lo + cpart);
             for (int c = c_lo; c < c_hi; c += 16) {
@@ -616,6 +633,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const GemmTcParams
                     const int64_t anchor = T.c_lo + T.c_sh * h;
                     if (anchor < n0 || anchor >= n0 + ON) continue;
                     if (p.splits > 1 && (h % nparts) != part) continue;  // split path: heads over the row's threads
+                    if (NHALF > 1 && (h % NHALF) != half) continue;      // 8 epilogue warps: heads over the halves
                     for (int i0 = 0; i0 < T.hd; i0 += 16) {
                         bf16 in[EW_MAX_IN][16];
 #pragma unroll
@@ -1071,7 +1089,7 @@ template <int BN, int ST, int MT, int EPI>
 void launch_variant(const GemmTcParams* dp, dim3 grid, const Tmaps& tmaps, cudaStream_t s) {
     constexpr size_t sm = smem_bytes<BN, ST, MT>();
     cudaFuncSetAttribute(gemm_tc_kernel<BN, ST, MT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-    launch_k(gemm_tc_kernel<BN, ST, MT, EPI>, grid, dim3(NTHREADS), sm, s, dp, tmaps);
+    launch_k(gemm_tc_kernel<BN, ST, MT, EPI>, grid, dim3(tc_threads<MT>()), sm, s, dp, tmaps);
 }
 
 int sm_count() {

@@ -33,7 +33,7 @@ struct Tuning {
     int gemv_stages = -1, gemv_pre = -1, gemv_l2pf = -1, chain_l2pf = -1, attn_ctas = -1;
     int64_t host_link_max = -1;
     bool no_ew_fast, no_ew_aff, no_tc_epi, no_tc_hfuse, no_skinny, no_skinny_norm, no_epi_fusion, debug_fusion,
-        no_tc_trees, no_row_fast, no_gemm_pair, gemm_cta_pair, no_coop_reduce, no_fmha, no_attn_window, separate_combine, attn_l2pf, chain, trace,
+        no_tc_trees, no_row_fast, gemm_pair, gemm_cta_pair, no_coop_reduce, no_fmha, no_attn_window, separate_combine, attn_l2pf, chain, trace,
         host_dma;
     static bool set(const char* k) { return std::getenv(k) != nullptr; }
     static bool on(const char* k) {
@@ -61,7 +61,7 @@ struct Tuning {
         t.debug_fusion = set("VTC_DEBUG_FUSION");
         t.no_tc_trees = set("VTC_NO_TC_TREES");
         t.no_row_fast = set("VTC_NO_ROW_FAST");
-        t.no_gemm_pair = set("VTC_NO_GEMM_PAIR");
+        t.gemm_pair = on("VTC_GEMM_PAIR");
         t.gemm_cta_pair = on("VTC_GEMM_CTA_PAIR");
         t.no_coop_reduce = set("VTC_NO_COOP_REDUCE");
         t.no_fmha = set("VTC_NO_FMHA");
@@ -2324,11 +2324,11 @@ void Executor::prepare(bool dry) {
                     if (ok) {
                         // prefill-sized M: 256-row tiles (two M=128 MMAs per B stage)
                         p.mt = (!p.a_gather && p.bn == 256 && M >= 4096) ? 2 : 1;
-                        // K <= 4096 without a SwiGLU epilogue: 128 x 256 tiles, two CTAs per SM, so one
-                        // CTA's epilogue overlaps the other's mainloop (C5 QKV 1585 -> 1519 us, O-proj
-                        // 1219 -> 1086 us; SwiGLU and K = 14336 measured slower).  VTC_NO_GEMM_PAIR=1: off
-                        if (p.mt == 2 && K <= 4096 && (p.epi == GEMM_EPI_PLAIN || p.epi == GEMM_EPI_TREES) &&
-                            !tun.no_gemm_pair) {
+                        // opt-in (VTC_GEMM_PAIR=1): 128 x 256 tiles, two CTAs per SM, so one CTA's epilogue
+                        // overlaps the other's mainloop.  It won while the 256-row tiles drained TMEM with 4
+                        // warps (C5 QKV 1585 -> 1519 us); with 8 epilogue warps the 256-row tiles are faster
+                        // again (QKV 2053 vs 2115 us, O-proj 1060 vs 1118 us on one box)
+                        if (p.mt == 2 && K <= 4096 && (p.epi == GEMM_EPI_PLAIN || p.epi == GEMM_EPI_TREES) && tun.gemm_pair) {
                             p.mt = 1;
                             p.pair = 1;
                         }

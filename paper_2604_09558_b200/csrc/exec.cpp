@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <unordered_map>
 #include <functional>
 #include <set>
 
@@ -991,7 +992,8 @@ void Executor::prepare(bool dry) {
         const OpNode* silu = nullptr;
         const OpNode* mul = nullptr;
         const OpNode* add = nullptr;
-        const OpNode* view = nullptr;  // tensor-core residual: an eliminated Reshape between MatMul and Add
+        const OpNode* view = nullptr;  // tensor-core residual: the last eliminated view between MatMul and Add
+        bool perm = false;             // ... a row-permuting chain: output / residual rows host-resolved
     };
     std::map<std::string, GemvFusion> fusion;
     std::map<std::string, const OpNode*> hfuse;  // first MatMul -> its horizontally fused sibling
@@ -1110,22 +1112,39 @@ void Executor::prepare(bool dry) {
                 const std::string& other = ad->inputs[0] == n.outputs[0] ? ad->inputs[1] : ad->inputs[0];
                 const OpNode* po = g_.producer(other);
                 if (!po || topo_pos[po->id] < topo_pos[n.id]) f.add = ad;
-            } else if (tc && !tun.no_tc_epi && !cs.empty() && only_consumer(n.outputs[0], cs[0]->id) &&
-                       cs[0]->kind == OpKind::Reshape &&
-                       elim.count(cs[0]->id) &&
-                       g_.tensor(cs[0]->outputs[0]).shape.back() == g_.tensor(n.outputs[0]).shape.back()) {
-                // MatMul -> (virtual) Reshape keeping the last axis -> Add: the residual is
-                // fused through [M, N] views of the Add's operands (Swin's MLP reshape)
-                const std::string& ro = cs[0]->outputs[0];
-                auto cs2 = g_.consumers(ro);
-                if (!cs2.empty() && only_consumer(ro, cs2[0]->id) && cs2[0]->kind == OpKind::Add &&
-                    cs2[0]->inputs[0] != cs2[0]->inputs[1]) {
+            } else if (tc && !tun.no_tc_epi && !cs.empty()) {
+                // MatMul -> virtual data-movement chain -> Add.  One Reshape keeping the last axis
+                // (Swin's MLP reshape): the residual is fused through [M, N] views of the Add's
+                // operands.  A longer chain that permutes whole rows (Swin's window reverse + roll
+                // after proj): the persistent shallow-K GEMM stores each product row at its
+                // host-resolved output row and reads the residual row there (f.perm)
+                std::string t = n.outputs[0];
+                const OpNode* last = nullptr;
+                int len = 0;
+                for (;;) {
+                    auto c = g_.consumers(t);
+                    if (c.empty() || !only_consumer(t, c[0]->id) || !is_data_movement(*c[0]) || !elim.count(c[0]->id) ||
+                        c[0]->outputs.size() != 1)
+                        break;
+                    last = c[0];
+                    t = c[0]->outputs[0];
+                    ++len;
+                }
+                auto cs2 = last ? g_.consumers(t) : std::vector<const OpNode*>{};
+                if (last && !cs2.empty() && only_consumer(t, cs2[0]->id) && cs2[0]->kind == OpKind::Add &&
+                    cs2[0]->inputs[0] != cs2[0]->inputs[1] && g_.tensor(t).shape.back() == g_.tensor(n.outputs[0]).shape.back()) {
                     const OpNode* ad = cs2[0];
-                    const std::string& other = ad->inputs[0] == ro ? ad->inputs[1] : ad->inputs[0];
+                    const std::string& other = ad->inputs[0] == t ? ad->inputs[1] : ad->inputs[0];
                     const OpNode* po = g_.producer(other);
-                    if (!po || topo_pos[po->id] < topo_pos[n.id]) {
+                    const bool reshape1 = len == 1 && last->kind == OpKind::Reshape;
+                    const Index& as = g_.tensor(n.inputs[0]).shape;
+                    const int64_t N = g_.tensor(n.inputs[1]).shape[1];
+                    const bool skinny_shape = !tun.no_skinny && as[0] >= 8192 && as[1] <= 512 && N <= 1024 && as[1] % 16 == 0 &&
+                                              N % 16 == 0;
+                    if ((!po || topo_pos[po->id] < topo_pos[n.id]) && (reshape1 || skinny_shape)) {
                         f.add = ad;
-                        f.view = cs[0];
+                        f.view = last;
+                        f.perm = !reshape1;
                     }
                 }
             }
@@ -2052,11 +2071,79 @@ void Executor::prepare(bool dry) {
                             table = d;
                             return true;
                         };
-                        sk = sk && rows_of(mn(cout), N, q.c_base, q.c_ld, q.c_rows, "H2D(skinny c_rows)");
-                        if (sk && f.add) {
+                        if (sk && f.perm) {
+                            // residual behind a row-permuting view chain: product row m goes to the Add's
+                            // output row r with pu[r, :] = C[m, :], and reads the residual row r there
                             const std::string& other = f.add->inputs[0] == f_in ? f.add->inputs[1] : f.add->inputs[0];
                             q.has_res = 1;
-                            sk = rows_of(mn(other), N, q.r_base, q.r_ld, q.r_rows, "H2D(skinny r_rows)");
+                            if (!impl_->dry) {
+                                const int64_t R = volume(g_.tensor(cout).shape) / N;
+                                auto rowview = [&](const std::string& t) {
+                                    return lower_map(VMap::affine(Index{R, N}, Index{N, 1}, 0, t)
+                                                         .compose([&](const std::string& x) -> const VMap* {
+                                                             return map_of(x).is_identity_of(x) ? nullptr : &map_of(x);
+                                                         }),
+                                                     target);
+                                };
+                                const vtc_map pv = rowview(f_in), yv = rowview(cout), xv = rowview(other);
+                                // product row m and view row r meet where both land in the same root
+                                // element (either side may be the virtual one)
+                                const vtc_map cv = lower_map(map_of(n.outputs[0]), target);
+                                std::vector<uint64_t> ct(static_cast<size_t>(M), 0), rt(static_cast<size_t>(M), 0);
+                                auto row_key = [&](const vtc_map& mp, int64_t row, uint64_t& key) {
+                                    int64_t ix[VTC_MAX_RANK] = {};
+                                    ix[0] = row;
+                                    int pa = -1, pb = -1;
+                                    const int64_t a = desc_eval(mp, ix, &pa);
+                                    ix[1] = N - 1;
+                                    const int64_t b = desc_eval(mp, ix, &pb);
+                                    if (pa < 0 || pb != pa || b != a + N - 1 || a < 0 || a >= (int64_t(1) << 47)) return false;
+                                    key = (uint64_t(mp.piece[pa].target) << 48) | uint64_t(a);
+                                    return true;
+                                };
+                                std::unordered_map<uint64_t, int64_t> view_row;
+                                view_row.reserve(size_t(R) * 2);
+                                for (int64_t r = 0; r < R && sk; ++r) {
+                                    uint64_t key = 0;
+                                    sk = row_key(pv, r, key) && view_row.emplace(key, r).second;
+                                }
+                                std::vector<char> used(static_cast<size_t>(R), 0);
+                                int64_t idx[VTC_MAX_RANK] = {};
+                                for (int64_t m = 0; m < M && sk; ++m) {
+                                    uint64_t key = 0;
+                                    sk = row_key(cv, m, key);
+                                    auto it = sk ? view_row.find(key) : view_row.end();
+                                    sk = sk && it != view_row.end() && !used[size_t(it->second)];
+                                    if (!sk) break;
+                                    const int64_t r = it->second;
+                                    used[size_t(r)] = 1;
+                                    idx[0] = r;
+                                    idx[1] = 0;
+                                    int py = -1, px = -1;
+                                    const int64_t oy = desc_eval(yv, idx, &py), ox = desc_eval(xv, idx, &px);
+                                    sk = py >= 0 && px >= 0;
+                                    if (!sk) break;
+                                    ct[size_t(m)] = yv.piece[py].ptr + uint64_t(oy) * es;
+                                    rt[size_t(m)] = xv.piece[px].ptr + uint64_t(ox) * es;
+                                    sk = ct[size_t(m)] % 16 == 0 && rt[size_t(m)] % 16 == 0;
+                                }
+                                for (int64_t m = 0; m < M && sk; ++m) sk = ct[size_t(m)] != 0;  // a permutation
+                                if (sk) {
+                                    auto* dc = static_cast<uint64_t*>(impl_->alloc(size_t(M) * 8, false));
+                                    auto* dr = static_cast<uint64_t*>(impl_->alloc(size_t(M) * 8, false));
+                                    ck(cudaMemcpy(dc, ct.data(), size_t(M) * 8, cudaMemcpyHostToDevice), "H2D(skinny perm rows)");
+                                    ck(cudaMemcpy(dr, rt.data(), size_t(M) * 8, cudaMemcpyHostToDevice), "H2D(skinny perm rows)");
+                                    q.c_rows = dc;
+                                    q.r_rows = dr;
+                                }
+                            }
+                        } else {
+                            sk = sk && rows_of(mn(cout), N, q.c_base, q.c_ld, q.c_rows, "H2D(skinny c_rows)");
+                            if (sk && f.add) {
+                                const std::string& other = f.add->inputs[0] == f_in ? f.add->inputs[1] : f.add->inputs[0];
+                                q.has_res = 1;
+                                sk = rows_of(mn(other), N, q.r_base, q.r_ld, q.r_rows, "H2D(skinny r_rows)");
+                            }
                         }
                         auto sn = skinny_norm.find(n.id);
                         if (sk && sn != skinny_norm.end()) {
@@ -2131,8 +2218,8 @@ void Executor::prepare(bool dry) {
                                 q.a_rows = at;
                             }
                         }
-                        if (!sk && sn != skinny_norm.end())
-                            throw UnsupportedError("gemm_skinny: " + n.id + " with a fused norm is not launchable");
+                        if (!sk && (sn != skinny_norm.end() || f.perm))
+                            throw UnsupportedError("gemm_skinny: " + n.id + " with a fused norm / permuted residual is not launchable");
                         if (sk) {
                             S->node = (sn != skinny_norm.end() ? sn->second->id + "+" : std::string()) + T->node +
                                       (f.add ? "+" + f.add->id : "") + (gl != tc_gelu.end() ? "+" + gl->second->id : "");

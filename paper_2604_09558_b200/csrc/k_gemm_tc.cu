@@ -634,7 +634,24 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
                     if (anchor < n0 || anchor >= n0 + ON) continue;
                     if (p.splits > 1 && (h % nparts) != part) continue;  // split path: heads over the row's threads
                     if (NHALF > 1 && (h % NHALF) != half) continue;      // 8 epilogue warps: heads over the halves
+                    // external operands (the cos / sin rows) of step i0 + 16 are requested while
+                    // step i0 computes: their L2 latency hides behind the TMEM loads and math
+                    uint4 ext[EW_MAX_IN][2], nxt[EW_MAX_IN][2];
+                    auto ext_load = [&](int i0n, uint4 (&buf)[EW_MAX_IN][2]) {
+#pragma unroll
+                        for (int k = 0; k < EW_MAX_IN; ++k) {
+                            if (k >= T.nin) break;
+                            const GemmTreeOp& op = T.op[1 + k];
+                            if (op.from_c || !live || i0n >= T.hd) continue;
+                            const int q = i0n >= op.split ? 1 : 0;
+                            const bf16* src = reinterpret_cast<const bf16*>(op.base[q]) + op.rs[q] * em + op.sh[q] * h + i0n;
+                            buf[k][0] = __ldg(reinterpret_cast<const uint4*>(src));
+                            buf[k][1] = __ldg(reinterpret_cast<const uint4*>(src + 8));
+                        }
+                    };
+                    ext_load(0, ext);
                     for (int i0 = 0; i0 < T.hd; i0 += 16) {
+                        ext_load(i0 + 16, nxt);
                         bf16 in[EW_MAX_IN][16];
 #pragma unroll
                         for (int k = 0; k < EW_MAX_IN; ++k) {
@@ -646,12 +663,16 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
                                     get16(int(op.ccol[q] + op.sh[q] * h + i0 - n0), v);
 #pragma unroll
                                     for (int j = 0; j < 16; ++j) in[k][j] = __float2bfloat16_rn(v[j]);
-                                } else if (live) {
-                                    const bf16* src = reinterpret_cast<const bf16*>(op.base[q]) + op.rs[q] * em + op.sh[q] * h + i0;
-                                    *reinterpret_cast<uint4*>(&in[k][0]) = __ldg(reinterpret_cast<const uint4*>(src));
-                                    *reinterpret_cast<uint4*>(&in[k][8]) = __ldg(reinterpret_cast<const uint4*>(src + 8));
+                                } else {
+                                    *reinterpret_cast<uint4*>(&in[k][0]) = ext[k][0];
+                                    *reinterpret_cast<uint4*>(&in[k][8]) = ext[k][1];
                                 }
                             }
+                        }
+#pragma unroll
+                        for (int k = 0; k < EW_MAX_IN; ++k) {
+                            ext[k][0] = nxt[k][0];
+                            ext[k][1] = nxt[k][1];
                         }
                         if (!live) continue;
                         bf16 o[16];

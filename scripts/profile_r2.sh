@@ -24,10 +24,10 @@ unset VTC_NO_PDL
 # sanitizers on the cross-CTA protocols: split-K counters (tcgen05 GEMM), strip flags (streamed
 # GEMV), the cooperative split-KV combine, the skinny GEMM's rings, the window attention
 timeout 1800 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu.py -q -x \
-   -k "llama_layer_small or gate_up or batch64 or fused_epilogues" > gpurun_out/r2_san_memcheck.log 2>&1; echo memcheck=$?
+   -k "llama_layer_small or gate_up or batch64 or fused_epilogues or skinny or window" > gpurun_out/r2_san_memcheck.log 2>&1; echo memcheck=$?
 tail -5 gpurun_out/r2_san_memcheck.log
 timeout 1800 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu.py -q -x \
-   -k "llama_layer_small" > gpurun_out/r2_san_racecheck.log 2>&1; echo racecheck=$?
+   -k "llama_layer_small or swin_window" > gpurun_out/r2_san_racecheck.log 2>&1; echo racecheck=$?
 tail -5 gpurun_out/r2_san_racecheck.log
 timeout 1800 compute-sanitizer --tool synccheck --print-limit 20 python -m pytest tests/test_gpu.py -q -x \
    -k "llama_layer_small or swin_block_small" > gpurun_out/r2_san_synccheck.log 2>&1; echo synccheck=$?

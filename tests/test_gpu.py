@@ -643,3 +643,65 @@ def test_prefill_gemms_cta_pair_match_fp64(vtc, oracle, monkeypatch, pair):
     rows = np.r_[0:64, 2040:2056, 4032:4096]  # first / middle / last rows: the oracle on a row sample
     want = oracle.bf16_to_f32(oracle.execute(doc, x)["y"])
     assert _relerr(got[rows], want[rows]) < 2e-2
+
+
+def _mm_graph(M, K, N, act=None, residual=False, swiglu=False):
+    from paper_2604_09558_b200.workloads import GraphBuilder
+    g = GraphBuilder("bf16")
+    g.input("a", [M, K])
+    g.input("w", [K, N])
+    if swiglu:
+        g.input("w2", [K, N])
+        g.node("mg", "MatMul", ["a", "w"], "gt")
+        g.node("mu", "MatMul", ["a", "w2"], "up")
+        g.node("s", "SiLU", ["gt"], "sg")
+        g.node("m", "Mul", ["sg", "up"], "y", out_kind="output")
+        return g.doc()
+    g.node("mm", "MatMul", ["a", "w"], "c")
+    last = "c"
+    if act:
+        g.node("act", act, ["c"], "h")
+        last = "h"
+    if residual:
+        g.input("r", [M, N])
+        g.node("add", "Add", ["r", last], "y", out_kind="output")
+    else:
+        g.node("id", "Reshape", [last], "y", {"shape": [M, N]}, out_kind="output")
+    return g.doc()
+
+
+@pytest.mark.parametrize("shape", [(10000, 96, 288, "GELU", False), (9000, 384, 96, None, True), (8200, 64, 1024, None, False)])
+def test_skinny_gemm_ragged_shapes_bit_identical(vtc, oracle, monkeypatch, shape):
+    """The persistent shallow-K GEMM at ragged M (a partial last 128-row tile), N cut into
+    several units (288 = 2 x 144, 1024 = 4 x 256), K = 64 / 96 / 384, GELU and residual
+    epilogues: the same bits as the tile GEMM."""
+    M, K, N, act, res = shape
+    doc = _mm_graph(M, K, N, act=act, residual=res)
+    x = oracle.random_inputs(doc, seed=11, scales={"w": 1.0 / np.sqrt(K)})
+    g = vtc.parse_graph(doc)
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert "gemm_skinny_bf16" in [l["kernel"] for l in p.info(dry=True)["launches"]]
+    got = vtc.execute(g, p, x)["y"]
+    monkeypatch.setenv("VTC_NO_SKINNY", "1")
+    ref = vtc.execute(g, vtc.Plan(g, vtc.MAX_ELIMINATION), x)["y"]
+    assert np.array_equal(got, ref), _relerr(oracle.bf16_to_f32(got), oracle.bf16_to_f32(ref))
+    want = oracle.bf16_to_f32(oracle.execute(doc, x)["y"])
+    assert _relerr(oracle.bf16_to_f32(got), want) < 2e-2
+
+
+@pytest.mark.parametrize("M", [48, 300, 4096])
+def test_swiglu_epilogue_ragged_n_bit_identical(vtc, oracle, monkeypatch, M):
+    """SwiGLU epilogue with N = 1000 (a partial last 128-column tile): decode-sized M
+    (K split, cooperative reduction), a mid M and a prefill M (256-row tiles, 8
+    epilogue warps) give the same bits as the unfused launches."""
+    K, N = 512, 1000
+    doc = _mm_graph(M, K, N, swiglu=True)
+    x = oracle.random_inputs(doc, seed=12, scales={"w": 1.0 / np.sqrt(K), "w2": 1.0 / np.sqrt(K)})
+    g = vtc.parse_graph(doc)
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert any(l["node"].endswith("+s+m") for l in p.info(dry=True)["launches"]), p.info(dry=True)["launches"]
+    got = vtc.execute(g, p, x)["y"]
+    monkeypatch.setenv("VTC_NO_TC_EPI", "1")
+    monkeypatch.setenv("VTC_NO_TC_HFUSE", "1")
+    ref = vtc.execute(g, vtc.Plan(g, vtc.MAX_ELIMINATION), x)["y"]
+    assert np.array_equal(got, ref), _relerr(oracle.bf16_to_f32(got), oracle.bf16_to_f32(ref))

@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(NT, D <= 32 ? 4 : 2) attn_prefill_kernel(const
 // bias rows are base + position * stride inside an item (host-proved), the
 // bases located through the maps once per item.
 template <int D>
-constexpr int window_warps() { return D <= 32 ? 16 : 8; }  // K / V tiles of every warp: 128 KB
+constexpr int window_warps() { return D <= 32 ? 12 : 8; }  // K / V tiles of every warp: 96-128 KB
 template <int D>
 __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(const AttnParams* __restrict__ pp) {
     constexpr int WW = window_warps<D>();
@@ -322,17 +322,23 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t kt = smem_u32(smem) + uint32_t(warp) * 2 * TILEB, vt = kt + TILEB;
     const int r = p.rank, ax_h = r - 3, ax_s = r - 2, ax_d = r - 1;
-    const int Sq = p.Sq, Sk = p.Sk;
-    const uint32_t nitems = uint32_t(p.Bt) * uint32_t(p.H);
+    // the parameter fields the loop uses, in registers: the staged block lives in shared
+    // memory, and every asm with a memory clobber (cp.async, ldmatrix) would force a reload
+    const int Sq = p.Sq, Sk = p.Sk, H = p.H;
+    const int64_t k_ss = p.k_sstride, v_ss = p.v_sstride, q_ss = p.q_sstride, o_ss = p.o_sstride;
+    const int64_t b_ss = p.b_sstride, b_ks = p.b_kstride;
+    const bool has_bias = p.has_bias != 0, causal = p.causal != 0;
+    const uint64_t* __restrict__ item_base = p.item_base;
+    const uint32_t nitems = uint32_t(p.Bt) * uint32_t(H);
     const float qscale = p.scale * LOG2E;
     dev::pdl_wait();
     dev::pdl_launch_dependents();
     for (uint32_t item = blockIdx.x * WW + warp; item < nitems; item += gridDim.x * WW) {
         int32_t idx[VTC_MAX_RANK] = {};
-        if (!p.item_base) {
+        if (!item_base) {
             uint32_t bh = item;
-            const uint32_t bq = bh / uint32_t(p.H);
-            const int h = int(bh - bq * uint32_t(p.H));
+            const uint32_t bq = bh / uint32_t(H);
+            const int h = int(bh - bq * uint32_t(H));
             bh = bq;
             for (int a = r - 4; a >= 0; --a) {
                 const uint32_t ext = uint32_t(p.q.m.shape[a]), nb = bh / ext;
@@ -345,8 +351,8 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
         }
         // item bases: the host-resolved table, else lanes 0..4 locate one map each
         uint64_t mine = 0;
-        if (p.item_base) {
-            if (lane < 5) mine = p.item_base[uint64_t(item) * 5 + lane];
+        if (item_base) {
+            if (lane < 5) mine = item_base[uint64_t(item) * 5 + lane];
         } else if (lane == 0) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.q.m, idx));
         else if (lane == 1) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.k.m, idx));
         else if (lane == 2) mine = reinterpret_cast<uint64_t>(dev::elem_ptr<bf16>(p.v.m, idx));
@@ -364,8 +370,8 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
             const int c = lane + 32 * i, row = c / CPR, ch = c % CPR;
             const bool ok = row < Sk;
             const int rr = ok ? row : 0;
-            cp_async16(kt + swz<D>(row, ch), kb + int64_t(rr) * p.k_sstride + ch * 8, ok);
-            cp_async16(vt + swz<D>(row, ch), vb + int64_t(rr) * p.v_sstride + ch * 8, ok);
+            cp_async16(kt + swz<D>(row, ch), kb + int64_t(rr) * k_ss + ch * 8, ok);
+            cp_async16(vt + swz<D>(row, ch), vb + int64_t(rr) * v_ss + ch * 8, ok);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         const int kc = (lane % 4) * 2;
@@ -376,23 +382,23 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
 #pragma unroll
             for (int ks = 0; ks < D / 16; ++ks) {
                 const int d0 = ks * 16 + kc;
-                qa[ks][0] = rA < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rA) * p.q_sstride + d0) : 0u;
-                qa[ks][1] = rB < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rB) * p.q_sstride + d0) : 0u;
-                qa[ks][2] = rA < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rA) * p.q_sstride + d0 + 8) : 0u;
-                qa[ks][3] = rB < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rB) * p.q_sstride + d0 + 8) : 0u;
+                qa[ks][0] = rA < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rA) * q_ss + d0) : 0u;
+                qa[ks][1] = rB < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rB) * q_ss + d0) : 0u;
+                qa[ks][2] = rA < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rA) * q_ss + d0 + 8) : 0u;
+                qa[ks][3] = rB < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rB) * q_ss + d0 + 8) : 0u;
             }
             const bf16 zero = __float2bfloat16_rn(0.f);
-            const bf16* rowA = bb + int64_t(rA) * p.b_sstride;
-            const bf16* rowB = bb + int64_t(rB) * p.b_sstride;
-            const int64_t ks_ = p.b_kstride;
+            const bf16* rowA = bb + int64_t(rA) * b_ss;
+            const bf16* rowB = bb + int64_t(rB) * b_ss;
+            const int64_t ks_ = b_ks;
 #pragma unroll
             for (int nt = 0; nt < TK / 8; ++nt)
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const int t = nt * 8 + kc + c;
                     const int64_t off = ks_ == 1 ? int64_t(t) : int64_t(t) * ks_;
-                    bA[nt][c] = (p.has_bias && t < Sk && rA < Sq) ? rowA[off] : zero;
-                    bB[nt][c] = (p.has_bias && t < Sk && rB < Sq) ? rowB[off] : zero;
+                    bA[nt][c] = (has_bias && t < Sk && rA < Sq) ? rowA[off] : zero;
+                    bB[nt][c] = (has_bias && t < Sk && rB < Sq) ? rowB[off] : zero;
                 }
         };
         uint32_t qcur[D / 16][4];
@@ -432,8 +438,8 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
                     mma_bf16(sc[nt], qa[2 * kp + 1], b2, b3);
                 }
             }
-            const int limA = p.causal ? rA + (Sk - Sq) : INT32_MAX;
-            const int limB = p.causal ? rB + (Sk - Sq) : INT32_MAX;
+            const int limA = causal ? rA + (Sk - Sq) : INT32_MAX;
+            const int limB = causal ? rB + (Sk - Sq) : INT32_MAX;
             float mA = -INFINITY, mB = -INFINITY;
 #pragma unroll
             for (int nt = 0; nt < TK / 8; ++nt)
@@ -491,8 +497,8 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
 #pragma unroll
             for (int i = 0; i < D / 8; ++i) {
                 const int d = i * 8 + kc;
-                if (rA < Sq) *reinterpret_cast<uint32_t*>(ob + int64_t(rA) * p.o_sstride + d) = pack_bf16(o[i][0] * iA, o[i][1] * iA);
-                if (rB < Sq) *reinterpret_cast<uint32_t*>(ob + int64_t(rB) * p.o_sstride + d) = pack_bf16(o[i][2] * iB, o[i][3] * iB);
+                if (rA < Sq) *reinterpret_cast<uint32_t*>(ob + int64_t(rA) * o_ss + d) = pack_bf16(o[i][0] * iA, o[i][1] * iA);
+                if (rB < Sq) *reinterpret_cast<uint32_t*>(ob + int64_t(rB) * o_ss + d) = pack_bf16(o[i][2] * iB, o[i][3] * iB);
             }
         }
         __syncwarp();  // this warp's K / V tiles are refilled by its next item

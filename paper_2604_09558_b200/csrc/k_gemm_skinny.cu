@@ -119,22 +119,43 @@ __global__ void __launch_bounds__((2 + NE + (NORM ? NPROD_NORM - 1 : 0)) * 32, 1
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     dev::pdl_launch_dependents();
-    // the weight, transposed into K-major swizzled k-tiles: thread reads 8 consecutive
-    // columns of one weight row (16 bytes) and scatters them to 8 B rows
+    // the weight, transposed into K-major swizzled k-tiles: an item is a pair of weight rows
+    // (k, k + 1) x 8 columns (two 16-byte loads) stored as 8 (k, k + 1) words of B rows
+    // n .. n + 7. Consecutive lanes take consecutive k pairs of one column group, so each
+    // 32-bit store instruction fills one 128-byte B row (no bank conflict); a thread issues
+    // all loads of a batch before its stores (one memory round trip per batch).
     if (!p.b_static) dev::pdl_wait();
     {
-        const int ngrp = (int(p.N) + 7) / 8;
-        const int64_t total = int64_t(KT) * BK * ngrp;
-        for (int64_t i = threadIdx.x; i < total; i += NTHREADS) {
-            const int k = int(i / ngrp), g = int(i % ngrp);
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (k < p.K) v = __ldg(reinterpret_cast<const uint4*>(static_cast<const bf16*>(p.w) + int64_t(k) * p.ldw + g * 8));
-            const uint16_t* e = reinterpret_cast<const uint16_t*>(&v);
-            const uint32_t tile = smem_u32(sB + size_t(k / BK) * NP * 128);
+        const int ngrp = (int(p.N) + 7) / 8, kpairs = KT * BK / 2;
+        const int total = kpairs * ngrp;
+        constexpr int UB = 4;
+        const bf16* w = static_cast<const bf16*>(p.w);
+        for (int i0 = threadIdx.x; i0 < total; i0 += UB * NTHREADS) {
+            uint4 v[UB][2];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int n = g * 8 + j;
-                if (n < NP) asm volatile("st.shared.u16 [%0], %1;" ::"r"(tile + sw128(n, k % BK)), "h"(e[j]) : "memory");
+            for (int u = 0; u < UB; ++u) {
+                const int i = i0 + u * NTHREADS;
+                const int g = i / kpairs, k = 2 * (i - g * kpairs);
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    v[u][h] = (i < total && k + h < p.K) ? __ldg(reinterpret_cast<const uint4*>(w + int64_t(k + h) * p.ldw + g * 8))
+                                                         : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < UB; ++u) {
+                const int i = i0 + u * NTHREADS;
+                if (i >= total) break;
+                const int g = i / kpairs, k = 2 * (i - g * kpairs);
+                const uint32_t tile = smem_u32(sB + size_t(k / BK) * NP * 128);
+                const uint32_t* e0 = reinterpret_cast<const uint32_t*>(&v[u][0]);
+                const uint32_t* e1 = reinterpret_cast<const uint32_t*>(&v[u][1]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int n = g * 8 + j;
+                    const uint32_t lo = (j & 1) ? (e0[j >> 1] >> 16) : (e0[j >> 1] & 0xffffu);
+                    const uint32_t hi = (j & 1) ? (e1[j >> 1] & 0xffff0000u) : (e1[j >> 1] << 16);
+                    if (n < NP) asm volatile("st.shared.u32 [%0], %1;" ::"r"(tile + sw128(n, k % BK)), "r"(lo | hi));
+                }
             }
         }
     }
@@ -378,13 +399,16 @@ __global__ void __launch_bounds__((2 + NE + (NORM ? NPROD_NORM - 1 : 0)) * 32, 1
                                    "=r"(r[7])
                                  : "r"(taddr + uint32_t(c)));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    bf16 o[8];
+                    uint32_t o[4];
+                    if (p.epi == 1) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const bf16 v = __float2bfloat16_rn(__uint_as_float(r[q]));
-                        o[q] = p.epi == 1 ? dev::gelu_bf16(v) : v;
+                        for (int q = 0; q < 4; ++q) o[q] = dev::gelu2_acc(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(o[q]) : "r"(r[2 * q + 1]), "r"(r[2 * q]));
                     }
-                    *reinterpret_cast<uint4*>(srow + c) = *reinterpret_cast<const uint4*>(o);
+                    *reinterpret_cast<uint4*>(srow + c) = make_uint4(o[0], o[1], o[2], o[3]);
                 }
                 // accumulator drained: the MMA warp may refill it
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -517,12 +517,13 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
                 *reinterpret_cast<uint4*>(&rv[0]) = __ldg(reinterpret_cast<const uint4*>(rrow + c));
                 *reinterpret_cast<uint4*>(&rv[8]) = __ldg(reinterpret_cast<const uint4*>(rrow + c + 8));
             }
+            if (EPI == GEMM_EPI_GELU) {
+#pragma unroll
+                for (int j = 0; j < 16; j += 2) *reinterpret_cast<uint32_t*>(&o[j]) = dev::gelu2_acc(v[j], v[j + 1]);
+            }
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                if (EPI == GEMM_EPI_GELU) {
-                    o[j] = dev::gelu_bf16(__float2bfloat16_rn(v[j]));
-                    continue;
-                }
+                if (EPI == GEMM_EPI_GELU) continue;
                 float f = __bfloat162float(__float2bfloat16_rn(v[j]));
                 if (rvec) f = __bfloat162float(rv[j]) + f;
                 else if (rrow && c + j < ncols) f = __bfloat162float(rrow[int64_t(c + j) * rs]) + f;

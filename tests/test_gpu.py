@@ -706,3 +706,45 @@ def test_swiglu_epilogue_ragged_n_bit_identical(vtc, oracle, monkeypatch, M):
     monkeypatch.setenv("VTC_NO_TC_HFUSE", "1")
     ref = vtc.execute(g, vtc.Plan(g, vtc.MAX_ELIMINATION), x)["y"]
     assert np.array_equal(got, ref), _relerr(oracle.bf16_to_f32(got), oracle.bf16_to_f32(ref))
+
+
+def test_gelu_epilogue_every_bf16_input(vtc, oracle, monkeypatch):
+    """The fused GELU epilogues evaluate erf with packed f32x2 arithmetic (dev::gelu2_acc);
+    fed every finite bf16 value (an identity weight, so the fp32 accumulator holds exactly
+    the input), the persistent shallow-K GEMM and the tile GEMM store the same bits as
+    the separate GELU kernel, which calls erff."""
+    M, K, N = 8192, 64, 64
+    doc = _mm_graph(M, K, N, act="GELU")
+    x = oracle.random_inputs(doc, seed=13)
+    pats = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    pats[(pats & 0x7F80) == 0x7F80] = 0  # inf / NaN would poison the whole row through 0 * inf
+    a = x["a"].copy()
+    a[:1024] = pats.reshape(1024, 64)
+    x["a"] = a
+    x["w"] = oracle.f32_to_bf16(np.eye(K, N, dtype=np.float32))
+    g = vtc.parse_graph(doc)
+    outs = {}
+    for mode, env in (("skinny", {}), ("tile", {"VTC_NO_SKINNY": "1"}), ("unfused", {"VTC_NO_TC_EPI": "1"})):
+        for k in ("VTC_NO_SKINNY", "VTC_NO_TC_EPI"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+        kern = [l["kernel"] for l in p.info(dry=True)["launches"]]
+        if mode == "skinny":
+            assert kern == ["gemm_skinny_bf16"], kern
+        elif mode == "tile":
+            assert len(kern) == 1 and kern[0] != "gemm_skinny_bf16", kern
+        else:
+            assert len(kern) == 2, kern
+        outs[mode] = vtc.execute(g, p, x)["y"]
+    assert np.array_equal(outs["skinny"], outs["unfused"])
+    assert np.array_equal(outs["tile"], outs["unfused"])
+    # and the unfused GELU itself against the numpy erf on the same bf16 inputs
+    xf = oracle.bf16_to_f32(pats.reshape(1024, 64))
+    from math import erf
+    ref = np.array([0.5 * v * (1.0 + erf(v * 0.70710678)) for v in xf.astype(np.float64).ravel()]).reshape(1024, 64)
+    ref = oracle.bf16_to_f32(oracle.f32_to_bf16(ref.astype(np.float32)))
+    diff = np.abs(oracle.bf16_to_f32(outs["unfused"][:1024]) - ref)
+    # 1 + erf(x / sqrt 2) cancels in fp32 below x ~ -4.5 (|GELU| < 1e-5 there): an absolute floor
+    assert np.all(diff <= 1e-2 * np.abs(ref) + 1e-7), diff.max()

@@ -31,6 +31,12 @@ constexpr float LOG2E = 1.4426950408889634f;
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// 32-bit global load (data the kernel never writes; no memory clobber, so loads batch)
+__device__ __forceinline__ uint32_t ld_g32(const void* p) {
+    uint32_t v;
+    asm("ld.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
 }
@@ -378,28 +384,49 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
         // Q fragments and additive bias of one 16-row m-tile (rows rA / rB of this thread),
         // fetched one m-tile ahead so their L2 latency overlaps the previous tile's math
         auto fetch = [&](int q0, uint32_t (&qa)[D / 16][4], bf16 (&bA)[TK / 8][2], bf16 (&bB)[TK / 8][2]) {
+            // rows past Sq read row 0 (finite values; those rows are never stored)
             const int rA = q0 + lane / 4, rB = rA + 8;
+            const int ra = rA < Sq ? rA : 0, rb = rB < Sq ? rB : 0;
+            const bf16* qA = qb + int64_t(ra) * q_ss + kc;
+            const bf16* qB = qb + int64_t(rb) * q_ss + kc;
 #pragma unroll
             for (int ks = 0; ks < D / 16; ++ks) {
-                const int d0 = ks * 16 + kc;
-                qa[ks][0] = rA < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rA) * q_ss + d0) : 0u;
-                qa[ks][1] = rB < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rB) * q_ss + d0) : 0u;
-                qa[ks][2] = rA < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rA) * q_ss + d0 + 8) : 0u;
-                qa[ks][3] = rB < Sq ? *reinterpret_cast<const uint32_t*>(qb + int64_t(rB) * q_ss + d0 + 8) : 0u;
+                qa[ks][0] = ld_g32(qA + ks * 16);
+                qa[ks][1] = ld_g32(qB + ks * 16);
+                qa[ks][2] = ld_g32(qA + ks * 16 + 8);
+                qa[ks][3] = ld_g32(qB + ks * 16 + 8);
             }
-            const bf16 zero = __float2bfloat16_rn(0.f);
-            const bf16* rowA = bb + int64_t(rA) * b_ss;
-            const bf16* rowB = bb + int64_t(rB) * b_ss;
-            const int64_t ks_ = b_ks;
+            // bias row r at key t: bb + r * b_ss + t (unit key stride). Reading a row's TK keys
+            // runs into the next row (b_ss + Sk >= TK, host-checked), so every row but the
+            // block's last loads unguarded at immediate offsets; keys t >= Sk get -inf
+            auto brow = [&](int r, bf16 (&b)[TK / 8][2]) {
+                const unsigned short* rp = reinterpret_cast<const unsigned short*>(bb + int64_t(r) * b_ss + kc);
+                if (!has_bias) {
 #pragma unroll
-            for (int nt = 0; nt < TK / 8; ++nt)
+                    for (int nt = 0; nt < TK / 8; ++nt) b[nt][0] = b[nt][1] = __ushort_as_bfloat16(0);
+                } else if (r < Sq - 1) {
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const int t = nt * 8 + kc + c;
-                    const int64_t off = ks_ == 1 ? int64_t(t) : int64_t(t) * ks_;
-                    bA[nt][c] = (has_bias && t < Sk && rA < Sq) ? rowA[off] : zero;
-                    bB[nt][c] = (has_bias && t < Sk && rB < Sq) ? rowB[off] : zero;
+                    for (int nt = 0; nt < TK / 8; ++nt)
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) b[nt][c] = __ushort_as_bfloat16(__ldg(rp + nt * 8 + c));
+                } else {
+#pragma unroll
+                    for (int nt = 0; nt < TK / 8; ++nt)
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            const int t = nt * 8 + kc + c;
+                            b[nt][c] = __ushort_as_bfloat16(t < Sk ? __ldg(rp + nt * 8 + c) : 0);
+                        }
                 }
+#pragma unroll
+                for (int nt = 0; nt < TK / 8; ++nt)
+                    if (nt * 8 + 8 > Sk)
+#pragma unroll
+                        for (int c = 0; c < 2; ++c)
+                            if (nt * 8 + kc + c >= Sk) b[nt][c] = __ushort_as_bfloat16(0xff80);  // -inf
+            };
+            brow(ra, bA);
+            brow(rb, bB);
         };
         uint32_t qcur[D / 16][4];
         bf16 bAc[TK / 8][2], bBc[TK / 8][2];
@@ -438,27 +465,39 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
                     mma_bf16(sc[nt], qa[2 * kp + 1], b2, b3);
                 }
             }
-            const int limA = causal ? rA + (Sk - Sq) : INT32_MAX;
-            const int limB = causal ? rB + (Sk - Sq) : INT32_MAX;
+            // log2-domain scores; masked keys carry a -inf bias (fetch), causal limits below
             float mA = -INFINITY, mB = -INFINITY;
 #pragma unroll
             for (int nt = 0; nt < TK / 8; ++nt)
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    const int t = nt * 8 + kc + c;
-                    float a = sc[nt][c] * qscale + bA[nt][c] * LOG2E, b = sc[nt][2 + c] * qscale + bB[nt][c] * LOG2E;
-                    if (t >= Sk || t > limA) a = -INFINITY;
-                    if (t >= Sk || t > limB) b = -INFINITY;
-                    sc[nt][c] = a;
-                    sc[nt][2 + c] = b;
-                    mA = fmaxf(mA, a);
-                    mB = fmaxf(mB, b);
+                    sc[nt][c] = fmaf(sc[nt][c], qscale, bA[nt][c] * LOG2E);
+                    sc[nt][2 + c] = fmaf(sc[nt][2 + c], qscale, bB[nt][c] * LOG2E);
                 }
+            if (causal) {
+                const int limA = rA + (Sk - Sq), limB = rB + (Sk - Sq);
+#pragma unroll
+                for (int nt = 0; nt < TK / 8; ++nt)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int t = nt * 8 + kc + c;
+                        if (t > limA) sc[nt][c] = -INFINITY;
+                        if (t > limB) sc[nt][2 + c] = -INFINITY;
+                    }
+            }
+#pragma unroll
+            for (int nt = 0; nt < TK / 8; ++nt) {
+                mA = fmaxf(mA, fmaxf(sc[nt][0], sc[nt][1]));
+                mB = fmaxf(mB, fmaxf(sc[nt][2], sc[nt][3]));
+            }
 #pragma unroll
             for (int off = 1; off < 4; off <<= 1) {
                 mA = fmaxf(mA, __shfl_xor_sync(0xffffffffu, mA, off));
                 mB = fmaxf(mB, __shfl_xor_sync(0xffffffffu, mB, off));
             }
+            // a row whose every key is masked: exp2(-inf - 0) = 0 for all, output 0
+            if (mA == -INFINITY) mA = 0.f;
+            if (mB == -INFINITY) mB = 0.f;
             float lA = 0.f, lB = 0.f;
             uint32_t pa[TK / 16][4];
 #pragma unroll
@@ -466,8 +505,8 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
                 float e[4];
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    e[c] = sc[nt][c] == -INFINITY ? 0.f : exp2f(sc[nt][c] - mA);
-                    e[2 + c] = sc[nt][2 + c] == -INFINITY ? 0.f : exp2f(sc[nt][2 + c] - mB);
+                    e[c] = dev::ex2_ftz(sc[nt][c] - mA);  // ex2(-inf) = +0
+                    e[2 + c] = dev::ex2_ftz(sc[nt][2 + c] - mB);
                     lA += e[c];
                     lB += e[2 + c];
                 }
@@ -527,7 +566,8 @@ void launch_d(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
 
 bool attn_window_supported(const AttnParams& p) {
     return p.dt == KDType::BF16 && p.D == p.Dv && (p.D == 32 || p.D == 64) && p.Sq <= TK && p.Sk <= TK && p.kv_affine &&
-           p.qo_affine && p.k.vec_ok && p.v.vec_ok && (!p.has_bias || p.bias_affine);
+           p.qo_affine && p.k.vec_ok && p.v.vec_ok &&
+           (!p.has_bias || (p.bias_affine && p.b_kstride == 1 && p.b_sstride + p.Sk >= TK));
 }
 
 template <int D>

@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(NT, D <= 32 ? 4 : 2) attn_prefill_kernel(const
 // single pass; persistent warps, no CTA-wide synchronisation.  Q / K / V / O /
 // bias rows are base + position * stride inside an item (host-proved), the
 // bases located through the maps once per item.
+constexpr int WIN_BIAS_ELEMS = 4096;  // per-warp bias staging (8 KB)
 template <int D>
 constexpr int window_warps() { return D <= 32 ? 12 : 8; }  // K / V tiles of every warp: 96-128 KB
 template <int D>
@@ -327,6 +328,8 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t kt = smem_u32(smem) + uint32_t(warp) * 2 * TILEB, vt = kt + TILEB;
+    // the item's bias block, staged by cp.async with K / V (WIN_BIAS_ELEMS per warp)
+    unsigned short* sbias = reinterpret_cast<unsigned short*>(smem + size_t(WW) * 2 * TILEB) + size_t(warp) * WIN_BIAS_ELEMS;
     const int r = p.rank, ax_h = r - 3, ax_s = r - 2, ax_d = r - 1;
     // the parameter fields the loop uses, in registers: the staged block lives in shared
     // memory, and every asm with a memory clobber (cp.async, ldmatrix) would force a reload
@@ -379,11 +382,24 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
             cp_async16(kt + swz<D>(row, ch), kb + int64_t(rr) * k_ss + ch * 8, ok);
             cp_async16(vt + swz<D>(row, ch), vb + int64_t(rr) * v_ss + ch * 8, ok);
         }
+        // the bias block (rows 0 .. Sq - 1, b_ss apart, unit key stride): the 4-byte words of the
+        // span from the element-aligned-down start, plus a lone trailing element; the block then
+        // sits at sbias + par. Reading a row's TK keys past its end stays inside the buffer
+        // (host-checked span + TK <= WIN_BIAS_ELEMS); keys t >= Sk are masked to -inf below.
+        const int par = int((reinterpret_cast<uintptr_t>(bb) >> 1) & 1);
+        if (has_bias) {
+            const int span = (Sq - 1) * int(b_ss) + Sk + par, nw = span / 2;
+            const uint32_t sb = smem_u32(sbias);
+            const char* src = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(bb) & ~uintptr_t(3));
+            for (int w = lane; w < nw; w += 32)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sb + 4u * w), "l"(src + 4 * w) : "memory");
+            if ((span & 1) && lane == 0) sbias[span - 1] = reinterpret_cast<const unsigned short*>(src)[span - 1];
+        }
         asm volatile("cp.async.commit_group;" ::: "memory");
         const int kc = (lane % 4) * 2;
-        // Q fragments and additive bias of one 16-row m-tile (rows rA / rB of this thread),
-        // fetched one m-tile ahead so their L2 latency overlaps the previous tile's math
-        auto fetch = [&](int q0, uint32_t (&qa)[D / 16][4], bf16 (&bA)[TK / 8][2], bf16 (&bB)[TK / 8][2]) {
+        // Q fragments of one 16-row m-tile (rows rA / rB of this thread), fetched one m-tile
+        // ahead so their L2 latency overlaps the previous tile's math
+        auto fetch_q = [&](int q0, uint32_t (&qa)[D / 16][4]) {
             // rows past Sq read row 0 (finite values; those rows are never stored)
             const int rA = q0 + lane / 4, rB = rA + 8;
             const int ra = rA < Sq ? rA : 0, rb = rB < Sq ? rB : 0;
@@ -396,28 +412,17 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
                 qa[ks][2] = ld_g32(qA + ks * 16 + 8);
                 qa[ks][3] = ld_g32(qB + ks * 16 + 8);
             }
-            // bias row r at key t: bb + r * b_ss + t (unit key stride). Reading a row's TK keys
-            // runs into the next row (b_ss + Sk >= TK, host-checked), so every row but the
-            // block's last loads unguarded at immediate offsets; keys t >= Sk get -inf
+        };
+        // additive bias of the m-tile's rows from the staged block
+        auto fetch_b = [&](int q0, bf16 (&bA)[TK / 8][2], bf16 (&bB)[TK / 8][2]) {
+            const int rA = q0 + lane / 4, rB = rA + 8;
+            const int ra = rA < Sq ? rA : 0, rb = rB < Sq ? rB : 0;
             auto brow = [&](int r, bf16 (&b)[TK / 8][2]) {
-                const unsigned short* rp = reinterpret_cast<const unsigned short*>(bb + int64_t(r) * b_ss + kc);
-                if (!has_bias) {
+                const unsigned short* rp = sbias + par + r * int(b_ss) + kc;
 #pragma unroll
-                    for (int nt = 0; nt < TK / 8; ++nt) b[nt][0] = b[nt][1] = __ushort_as_bfloat16(0);
-                } else if (r < Sq - 1) {
+                for (int nt = 0; nt < TK / 8; ++nt)
 #pragma unroll
-                    for (int nt = 0; nt < TK / 8; ++nt)
-#pragma unroll
-                        for (int c = 0; c < 2; ++c) b[nt][c] = __ushort_as_bfloat16(__ldg(rp + nt * 8 + c));
-                } else {
-#pragma unroll
-                    for (int nt = 0; nt < TK / 8; ++nt)
-#pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            const int t = nt * 8 + kc + c;
-                            b[nt][c] = __ushort_as_bfloat16(t < Sk ? __ldg(rp + nt * 8 + c) : 0);
-                        }
-                }
+                    for (int c = 0; c < 2; ++c) b[nt][c] = __ushort_as_bfloat16(has_bias ? rp[nt * 8 + c] : 0);
 #pragma unroll
                 for (int nt = 0; nt < TK / 8; ++nt)
                     if (nt * 8 + 8 > Sk)
@@ -430,7 +435,10 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
         };
         uint32_t qcur[D / 16][4];
         bf16 bAc[TK / 8][2], bBc[TK / 8][2];
-        fetch(0, qcur, bAc, bBc);
+        fetch_q(0, qcur);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        fetch_b(0, bAc, bBc);
         for (int q0 = 0; q0 < Sq; q0 += 16) {
             const int rA = q0 + lane / 4, rB = rA + 8;
             uint32_t qa[D / 16][4];
@@ -446,10 +454,9 @@ __global__ void __launch_bounds__(window_warps<D>() * 32, 1) attn_window_kernel(
                     bA[nt][c] = __bfloat162float(bAc[nt][c]);
                     bB[nt][c] = __bfloat162float(bBc[nt][c]);
                 }
-            if (q0 + 16 < Sq) fetch(q0 + 16, qcur, bAc, bBc);
-            if (q0 == 0) {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-                __syncwarp();
+            if (q0 + 16 < Sq) {
+                fetch_q(q0 + 16, qcur);
+                fetch_b(q0 + 16, bAc, bBc);
             }
             float sc[TK / 8][4];
 #pragma unroll
@@ -567,13 +574,14 @@ void launch_d(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
 bool attn_window_supported(const AttnParams& p) {
     return p.dt == KDType::BF16 && p.D == p.Dv && (p.D == 32 || p.D == 64) && p.Sq <= TK && p.Sk <= TK && p.kv_affine &&
            p.qo_affine && p.k.vec_ok && p.v.vec_ok &&
-           (!p.has_bias || (p.bias_affine && p.b_kstride == 1 && p.b_sstride + p.Sk >= TK));
+           (!p.has_bias || (p.bias_affine && p.b_kstride == 1 && p.b_sstride >= 0 &&
+                            (p.Sq - 1) * p.b_sstride + p.Sk + 2 + TK <= WIN_BIAS_ELEMS));
 }
 
 template <int D>
 void launch_w(const AttnParams& p, const AttnParams* dp, cudaStream_t s) {
     constexpr int WW = window_warps<D>();
-    const size_t smem = size_t(WW) * 2 * TK * D * 2;
+    const size_t smem = size_t(WW) * (2 * TK * D * 2 + WIN_BIAS_ELEMS * 2);
     allow_max_smem(attn_window_kernel<D>);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

@@ -126,6 +126,25 @@ struct Tmaps {
 template <int MT>
 constexpr int tc_threads() { return MT == 2 ? 256 : NTHREADS; }
 
+// The general case of the epilogue's 16-column emit (strided or unaligned output / residual, a
+// partial last column group): out of line, so the common path stays short.
+__device__ __noinline__ void emit_slow(bf16* dst, int64_t cs, const bf16* rrow, int64_t rs, int c, int ncols,
+                                       const float* v, bool gelu) {
+#pragma unroll 1
+    for (int j = 0; j < 16; ++j) {
+        if (c + j >= ncols) break;
+        bf16 o;
+        if (gelu) {
+            o = dev::gelu_bf16(__float2bfloat16_rn(v[j]));
+        } else {
+            float f = __bfloat162float(__float2bfloat16_rn(v[j]));
+            if (rrow) f = __bfloat162float(rrow[int64_t(c + j) * rs]) + f;
+            o = __float2bfloat16_rn(f);
+        }
+        dst[int64_t(j) * cs] = o;
+    }
+}
+
 template <int BN, int STAGES, int MT, int EPI>
 __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const GemmTcParams* __restrict__ pp,
                                                                        const __grid_constant__ Tmaps tm) {
@@ -411,13 +430,15 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
                 for (int j = 0; j < 16; ++j) mine[int64_t(c + j) * BM] = v[j];
             }
         }
-        __threadfence();
+        // release: the barrier orders the CTA's partial stores before thread 0's gpu-scope fence
+        // and arrival (fence cumulativity), so one fence per CTA, not one per thread
         __syncthreads();
         if (p.coop_reduce) {
             // every split reduces its own slice of the tile's columns once all partials are
             // written (the host enables this only when the whole grid is co-resident, so the
             // wait cannot deadlock); the last split out resets the counters for the next replay
             if (threadIdx.x == 0) {
+                __threadfence();
                 atomicAdd(&p.counters[tile], 1u);
                 unsigned v;
                 long long spins = 0;
@@ -428,16 +449,16 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
                     if (++spins > (1ll << 26)) __trap();  // a missing split: fail loudly, never hang
                 }
             }
-            __syncthreads();
-            __threadfence();
+            __syncthreads();  // thread 0's acquire, then the barrier: the CTA reads after every arrival
         } else {
-            if (threadIdx.x == 0) s_last = atomicAdd(&p.counters[tile], 1u) == unsigned(p.splits - 1) ? 1u : 0u;
+            if (threadIdx.x == 0) {
+                __threadfence();
+                s_last = atomicAdd(&p.counters[tile], 1u) == unsigned(p.splits - 1) ? 1u : 0u;
+                __threadfence();  // acquire: the other splits' partials, for the whole CTA (barrier below)
+                if (s_last) p.counters[tile] = 0u;
+            }
             __syncthreads();
             do_epilogue = s_last != 0;
-            if (do_epilogue) {
-                __threadfence();
-                if (threadIdx.x == 0) p.counters[tile] = 0u;
-            }
         }
     }
 
@@ -507,37 +528,37 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
                 tmem_ld16(c, v);
             }
         };
-        // 16 finished columns c..c+15 of this row: round, activation / residual, store through C's map
+        // 16 finished columns c..c+15 of this row: round, activation / residual, store through C's map.
+        // The contiguous aligned case is a short straight line (the epilogue runs once per CTA, so
+        // its code is fetched cold: i-cache misses, not math, bound it); anything else goes to a
+        // shared out-of-line routine.
         auto emit = [&](int c, const float (&v)[16]) {
-            bf16 o[16];
-            // the residual's 16 columns: two 16-byte loads when contiguous and aligned
-            bf16 rv[16];
-            const bool rvec = rrow && rs == 1 && c + 16 <= ncols && (reinterpret_cast<uintptr_t>(rrow + c) & 15) == 0;
-            if (rvec) {
-                *reinterpret_cast<uint4*>(&rv[0]) = __ldg(reinterpret_cast<const uint4*>(rrow + c));
-                *reinterpret_cast<uint4*>(&rv[8]) = __ldg(reinterpret_cast<const uint4*>(rrow + c + 8));
+            bf16* dst = crow + int64_t(c) * cs;
+            const bool fast = cs == 1 && c + 16 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 &&
+                              (!rrow || (rs == 1 && (reinterpret_cast<uintptr_t>(rrow + c) & 15) == 0));
+            if (!fast) {
+                emit_slow(dst, cs, rrow, rs, c, ncols, v, EPI == GEMM_EPI_GELU);
+                return;
             }
+            uint32_t o[8];
             if (EPI == GEMM_EPI_GELU) {
 #pragma unroll
-                for (int j = 0; j < 16; j += 2) *reinterpret_cast<uint32_t*>(&o[j]) = dev::gelu2_acc(v[j], v[j + 1]);
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                if (EPI == GEMM_EPI_GELU) continue;
-                float f = __bfloat162float(__float2bfloat16_rn(v[j]));
-                if (rvec) f = __bfloat162float(rv[j]) + f;
-                else if (rrow && c + j < ncols) f = __bfloat162float(rrow[int64_t(c + j) * rs]) + f;
-                o[j] = __float2bfloat16_rn(f);
-            }
-            bf16* dst = crow + int64_t(c) * cs;
-            if (cs == 1 && c + 16 <= ncols && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-                reinterpret_cast<uint4*>(dst)[0] = *reinterpret_cast<const uint4*>(&o[0]);
-                reinterpret_cast<uint4*>(dst)[1] = *reinterpret_cast<const uint4*>(&o[8]);
+                for (int j = 0; j < 8; ++j) o[j] = dev::gelu2_acc(v[2 * j], v[2 * j + 1]);
             } else {
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (c + j < ncols) dst[int64_t(j) * cs] = o[j];
+                for (int j = 0; j < 8; ++j) o[j] = dev::pack_bf16x2(v[2 * j], v[2 * j + 1]);
+                if (rrow) {  // bf16(bf16(acc) + residual), as the unfused Add rounds
+                    uint32_t rv[8];
+                    *reinterpret_cast<uint4*>(&rv[0]) = __ldg(reinterpret_cast<const uint4*>(rrow + c));
+                    *reinterpret_cast<uint4*>(&rv[4]) = __ldg(reinterpret_cast<const uint4*>(rrow + c + 8));
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        o[j] = dev::pack_bf16x2(__uint_as_float(o[j] << 16) + __uint_as_float(rv[j] << 16),
+                                                __uint_as_float(o[j] & 0xffff0000u) + __uint_as_float(rv[j] & 0xffff0000u));
+                }
             }
+            reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+            reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
         };
         // shallow-K variants (epilogue-bound): 64 accumulator columns per TMEM
         // round trip (4 loads, one wait), indices static so they stay in registers
@@ -628,12 +649,18 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
         if (EPI == GEMM_EPI_TREES) {
             // elementwise trees over views of this tile (e.g. RoPE: x * cos + rotate_half(x) * sin):
             // head h of tree tr reads C columns of this tile only; 16 elements i0..i0+15 per step
+            // split-K: the tile's (head, 16-element step) items are spread over every split's
+            // threads (cooperative reduction) or the row's threads, one item each in turn, so
+            // no split repeats another's work and each thread waits on few partial round trips
+            const bool spread = p.splits > 1;
+            const int nwork = spread ? (p.coop_reduce ? p.splits : 1) * nparts : 1;
+            const int wid = spread ? (p.coop_reduce ? split : 0) * nparts + part : 0;
+            int wk = 0;
             for (int tr = 0; tr < p.ntree; ++tr) {
                 const GemmTree& T = p.tree[tr];
                 for (int h = 0; h < T.nh; ++h) {
                     const int64_t anchor = T.c_lo + T.c_sh * h;
                     if (anchor < n0 || anchor >= n0 + ON) continue;
-                    if (p.splits > 1 && (h % nparts) != part) continue;  // split path: heads over the row's threads
                     if (NHALF > 1 && (h % NHALF) != half) continue;      // 8 epilogue warps: heads over the halves
                     // external operands (the cos / sin rows) of step i0 + 16 are requested while
                     // step i0 computes: their L2 latency hides behind the TMEM loads and math
@@ -650,9 +677,14 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
                             buf[k][1] = __ldg(reinterpret_cast<const uint4*>(src + 8));
                         }
                     };
-                    ext_load(0, ext);
+                    if (!spread) ext_load(0, ext);
                     for (int i0 = 0; i0 < T.hd; i0 += 16) {
-                        ext_load(i0 + 16, nxt);
+                        if (spread) {
+                            if ((wk++) % nwork != wid) continue;
+                            ext_load(i0, ext);
+                        } else {
+                            ext_load(i0 + 16, nxt);
+                        }
                         bf16 in[EW_MAX_IN][16];
 #pragma unroll
                         for (int k = 0; k < EW_MAX_IN; ++k) {
@@ -670,11 +702,12 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
                                 }
                             }
                         }
+                        if (!spread)
 #pragma unroll
-                        for (int k = 0; k < EW_MAX_IN; ++k) {
-                            ext[k][0] = nxt[k][0];
-                            ext[k][1] = nxt[k][1];
-                        }
+                            for (int k = 0; k < EW_MAX_IN; ++k) {
+                                ext[k][0] = nxt[k][0];
+                                ext[k][1] = nxt[k][1];
+                            }
                         if (!live) continue;
                         bf16 o[16];
                         if (T.pat == 3) {  // (in0 * in1) + (in2 * in3): RoPE, in registers

@@ -462,11 +462,27 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
         }
     }
 
+    // a short SwiGLU tile without a K split (decode gate / up: 64 live rows, so only lane quadrants
+    // 0-1 of TMEM hold data): warps 0-1 stage those rows' accumulators in the drained pipeline
+    // buffers, then all four warps share the SiLU * Mul epilogue, columns spread over each row's threads
+    const bool staged = EPI == GEMM_EPI_SWIGLU && MT == 1 && NHALF == 1 && p.splits == 1 && p.M - m0 <= 64;
+    float* sacc = reinterpret_cast<float*>(smem);  // [BN][64] fp32
+    if (staged) {
+        if (warp < 2) {
+            for (int c = 0; c < BN; c += 16) {
+                float v[16];
+                tmem_ld16(c, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sacc[(c + j) * 64 + row] = v[j];
+            }
+        }
+        __syncthreads();
+    }
     if (do_epilogue) {
         // split-K reduction (partials from global, no TMEM): short tiles (decode M)
         // spread each row's columns over several threads so all 128 reduce
         int erow = row, part = 0, nparts = 1;
-        if (p.splits > 1) {
+        if (p.splits > 1 || staged) {
             const int64_t rows_live = p.M - (m0 + int64_t(t) * BM);
             const int rp = rows_live <= 32 ? 32 : rows_live <= 64 ? 64 : 128;
             erow = int(threadIdx.x) % rp;
@@ -524,6 +540,9 @@ __global__ void __launch_bounds__(tc_threads<MT>(), 1) gemm_tc_kernel(const Gemm
 #pragma unroll
                             for (int j = 0; j < 16; ++j) v[j] += tq[q][j];
                 }
+            } else if (staged) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = live ? sacc[(c + j) * 64 + erow] : 0.f;
             } else {
                 tmem_ld16(c, v);
             }

@@ -41,4 +41,4 @@ tr = p.trace().astype(np.int64)
 t0 = tr[:, 0][tr[:, 0] > 0].min()
 for l, row in zip(p.info()["launches"], tr):
     print(f"{l['node'][:40]:40s} {l['kernel']:24s} entry {(row[0]-t0)/1e3:8.2f} exit {(row[1]-t0)/1e3:8.2f} us  acc",
-          [int(x) for x in row[2:8]])
+          [round((int(x) - t0) / 1e3, 2) if x > 10**17 else int(x) for x in row[2:8]])

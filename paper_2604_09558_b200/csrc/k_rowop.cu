@@ -264,8 +264,10 @@ __global__ void __launch_bounds__(256) row_vec_kernel(const RowParams* __restric
     const bf16* xb = reinterpret_cast<const bf16*>(p.x.m.piece[0].ptr) + p.x.m.piece[0].base;
     bf16* yb = reinterpret_cast<bf16*>(p.out.m.piece[0].ptr) + p.out.m.piece[0].base;
     const int64_t nrw = int64_t(gridDim.x) * 64;  // rows per grid step
-    for (int64_t row = int64_t(blockIdx.x) * 64 + threadIdx.x / 4; row < p.rows; row += nrw) {
-        const uint4* xr = reinterpret_cast<const uint4*>(xb + row * D);
+    // a warp's eight rows iterate together (the row reductions shuffle across the whole warp);
+    // rows past the end load the last row and store nothing
+    for (int64_t row = int64_t(blockIdx.x) * 64 + threadIdx.x / 4; row - lane / 4 < p.rows; row += nrw) {
+        const uint4* xr = reinterpret_cast<const uint4*>(xb + (row < p.rows ? row : p.rows - 1) * D);
         float x[U][8];
 #pragma unroll
         for (int u = 0; u < U; ++u) unpack(__ldcs(xr + q + 4 * u), x[u]);
@@ -291,6 +293,7 @@ __global__ void __launch_bounds__(256) row_vec_kernel(const RowParams* __restric
         s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
         s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
         const float r = rsqrtf(s2 / float(D) + p.eps);
+        if (row >= p.rows) continue;
         uint4* yr = reinterpret_cast<uint4*>(yb + row * D);
 #pragma unroll
         for (int u = 0; u < U; ++u) {

@@ -748,3 +748,29 @@ def test_gelu_epilogue_every_bf16_input(vtc, oracle, monkeypatch):
     diff = np.abs(oracle.bf16_to_f32(outs["unfused"][:1024]) - ref)
     # 1 + erf(x / sqrt 2) cancels in fp32 below x ~ -4.5 (|GELU| < 1e-5 there): an absolute floor
     assert np.all(diff <= 1e-2 * np.abs(ref) + 1e-7), diff.max()
+
+
+@pytest.mark.parametrize("rows", [1003, 77])
+def test_vectorised_layernorm_ragged_rows(vtc, oracle, monkeypatch, rows):
+    """The four-lanes-per-row LayerNorm kernel at a row count that leaves a warp's eight
+    rows partly past the end (the warp's rows iterate together: the reductions shuffle
+    across the whole warp): every row written, within one bf16 ulp of the generic row
+    kernel (a warp-wide reduction, another summation order) and close to the oracle."""
+    from paper_2604_09558_b200.workloads import GraphBuilder
+    g0 = GraphBuilder("bf16")
+    g0.input("x", [rows, 96])
+    g0.input("w", [96])
+    g0.input("b", [96])
+    g0.node("ln", "LayerNorm", ["x", "w", "b"], "y", {"eps": 1e-5}, out_kind="output")
+    doc = g0.doc()
+    x = oracle.random_inputs(doc, seed=21)
+    g = vtc.parse_graph(doc)
+    p = vtc.Plan(g, vtc.MAX_ELIMINATION)
+    assert [l["kernel"] for l in p.info(dry=True)["launches"]] == ["rowop"]
+    fast = vtc.execute(g, p, x)["y"]
+    monkeypatch.setenv("VTC_NO_ROW_FAST", "1")
+    generic = vtc.execute(g, vtc.Plan(g, vtc.MAX_ELIMINATION), x)["y"]
+    f, r = oracle.bf16_to_f32(fast), oracle.bf16_to_f32(generic)
+    assert np.all(np.abs(f - r) <= np.abs(r) * 2.0 ** -7 + 1e-6)
+    want = oracle.execute(doc, x)["y"]
+    assert _relerr(f, oracle.bf16_to_f32(want)) < 1e-2

@@ -34,7 +34,7 @@ struct Tuning {
     int gemv_stages = -1, gemv_pre = -1, gemv_l2pf = -1, chain_l2pf = -1, attn_ctas = -1;
     int64_t host_link_max = -1;
     bool no_ew_fast, no_ew_aff, no_tc_epi, no_tc_hfuse, no_skinny, no_skinny_norm, no_epi_fusion, debug_fusion,
-        no_tc_trees, no_row_fast, gemm_pair, gemm_cta_pair, no_coop_reduce, no_fmha, no_attn_window, separate_combine, attn_l2pf, chain, trace,
+        no_tc_trees, no_row_fast, gemm_pair, gemm_cta_pair, no_coop_reduce, no_fmha, no_attn_window, separate_combine, attn_l2pf, chain, trace, tree_coop,
         host_dma;
     static bool set(const char* k) { return std::getenv(k) != nullptr; }
     static bool on(const char* k) {
@@ -61,6 +61,7 @@ struct Tuning {
         t.no_epi_fusion = set("VTC_NO_EPI_FUSION");
         t.debug_fusion = set("VTC_DEBUG_FUSION");
         t.no_tc_trees = set("VTC_NO_TC_TREES");
+        t.tree_coop = set("VTC_TREE_COOP");
         t.no_row_fast = set("VTC_NO_ROW_FAST");
         t.gemm_pair = on("VTC_GEMM_PAIR");
         t.gemm_cta_pair = on("VTC_GEMM_CTA_PAIR");
@@ -220,6 +221,10 @@ void dyn_ops(GemmTcParams& p, DynCtx& c) {
         throw UnsupportedError("dynamic position: host-resolved rows of " + c.node + " address a cache");
     c.operand(p.head, &p, p.c, true);
     if (p.has_res) c.operand(p.head, &p, p.res, false);
+    // fused trees storing into the position's cache row (the roped K row): both piece bases move
+    for (int k = 0; p.epi == GEMM_EPI_TREES && k < p.ntree; ++k)
+        if (p.tree[k].out_dyn)
+            for (int q = 0; q < 2; ++q) c.add(p.head, &p, &p.tree[k].op[0].base[q], 8, p.tree[k].out_dyn);
 }
 void dyn_ops(SkinnyParams& p, DynCtx& c) {
     // every address is host-resolved: none may point into a position-dependent cache
@@ -1447,7 +1452,7 @@ void Executor::prepare(bool dry) {
     // (VTC_NO_TC_TREES=1: off.)  With one CTA per SM the per-row epilogue's table loads
     // serialised (QKV + trees 2.53 ms vs 1.64 + 0.67 ms at C5); with two 128-row CTAs per SM
     // the co-resident CTA's mainloop hides them (1.98 ms vs 1.48 + 0.65 ms)
-    if (opt_.fuse && !tun.no_tc_trees && !tun.no_tc_epi && !impl_->dyn_on) {
+    if (opt_.fuse && !tun.no_tc_trees && !tun.no_tc_epi) {
         const auto gouts = g_.graph_outputs();
         const std::set<std::string> graph_out(gouts.begin(), gouts.end());
         for (const auto& n : g_.nodes()) {
@@ -1457,10 +1462,45 @@ void Executor::prepare(bool dry) {
             const std::string& C = n.outputs[0];
             if (g_.tensor(C).kind != TensorKind::Intermediate) continue;
             const int64_t M = g_.tensor(C).shape[0], N = g_.tensor(C).shape[1];
+            // decode-sized M (fewer tiles than SMs: the GEMM takes K splits): the trees in the
+            // split-K epilogue measured slower than the separate eltwise launch (C3 QKV 58.7 us
+            // last-split, 41.1 us cooperative, vs 25.0 + 7.7 us); VTC_TREE_COOP=1 fuses them anyway
+            if ((M + 127) / 128 * ((N + 255) / 256) < (impl_->dry ? 148 : device_sms()) && !tun.tree_coop) continue;
             int64_t ldc = 0, cc0 = 0;
-            if (!affine2d(map_of(C), ldc, cc0)) continue;
-            const std::string R = map_of(C).pieces()[0].target;
+            std::string R;
+            // C's roots the trees may read by column: root index -> (row stride, column-0 offset)
+            std::map<int, std::pair<int64_t, int64_t>> croots;
+            std::set<std::string> cnames;
+            if (affine2d(map_of(C), ldc, cc0)) {
+                R = map_of(C).pieces()[0].target;
+            } else {
+                // C split over roots (decode QKV: Q and K columns into two intermediates, V straight
+                // into the cache row): the trees read the row-affine pieces on intermediate roots
+                for (const VPiece& pc : map_of(C).pieces()) {
+                    bool axes = pc.lo[0] == 0 && pc.hi[0] == M && g_.tensor(pc.target).kind == TensorKind::Intermediate;
+                    for (const auto& tm : pc.off.t) axes = axes && tm.a->kind == AtomKind::Axis;
+                    if (!axes) continue;
+                    auto s0 = VMap::tile_stride(pc, 0, M), s1 = VMap::tile_stride(pc, 1, pc.hi[1] - pc.lo[1]);
+                    if (!s0 || !s1 || *s1 != 1 || *s0 % 8 || pc.off.c0 % 8) continue;
+                    const int ti = target(pc.target).index;
+                    if (croots.count(ti)) {  // one root in two pieces: not resolved here
+                        R.clear();
+                        break;
+                    }
+                    croots[ti] = {*s0, pc.off.c0};
+                    cnames.insert(pc.target);
+                    if (R.empty()) R = pc.target;
+                }
+                if (R.empty()) {
+                    if (dbg_fuse) fprintf(stderr, "[vtc fuse] %s: output map has no row-affine intermediate piece\n", n.id.c_str());
+                    continue;
+                }
+            }
             const int Ridx = target(R).index;
+            if (croots.empty()) {
+                croots[Ridx] = {ldc, cc0};
+                cnames.insert(R);
+            }
             const int pos_n = topo_pos.at(n.id);
             TcTrees tt;
             std::vector<std::string> roots_fused;
@@ -1469,7 +1509,7 @@ void Executor::prepare(bool dry) {
                 if (absorbed.count(root) || int(tt.trees.size()) == GEMM_MAX_TREES) continue;
                 bool hits = false;
                 for (const auto& in : t.in_names)
-                    for (const auto& r : targets_of(map_of(in))) hits |= r == R;
+                    for (const auto& r : targets_of(map_of(in))) hits |= cnames.count(r) > 0;
                 if (!hits) continue;
                 const OpNode* rn = g_.node(root);
                 const std::string& O = rn->outputs[0];
@@ -1485,7 +1525,7 @@ void Executor::prepare(bool dry) {
                 bool ok = true;
                 for (const auto& in : t.in_names) {
                     bool fromc = false;
-                    for (const auto& r2 : targets_of(map_of(in))) fromc |= r2 == R;
+                    for (const auto& r2 : targets_of(map_of(in))) fromc |= cnames.count(r2) > 0;
                     if (fromc) continue;
                     const OpNode* pr = g_.producer(in);  // an eliminated view runs nothing: its roots count
                     if (pr && !(is_data_movement(*pr) && elim.count(pr->id)) && topo_pos.at(pr->id) >= pos_n) ok = false;
@@ -1553,14 +1593,15 @@ void Executor::prepare(bool dry) {
                             if (shp[size_t(d)] > 1 && pc.aff[d] != want) return false;  // unit axes: any stride
                             want *= shp[size_t(d)];
                         }
-                        const bool c_side = pc.target == Ridx;
+                        const auto cr = croots.find(pc.target);
+                        const bool c_side = cr != croots.end();
                         if (fromc >= 0 && fromc != int(c_side)) return false;
                         fromc = int(c_side);
                         op.rs[q] = rs;
                         op.sh[q] = pc.aff[r - 2];
                         if (c_side) {
-                            if (is_out || rs != ldc) return false;
-                            op.ccol[q] = pc.base - cc0;
+                            if (is_out || rs != cr->second.first) return false;
+                            op.ccol[q] = pc.base - cr->second.second;
                             const int64_t lo_i = q == 0 ? 0 : op.split, hi_i = q == 0 && lm.npieces == 2 ? op.split : hd;
                             if (csh != INT64_MIN && csh != op.sh[q]) return false;
                             csh = op.sh[q];
@@ -1570,6 +1611,16 @@ void Executor::prepare(bool dry) {
                             if (pc.target == Ridx) return false;
                             if ((pc.base * 2) % 16 || rs % 8 || op.sh[q] % 8) return false;
                             op.base[q] = pc.ptr + uint64_t(pc.base * 2);
+                            // dynamic position: only the output may address a cache, inside the
+                            // position's row (its bases are patched per step); inputs stay static
+                            if (const DynRoot* dr = impl_->dyn_on ? impl_->dyn.find(pc.target) : nullptr) {
+                                int64_t lo = 0, hi = 0;
+                                const int64_t row = dr->rs * dr->es;
+                                if (!is_out || !DynCtx::piece_range(lm, q, lo, hi) || lo < impl_->dyn.p0 * dr->rs ||
+                                    hi >= (impl_->dyn.p0 + 1) * dr->rs || (T.out_dyn && T.out_dyn != row))
+                                    return false;
+                                T.out_dyn = row;
+                            }
                         }
                     }
                     if (lm.npieces == 1) {
@@ -1634,7 +1685,7 @@ void Executor::prepare(bool dry) {
             std::set<std::string> members;
             for (const auto& root : roots_fused)
                 for (const auto& m2 : ew_trees.at(root).members) members.insert(m2);
-            bool clean = best_hi > best_lo && !graph_out.count(R) && ldc == N && cc0 == 0;
+            bool clean = best_hi > best_lo && croots.size() == 1 && !graph_out.count(R) && ldc == N && cc0 == 0;
             for (const auto& [tid, m] : ptg_.resolved) {
                 if (!clean) break;
                 const auto mt = m.targets();
@@ -2456,7 +2507,7 @@ void Executor::prepare(bool dry) {
                             p.ntiles_total = int32_t(tiles);
                             // the split-K reduction spread over every split (one CTA per SM, so the
                             // grid is co-resident when it fits the SMs): VTC_NO_COOP_REDUCE=1 off
-                            p.coop_reduce = (tiles * splits <= sms && p.mt == 1 && p.epi != GEMM_EPI_TREES &&
+                            p.coop_reduce = (tiles * splits <= sms && p.mt == 1 && (p.epi != GEMM_EPI_TREES || tun.tree_coop) &&
                                              !tun.no_coop_reduce)
                                                 ? 1
                                                 : 0;

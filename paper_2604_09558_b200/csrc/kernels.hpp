@@ -257,6 +257,7 @@ struct GemmTree {
     int32_t nin, nprog, result, hd;
     int32_t nh, pat;  // pat 3: the program is (in0 * in1) + (in2 * in3) (RoPE), evaluated in registers
     int64_t c_lo, c_sh;
+    int64_t out_dyn;  // dynamic-position plans: bytes per position the output bases move (0: static)
     EwInstr prog[EW_MAX_PROG];
     GemmTreeOp op[EW_MAX_IN + 1];  // [0] = output
 };

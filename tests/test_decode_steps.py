@@ -21,10 +21,23 @@ def _relerr(got, want):
 
 @pytest.mark.parametrize("cfg", [
     dict(B=2, L=64, D=256, Hq=4, Hkv=2, hd=64, F=512),      # streamed GEMV path (M <= 4), fused RoPE epilogue
-    dict(B=32, L=96, D=256, Hq=4, Hkv=2, hd=128, F=512),    # tcgen05 GEMM + RoPE eltwise path
+    dict(B=32, L=96, D=256, Hq=4, Hkv=2, hd=128, F=512),    # tcgen05 GEMM, RoPE trees in its epilogue
+    dict(B=64, L=256, D=4096, Hq=32, Hkv=8, hd=128, F=14336),  # C3 widths: split-K GEMMs, trees spread over splits
     dict(B=1, L=2048, D=4096, Hq=32, Hkv=8, hd=128, F=14336),  # BASELINE configs[1] shape
 ])
 def test_dynamic_position_consecutive_steps(vtc, oracle, cfg):
+    _consecutive_steps(vtc, oracle, cfg)
+
+
+def test_dynamic_position_rope_trees_in_split_k_epilogue(vtc, oracle, monkeypatch):
+    # opt-in (VTC_TREE_COOP=1): the Q / K RoPE trees run in the cooperative split-K epilogue of
+    # the decode QKV GEMM, the roped K row stored into the cache at the runtime position
+    monkeypatch.setenv("VTC_TREE_COOP", "1")
+    launches = _consecutive_steps(vtc, oracle, dict(B=64, L=256, D=4096, Hq=32, Hkv=8, hd=128, F=14336))
+    assert "eltwise_aff" not in launches and "eltwise" not in launches, launches
+
+
+def _consecutive_steps(vtc, oracle, cfg):
     from paper_2604_09558_b200 import workloads as W
     B, L, hd = cfg["B"], cfg["L"], cfg["hd"]
     doc = W.llama_decode_layer(**cfg)  # ScatterND row L - 1: the largest position
@@ -66,6 +79,7 @@ def test_dynamic_position_consecutive_steps(vtc, oracle, cfg):
     assert _relerr(oracle.bf16_to_f32(gv[rows]), oracle.bf16_to_f32(vc[rows])) < 2e-2
     keep = np.r_[0:start, start + 8:L]
     assert np.array_equal(gk[keep], x0["k_cache"][keep]) and np.array_equal(gv[keep], x0["v_cache"][keep])
+    return launches
 
 
 def test_dynamic_position_errors(vtc, oracle):

@@ -1462,10 +1462,10 @@ void Executor::prepare(bool dry) {
             const std::string& C = n.outputs[0];
             if (g_.tensor(C).kind != TensorKind::Intermediate) continue;
             const int64_t M = g_.tensor(C).shape[0], N = g_.tensor(C).shape[1];
-            // decode-sized M (fewer tiles than SMs: the GEMM takes K splits): the trees in the
+            // decode batch (one 128-row tile, K splits over the weight stream): the trees in the
             // split-K epilogue measured slower than the separate eltwise launch (C3 QKV 58.7 us
             // last-split, 41.1 us cooperative, vs 25.0 + 7.7 us); VTC_TREE_COOP=1 fuses them anyway
-            if ((M + 127) / 128 * ((N + 255) / 256) < (impl_->dry ? 148 : device_sms()) && !tun.tree_coop) continue;
+            if (M <= 128 && !tun.tree_coop) continue;
             int64_t ldc = 0, cc0 = 0;
             std::string R;
             // C's roots the trees may read by column: root index -> (row stride, column-0 offset)
